@@ -1,0 +1,71 @@
+"""Seeded synthetic inputs shared by the golden generator and the tests.
+
+Everything is regenerated from a seed (numpy PCG64), so the committed golden
+files only hold reference OUTPUTS.  Q/K/V are rounded to bfloat16-exact
+values (stored as float32/float64) so that the GPU's bf16 storage of the
+full-precision rows is lossless, as SURVEY.md §8(d) prescribes.
+"""
+
+import numpy as np
+
+
+def round_bf16(x):
+    """Round-to-nearest-even to bfloat16, returned as float32."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).reshape(x.shape)
+
+
+def qkv(seed, h_q, h_kv, n, d, heavy=0):
+    """Q [h_q, n, d], K/V [h_kv, n, d] bf16-exact float32.  ``heavy`` plants
+    that many large-norm early keys per head (harness.py:59-64 pattern)."""
+    rng = np.random.default_rng(seed)
+    Q = round_bf16(rng.standard_normal((h_q, n, d)))
+    K = round_bf16(rng.standard_normal((h_kv, n, d)))
+    V = round_bf16(rng.standard_normal((h_kv, n, d)))
+    if heavy:
+        for h in range(h_kv):
+            idx = rng.choice(max(1, n // 2), size=min(heavy, max(1, n // 2)), replace=False)
+            K[h, idx] = round_bf16(K[h, idx] * 5.0)
+            V[h, idx] = round_bf16(V[h, idx] * 3.0)
+    return Q, K, V
+
+
+def codebooks(seed, h_kv, m, d_sub, scale=1.0):
+    """Per-KV-head float32 codebooks [h_kv, m, d_sub] (K and V)."""
+    rng = np.random.default_rng(seed + 7919)
+    ck = (scale * rng.standard_normal((h_kv, m, d_sub))).astype(np.float32)
+    cv = (scale * rng.standard_normal((h_kv, m, d_sub))).astype(np.float32)
+    return ck, cv
+
+
+# name: (seed, n, d, notation, window, frac, count, policy, steps, pos_stride, blocks)
+CACHE_CASES = {
+    "c1_d8_d4m16": (11, 48, 8, "d4m16", 8, 0.05, None, "by_sum", 12, 1, 16),
+    "c2_d128_d8m256": (12, 256, 128, "d8m256", 32, 0.01, None, "by_sum", 64, 1, 64),
+    "c3_d64_d32m4096": (13, 128, 64, "d32m4096", 16, 0.02, None, "by_sum", 8, 1, 64),
+    "c4_d16_d4m32_byk_stride3": (14, 96, 16, "d4m32", 8, 0.05, 5, "by_k", 16, 3, 16),
+    "c5_d32_d2m256_byv": (15, 64, 32, "d2m256", 4, 0.03, None, "by_v", 10, 1, 16),
+    "c6_d128_d8m256_all_anchor": (16, 40, 128, "d8m256", 4, 1.0, None, "by_sum", 6, 1, 8),
+    "c7_d128_d8m256_no_window": (17, 70, 128, "d8m256", 0, 0.0, None, "by_sum", 6, 1, 32),
+}
+
+
+
+FA_CASES = {"small": (77, 16, 16, 8, 101), "d128": (200, 128, 64, 64, 102),
+            "ragged": (33, 10, 7, 5, 103)}
+AN_CASES = {"d8m256": (2000, 256, 8, 201), "d4m16": (500, 16, 4, 202),
+            "d32m4096": (64, 4096, 32, 203), "d2m256": (700, 256, 2, 204)}
+
+
+def fa_inputs(n, d, seed):
+    rng = np.random.default_rng(seed)
+    return tuple(rng.standard_normal((n, d)) for _ in range(3))
+
+
+def an_inputs(N, m, ds, seed):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((N, ds))
+    C = rng.standard_normal((m, ds)).astype(np.float32).astype(np.float64)
+    return X, C
