@@ -1,0 +1,536 @@
+"""Benchmark of the AnTKV decode path on B200 (contract: see DESIGN.md §6).
+
+Workload (BASELINE.json metric, configs[2]/north star shape on one GPU):
+LLaMA-3-8B attention shapes (32 Q / 8 KV heads, d=128), 128K-token context
+per GPU, 1-bit VQ KV (d8m256), 1 % anchors, 32-token window, batch 1.  One
+step = one decode token through the attention of all 32 layers (each layer
+has its own cache: ~1.2 GB of state per step, far above the 126 MB L2, so no
+L2 flush is needed).  Per layer the step appends the token, runs split-KV
+decode attention over codes + anchors + window with RoPE after
+reconstruction, merges the splits and evicts/encodes the oldest window row.
+
+value = decode-attention tok/s as BASELINE.md defines it
+        (batch / time of one layer's decode-attention call, all heads),
+        aggregated over ranks (weak scaling: 128K context per GPU, the
+        sequence is sharded and partials are merged with NCCL).
+--impl reference times the reference algorithm (oracle port of
+cache.py:149-194, numpy, one process per KV head on the host cores) on a
+bounded sample of the same workload.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HQ, HKV, D = 32, 8, 128
+METRIC = "decode attn tok/s & HBM GB/s at 128K ctx, 1-bit VQ KV; encode tok/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--ctx", type=int, default=131072, help="context tokens per GPU")
+    p.add_argument("--layers", type=int, default=32)
+    p.add_argument("--batch", type=int, default=1)
+    p.add_argument("--notation", default="d8m256")
+    p.add_argument("--kernel", default="fast", choices=["fast", "generic"])
+    p.add_argument("--splits", type=int, default=0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        return float(j["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ ours
+def build_layers(args, rank, world, torch):
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.anchors import select_anchors_device
+    vq = VqConfig.from_notation(args.notation)
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=500000.0)
+    n = args.ctx
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    rng = np.random.default_rng(1000 + rank)
+    caches = []
+    global_n = n * world
+    offset = rank * n
+    for layer in range(args.layers):
+        ck = rng.standard_normal((HKV, vq.m, vq.d_sub)).astype(np.float32)
+        cv = rng.standard_normal((HKV, vq.m, vq.d_sub)).astype(np.float32)
+        cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), batch=args.batch,
+                                 q_heads=HQ, fast=(args.kernel == "fast"), splits=args.splits,
+                                 capacity=n + args.steps + args.warmup + 64, token_offset=offset)
+        K = torch.randn((args.batch, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
+        V = torch.randn((args.batch, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
+        # anchors: the real top-k kernel on synthetic anchor scores; this
+        # shard holds 1 % of its tokens (its share of the global budget)
+        budget = cfg.budget_for(n)
+        sc_k = torch.rand((args.batch * HKV, n), device="cuda", generator=g)
+        sc_v = torch.rand((args.batch * HKV, n), device="cuda", generator=g)
+        anchors = select_anchors_device(sc_k, sc_v, budget).view(args.batch, HKV, budget)
+        pos = (torch.arange(n, device="cuda", dtype=torch.int64) + offset)[None].repeat(args.batch, 1)
+        cache.build_from(K, V, pos, anchors)
+        if world > 1 and rank == world - 1:
+            # the tail shard promotes window rows against the global budget:
+            # it counts every shard's anchors (each shard holds `budget`)
+            cache.tensors["hstate"][:, :, 0] = budget * world
+        del K, V, sc_k, sc_v
+        caches.append(cache)
+    torch.cuda.synchronize()
+    return caches, cfg
+
+
+def algorithmic_bytes(cache, torch):
+    """Bytes one decode-attention call must move (SURVEY.md §8d formula):
+    H_kv*[n_q*(code bytes/token) + n_fp*2*d*2] + 2*H_q*d*2 + codebooks."""
+    t = cache.tensors
+    n = cache.token_count
+    vq = cache.config.vq
+    code_b = 2 * (D // vq.d_sub) * vq.index_bits / 8.0
+    total = 0.0
+    hs = t["hstate"].cpu().numpy()
+    for b in range(cache.B):
+        for h in range(cache.Hkv):
+            n_fp = int((t["pool_kind"][b, h] >= 0).sum())
+            total += (n - n_fp) * code_b + n_fp * 2 * D * 2
+    total += cache.B * (2 * HQ * D * 2)
+    total += cache.Hkv * 2 * vq.m * vq.d_sub * 4
+    return total
+
+
+def encode_throughput(torch, n=131072, reps=5):
+    """tokens/s through K+V encoding of all 8 KV heads of one layer."""
+    from paper_2506_19505_b200 import _lib
+    vq_m, d_sub = 256, 8
+    g = torch.Generator(device="cuda").manual_seed(7)
+    X = torch.randn((2 * HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
+    C = torch.randn((2 * HKV, vq_m, d_sub), device="cuda", generator=g)
+    codes = torch.empty((2 * HKV, n, D // d_sub), dtype=torch.uint8, device="cuda")
+    st = _lib.stream()
+
+    def run():
+        for i in range(2 * HKV):
+            _lib.call("antkv_vq_encode", _lib.ptr(X[i]), _lib.BF16, n, D, _lib.ptr(C[i]), vq_m,
+                      d_sub, _lib.ptr(codes[i]), 1, st)
+    run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = n * 2 * HKV * (D // d_sub) * vq_m * d_sub * 2
+    return {"value": n / (ms / 1e3), "unit": "tok/s", "ms_per_layer": ms, "tokens": n,
+            "config": "d8m256, K+V, 8 KV heads, d=128, float32 distances",
+            "tflops": flops / (ms / 1e3) / 1e12}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_19505_b200 import _lib
+    from paper_2506_19505_b200.parallel import gather_partials, lse_merge
+    _lib.load()
+    caches, cfg = build_layers(args, rank, world, torch)
+    L, B = args.layers, args.batch
+    n0 = caches[0].token_count
+    is_tail = rank == world - 1
+    g = torch.Generator(device="cuda").manual_seed(77)
+    total_steps = args.warmup + args.steps
+    qs = torch.randn((total_steps, L, B, HQ, D), device="cuda", generator=g).to(torch.bfloat16)
+    ks = torch.randn((total_steps, L, B, HKV, D), device="cuda", generator=g).to(torch.bfloat16)
+    vs = torch.randn((total_steps, L, B, HKV, D), device="cuda", generator=g).to(torch.bfloat16)
+    gpos0 = n0 * world
+    qpos = [torch.full((B,), gpos0 + s, dtype=torch.int64, device="cuda") for s in range(total_steps)]
+    out = torch.empty((B, HQ, D), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, HQ), dtype=torch.float32, device="cuda")
+    merged = torch.empty((B, HQ, D), dtype=torch.float32, device="cuda")
+
+    def layer_step(s, l, cache):
+        if world == 1:
+            cache.step_device(qs[s, l], ks[s, l], vs[s, l], qpos[s], out)
+            return out
+        if is_tail:
+            import ctypes
+            D_ = ctypes.byref(cache.desc)
+            lib = _lib.load(check_device=False)
+            _lib.check(lib.antkv_cache_append(D_, _lib.ptr(ks[s, l]), _lib.ptr(vs[s, l]), _lib.BF16,
+                                              _lib.ptr(qpos[s]), _lib.stream()))
+        cache.attend_device(qs[s, l], qpos[s], out, lse)
+        if is_tail:
+            _lib.check(_lib.load(check_device=False).antkv_cache_evict(ctypes.byref(cache.desc),
+                                                                        _lib.stream()))
+        o_all, l_all = gather_partials(out, lse)
+        return lse_merge(o_all, l_all, merged)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(args.warmup):
+        for l in range(L):
+            layer_step(s, l, caches[l])
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record()
+        for s in range(args.warmup, total_steps):
+            for l in range(L):
+                layer_step(s, l, caches[l])
+        e1.record()
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    for c in caches:
+        c._n += args.warmup + args.steps if is_tail else 0
+
+    # attention-kernel-only timing on the same caches (no append/evict)
+    reps = max(3, min(args.steps, 10))
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qlast = qpos[-1]
+    for l in range(L):
+        caches[l].attend_device(qs[0, l], qlast, out)
+    torch.cuda.synchronize()
+    a0.record()
+    for r in range(reps):
+        for l in range(L):
+            caches[l].attend_device(qs[r % total_steps, l], qlast, out)
+    a1.record()
+    torch.cuda.synchronize()
+    attn_ms = a0.elapsed_time(a1) / (reps * L)
+    alg_bytes = algorithmic_bytes(caches[0], torch)
+
+    # e2e through the public step API with pinned host buffers
+    qh = qs[: min(total_steps, 4)].cpu().pin_memory()
+    kh = ks[: min(total_steps, 4)].cpu().pin_memory()
+    vh = vs[: min(total_steps, 4)].cpu().pin_memory()
+    outh = torch.empty((L, B, HQ, D), dtype=torch.float32).pin_memory()
+    dq = torch.empty_like(qs[0, 0])
+    dk = torch.empty_like(ks[0, 0])
+    dv = torch.empty_like(vs[0, 0])
+    e2e_steps = max(3, min(args.steps, 8))
+    base = total_steps
+    cap_left = min(c.capacity for c in caches) - caches[0].token_count - 2
+    e2e_steps = min(e2e_steps, max(1, cap_left))
+    barrier()
+    h0 = time.perf_counter()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for s in range(e2e_steps):
+        p = torch.full((B,), gpos0 + base + s, dtype=torch.int64).pin_memory().cuda(non_blocking=True)
+        for l in range(L):
+            i = s % qh.shape[0]
+            dq.copy_(qh[i, l], non_blocking=True)
+            dk.copy_(kh[i, l], non_blocking=True)
+            dv.copy_(vh[i, l], non_blocking=True)
+            if world == 1:
+                caches[l].step_device(dq, dk, dv, p, out)
+                outh[l].copy_(out, non_blocking=True)
+            else:
+                caches[l].attend_device(dq, p, out, lse)
+                o_all, l_all = gather_partials(out, lse)
+                outh[l].copy_(lse_merge(o_all, l_all, merged), non_blocking=True)
+    x1.record()
+    torch.cuda.synchronize()
+    e2e_ms = x0.elapsed_time(x1) / e2e_steps
+    t = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    enc = encode_throughput(torch) if rank == 0 else None
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / (attn_ms / 1e3) / 1e9
+    value = B * L / (ms / 1e3) * world          # weak scaling: 128K-context equivalents
+    result = None
+    if rank == 0:
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "tok/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f16-mma/f32-accum" if args.kernel == "fast" else "f32",
+            "data": "synthetic (seeded randn bf16 K/V, random N(0,1) codebooks)",
+            "config": {
+                "workload": f"decode attention, {args.ctx // 1024}K ctx per GPU x {world} GPU(s), "
+                            f"{args.notation} (1-bit), 1% anchors, window 32, {HQ} Q / {HKV} KV heads, "
+                            f"d={D}, batch {B}, {L} layers per step",
+                "ctx_per_gpu": args.ctx, "layers_per_step": L, "batch": B, "kernel": args.kernel,
+                "l2": f"no flush: per-step working set {alg_bytes * L / 1e9:.2f} GB > 126 MB L2",
+                "tok_s_definition": "batch * layers / step time (BASELINE.md: batch / one layer's "
+                                    "decode-attention call) x GPUs (weak scaling)",
+                "model_tok_s": B / (ms / 1e3),
+            },
+            "hbm_gbs": achieved,
+            "roofline": {"bound": "hbm", "kernel": "decode attention (split-KV + combine)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "traffic": None, "algorithmic_bytes_per_launch": alg_bytes,
+                         "launch_ms": attn_ms},
+            "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
+                    "h2d_bytes_per_step": L * (qh[0, 0].numel() + 2 * kh[0, 0].numel()) * 2 + 8,
+                    "d2h_bytes_per_step": L * B * HQ * D * 4, "ms_per_step": e2e_ms},
+            "gpu_launches": args.steps * L * (4 if world == 1 else 3),
+            "clocks": clk.summary(),
+            "encode": enc,
+        }
+    return result, caches
+
+
+# ------------------------------------------------------------- reference
+def _cpu_head_worker(args_tuple):
+    """One KV head of one layer-step with the reference's decode math
+    (cache.py:168-178 via the oracle restatement): dequantize every token
+    with a per-token centroid lookup, RoPE all keys in float64, softmax, AV
+    for the group's query heads."""
+    import antkv_oracle as O
+    kcodes, vcodes, qbits, rows_k, rows_v, fp_tok, ck, cv, q, qpos, theta = args_tuple
+    t0 = time.perf_counter()
+    n = len(qbits)
+    Khat = np.empty((n, D), dtype=np.float32)
+    Vhat = np.empty((n, D), dtype=np.float32)
+    for j in range(n):           # dequantize() loop, cache.py:204-210
+        if qbits[j]:
+            Khat[j] = O.decode_rows(kcodes[j][None], ck)[0]
+            Vhat[j] = O.decode_rows(vcodes[j][None], cv)[0]
+    Khat[fp_tok] = rows_k
+    Vhat[fp_tok] = rows_v
+    pos = np.arange(n, dtype=np.int64)
+    Kr = O.apply_rope(Khat.astype(np.float64), pos, theta)
+    outs = []
+    for hq in range(q.shape[0]):
+        qr = O.apply_rope(q[hq][None], np.array([qpos]), theta)
+        A = O.softmax_rows((qr @ Kr.T) / np.sqrt(D))
+        outs.append((A @ Vhat.astype(np.float64))[0])
+    return time.perf_counter() - t0
+
+
+def cpu_sample_from_cache(cache, n_heads):
+    """Host copies of (b=0) heads of a GPU cache for the CPU reference arm."""
+    import torch
+    t = cache.tensors
+    n = cache.token_count
+    G = D // cache.config.vq.d_sub
+    codes = t["codes"][0, :n_heads, :n].cpu().numpy().reshape(n_heads, n, 2, G)
+    qm = t["qmask"][0, :n_heads].cpu().numpy().view(np.uint32)
+    items = []
+    rng = np.random.default_rng(5)
+    for h in range(n_heads):
+        bits = np.unpackbits(qm[h].view(np.uint8), bitorder="little")[:n].astype(bool)
+        kind = t["pool_kind"][0, h].cpu().numpy()
+        tok = t["pool_tok"][0, h].cpu().numpy()
+        live = (kind >= 0) & (tok >= 0) & (tok < n)
+        rows = t["pool_rows"][0, h].float().cpu().numpy()
+        items.append((codes[h, :, 0].astype(np.int64), codes[h, :, 1].astype(np.int64), bits,
+                      rows[live, 0], rows[live, 1], tok[live],
+                      t["cb_k"][h].cpu().numpy(), t["cb_v"][h].cpu().numpy(),
+                      rng.standard_normal((HQ // HKV, D)), n, cache.config.theta_base))
+    return items
+
+
+def run_cpu(items, repeats):
+    """Time `repeats` layer-steps (all KV heads in parallel over host cores)."""
+    import multiprocessing as mp
+    cores = min(len(items), os.cpu_count() or 1)
+    sys.path.insert(0, str(ROOT / "oracle"))
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    walls = []
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            pool.map(_cpu_head_worker, items)
+            walls.append(time.perf_counter() - t0)
+    return walls, cores
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port) on the host."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import torch
+    sys.path.insert(0, str(ROOT / "oracle"))
+    # the CPU arm needs the same cache contents; build one layer on the GPU
+    # (if present) to get identical codes, otherwise synthesise on the host
+    a = argparse.Namespace(**vars(args))
+    a.layers = 1
+    if torch.cuda.is_available():
+        from paper_2506_19505_b200 import _lib
+        _lib.load()
+        caches, _ = build_layers(a, 0, 1, torch)
+        items = cpu_sample_from_cache(caches[0], HKV)
+    else:
+        items = _host_items(args.ctx)
+    steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0
+    walls, cores = run_cpu(items, warm + steps)
+    walls = walls[warm:]
+    t = float(np.mean(walls))
+    value = args.batch / t
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "tok/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warm,
+        "ms_per_step": t * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (same cache contents as the GPU arm)",
+        "config": {"workload": f"decode attention, {args.ctx // 1024}K ctx, {args.notation}, "
+                               f"1% anchors, window 32, {HQ} Q / {HKV} KV heads, d={D}, batch "
+                               f"{args.batch}; one step = one layer's decode-attention call",
+                   "ctx_per_gpu": args.ctx},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
+                         "sample": f"{steps} layer-step(s) at {args.ctx} tokens, "
+                                   f"{HKV} KV heads in parallel processes"},
+        "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def _host_items(n):
+    rng = np.random.default_rng(0)
+    items = []
+    for h in range(HKV):
+        bits = np.ones(n, dtype=bool)
+        fp = np.sort(rng.choice(n, size=math.ceil(0.01 * n) + 32, replace=False))
+        bits[fp] = False
+        items.append((rng.integers(256, size=(n, 16)), rng.integers(256, size=(n, 16)), bits,
+                      rng.standard_normal((len(fp), D)).astype(np.float32),
+                      rng.standard_normal((len(fp), D)).astype(np.float32), fp,
+                      rng.standard_normal((256, 8)).astype(np.float32),
+                      rng.standard_normal((256, 8)).astype(np.float32),
+                      rng.standard_normal((HQ // HKV, D)), n, 500000.0))
+    return items
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        res = run_reference(args)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res, caches = run_ours(args)
+    rank = int(os.environ.get("RANK", "0"))
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            items = cpu_sample_from_cache(caches[0], HKV)
+            walls, cores = run_cpu(items, 2)
+            t = float(np.mean(walls[1:])) if len(walls) > 1 else walls[0]
+            res["cpu_baseline"] = {"value": args.batch / t, "unit": "tok/s", "cores": cores,
+                                   "kind": "port",
+                                   "sample": f"1 layer-step at {args.ctx} tokens ({HKV} KV heads, "
+                                             f"reference decode math per head, one process per "
+                                             f"head), {t:.2f} s wall"}
+        print(json.dumps(res), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,235 @@
+/*
+ * antkv_b200.h — C ABI of the B200-native AnTKV anchor-token sub-bit KV-cache
+ * path (libantkv_b200.so, built for sm_100a).
+ *
+ * Every entry point takes plain device pointers and sizes plus a CUDA stream
+ * (as void*, NULL = default stream) and returns an ANTKV_* status code.  No
+ * entry point synchronises the stream; outputs are ready when the stream
+ * reaches them.  antkv_last_error() returns the message of the last failure
+ * on the calling thread.  Invalid arguments (the reference's ValueError)
+ * return ANTKV_EINVAL before anything is launched.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/antkv):
+ *   antkv_flash_aux        <- kernels.flash_aux      (_ckernels.pyx:10-88,
+ *                             kernels/__init__.py:35)
+ *   antkv_ans_blocked      <- kernels.ans_blocked    (_ckernels.pyx:91-131,
+ *                             kernels/__init__.py:36)
+ *   antkv_assign_nearest   <- kernels.assign_nearest (_ckernels.pyx:134-163,
+ *                             kernels/__init__.py:37)
+ *   antkv_prefill_attention <- attention.flash_attention_aux (attention.py:146-169)
+ *                             with RoPE (attention.py:89-106) fused, GQA-batched
+ *   antkv_prefill_anchor_scores <- anchors.anchor_scores_blocked (anchors.py:235-256)
+ *   antkv_select_anchors   <- anchors.select_anchors  (anchors.py:265-301)
+ *   antkv_cache_build      <- QuantizedKVCache.prefill layout step (cache.py:122-139)
+ *   antkv_cache_append     <- QuantizedKVCache.decode_step append (cache.py:157-166)
+ *   antkv_decode_attention <- QuantizedKVCache.decode_step math (cache.py:168-178)
+ *   antkv_cache_evict      <- QuantizedKVCache.decode_step eviction (cache.py:180-193)
+ *   antkv_cache_dequantize <- QuantizedKVCache.dequantize (cache.py:196-211)
+ *   antkv_vq_encode        <- vq.encode_rows (vq.py:226-232)
+ *   antkv_vq_decode        <- vq.decode_rows (vq.py:243-248)
+ *   antkv_lse_combine      <- (new) split-KV / sequence-shard log-sum-exp merge
+ */
+#ifndef ANTKV_B200_H
+#define ANTKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ANTKV_API __attribute__((visibility("default")))
+#else
+#define ANTKV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ANTKV_OK 0
+#define ANTKV_EINVAL 1       /* invalid argument (reference ValueError)      */
+#define ANTKV_ECUDA 2        /* CUDA runtime error                           */
+#define ANTKV_EUNSUPPORTED 3 /* configuration not supported by this build    */
+
+#define ANTKV_POLICY_BY_K 0
+#define ANTKV_POLICY_BY_V 1
+#define ANTKV_POLICY_BY_SUM 2
+
+#define ANTKV_KIND_ANCHOR 0
+#define ANTKV_KIND_QUANTIZED 1
+#define ANTKV_KIND_WINDOWED 2
+#define ANTKV_KIND_FREE -1
+
+#define ANTKV_HSTATE_WORDS 8 /* per (sequence, kv head) state words         */
+#define ANTKV_HS_ANCHORS 0   /* anchor count                                */
+#define ANTKV_HS_WIN_HEAD 1  /* index of the oldest windowed slot in ring   */
+#define ANTKV_HS_WIN_COUNT 2 /* number of windowed rows                     */
+#define ANTKV_HS_FREE_TOP 3  /* free-stack size                             */
+#define ANTKV_HS_POOL_HIGH 4 /* high-water mark of used pool slots          */
+
+/* dtype tags for row inputs */
+#define ANTKV_F32 0
+#define ANTKV_BF16 1
+#define ANTKV_F16 2
+
+ANTKV_API const char *antkv_last_error(void);
+ANTKV_API int antkv_version(void);
+/* 1 when the running device is sm_100 (B200) and the library kernels load. */
+ANTKV_API int antkv_device_check(int device);
+
+/* ------------------------------------------------------------------------
+ * Reference FFI (antkv._ckernels).  Batched over `heads` query heads; query
+ * head h reads K/V head h / (heads / kv_heads).  Inputs are float32, row
+ * major, already RoPE-rotated, Qs pre-scaled by 1/sqrt(d) — exactly the
+ * contract of the reference kernels.  Block sizes only change the reference's
+ * rounding order; the GPU tiles internally and accepts any block >= 1.
+ *   Qs [heads][n_q][d], Kr [kv_heads][n_k][d], V [kv_heads][n_k][dv]
+ *   O [heads][n_q][dv], L/M [heads][n_q]
+ * causal requires n_q == n_k (attention.py:160-161).
+ * ---------------------------------------------------------------------- */
+ANTKV_API int antkv_flash_aux(const float *Qs, const float *Kr, const float *V,
+                    int heads, int kv_heads, int n_q, int n_k, int d, int dv,
+                    int block_q, int block_k, int causal,
+                    float *O, float *L, float *M, void *stream);
+
+/* ans_k/ans_v [heads][n_k]: per query head (no GQA summation here). */
+ANTKV_API int antkv_ans_blocked(const float *Qs, const float *Kr, const float *M,
+                      const float *L, const float *q_norms,
+                      int heads, int kv_heads, int n_q, int n_k, int d,
+                      int block_q, int block_k, int causal,
+                      float *ans_k, float *ans_v, void *stream);
+
+/* X [n][d_sub], C [m][d_sub] float32 -> idx int64 [n], d2 float32 [n].
+ * Strict-< argmin over centroids in index order: ties -> lowest index. */
+ANTKV_API int antkv_assign_nearest(const float *X, const float *C, int64_t n, int m,
+                         int d_sub, int64_t *idx, float *d2, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Path kernels.
+ * ---------------------------------------------------------------------- */
+
+/* Causal prefill attention with RoPE applied in-kernel (interleaved pairs,
+ * fp64-accurate angles), GQA.  Q [B][Hq][n][d], K/V [B][Hkv][n][d] in
+ * `dtype`; positions int64 [B][n].  Outputs O float32 [B][Hq][n][d],
+ * M/L float32 [B][Hq][n] (scaled-logit max / normaliser at M) and q_norms
+ * float32 [B][Hq][n] of the PRE-RoPE queries (attention.py:167). */
+ANTKV_API int antkv_prefill_attention(const void *Q, const void *K, const void *V, int dtype,
+                            const int64_t *positions, int B, int Hq, int Hkv,
+                            int n, int d, double theta_base,
+                            float *O, float *M, float *L, float *q_norms,
+                            void *stream);
+
+/* RoPE (attention.py:89-106): X [B][H][n][d] (dtype) rotated at positions
+ * int64 [B][n] (NULL = no rotation), times `scale`, into out float32; norms
+ * (optional) float32 [B][H][n] = L2 norm of the un-rotated row. */
+ANTKV_API int antkv_rope_rotate(const void *X, int dtype, const int64_t *positions,
+                                int B, int H, int n, int d, double theta_base,
+                                float scale, float *out, float *norms, void *stream);
+
+/* Anchor scores (Alg. 1 second pass) summed over each KV head's Q group:
+ * ans_k/ans_v float32 [B][Hkv][n]. */
+ANTKV_API int antkv_prefill_anchor_scores(const void *Q, const void *K, int dtype,
+                                const int64_t *positions, const float *M,
+                                const float *L, const float *q_norms,
+                                int B, int Hq, int Hkv, int n, int d,
+                                double theta_base, float *ans_k, float *ans_v,
+                                void *stream);
+
+/* Top-budget selection per (b, kv head) under `policy`, ties to the lower
+ * index, result sorted ascending: anchors int32 [B][Hkv][budget].
+ * budget is clipped to [0, n] by the caller (anchors.py:273). */
+ANTKV_API int antkv_select_anchors(const float *ans_k, const float *ans_v, int B, int Hkv,
+                         int n, int budget, int policy, int32_t *anchors,
+                         void *stream);
+
+/* Encode rows: X [rows][d] (dtype) with codebook [m][d_sub] float32 into
+ * codes [rows][d/d_sub] of width code_bytes (1, 2, or 8 = int64). */
+ANTKV_API int antkv_vq_encode(const void *X, int dtype, int64_t rows, int d,
+                    const float *codebook, int m, int d_sub,
+                    void *codes, int code_bytes, void *stream);
+
+/* Gather: codes [rows][groups] (code_bytes wide) -> out float32 [rows][groups*d_sub]. */
+ANTKV_API int antkv_vq_decode(const void *codes, int code_bytes, int64_t rows, int groups,
+                    const float *codebook, int m, int d_sub, float *out,
+                    void *stream);
+
+/* Quantized KV cache for B sequences x Hkv heads.  All buffers are device
+ * memory owned by the caller; sizes follow the bracketed shapes. */
+typedef struct antkv_cache_desc {
+  int B, Hq, Hkv, d, d_sub, m, groups, index_bits;
+  int code_bytes;      /* 1 when index_bits <= 8, else 2                   */
+  int capacity;        /* token slots per sequence                         */
+  int pool_capacity;   /* full-precision row slots per (b, kv head)        */
+  int window_size;
+  int policy;
+  int anchor_count;    /* < 0: use anchor_fraction (cache.py:54-57)        */
+  double anchor_fraction;
+  double theta_base;
+  int64_t token_offset;/* global index of slot 0 (sequence sharding)       */
+  uint8_t *codes;      /* [B][Hkv][capacity][2][groups*code_bytes]         */
+  uint32_t *qmask;     /* [B][Hkv][capacity/32] bit = slot holds codes     */
+  uint16_t *pool_rows; /* bf16 [B][Hkv][pool_capacity][2][d] (K row, V row)*/
+  int32_t *pool_tok;   /* [B][Hkv][pool_capacity] token slot, -1 free      */
+  int8_t *pool_kind;   /* [B][Hkv][pool_capacity] ANTKV_KIND_*             */
+  int32_t *win_ring;   /* [B][Hkv][window_size+1] pool slots, FIFO          */
+  int32_t *free_stack; /* [B][Hkv][pool_capacity]                           */
+  int32_t *hstate;     /* [B][Hkv][ANTKV_HSTATE_WORDS]                      */
+  int32_t *seq_len;    /* [B] tokens currently held                         */
+  int64_t *positions;  /* [B][capacity]                                     */
+  const float *codebook_k; /* [Hkv][m][d_sub] float32                       */
+  const float *codebook_v;
+  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8 copies][8] fp16    */
+  float *tile_cs;      /* fast path: [B][capacity/16][d/2][2] cos/sin of the
+                          16-slot tile base angle (float32)                 */
+} antkv_cache_desc;
+
+/* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */
+ANTKV_API int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int splits);
+
+/* Populate an EMPTY cache from prefill results (cache.py:122-139):
+ * K/V [B][Hkv][n][d] (dtype), positions int64 [B][n], anchors int32
+ * [B][Hkv][n_anchors] sorted.  Anchors keep full-precision rows, the last
+ * window_size non-anchor tokens are windowed, the rest are encoded. */
+ANTKV_API int antkv_cache_build(const antkv_cache_desc *c, const void *K, const void *V,
+                      int dtype, const int64_t *positions, int n,
+                      const int32_t *anchors, int n_anchors, void *stream);
+
+/* Append one token per sequence as WINDOWED (cache.py:157-166):
+ * k/v [B][Hkv][d] (dtype), position int64 [B].  seq_len[b] must be < capacity
+ * (checked on the host side by the caller's shadow). */
+ANTKV_API int antkv_cache_append(const antkv_cache_desc *c, const void *k, const void *v,
+                       int dtype, const int64_t *position, void *stream);
+
+/* Decode attention of q [B][Hq][d] (dtype) at positions qpos int64 [B]
+ * against the whole cache (anchors + window + codes), RoPE after
+ * reconstruction, split-KV with an LSE merge.  Writes out float32
+ * [B][Hq][d]; when lse != NULL also writes the log-sum-exp (natural log,
+ * scaled logits) float32 [B][Hq] so sequence shards can be merged.
+ * fast: 1 = use the sm_100a tensor-core kernel when the config allows
+ * (d == 128, d_sub == 8, m <= 256), 0 = generic fp32 kernel. */
+ANTKV_API int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
+                           const int64_t *qpos, float *out, float *lse,
+                           void *workspace, int64_t workspace_bytes, int splits,
+                           int fast, void *stream);
+
+/* Evict the oldest windowed row of every (b, head) whose window exceeds
+ * window_size: promote to anchor while the budget has headroom, otherwise
+ * encode it into the code slots (cache.py:180-193). */
+ANTKV_API int antkv_cache_evict(const antkv_cache_desc *c, void *stream);
+
+/* K_hat / V_hat float32 [B][Hkv][n][d], pre-RoPE (cache.py:196-211). */
+ANTKV_API int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *Khat,
+                           float *Vhat, void *stream);
+
+/* Merge P partial results: o [P][rows][d] (normalised), lse [P][rows] ->
+ * out [rows][d], lse_out [rows] (may be NULL). */
+ANTKV_API int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows,
+                      int d, float *out, float *lse_out, void *stream);
+
+/* Build the fast-path fp16 replicated codebook layout from codebook_k/v and
+ * the per-16-slot RoPE base tables for the tokens currently held. */
+ANTKV_API int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANTKV_B200_H */

@@ -1,0 +1,93 @@
+"""Anchor scores and selection, mirroring antkv.anchors (anchors.py:201-301).
+
+anchor_scores_blocked reconstructs A = exp(S - M)/L blockwise on the GPU
+(antkv_ans_blocked); select_anchors runs the radix top-k selection kernel
+(antkv_select_anchors) with the reference's policies and tie rule."""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import as_cuda, back
+from .attention import AttentionAux, _check, rope_device
+
+__all__ = ["AnchorScores", "AnchorSelection", "POLICIES", "anchor_scores_blocked",
+           "select_anchors", "select_anchors_device"]
+
+POLICIES = ("by_k", "by_v", "by_sum")
+
+
+@dataclass
+class AnchorScores:
+    ans_k: object
+    ans_v: object
+
+
+@dataclass
+class AnchorSelection:
+    indices: np.ndarray
+    budget: int
+    policy: str
+
+
+def anchor_scores_blocked(Q, K, V, aux: AttentionAux, block_q, block_k, rope=None,
+                          causal=False):
+    """Blockwise AnS from the attention auxiliaries (anchors.py:235-256)."""
+    Qt, was_np = _check(Q, "Q")
+    Kt, _ = _check(K, "K")
+    H, n_q, d = Qt.shape
+    Hk, n_k, _ = Kt.shape
+    M, _ = as_cuda(aux.M, torch.float32)
+    L, _ = as_cuda(aux.L, torch.float32)
+    qn, _ = as_cuda(aux.q_norms, torch.float32)
+    if M.numel() != H * n_q or L.numel() != H * n_q:
+        raise ValueError("aux statistics do not match the query count")
+    if block_q < 1 or block_k < 1:
+        raise ValueError("block sizes must be >= 1")
+    if causal and n_q != n_k:
+        raise ValueError("causal attention requires matching Q/K token counts")
+    pos = rope.positions if rope is not None else None
+    theta = rope.theta_base if rope is not None else 10000.0
+    Qs, _ = rope_device(Qt, pos, theta, 1.0 / np.sqrt(d))
+    Kr, _ = rope_device(Kt, pos, theta, 1.0)
+    ak = torch.empty((H, n_k), dtype=torch.float32, device=Qt.device)
+    av = torch.empty((H, n_k), dtype=torch.float32, device=Qt.device)
+    _lib.call("antkv_ans_blocked", _lib.ptr(Qs), _lib.ptr(Kr), _lib.ptr(M.contiguous()),
+              _lib.ptr(L.contiguous()), _lib.ptr(qn.contiguous()), H, Hk, n_q, n_k, d,
+              int(block_q), int(block_k), int(bool(causal)), _lib.ptr(ak), _lib.ptr(av),
+              _lib.stream())
+    single = was_np or (isinstance(Q, torch.Tensor) and Q.ndim == 2)
+    if single:
+        ak, av = ak[0], av[0]
+    return AnchorScores(ans_k=back(ak, was_np), ans_v=back(av, was_np))
+
+
+def select_anchors_device(ans_k, ans_v, budget, policy="by_sum"):
+    """ans_k/ans_v float32 CUDA [R, n] -> int32 [R, budget] sorted indices."""
+    R, n = ans_k.shape
+    out = torch.empty((R, budget), dtype=torch.int32, device=ans_k.device)
+    if budget > 0:
+        _lib.call("antkv_select_anchors", _lib.ptr(ans_k.contiguous()), _lib.ptr(ans_v.contiguous()),
+                  1, R, n, int(budget), _lib.POLICY[policy], _lib.ptr(out), _lib.stream())
+    return out
+
+
+def select_anchors(scores: AnchorScores, budget, policy="by_sum"):
+    """Top-budget tokens under the policy, ties to the lower index
+    (anchors.py:265-301).  Scores are compared in float32 on the GPU."""
+    if policy not in POLICIES:
+        raise ValueError(f"unknown policy {policy!r}")
+    k, was_np = as_cuda(scores.ans_k, torch.float32)
+    v, _ = as_cuda(scores.ans_v, torch.float32)
+    n = k.shape[-1]
+    budget = int(np.clip(budget, 0, n))
+    single = k.ndim == 1
+    k2 = k.reshape(-1, n)
+    v2 = v.reshape(-1, n)
+    idx = select_anchors_device(k2, v2, budget, policy).to(torch.int64)
+    if single:
+        idx = idx[0]
+    return AnchorSelection(indices=idx.cpu().numpy() if was_np or single else idx,
+                           budget=budget, policy=policy)

@@ -1,0 +1,527 @@
+// Vector quantisation (encode / decode) and the quantised KV-cache state
+// machine: build from prefill (cache.py:122-139), append (cache.py:157-166),
+// evict with promotion or encoding (cache.py:180-193) and dequantise
+// (cache.py:196-211).  All state lives on the device; every call is
+// stream-ordered and capturable in a CUDA graph.
+#include "common.cuh"
+
+namespace antkv {
+
+constexpr int ENC_THREADS = 256;
+constexpr int ENC_CHUNK_FLOATS = 8192;  // 32 KB of centroids per smem stage
+
+// Nearest centroid for one sub-vector held in registers: float32
+// sum_t (x_t - c_t)^2 in index order, strict-< argmin (lowest index on ties,
+// _ckernels.pyx:150-162).
+template <int MAXD>
+__device__ __forceinline__ void nearest_update(const float (&x)[MAXD], const float *c, int d_sub,
+                                               int cidx, float &best, int &best_i) {
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t < MAXD; ++t) {
+    if (t < d_sub) {
+      float df = x[t] - c[t];
+      s = fmaf(df, df, s);
+    }
+  }
+  if (s < best) {
+    best = s;
+    best_i = cidx;
+  }
+}
+
+__device__ __forceinline__ void store_code(void *codes, int64_t off_elems, int code_bytes,
+                                           int v) {
+  if (code_bytes == 1) reinterpret_cast<uint8_t *>(codes)[off_elems] = static_cast<uint8_t>(v);
+  else if (code_bytes == 2) reinterpret_cast<uint16_t *>(codes)[off_elems] = static_cast<uint16_t>(v);
+  else if (code_bytes == 4) reinterpret_cast<int32_t *>(codes)[off_elems] = v;
+  else reinterpret_cast<int64_t *>(codes)[off_elems] = v;
+}
+
+__device__ __forceinline__ int load_code(const void *codes, int64_t off_elems, int code_bytes) {
+  if (code_bytes == 1) return reinterpret_cast<const uint8_t *>(codes)[off_elems];
+  if (code_bytes == 2) return reinterpret_cast<const uint16_t *>(codes)[off_elems];
+  if (code_bytes == 4) return reinterpret_cast<const int32_t *>(codes)[off_elems];
+  return static_cast<int>(reinterpret_cast<const int64_t *>(codes)[off_elems]);
+}
+
+// Bulk encoder.  grid = (ceil(rows*groups / 256), nsets): each set s has its
+// own input base (x_set_stride elements), output base (code_set_stride code
+// elements) and codebook (set % cb_mod).  Output code for (row r, group g) is
+// at codes[s*code_set_stride + r*code_row_stride + g].
+template <int MAXD>
+__global__ void __launch_bounds__(ENC_THREADS)
+vq_encode_kernel(const void *__restrict__ X, int dtype, int64_t rows, int d,
+                 int64_t x_set_stride, const float *__restrict__ codebooks, int cb_mod,
+                 int m, int d_sub, void *__restrict__ codes, int code_bytes,
+                 int64_t code_set_stride, int64_t code_row_stride, float *__restrict__ d2out) {
+  __shared__ float sC[ENC_CHUNK_FLOATS];
+  const int groups = d / d_sub;
+  const int set = blockIdx.y;
+  const float *cb = codebooks + (int64_t)(set % cb_mod) * m * d_sub;
+  const int64_t item = (int64_t)blockIdx.x * ENC_THREADS + threadIdx.x;
+  const bool live = item < rows * groups;
+  const int64_t r = live ? item / groups : 0;
+  const int g = live ? static_cast<int>(item - r * groups) : 0;
+  float x[MAXD];
+  const int64_t xbase = set * x_set_stride + r * d + (int64_t)g * d_sub;
+#pragma unroll
+  for (int t = 0; t < MAXD; ++t) x[t] = (live && t < d_sub) ? load_elem(X, xbase + t, dtype) : 0.f;
+  float best = INFINITY;
+  int best_i = 0;
+  const int chunk = (ENC_CHUNK_FLOATS / d_sub) < m ? (ENC_CHUNK_FLOATS / d_sub) : m;
+  for (int c0 = 0; c0 < m; c0 += chunk) {
+    const int cn = min(chunk, m - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cn * d_sub; i += ENC_THREADS) sC[i] = cb[(int64_t)c0 * d_sub + i];
+    __syncthreads();
+    if (live)
+      for (int c = 0; c < cn; ++c) nearest_update<MAXD>(x, sC + c * d_sub, d_sub, c0 + c, best, best_i);
+  }
+  if (live) {
+    store_code(codes, set * code_set_stride + r * code_row_stride + g, code_bytes, best_i);
+    if (d2out) d2out[set * rows * groups + item] = best;
+  }
+}
+
+int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride,
+                  int nsets, const float *codebooks, int cb_mod, int m, int d_sub,
+                  void *codes, int code_bytes, int64_t code_set_stride,
+                  int64_t code_row_stride, float *d2, cudaStream_t st) {
+  ANTKV_REQUIRE(d_sub >= 1 && d_sub <= 64, "d_sub must be in [1, 64] on the GPU path");
+  ANTKV_REQUIRE(d % d_sub == 0, "d=%d not divisible by d_sub=%d", d, d_sub);
+  ANTKV_REQUIRE(m >= 1, "empty codebook");
+  const int64_t items = rows * (d / d_sub);
+  if (items == 0 || nsets == 0) return ANTKV_OK;
+  dim3 grid(ceil_div(items, ENC_THREADS), nsets);
+#define ENC_LAUNCH(MD)                                                                       \
+  vq_encode_kernel<MD><<<grid, ENC_THREADS, 0, st>>>(X, dtype, rows, d, x_set_stride,        \
+                                                     codebooks, cb_mod, m, d_sub, codes,     \
+                                                     code_bytes, code_set_stride,            \
+                                                     code_row_stride, d2)
+  if (d_sub <= 2) ENC_LAUNCH(2);
+  else if (d_sub <= 4) ENC_LAUNCH(4);
+  else if (d_sub <= 8) ENC_LAUNCH(8);
+  else if (d_sub <= 16) ENC_LAUNCH(16);
+  else if (d_sub <= 32) ENC_LAUNCH(32);
+  else ENC_LAUNCH(64);
+#undef ENC_LAUNCH
+  ANTKV_LAUNCH_CHECK("vq_encode_kernel");
+  return ANTKV_OK;
+}
+
+__global__ void vq_decode_kernel(const void *__restrict__ codes, int code_bytes, int64_t rows,
+                                 int groups, const float *__restrict__ cb, int m, int d_sub,
+                                 float *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = rows * groups * d_sub;
+  if (i >= total) return;
+  const int t = static_cast<int>(i % d_sub);
+  const int64_t rg = i / d_sub;
+  int c = load_code(codes, rg, code_bytes);
+  out[i] = (c >= 0 && c < m) ? cb[(int64_t)c * d_sub + t] : NAN;
+}
+
+// ------------------------------------------------------------ cache state
+__device__ __forceinline__ int64_t bh_index(int b, int h, int H) { return (int64_t)b * H + h; }
+
+__device__ __forceinline__ int rec_bytes(const antkv_cache_desc &c) {
+  return 2 * c.groups * c.code_bytes;
+}
+
+// Per (b, head) layout from the sorted anchor list (cache.py:126-139).
+// One CTA per (b, head); the codes were written by the bulk encoder.
+__global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ K,
+                                   const void *__restrict__ V, int dtype,
+                                   const int64_t *__restrict__ positions, int n,
+                                   const int32_t *__restrict__ anchors, int n_anchors) {
+  const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
+  const int64_t bh = bh_index(b, h, c.Hkv);
+  const int32_t *anc = anchors + bh * n_anchors;
+  uint32_t *qm = c.qmask + bh * (c.capacity / 32);
+  // quantized bit = not anchor and j < n - window
+  const int wstart = n - c.window_size > 0 ? n - c.window_size : 0;
+  for (int w = threadIdx.x; w < c.capacity / 32; w += blockDim.x) {
+    uint32_t bits = 0;
+    for (int k = 0; k < 32; ++k) {
+      int j = w * 32 + k;
+      if (j < wstart) bits |= 1u << k;
+    }
+    qm[w] = bits;
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < n_anchors; a += blockDim.x) {
+    int j = anc[a];
+    if (j < wstart) atomicAnd(&qm[j / 32], ~(1u << (j % 32)));
+  }
+  // pool: anchors first (ascending), then windowed tokens (ascending)
+  __shared__ int s_used;
+  __shared__ int s_win;
+  if (threadIdx.x == 0) {
+    int slot = 0;
+    int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
+    int8_t *pkind = c.pool_kind + bh * c.pool_capacity;
+    for (int a = 0; a < n_anchors; ++a) {
+      ptok[slot] = anc[a];
+      pkind[slot] = ANTKV_KIND_ANCHOR;
+      ++slot;
+    }
+    int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+    int ai = 0, nw = 0;
+    for (int j = wstart; j < n; ++j) {
+      while (ai < n_anchors && anc[ai] < j) ++ai;
+      if (ai < n_anchors && anc[ai] == j) continue;
+      ptok[slot] = j;
+      pkind[slot] = ANTKV_KIND_WINDOWED;
+      ring[nw++] = slot;
+      ++slot;
+    }
+    for (int s = slot; s < c.pool_capacity; ++s) {
+      ptok[s] = -1;
+      pkind[s] = ANTKV_KIND_FREE;
+    }
+    int32_t *fs = c.free_stack + bh * c.pool_capacity;
+    int top = 0;
+    for (int s = c.pool_capacity - 1; s >= slot; --s) fs[top++] = s;
+    int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+    hs[ANTKV_HS_ANCHORS] = n_anchors;
+    hs[ANTKV_HS_WIN_HEAD] = 0;
+    hs[ANTKV_HS_WIN_COUNT] = nw;
+    hs[ANTKV_HS_FREE_TOP] = top;
+    hs[ANTKV_HS_POOL_HIGH] = slot;
+    s_used = slot;
+    s_win = nw;
+  }
+  __syncthreads();
+  // copy rows into the pool (bf16)
+  const int used = s_used;
+  const int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
+  for (int s = 0; s < used; ++s) {
+    const int j = ptok[s];
+    const int64_t src = (bh * n + j) * c.d;
+    uint16_t *dst = c.pool_rows + (bh * c.pool_capacity + s) * 2 * c.d;
+    for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
+      dst[t] = float_to_bf16_bits(load_elem(K, src + t, dtype));
+      dst[c.d + t] = float_to_bf16_bits(load_elem(V, src + t, dtype));
+    }
+  }
+  if (h == 0) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x)
+      c.positions[(int64_t)b * c.capacity + j] = positions[(int64_t)b * n + j];
+    if (threadIdx.x == 0) c.seq_len[b] = n;
+  }
+  (void)s_win;
+}
+
+// cos/sin of omega_i * P0 for the 16-slot tile starting at `slot` (fast path).
+__device__ void write_tile_cs(const antkv_cache_desc &c, int b, int slot, int64_t pos) {
+  if (!c.tile_cs || (slot & 15)) return;
+  float *dst = c.tile_cs + ((int64_t)b * (c.capacity / 16) + slot / 16) * c.d;
+  for (int i = threadIdx.x; i < c.d / 2; i += blockDim.x) {
+    float cs, sn;
+    rope_cs((double)pos * rope_freq(c.theta_base, i, c.d), cs, sn);
+    dst[2 * i] = cs;
+    dst[2 * i + 1] = sn;
+  }
+}
+
+__global__ void cache_tile_cs_kernel(antkv_cache_desc c, int n) {
+  const int b = blockIdx.y;
+  const int tile = blockIdx.x;
+  if (n < 0) n = c.seq_len[b];
+  if (tile * 16 >= n) return;
+  write_tile_cs(c, b, tile * 16, c.positions[(int64_t)b * c.capacity + tile * 16]);
+}
+
+// Append one token per sequence (one CTA per sequence, loops over heads).
+__global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__ k,
+                                    const void *__restrict__ v, int dtype,
+                                    const int64_t *__restrict__ position) {
+  const int b = blockIdx.x;
+  const int j = c.seq_len[b];
+  __shared__ int s_slot;
+  for (int h = 0; h < c.Hkv; ++h) {
+    const int64_t bh = bh_index(b, h, c.Hkv);
+    int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+    if (threadIdx.x == 0) {
+      int top = hs[ANTKV_HS_FREE_TOP] - 1;
+      int slot = top >= 0 ? c.free_stack[bh * c.pool_capacity + top] : -1;
+      if (slot >= 0) {
+        hs[ANTKV_HS_FREE_TOP] = top;
+        c.pool_tok[bh * c.pool_capacity + slot] = j;
+        c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_WINDOWED;
+        int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+        int pos = (hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % (c.window_size + 1);
+        ring[pos] = slot;
+        hs[ANTKV_HS_WIN_COUNT] += 1;
+        if (slot + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot + 1;
+      }
+      s_slot = slot;
+    }
+    __syncthreads();
+    const int slot = s_slot;
+    if (slot >= 0) {
+      uint16_t *dst = c.pool_rows + (bh * c.pool_capacity + slot) * 2 * c.d;
+      const int64_t src = bh * c.d;
+      for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
+        dst[t] = float_to_bf16_bits(load_elem(k, src + t, dtype));
+        dst[c.d + t] = float_to_bf16_bits(load_elem(v, src + t, dtype));
+      }
+    }
+    __syncthreads();
+  }
+  // the slot's code bits stay clear (qmask initialised to zero above n)
+  write_tile_cs(c, b, j, position[b]);
+  if (threadIdx.x == 0) {
+    c.positions[(int64_t)b * c.capacity + j] = position[b];
+    c.seq_len[b] = j + 1;
+  }
+}
+
+// Evict (cache.py:180-193).  One CTA (256 threads) per (b, head).  Encoding
+// splits each (K/V, group) over a team of threads that scans a slice of the
+// codebook, then reduces (distance, index) with the lowest index on ties.
+__global__ void __launch_bounds__(256)
+cache_evict_kernel(antkv_cache_desc c) {
+  const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
+  const int64_t bh = bh_index(b, h, c.Hkv);
+  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  __shared__ int s_slot, s_encode;
+  if (threadIdx.x == 0) {
+    s_slot = -1;
+    s_encode = 0;
+    if (hs[ANTKV_HS_WIN_COUNT] > c.window_size) {
+      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+      int slot = ring[hs[ANTKV_HS_WIN_HEAD]];
+      hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % (c.window_size + 1);
+      hs[ANTKV_HS_WIN_COUNT] -= 1;
+      const int n = c.seq_len[b];
+      const int budget = budget_for((int64_t)n + c.token_offset, c.anchor_count, c.anchor_fraction);
+      if (hs[ANTKV_HS_ANCHORS] < budget) {
+        c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_ANCHOR;
+        hs[ANTKV_HS_ANCHORS] += 1;
+      } else {
+        s_slot = slot;
+        s_encode = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_encode) return;
+  const int slot = s_slot;
+  const int j = c.pool_tok[bh * c.pool_capacity + slot];
+  const uint16_t *row = c.pool_rows + (bh * c.pool_capacity + slot) * 2 * c.d;
+  const int units = 2 * c.groups;             // (kv, group) pairs
+  const int team = max(1, 256 / units);       // threads per unit (>= 1)
+  const int u = threadIdx.x / team, lane = threadIdx.x % team;
+  float best = INFINITY;
+  int best_i = 0x7fffffff;
+  if (u < units) {
+    const int kv = u / c.groups, g = u % c.groups;
+    const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
+    const uint16_t *x = row + kv * c.d + g * c.d_sub;
+    for (int ci = lane; ci < c.m; ci += team) {
+      float s = 0.f;
+      for (int t = 0; t < c.d_sub; ++t) {
+        float df = bf16_bits_to_float(x[t]) - cb[(int64_t)ci * c.d_sub + t];
+        s = fmaf(df, df, s);
+      }
+      if (s < best) { best = s; best_i = ci; }
+    }
+  }
+  // team reduction through shared memory (teams may span warps)
+  __shared__ float s_best[256];
+  __shared__ int s_idx[256];
+  s_best[threadIdx.x] = best;
+  s_idx[threadIdx.x] = best_i;
+  __syncthreads();
+  if (u < units && lane == 0) {
+    for (int l = 1; l < team; ++l) {
+      float o = s_best[threadIdx.x + l];
+      int oi = s_idx[threadIdx.x + l];
+      if (o < best || (o == best && oi < best_i)) { best = o; best_i = oi; }
+    }
+    const int kv = u / c.groups, g = u % c.groups;
+    uint8_t *rec = c.codes + (bh * c.capacity + j) * rec_bytes(c) + kv * c.groups * c.code_bytes;
+    if (c.code_bytes == 1) rec[g] = static_cast<uint8_t>(best_i);
+    else reinterpret_cast<uint16_t *>(rec)[g] = static_cast<uint16_t>(best_i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
+    c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_FREE;
+    c.pool_tok[bh * c.pool_capacity + slot] = -1;
+    c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = slot;
+    hs[ANTKV_HS_FREE_TOP] += 1;
+  }
+}
+
+// Dequantise: codes for quantized slots, pool rows scattered to their tokens.
+__global__ void cache_dequant_codes_kernel(antkv_cache_desc c, int n, float *__restrict__ Khat,
+                                           float *__restrict__ Vhat) {
+  const int64_t bh = blockIdx.y;
+  const int h = static_cast<int>(bh % c.Hkv);
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * c.d) return;
+  const int j = static_cast<int>(i / c.d), t = static_cast<int>(i % c.d);
+  const uint32_t bits = c.qmask[bh * (c.capacity / 32) + j / 32];
+  float kv = NAN, vv = NAN;
+  if (bits & (1u << (j % 32))) {
+    const uint8_t *rec = c.codes + (bh * c.capacity + j) * rec_bytes(c);
+    const int g = t / c.d_sub, e = t % c.d_sub;
+    int ck, cv;
+    if (c.code_bytes == 1) { ck = rec[g]; cv = rec[c.groups + g]; }
+    else { ck = reinterpret_cast<const uint16_t *>(rec)[g];
+           cv = reinterpret_cast<const uint16_t *>(rec)[c.groups + g]; }
+    kv = c.codebook_k[((int64_t)h * c.m + ck) * c.d_sub + e];
+    vv = c.codebook_v[((int64_t)h * c.m + cv) * c.d_sub + e];
+  }
+  Khat[(bh * n + j) * c.d + t] = kv;
+  Vhat[(bh * n + j) * c.d + t] = vv;
+}
+
+__global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__restrict__ Khat,
+                                          float *__restrict__ Vhat) {
+  const int64_t bh = blockIdx.y;
+  const int s = blockIdx.x;
+  const int j = c.pool_tok[bh * c.pool_capacity + s];
+  if (j < 0 || j >= n || c.pool_kind[bh * c.pool_capacity + s] == ANTKV_KIND_FREE) return;
+  const uint16_t *row = c.pool_rows + (bh * c.pool_capacity + s) * 2 * c.d;
+  for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
+    Khat[(bh * n + j) * c.d + t] = bf16_bits_to_float(row[t]);
+    Vhat[(bh * n + j) * c.d + t] = bf16_bits_to_float(row[c.d + t]);
+  }
+}
+
+// Fast-path codebook: [Hkv][2][256][8 copies][8] fp16.  Row c of a codebook
+// holds centroid c eight times, one copy per 16-byte bank group, so the eight
+// row addresses of one ldmatrix phase (one per copy) never conflict.
+__global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
+  const int h = blockIdx.x / 2, kv = blockIdx.x % 2;
+  const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
+  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 64;
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
+    const int code = i / 64, t = i % 8;
+    const float val = code < c.m ? cb[(int64_t)code * 8 + t] : 0.f;
+    dst[i] = __float2half_rn(val);
+  }
+}
+
+}  // namespace antkv
+
+using namespace antkv;
+
+static int check_desc(const antkv_cache_desc *c) {
+  ANTKV_REQUIRE(c != nullptr, "null cache descriptor");
+  ANTKV_REQUIRE(c->B >= 1 && c->Hkv >= 1 && c->Hq % c->Hkv == 0, "bad head counts");
+  ANTKV_REQUIRE(c->d >= 2 && c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
+  ANTKV_REQUIRE(c->d_sub >= 1 && c->d % c->d_sub == 0, "d=%d not divisible by d_sub=%d", c->d, c->d_sub);
+  ANTKV_REQUIRE(c->groups == c->d / c->d_sub, "groups mismatch");
+  ANTKV_REQUIRE(c->code_bytes == (c->index_bits <= 8 ? 1 : 2), "code_bytes mismatch");
+  ANTKV_REQUIRE(c->index_bits <= 16, "index_bits > 16 unsupported");
+  ANTKV_REQUIRE(c->capacity % 32 == 0 && c->capacity > 0, "capacity must be a positive multiple of 32");
+  ANTKV_REQUIRE(c->window_size >= 0 && c->pool_capacity > c->window_size, "pool too small");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_assign_nearest(const float *X, const float *C, int64_t n, int m, int d_sub,
+                                    int64_t *idx, float *d2, void *stream) {
+  return launch_encode(X, ANTKV_F32, n, d_sub, 0, 1, C, 1, m, d_sub, idx, 8, 0, 1, d2,
+                       as_stream(stream));
+}
+
+extern "C" int antkv_vq_encode(const void *X, int dtype, int64_t rows, int d,
+                               const float *codebook, int m, int d_sub, void *codes,
+                               int code_bytes, void *stream) {
+  ANTKV_REQUIRE(code_bytes == 1 || code_bytes == 2 || code_bytes == 4 || code_bytes == 8,
+                "code_bytes must be 1, 2, 4 or 8");
+  ANTKV_REQUIRE(code_bytes >= 8 || m <= (1 << (8 * code_bytes)), "codes do not fit");
+  return launch_encode(X, dtype, rows, d, 0, 1, codebook, 1, m, d_sub, codes, code_bytes, 0,
+                       d / d_sub, nullptr, as_stream(stream));
+}
+
+extern "C" int antkv_vq_decode(const void *codes, int code_bytes, int64_t rows, int groups,
+                               const float *codebook, int m, int d_sub, float *out,
+                               void *stream) {
+  int64_t total = rows * groups * d_sub;
+  if (total == 0) return ANTKV_OK;
+  vq_decode_kernel<<<ceil_div(total, 256), 256, 0, as_stream(stream)>>>(
+      codes, code_bytes, rows, groups, codebook, m, d_sub, out);
+  ANTKV_LAUNCH_CHECK("vq_decode_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const void *V,
+                                 int dtype, const int64_t *positions, int n,
+                                 const int32_t *anchors, int n_anchors, void *stream) {
+  int rc = check_desc(c);
+  if (rc) return rc;
+  ANTKV_REQUIRE(n >= 0 && n <= c->capacity, "prefill length exceeds capacity");
+  ANTKV_REQUIRE(n_anchors + c->window_size + 1 <= c->pool_capacity, "pool capacity too small");
+  cudaStream_t st = as_stream(stream);
+  const int nsets = c->B * c->Hkv;
+  const int rec = 2 * c->groups * c->code_bytes;
+  // K codes then V codes: code element index within a record is g (+groups for V)
+  rc = launch_encode(K, dtype, n, c->d, (int64_t)n * c->d, nsets, c->codebook_k, c->Hkv, c->m,
+                     c->d_sub, c->codes, c->code_bytes, (int64_t)c->capacity * rec / c->code_bytes,
+                     rec / c->code_bytes, nullptr, st);
+  if (rc) return rc;
+  rc = launch_encode(V, dtype, n, c->d, (int64_t)n * c->d, nsets, c->codebook_v, c->Hkv, c->m,
+                     c->d_sub, c->codes + c->groups * c->code_bytes, c->code_bytes,
+                     (int64_t)c->capacity * rec / c->code_bytes, rec / c->code_bytes, nullptr, st);
+  if (rc) return rc;
+  cache_build_kernel<<<nsets, 256, 0, st>>>(*c, K, V, dtype, positions, n, anchors, n_anchors);
+  ANTKV_LAUNCH_CHECK("cache_build_kernel");
+  if (c->tile_cs && n > 0) {
+    cache_tile_cs_kernel<<<dim3(ceil_div(n, 16), c->B), 64, 0, st>>>(*c, n);
+    ANTKV_LAUNCH_CHECK("cache_tile_cs_kernel");
+  }
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_cache_append(const antkv_cache_desc *c, const void *k, const void *v,
+                                  int dtype, const int64_t *position, void *stream) {
+  int rc = check_desc(c);
+  if (rc) return rc;
+  cache_append_kernel<<<c->B, 128, 0, as_stream(stream)>>>(*c, k, v, dtype, position);
+  ANTKV_LAUNCH_CHECK("cache_append_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_cache_evict(const antkv_cache_desc *c, void *stream) {
+  int rc = check_desc(c);
+  if (rc) return rc;
+  cache_evict_kernel<<<c->B * c->Hkv, 256, 0, as_stream(stream)>>>(*c);
+  ANTKV_LAUNCH_CHECK("cache_evict_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *Khat, float *Vhat,
+                                      void *stream) {
+  int rc = check_desc(c);
+  if (rc) return rc;
+  if (n == 0) return ANTKV_OK;
+  cudaStream_t st = as_stream(stream);
+  dim3 g1(ceil_div((int64_t)n * c->d, 256), c->B * c->Hkv);
+  cache_dequant_codes_kernel<<<g1, 256, 0, st>>>(*c, n, Khat, Vhat);
+  ANTKV_LAUNCH_CHECK("cache_dequant_codes_kernel");
+  dim3 g2(c->pool_capacity, c->B * c->Hkv);
+  cache_dequant_pool_kernel<<<g2, 128, 0, st>>>(*c, n, Khat, Vhat);
+  ANTKV_LAUNCH_CHECK("cache_dequant_pool_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream) {
+  int rc = check_desc(c);
+  if (rc) return rc;
+  ANTKV_REQUIRE(c->d_sub == 8 && c->m <= 256 && c->codebook_f16, "fast path needs d_sub=8, m<=256");
+  cudaStream_t st = as_stream(stream);
+  cache_prepare_fast_kernel<<<c->Hkv * 2, 256, 0, st>>>(*c);
+  ANTKV_LAUNCH_CHECK("cache_prepare_fast_kernel");
+  if (c->tile_cs) {
+    cache_tile_cs_kernel<<<dim3(c->capacity / 16, c->B), 64, 0, st>>>(*c, -1);
+    ANTKV_LAUNCH_CHECK("cache_tile_cs_kernel");
+  }
+  return ANTKV_OK;
+}

@@ -1,0 +1,98 @@
+// Shared helpers for the AnTKV B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/antkv_b200.h"
+
+namespace antkv {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+int cuda_status(cudaError_t e, const char *where);
+
+#define ANTKV_REQUIRE(cond, ...)                                              \
+  do {                                                                        \
+    if (!(cond)) {                                                            \
+      ::antkv::set_error(__VA_ARGS__);                                        \
+      return ANTKV_EINVAL;                                                    \
+    }                                                                         \
+  } while (0)
+
+#define ANTKV_LAUNCH_CHECK(where)                                             \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) return ::antkv::cuda_status(_e, where);            \
+  } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------- dtypes
+__device__ __forceinline__ float load_elem(const void *p, int64_t i, int dtype) {
+  if (dtype == ANTKV_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);
+  if (dtype == ANTKV_F16) return __half2float(reinterpret_cast<const __half *>(p)[i]);
+  return reinterpret_cast<const float *>(p)[i];
+}
+
+__device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {
+  return __uint_as_float(static_cast<uint32_t>(b) << 16);
+}
+
+__device__ __forceinline__ uint16_t float_to_bf16_bits(float f) {
+  __nv_bfloat16 h = __float2bfloat16_rn(f);
+  return *reinterpret_cast<uint16_t *>(&h);
+}
+
+// ---------------------------------------------------------------- RoPE
+// Frequencies theta^(-2i/d) in float64 (attention.py:84).
+__device__ __forceinline__ double rope_freq(double theta, int i, int d) {
+  return pow(theta, -2.0 * (double)i / (double)d);
+}
+
+// cos/sin of pos*freq, angle formed in float64 and reduced mod 2*pi before a
+// float32 sincos (SURVEY.md §7 hard part 4: fp32 angles are off by ~4e-3 rad
+// at 128K; this keeps the error near 1e-7 rad).
+__device__ __forceinline__ void rope_cs(double angle, float &c, float &s) {
+  const double two_pi = 6.283185307179586476925286766559;
+  double k = rint(angle * (1.0 / two_pi));
+  double r = fma(-k, two_pi, angle);
+  r = fma(-k, 2.4492935982947064e-16, r);  // low part of 2*pi
+  sincosf(static_cast<float>(r), &s, &c);
+}
+
+// ---------------------------------------------------------------- ordering
+// Order-preserving map float -> uint32 (larger float -> larger key).
+__device__ __forceinline__ uint32_t float_order_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+// budget_for(n) (cache.py:54-57), evaluated with the same float64 product.
+__host__ __device__ inline int budget_for(int64_t n, int anchor_count, double frac) {
+  if (anchor_count >= 0) return static_cast<int>(anchor_count < n ? anchor_count : n);
+  double b = ceil(frac * static_cast<double>(n));
+  if (b < 0) b = 0;
+  if (b > static_cast<double>(n)) b = static_cast<double>(n);
+  return static_cast<int>(b);
+}
+
+}  // namespace antkv

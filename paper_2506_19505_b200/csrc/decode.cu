@@ -1,0 +1,336 @@
+// Decode attention over the quantised cache (cache.py:168-178):
+//   out_h = softmax(RoPE(q_h, p_q) . RoPE(K_hat_j, p_j) / sqrt(d)) V_hat
+// with K_hat/V_hat reconstructed from codes (quantised slots) or read from
+// the bf16 full-precision pool (anchors + window), split-KV partials and a
+// log-sum-exp combine.  This file holds the generic float32 kernel (any
+// d <= 256, d_sub, m) and the combine; decode_fast.cu holds the sm_100a
+// tensor-core kernel for the 1-bit d8m256 configuration.
+#include "common.cuh"
+
+namespace antkv {
+
+constexpr int DG_T = 128;  // items per chunk == threads per CTA
+
+int decode_fast_launch(const antkv_cache_desc &c, const void *q, int dtype,
+                       const int64_t *qpos, float *ws_o, float *ws_m, float *ws_l,
+                       int splits, cudaStream_t st);
+int decode_fast_supported(const antkv_cache_desc &c);
+
+template <int GQ, bool CB_SMEM>
+__global__ void __launch_bounds__(DG_T)
+decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
+                      const int64_t *__restrict__ qpos, float *__restrict__ ws_o,
+                      float *__restrict__ ws_m, float *__restrict__ ws_l) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int d = c.d, G = c.groups, dsub = c.d_sub;
+  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x, splits = gridDim.x;
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  double *sFreq = reinterpret_cast<double *>(smraw);                // [d/2]
+  float *sQ = reinterpret_cast<float *>(sFreq + d / 2);             // [GQ][d]
+  float *sS = sQ + GQ * d;                                          // [GQ][T]
+  float *sRed = sS + GQ * DG_T;                                     // [GQ][4] + [GQ][4]
+  int *sSrc = reinterpret_cast<int *>(sRed + 8 * GQ);               // [T] source tag
+  int *sVc = sSrc + DG_T;                                           // [T][G] V codes
+  float *sCbK = reinterpret_cast<float *>(sVc + DG_T * G);          // [m][dsub]
+  float *sCbV = sCbK + (CB_SMEM ? c.m * dsub : 0);
+  const float *cbK = CB_SMEM ? sCbK : c.codebook_k + (int64_t)h * c.m * dsub;
+  const float *cbV = CB_SMEM ? sCbV : c.codebook_v + (int64_t)h * c.m * dsub;
+
+  for (int i = threadIdx.x; i < d / 2; i += DG_T) sFreq[i] = rope_freq(c.theta_base, i, d);
+  if (CB_SMEM) {
+    const float *gk = c.codebook_k + (int64_t)h * c.m * dsub;
+    const float *gv = c.codebook_v + (int64_t)h * c.m * dsub;
+    for (int i = threadIdx.x; i < c.m * dsub; i += DG_T) {
+      sCbK[i] = gk[i];
+      sCbV[i] = gv[i];
+    }
+  }
+  __syncthreads();
+  // rotated, scaled queries of the group (attention.py:89-106 at p_q)
+  const double pq = static_cast<double>(qpos[b]);
+  const float scale = rsqrtf(static_cast<float>(d));
+  for (int i = threadIdx.x; i < GQ * (d / 2); i += DG_T) {
+    const int hh = i / (d / 2), p = i % (d / 2);
+    const int64_t qb = ((int64_t)b * c.Hq + h * GQ + hh) * d;
+    float x0 = load_elem(q, qb + 2 * p, dtype), x1 = load_elem(q, qb + 2 * p + 1, dtype);
+    float cs, sn;
+    rope_cs(pq * sFreq[p], cs, sn);
+    sQ[hh * d + 2 * p] = (x0 * cs - x1 * sn) * scale;
+    sQ[hh * d + 2 * p + 1] = (x0 * sn + x1 * cs) * scale;
+  }
+  const int n = c.seq_len[b];
+  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+  const int total = n + pool_high;
+  const int per = (total + splits - 1) / splits;
+  const int s0 = split * per, s1 = min(total, s0 + per);
+  const int rec = 2 * G * c.code_bytes;
+  const uint8_t *codes = c.codes + bh * c.capacity * rec;
+  const uint32_t *qm = c.qmask + bh * (c.capacity / 32);
+  const uint16_t *pool = c.pool_rows + bh * c.pool_capacity * 2 * d;
+
+  float m_run[GQ], l_run[GQ], acc[GQ][2];
+#pragma unroll
+  for (int hh = 0; hh < GQ; ++hh) {
+    m_run[hh] = -INFINITY;
+    l_run[hh] = 0.f;
+    acc[hh][0] = acc[hh][1] = 0.f;
+  }
+  __syncthreads();
+  for (int c0 = s0; c0 < s1; c0 += DG_T) {
+    // ---- K side: one item per thread
+    const int it = c0 + threadIdx.x;
+    int src = -1;          // >= 0 code slot, <= -2 pool slot (-2 - s), -1 invalid
+    int64_t tok = -1;
+    if (it < s1) {
+      if (it < n) {
+        if (qm[it >> 5] & (1u << (it & 31))) { src = it; tok = it; }
+      } else {
+        const int s = it - n;
+        const int8_t kind = c.pool_kind[bh * c.pool_capacity + s];
+        const int t = c.pool_tok[bh * c.pool_capacity + s];
+        if (kind != ANTKV_KIND_FREE && t >= 0 && t < n) { src = -2 - s; tok = t; }
+      }
+    }
+    float sc[GQ];
+#pragma unroll
+    for (int hh = 0; hh < GQ; ++hh) sc[hh] = 0.f;
+    if (src != -1) {
+      const double pj = static_cast<double>(c.positions[(int64_t)b * c.capacity + tok]);
+      const uint8_t *r = src >= 0 ? codes + (int64_t)src * rec : nullptr;
+      const uint16_t *prow = src >= 0 ? nullptr : pool + (int64_t)(-2 - src) * 2 * d;
+      for (int p = 0; p < d / 2; ++p) {
+        float k0, k1;
+        if (r) {
+          const int e = 2 * p, g = e / dsub, o = e % dsub;
+          const int code = c.code_bytes == 1 ? r[g] : reinterpret_cast<const uint16_t *>(r)[g];
+          k0 = cbK[code * dsub + o];
+          const int e1 = e + 1, g1 = e1 / dsub, o1 = e1 % dsub;
+          const int code1 = g1 == g ? code : (c.code_bytes == 1 ? r[g1] : reinterpret_cast<const uint16_t *>(r)[g1]);
+          k1 = cbK[code1 * dsub + o1];
+        } else {
+          k0 = bf16_bits_to_float(prow[2 * p]);
+          k1 = bf16_bits_to_float(prow[2 * p + 1]);
+        }
+        float cs, sn;
+        rope_cs(pj * sFreq[p], cs, sn);
+        const float r0 = k0 * cs - k1 * sn, r1 = k0 * sn + k1 * cs;
+#pragma unroll
+        for (int hh = 0; hh < GQ; ++hh)
+          sc[hh] = fmaf(sQ[hh * d + 2 * p], r0, fmaf(sQ[hh * d + 2 * p + 1], r1, sc[hh]));
+      }
+      if (r)
+        for (int g = 0; g < G; ++g)
+          sVc[threadIdx.x * G + g] = c.code_bytes == 1 ? r[G + g] : reinterpret_cast<const uint16_t *>(r)[G + g];
+    }
+    sSrc[threadIdx.x] = src;
+#pragma unroll
+    for (int hh = 0; hh < GQ; ++hh) sS[hh * DG_T + threadIdx.x] = src != -1 ? sc[hh] : -INFINITY;
+    __syncthreads();
+    // ---- online softmax over the chunk
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int hh = 0; hh < GQ; ++hh) {
+      float v = warp_max(sS[hh * DG_T + threadIdx.x]);
+      if (lane == 0) sRed[hh * 4 + warp] = v;
+    }
+    __syncthreads();
+    float m_new[GQ], alpha[GQ];
+#pragma unroll
+    for (int hh = 0; hh < GQ; ++hh) {
+      float cm = fmaxf(fmaxf(sRed[hh * 4], sRed[hh * 4 + 1]), fmaxf(sRed[hh * 4 + 2], sRed[hh * 4 + 3]));
+      m_new[hh] = fmaxf(m_run[hh], cm);
+      alpha[hh] = (m_run[hh] == -INFINITY) ? 0.f : __expf(m_run[hh] - m_new[hh]);
+      const float sv = sS[hh * DG_T + threadIdx.x];
+      const float p = (sv == -INFINITY) ? 0.f : __expf(sv - m_new[hh]);
+      sS[hh * DG_T + threadIdx.x] = p;
+      const float ps = warp_sum(p);
+      if (lane == 0) sRed[4 * GQ + hh * 4 + warp] = ps;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int hh = 0; hh < GQ; ++hh) {
+      const float cs = sRed[4 * GQ + hh * 4] + sRed[4 * GQ + hh * 4 + 1] +
+                       sRed[4 * GQ + hh * 4 + 2] + sRed[4 * GQ + hh * 4 + 3];
+      l_run[hh] = l_run[hh] * alpha[hh] + cs;
+      m_run[hh] = m_new[hh];
+      acc[hh][0] *= alpha[hh];
+      acc[hh][1] *= alpha[hh];
+    }
+    // ---- V side: one (or two) dims per thread
+    const int cnt = min(DG_T, s1 - c0);
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int dim = threadIdx.x + half * DG_T;
+      if (dim >= d) continue;
+      const int g = dim / dsub, o = dim % dsub;
+      float a[GQ];
+#pragma unroll
+      for (int hh = 0; hh < GQ; ++hh) a[hh] = acc[hh][half];
+      for (int t = 0; t < cnt; ++t) {
+        const int s = sSrc[t];
+        if (s == -1) continue;
+        float v;
+        if (s >= 0) v = cbV[sVc[t * G + g] * dsub + o];
+        else v = bf16_bits_to_float(pool[(int64_t)(-2 - s) * 2 * d + d + dim]);
+#pragma unroll
+        for (int hh = 0; hh < GQ; ++hh) a[hh] = fmaf(sS[hh * DG_T + t], v, a[hh]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < GQ; ++hh) acc[hh][half] = a[hh];
+    }
+    __syncthreads();
+  }
+  // ---- partials
+#pragma unroll
+  for (int hh = 0; hh < GQ; ++hh) {
+    const int64_t row = ((int64_t)split * c.B + b) * c.Hq + h * GQ + hh;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int dim = threadIdx.x + half * DG_T;
+      if (dim < d) ws_o[row * d + dim] = acc[hh][half];
+    }
+    if (threadIdx.x == 0) {
+      ws_m[row] = m_run[hh];
+      ws_l[row] = l_run[hh];
+    }
+  }
+}
+
+// Split-KV combine: unnormalised partial o_s with (m_s, l_s) per split.
+__global__ void decode_combine_kernel(const float *__restrict__ ws_o, const float *__restrict__ ws_m,
+                                      const float *__restrict__ ws_l, int splits, int64_t rows,
+                                      int d, float *__restrict__ out, float *__restrict__ lse) {
+  const int64_t row = blockIdx.x;
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s) M = fmaxf(M, ws_m[s * rows + row]);
+  float L = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float ms = ws_m[s * rows + row];
+    if (ms != -INFINITY) L += __expf(ms - M) * ws_l[s * rows + row];
+  }
+  const float inv = 1.f / L;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float ms = ws_m[s * rows + row];
+      if (ms != -INFINITY) acc = fmaf(__expf(ms - M), ws_o[(s * rows + row) * d + t], acc);
+    }
+    out[row * d + t] = acc * inv;
+  }
+  if (lse && threadIdx.x == 0) lse[row] = M + logf(L);
+}
+
+// Merge of P normalised shard results with their LSE (sequence sharding).
+__global__ void lse_combine_kernel(const float *__restrict__ o, const float *__restrict__ lse,
+                                   int P, int64_t rows, int d, float *__restrict__ out,
+                                   float *__restrict__ lse_out) {
+  const int64_t row = blockIdx.x;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, lse[p * rows + row]);
+  float W = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float l = lse[p * rows + row];
+    if (l != -INFINITY) W += __expf(l - M);
+  }
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float l = lse[p * rows + row];
+      if (l != -INFINITY) acc = fmaf(__expf(l - M), o[(p * rows + row) * d + t], acc);
+    }
+    out[row * d + t] = acc / W;
+  }
+  if (lse_out && threadIdx.x == 0) lse_out[row] = M + logf(W);
+}
+
+static size_t generic_smem(const antkv_cache_desc &c, int gq, bool cb_smem) {
+  size_t s = sizeof(double) * (c.d / 2) + sizeof(float) * (gq * c.d + gq * DG_T + 8 * gq) +
+             sizeof(int) * (DG_T + DG_T * c.groups);
+  if (cb_smem) s += sizeof(float) * 2 * c.m * c.d_sub;
+  return s;
+}
+
+template <int GQ>
+static int launch_generic(const antkv_cache_desc &c, const void *q, int dtype, const int64_t *qpos,
+                          float *wo, float *wm, float *wl, int splits, cudaStream_t st) {
+  const bool cb_smem = sizeof(float) * 2 * (size_t)c.m * c.d_sub <= 96 * 1024;
+  const size_t smem = generic_smem(c, GQ, cb_smem);
+  ANTKV_REQUIRE(smem <= 200 * 1024, "decode shared memory %zu too large", smem);
+  dim3 grid(splits, c.Hkv, c.B);
+  if (cb_smem) {
+    cudaFuncSetAttribute(decode_generic_kernel<GQ, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    decode_generic_kernel<GQ, true><<<grid, DG_T, smem, st>>>(c, q, dtype, qpos, wo, wm, wl);
+  } else {
+    cudaFuncSetAttribute(decode_generic_kernel<GQ, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    decode_generic_kernel<GQ, false><<<grid, DG_T, smem, st>>>(c, q, dtype, qpos, wo, wm, wl);
+  }
+  ANTKV_LAUNCH_CHECK("decode_generic_kernel");
+  return ANTKV_OK;
+}
+
+static int auto_splits(const antkv_cache_desc &c) {
+  // enough CTAs for ~2 waves on 148 SMs; each split covers >= 256 items
+  int64_t items = (int64_t)c.capacity + c.pool_capacity;
+  int want = (2 * 148 + c.B * c.Hkv - 1) / (c.B * c.Hkv);
+  int maxs = static_cast<int>((items + 255) / 256);
+  int s = want < maxs ? want : maxs;
+  return s < 1 ? 1 : (s > 1024 ? 1024 : s);
+}
+
+}  // namespace antkv
+
+using namespace antkv;
+
+extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int splits) {
+  if (!c) return -1;
+  if (splits <= 0) splits = auto_splits(*c);
+  const int64_t rows = (int64_t)c->B * c->Hq;
+  return (int64_t)splits * rows * (c->d + 2) * sizeof(float) + 256;
+}
+
+extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
+                                      const int64_t *qpos, float *out, float *lse,
+                                      void *workspace, int64_t workspace_bytes, int splits,
+                                      int fast, void *stream) {
+  ANTKV_REQUIRE(c != nullptr && q != nullptr && out != nullptr, "null argument");
+  ANTKV_REQUIRE(c->Hq % c->Hkv == 0, "Hq must be a multiple of Hkv");
+  ANTKV_REQUIRE(c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
+  if (splits <= 0) splits = auto_splits(*c);
+  const int64_t rows = (int64_t)c->B * c->Hq;
+  ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits),
+                "decode workspace too small");
+  float *wo = reinterpret_cast<float *>(workspace);
+  float *wm = wo + (int64_t)splits * rows * c->d;
+  float *wl = wm + (int64_t)splits * rows;
+  cudaStream_t st = as_stream(stream);
+  const int gq = c->Hq / c->Hkv;
+  int rc;
+  if (fast && decode_fast_supported(*c)) {
+    rc = decode_fast_launch(*c, q, dtype, qpos, wo, wm, wl, splits, st);
+  } else {
+    switch (gq) {
+      case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
+      case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
+      case 4: rc = launch_generic<4>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
+      case 8: rc = launch_generic<8>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
+      default:
+        set_error("GQA group size %d unsupported (1, 2, 4, 8)", gq);
+        return ANTKV_EUNSUPPORTED;
+    }
+  }
+  if (rc) return rc;
+  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, splits, rows, c->d, out, lse);
+  ANTKV_LAUNCH_CHECK("decode_combine_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows, int d,
+                                 float *out, float *lse_out, void *stream) {
+  ANTKV_REQUIRE(P >= 1 && d >= 1, "bad combine shape");
+  if (rows == 0) return ANTKV_OK;
+  lse_combine_kernel<<<(unsigned)rows, 128, 0, as_stream(stream)>>>(o, lse, P, rows, d, out, lse_out);
+  ANTKV_LAUNCH_CHECK("lse_combine_kernel");
+  return ANTKV_OK;
+}

@@ -1,0 +1,47 @@
+// Error reporting and device checks for the C ABI.
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace antkv {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char *where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return ANTKV_ECUDA;
+}
+
+__global__ void probe_kernel(int *out) { *out = 100; }
+
+}  // namespace antkv
+
+using namespace antkv;
+
+extern "C" const char *antkv_last_error(void) { return g_err; }
+
+extern "C" int antkv_version(void) { return 1; }
+
+extern "C" int antkv_device_check(int device) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDeviceProperties") ? 0 : 0;
+  if (p.major != 10 || p.minor != 0) {
+    set_error("device %d is sm_%d%d; this library is built for sm_100a", device, p.major, p.minor);
+    return 0;
+  }
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, probe_kernel);
+  if (e != cudaSuccess) {
+    cuda_status(e, "kernel image");
+    return 0;
+  }
+  return 1;
+}

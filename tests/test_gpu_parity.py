@@ -1,0 +1,409 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden outputs and the pinned oracle, on the same seeded inputs.
+
+Tolerances (north_star):
+  * code indices bit-exact except where the float64 distance margin between
+    the two candidates is below 1e-6 * (|x|^2 + max|c|^2);
+  * anchor sets bit-exact except tokens whose float64 score is within 1e-4
+    (relative to the largest score) of the selection boundary;
+  * outputs <= 1e-3 relative (generic float32 kernel) and <= 2e-2 relative
+    (tensor-core kernel: fp16 centroids / rotated keys, fp32 accumulation),
+    measured as max|o - o_ref| / max|o_ref| per check.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import antkv_oracle as O
+from fixtures_gen import AN_CASES, CACHE_CASES, FA_CASES, an_inputs, codebooks, fa_inputs, qkv
+
+pytestmark = pytest.mark.gpu
+
+GOLD = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+KER = np.load(GOLD / "kernels.npz")
+KIND = {"anchor": 0, "quantized": 1, "windowed": 2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_19505_b200 import _lib
+    _lib.load()          # fails loudly if the library or device is wrong
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-30)
+
+
+def assert_codes_parity(X, C, got, ref):
+    """got/ref int codes for sub-vectors X [N, d_sub] with codebook C."""
+    X = np.asarray(X, np.float64).reshape(-1, C.shape[1])
+    got = np.asarray(got).reshape(-1)
+    ref = np.asarray(ref).reshape(-1)
+    bad = np.flatnonzero(got != ref)
+    if bad.size == 0:
+        return 0
+    C = C.astype(np.float64)
+    scale = (X[bad] ** 2).sum(1) + (C ** 2).sum(1).max()
+    dg = ((X[bad] - C[got[bad]]) ** 2).sum(1)
+    dr = ((X[bad] - C[ref[bad]]) ** 2).sum(1)
+    assert np.all(np.abs(dg - dr) <= 1e-6 * scale), (bad[:5], dg[:5], dr[:5])
+    return bad.size
+
+
+def assert_anchor_parity(got, ref, sk, sv):
+    got, ref = set(int(j) for j in got), set(int(j) for j in ref)
+    if got == ref:
+        return
+    diff = got ^ ref
+    for j in diff:
+        ok = False
+        for s in (sk, sv):
+            s = np.asarray(s, np.float64)
+            top = np.abs(s).max()
+            # boundary = smallest selected score of the reference set in s
+            ref_scores = s[list(ref)] if ref else np.array([0.0])
+            if abs(s[j] - ref_scores.min()) <= 1e-4 * top:
+                ok = True
+        assert ok, f"anchor {j} differs beyond the float32 margin"
+
+
+# ---------------------------------------------------------------- kernels
+@pytest.mark.parametrize("tag", list(FA_CASES))
+@pytest.mark.parametrize("causal", [0, 1])
+def test_ckernels_shim_flash_and_ans(tag, causal):
+    from paper_2506_19505_b200 import kernels
+    n, d, bq, bk, seed = FA_CASES[tag]
+    Q, K, V = fa_inputs(n, d, seed)
+    Qs = Q / np.sqrt(d)
+    key = f"{tag}_{causal}"
+    Og, Lg, Mg = kernels.flash_aux(Qs, K, V, bq, bk, bool(causal))
+    assert np.abs(Og - KER[f"fa_O_{key}"]).max() < 1e-4           # test_attention.py:140-148
+    assert np.abs(Mg - KER[f"fa_M_{key}"]).max() < 1e-5
+    assert np.abs((Lg - KER[f"fa_L_{key}"]) / KER[f"fa_L_{key}"]).max() < 1e-5
+    qn = np.sqrt((Q ** 2).sum(axis=1))
+    ak, av = kernels.ans_blocked(Qs, K, KER[f"fa_M_{key}"], KER[f"fa_L_{key}"], qn, bq, bk,
+                                 bool(causal))
+    assert rel(ak, KER[f"ans_k_{key}"]) < 1e-4                      # test_anchors.py:86-97
+    assert rel(av, KER[f"ans_v_{key}"]) < 1e-4
+
+
+@pytest.mark.parametrize("tag", list(AN_CASES))
+def test_ckernels_shim_assign_nearest(tag):
+    from paper_2506_19505_b200 import kernels
+    N, m, ds, seed = AN_CASES[tag]
+    X, C = an_inputs(N, m, ds, seed)
+    idx, d2 = kernels.assign_nearest(X, C)
+    flips = assert_codes_parity(X, C, idx, KER[f"an_idx_{tag}"])
+    assert flips <= max(1, N // 1000)
+    assert np.abs(d2 - KER[f"an_d2_{tag}"]).max() <= 1e-5 * (1 + np.abs(KER[f"an_d2_{tag}"]).max())
+
+
+def test_assign_nearest_tie_and_kats():
+    from paper_2506_19505_b200 import Codebook, VqConfig, decode_token, encode_token, kernels
+    idx, d2 = kernels.assign_nearest(np.array([[1.0]]), np.array([[0.0], [2.0], [0.0], [2.0]]))
+    assert idx[0] == 0 and d2[0] == 1.0                               # test_kernels.py:46-52
+    C = np.zeros((6, 2), np.float32)
+    C[5] = [2, 0]; C[0] = [10, 10]; C[1] = [10, -10]; C[3] = [-10, 10]; C[4] = [-10, -10]
+    cb = Codebook(VqConfig(2, 6), C)
+    assert encode_token(np.array([1.0, 0.0]), cb)[0] == 2              # test_vq.py:123-133
+    rng = np.random.default_rng(0)
+    cb = Codebook(VqConfig(4, 8), rng.standard_normal((8, 4)).astype(np.float32))
+    row = np.concatenate([cb.centroids[3], cb.centroids[7]])
+    codes = encode_token(row, cb)
+    assert list(codes) == [3, 7] and np.array_equal(decode_token(codes, cb), row)
+    with pytest.raises(ValueError):
+        decode_token(np.array([0, 8]), cb)
+
+
+def test_select_matches_golden():
+    from paper_2506_19505_b200 import AnchorScores, select_anchors
+    sk, sv = KER["sel_k"], KER["sel_v"]
+    for policy in ("by_k", "by_v", "by_sum"):
+        for budget in (0, 1, 7, 21, 400, 999, 1000, 5000):
+            got = select_anchors(AnchorScores(sk, sv), budget, policy).indices
+            assert np.array_equal(got, KER[f"sel_{policy}_{budget}"]), (policy, budget)
+
+
+def test_select_kats():
+    from paper_2506_19505_b200 import AnchorScores, select_anchors
+    S = lambda k, v: AnchorScores(np.array(k, float), np.array(v, float))
+    assert list(select_anchors(S([0.1, 9, 3, 9], [5, 0, 7, 1]), 2, "by_k").indices) == [1, 3]
+    assert list(select_anchors(S([0.1, 9, 3, 9], [5, 0, 7, 1]), 2, "by_v").indices) == [0, 2]
+    assert list(select_anchors(S([0, 10, 5, 1], [10, 9, 0, 0]), 2, "by_sum").indices) == [0, 1]
+    assert list(select_anchors(S([1, 1, 1, 1], [1, 2, 2, 2]), 2, "by_v").indices) == [1, 2]
+    assert len(select_anchors(S([1, 2, 3], [1, 2, 3]), 10, "by_v").indices) == 3
+    with pytest.raises(ValueError):
+        select_anchors(S([1], [1]), 1, "by_magic")
+
+
+def test_select_large_random_matches_oracle():
+    from paper_2506_19505_b200.anchors import select_anchors_device
+    rng = np.random.default_rng(9)
+    n = 131072
+    sk = rng.random((3, n)).astype(np.float32)
+    sv = rng.random((3, n)).astype(np.float32)
+    sv[:, ::97] = 0.75                                   # heavy ties
+    for policy in ("by_k", "by_v", "by_sum"):
+        got = select_anchors_device(torch.from_numpy(sk).cuda(), torch.from_numpy(sv).cuda(), 1311,
+                                    policy).cpu().numpy()
+        for r in range(3):
+            ref = O.select_anchors(sk[r].astype(np.float64), sv[r].astype(np.float64), 1311, policy)
+            assert np.array_equal(got[r], ref), policy
+
+
+def test_rope_matches_oracle():
+    from paper_2506_19505_b200 import RopeParams, apply_rope
+    rng = np.random.default_rng(1)
+    X = rng.standard_normal((64, 128))
+    for pos, theta in ((np.arange(64) * 2053, 10000.0), (np.arange(64) + 131000, 5e5),
+                       (np.arange(64) + 839000, 5e5)):
+        got = apply_rope(X, RopeParams(pos, theta))
+        assert np.abs(got - O.apply_rope(X, pos, theta)).max() < 2e-5   # fp64-reduced angles
+
+
+# ------------------------------------------------------------ cache cases
+def _gpu_case(name, fast=True):
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    seed, n, d, notation, window, frac, count, policy, steps, stride, blk = CACHE_CASES[name]
+    cfg = CacheConfig(vq=VqConfig.from_notation(notation), anchor_fraction=frac,
+                      anchor_count=count, window_size=window, policy=policy, block_q=blk,
+                      block_k=blk)
+    Q, K, V = qkv(seed, 1, 1, n + steps, d, heavy=2)
+    ck, cv = codebooks(seed, 1, cfg.vq.m, cfg.vq.d_sub)
+    cache = QuantizedKVCache(cfg, Codebook(cfg.vq, ck[0]), Codebook(cfg.vq, cv[0]), fast=fast)
+    positions = np.arange(n + steps, dtype=np.int64) * stride
+    Op = cache.prefill(Q[0, :n].astype(np.float64), K[0, :n].astype(np.float64),
+                       V[0, :n].astype(np.float64), positions[:n])
+    return cache, Op, (Q, K, V, ck, cv, positions, n, steps)
+
+
+@pytest.mark.parametrize("name", list(CACHE_CASES))
+@pytest.mark.parametrize("fast", [False, True])
+def test_cache_case_matches_reference_golden(name, fast):
+    g = np.load(GOLD / f"cache_{name}.npz")
+    cache, Op, (Q, K, V, ck, cv, positions, n, steps) = _gpu_case(name, fast)
+    tol = 2e-2 if (fast and name in ("c2_d128_d8m256", "c6_d128_d8m256_all_anchor",
+                                      "c7_d128_d8m256_no_window")) else 1e-3
+    assert rel(Op, g["prefill_O"]) < 1e-4
+    ref = O.OracleCache(ck, cv, anchor_fraction=cache.config.anchor_fraction,
+                        anchor_count=cache.config.anchor_count,
+                        window_size=cache.config.window_size, policy=cache.config.policy)
+    ref.prefill(Q[:, :n], K[:, :n], V[:, :n], positions[:n])
+    sk, sv = ref.last_scores
+    assert_anchor_parity(cache.anchor_indices, g["anchors0"], sk[0], sv[0])
+    same_anchors = np.array_equal(cache.anchor_indices, g["anchors0"])
+    if same_anchors:
+        kinds = [KIND[k] for k in cache.kinds]
+        assert np.array_equal(kinds, g["kinds0"])
+        kc, vc = cache.codes_of()
+        for j, c in kc.items():
+            d_sub = cache.config.vq.d_sub
+            assert_codes_parity(K[0, j], ck[0], c, g["kcodes0"][j])
+            assert_codes_parity(V[0, j], cv[0], vc[j], g["vcodes0"][j])
+    outs = []
+    for t in range(n, n + steps):
+        outs.append(cache.decode_step(Q[0, t].astype(np.float64), K[0, t].astype(np.float64),
+                                      V[0, t].astype(np.float64), int(positions[t])))
+    outs = np.array(outs)
+    if same_anchors:
+        for i in range(steps):
+            assert rel(outs[i], g["decode_out"][i]) < tol, (i, rel(outs[i], g["decode_out"][i]))
+        assert np.array_equal(cache.anchor_indices, g["anchors1"])
+        assert np.array_equal([KIND[k] for k in cache.kinds], g["kinds1"])
+        rep = cache.memory_report()
+        assert [rep.payload_bits, rep.codebook_bits, rep.fp_baseline_bits] == list(g["mem"])
+        N = cache.token_count
+        attn = cache.attention_from_cache(Q[0, :N].astype(np.float64))
+        assert rel(attn, g["attn_from_cache"]) < 1e-3
+
+
+def test_decode_position_must_increase():
+    cache, _, (Q, K, V, ck, cv, positions, n, steps) = _gpu_case("c1_d8_d4m16")
+    with pytest.raises(ValueError):
+        cache.decode_step(Q[0, 0], K[0, 0], V[0, 0], int(positions[n - 1]))
+
+
+def test_window_discipline_and_anchor_immutability():
+    cache, _, (Q, K, V, ck, cv, positions, n, steps) = _gpu_case("c1_d8_d4m16")
+    before = {j: cache.dequantize()[0][j].copy() for j in cache.anchor_indices}
+    W = cache.config.window_size
+    for t in range(n, n + steps):
+        cache.decode_step(Q[0, t], K[0, t], V[0, t], int(positions[t]))
+        win = [j for j, k in enumerate(cache.kinds) if k == "windowed"]
+        assert len(win) == W and win == list(range(cache.token_count - W, cache.token_count))
+    Kh, _ = cache.dequantize()
+    for j, row in before.items():
+        assert cache.kinds[j] == "anchor" and np.array_equal(Kh[j], row)
+
+
+def test_perfect_codebook_is_lossless():
+    """test_cache.py:90-103,174-193: with centroids equal to the data the
+    quantised cache reproduces exact attention through decode."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    rng = np.random.default_rng(4)
+    n, d, steps = 64, 8, 24
+    K = rng.standard_normal((n + steps, d)).astype(np.float32).astype(np.float64)
+    V = rng.standard_normal((n + steps, d)).astype(np.float32).astype(np.float64)
+    Qm = rng.standard_normal((n + steps, d))
+    subs = np.unique(np.concatenate([K.reshape(-1, 4), V.reshape(-1, 4)]).astype(np.float32), axis=0)
+    cfg = VqConfig(4, len(subs))
+    cb = Codebook(cfg, subs)
+    cache = QuantizedKVCache(CacheConfig(vq=cfg, anchor_fraction=0.05, window_size=8), cb, cb)
+    cache.prefill(Qm[:n], K[:n], V[:n], np.arange(n))
+    Kh, Vh = cache.dequantize()
+    kinds = cache.kinds
+    for j in range(n):
+        if kinds[j] == "quantized":
+            assert np.array_equal(Kh[j], K[j].astype(np.float32))
+    for t in range(n, n + steps):
+        out = cache.decode_step(Qm[t], K[t], V[t], t)
+        expect = O.attention_exact(Qm[t][None], K[:t + 1], V[:t + 1])[0] if False else None
+        Kr = O.apply_rope(K[:t + 1], np.arange(t + 1))
+        qr = O.apply_rope(Qm[t][None], np.array([t]))
+        A = O.softmax_rows((qr @ Kr.T) / np.sqrt(d))
+        assert np.abs(out - (A @ V[:t + 1])[0]).max() < 1e-5
+
+
+# -------------------------------------------------------------- GQA path
+def _gqa(seed, B, Hq, Hkv, n, d, notation, steps, window=32, frac=0.01, policy="by_sum",
+         theta=10000.0, fast=True):
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation(notation)
+    cfg = CacheConfig(vq=vq, anchor_fraction=frac, window_size=window, policy=policy,
+                      theta_base=theta)
+    Q, K, V = qkv(seed, B * Hq, B * Hkv, n + steps, d, heavy=3)
+    Q = Q.reshape(B, Hq, n + steps, d)
+    K = K.reshape(B, Hkv, n + steps, d)
+    V = V.reshape(B, Hkv, n + steps, d)
+    ck, cv = codebooks(seed, Hkv, vq.m, vq.d_sub)
+    cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), batch=B, fast=fast)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    Og = cache.prefill(dev(Q[:, :, :n]), dev(K[:, :, :n]), dev(V[:, :, :n]), np.arange(n))
+    outs = []
+    for t in range(n, n + steps):
+        outs.append(cache.decode_step(dev(Q[:, :, t]), dev(K[:, :, t]), dev(V[:, :, t]), t)
+                    .cpu().numpy())
+    refs = []
+    for b in range(B):
+        ref = O.OracleCache(ck, cv, anchor_fraction=frac, window_size=window, policy=policy,
+                            theta_base=theta)
+        Or = ref.prefill(Q[b, :, :n], K[b, :, :n], V[b, :, :n], np.arange(n))
+        assert rel(Og[b].cpu().numpy(), Or) < 1e-4
+        sk, sv = ref.last_scores
+        for h in range(Hkv):
+            assert_anchor_parity(cache.anchor_indices_of(b, h), ref.heads[h].anchor_indices,
+                                 sk[h], sv[h])
+        refs.append([ref.decode_step(Q[b, :, t], K[b, :, t], V[b, :, t], t)
+                     for t in range(n, n + steps)])
+    return cache, np.array(outs), np.array(refs).transpose(1, 0, 2, 3)
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_gqa_llama3_shapes_vs_oracle(fast):
+    """Config #1 shapes (32 Q / 8 KV heads, d=128, d8m256), shortened."""
+    cache, outs, refs = _gqa(21, 1, 32, 8, 640, 128, "d8m256", 24, fast=fast)
+    tol = 2e-2 if fast else 1e-3
+    for i in range(outs.shape[0]):
+        assert rel(outs[i], refs[i]) < tol
+
+
+def test_gqa_batch2_theta5e5_generic_d4m256():
+    cache, outs, refs = _gqa(22, 2, 8, 2, 300, 64, "d4m256", 12, window=16, theta=5e5, fast=False)
+    for i in range(outs.shape[0]):
+        assert rel(outs[i], refs[i]) < 1e-3
+
+
+def test_gqa_d32m4096_generic():
+    cache, outs, refs = _gqa(23, 1, 4, 1, 200, 128, "d32m4096", 6, window=8, frac=0.02, fast=False)
+    for i in range(outs.shape[0]):
+        assert rel(outs[i], refs[i]) < 1e-3
+
+
+def test_snapshot_roundtrip_and_reference_format(tmp_path):
+    from paper_2506_19505_b200 import FormatError, QuantizedKVCache
+    cache, _, (Q, K, V, ck, cv, positions, n, steps) = _gpu_case("c4_d16_d4m32_byk_stride3")
+    for t in range(n, n + 5):
+        cache.decode_step(Q[0, t], K[0, t], V[0, t], int(positions[t]))
+    out = cache.save(tmp_path / "snap")
+    loaded = QuantizedKVCache.load(out)
+    assert loaded.kinds == cache.kinds and loaded.positions == cache.positions
+    K1, V1 = cache.dequantize()
+    K2, V2 = loaded.dequantize()
+    assert np.array_equal(K1, K2) and np.array_equal(V1, V2)
+    Qp = np.random.default_rng(0).standard_normal((cache.token_count, 16))
+    assert np.array_equal(cache.attention_from_cache(Qp), loaded.attention_from_cache(Qp))
+    # the codes section decodes with the reference's own unpacker
+    import json
+    man = json.loads((out / "manifest.json").read_text())
+    G = 16 // 4
+    tb = (2 * G * 5 + 7) // 8
+    raw = (out / "codes.bin").read_bytes()
+    kc, vc = cache.codes_of()
+    qj = [j for j, k in enumerate(man["kinds"]) if k == "quantized"]
+    for i, j in enumerate(qj[:10]):
+        both = O.unpack_indices(raw[i * tb:(i + 1) * tb], 5, 2 * G)
+        assert list(both[:G]) == list(kc[j]) and list(both[G:]) == list(vc[j])
+    (out / "codes.bin").write_bytes(raw[:-1])
+    with pytest.raises(FormatError):
+        QuantizedKVCache.load(out)
+
+
+def test_lse_combine_kernel():
+    from paper_2506_19505_b200.parallel import lse_merge
+    rng = np.random.default_rng(5)
+    o = torch.from_numpy(rng.standard_normal((4, 6, 128)).astype(np.float32)).cuda()
+    l = torch.from_numpy(rng.standard_normal((4, 6)).astype(np.float32) * 3).cuda()
+    got = lse_merge(o, l).cpu().numpy()
+    w = np.exp(l.cpu().numpy() - l.cpu().numpy().max(0))
+    ref = (w[..., None] * o.cpu().numpy()).sum(0) / w.sum(0)[..., None]
+    assert np.abs(got - ref).max() < 1e-5
+
+
+def test_fast_matches_generic_at_128k():
+    """Full-size property: the tensor-core and generic kernels agree on a
+    131072-token d8m256 cache (32 Q / 8 KV heads), and the result equals a
+    float64 attention over the dequantised cache."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.anchors import select_anchors_device
+    n, Hq, Hkv, d = 131072, 32, 8, 128
+    vq = VqConfig(8, 256)
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=5e5)
+    ck, cv = codebooks(31, Hkv, 256, 8)
+    g = torch.Generator(device="cuda").manual_seed(31)
+    K = torch.randn((1, Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    V = torch.randn((1, Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    scores = torch.rand((Hkv, n), device="cuda", generator=g)
+    anchors = select_anchors_device(scores, scores.flip(-1), cfg.budget_for(n)).view(1, Hkv, -1)
+    pos = torch.arange(n, device="cuda", dtype=torch.int64)[None]
+    cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    cache.build_from(K, V, pos, anchors)
+    q = torch.randn((1, Hq, d), device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn((1, Hkv, d), device="cuda", generator=g).to(torch.bfloat16)
+    v = torch.randn((1, Hkv, d), device="cuda", generator=g).to(torch.bfloat16)
+    qp = torch.tensor([n], device="cuda", dtype=torch.int64)
+    cache._ensure_capacity(n + 2)
+    lib = __import__("paper_2506_19505_b200._lib", fromlist=["x"])
+    import ctypes
+    lib.call("antkv_cache_append", ctypes.byref(cache.desc), lib.ptr(k), lib.ptr(v), lib.BF16,
+             lib.ptr(qp), lib.stream())
+    cache._n += 1
+    outs = {}
+    for fast in (True, False):
+        out = torch.empty((1, Hq, d), device="cuda", dtype=torch.float32)
+        cache.attend_device(q, qp, out, fast=fast)
+        outs[fast] = out.cpu().numpy()[0]
+    assert rel(outs[True], outs[False]) < 2e-2
+    Kh, Vh = cache.dequantize()
+    for h in (0, 5):
+        Kr = O.apply_rope(Kh[0, h].cpu().numpy(), np.arange(n + 1), 5e5)
+        for hq in (4 * h, 4 * h + 3):
+            qr = O.apply_rope(q[0, hq].float().cpu().numpy()[None], np.array([n]), 5e5)
+            A = O.softmax_rows((qr @ Kr.T) / np.sqrt(d))
+            ref = (A @ Vh[0, h].cpu().numpy().astype(np.float64))[0]
+            assert rel(outs[False][hq], ref) < 1e-3
+            assert rel(outs[True][hq], ref) < 2e-2
