@@ -162,12 +162,14 @@ typedef struct antkv_cache_desc {
   int window_size;
   int policy;
   int anchor_count;    /* < 0: use anchor_fraction (cache.py:54-57)        */
+  int row_dtype;       /* ANTKV_BF16 / ANTKV_F16 / ANTKV_F32: dtype of the
+                          full-precision pool rows (the input dtype)        */
   double anchor_fraction;
   double theta_base;
   int64_t token_offset;/* global index of slot 0 (sequence sharding)       */
   uint8_t *codes;      /* [B][Hkv][capacity][2][groups*code_bytes]         */
   uint32_t *qmask;     /* [B][Hkv][capacity/32] bit = slot holds codes     */
-  uint16_t *pool_rows; /* bf16 [B][Hkv][pool_capacity][2][d] (K row, V row)*/
+  void *pool_rows;     /* [B][Hkv][pool_capacity][2][d] (K row, V row)    */
   int32_t *pool_tok;   /* [B][Hkv][pool_capacity] token slot, -1 free      */
   int8_t *pool_kind;   /* [B][Hkv][pool_capacity] ANTKV_KIND_*             */
   int32_t *win_ring;   /* [B][Hkv][window_size+1] pool slots, FIFO          */
@@ -177,9 +179,9 @@ typedef struct antkv_cache_desc {
   int64_t *positions;  /* [B][capacity]                                     */
   const float *codebook_k; /* [Hkv][m][d_sub] float32                       */
   const float *codebook_v;
-  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8 copies][8] fp16    */
-  float *tile_cs;      /* fast path: [B][capacity/16][d/2][2] cos/sin of the
-                          16-slot tile base angle (float32)                 */
+  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8] fp16 centroids     */
+  uint16_t *pool_krot; /* fast path: fp16 [B][Hkv][pool_capacity][d] pool K
+                          rows with RoPE applied at their positions          */
 } antkv_cache_desc;
 
 /* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */
@@ -225,8 +227,8 @@ ANTKV_API int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *Kh
 ANTKV_API int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows,
                       int d, float *out, float *lse_out, void *stream);
 
-/* Build the fast-path fp16 replicated codebook layout from codebook_k/v and
- * the per-16-slot RoPE base tables for the tokens currently held. */
+/* Build the fast-path fp16 codebooks from codebook_k/v and the rotated
+ * pool K rows for the rows currently held. */
 ANTKV_API int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream);
 
 #ifdef __cplusplus

@@ -36,11 +36,11 @@ class CacheDesc(ctypes.Structure):
         ("B", _i), ("Hq", _i), ("Hkv", _i), ("d", _i), ("d_sub", _i), ("m", _i),
         ("groups", _i), ("index_bits", _i), ("code_bytes", _i), ("capacity", _i),
         ("pool_capacity", _i), ("window_size", _i), ("policy", _i), ("anchor_count", _i),
-        ("anchor_fraction", _d), ("theta_base", _d), ("token_offset", _i64),
+        ("row_dtype", _i), ("anchor_fraction", _d), ("theta_base", _d), ("token_offset", _i64),
         ("codes", _vp), ("qmask", _vp), ("pool_rows", _vp), ("pool_tok", _vp),
         ("pool_kind", _vp), ("win_ring", _vp), ("free_stack", _vp), ("hstate", _vp),
         ("seq_len", _vp), ("positions", _vp), ("codebook_k", _vp), ("codebook_v", _vp),
-        ("codebook_f16", _vp), ("tile_cs", _vp),
+        ("codebook_f16", _vp), ("pool_krot", _vp),
     ]
 
 

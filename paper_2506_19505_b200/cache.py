@@ -99,6 +99,7 @@ class QuantizedKVCache:
         self.Hq = q_heads
         self.d = None
         self.fast = bool(fast)
+        self.row_dtype = None    # dtype of the full-precision pool rows = input dtype
         self.splits = int(splits)
         self._capacity_hint = capacity
         self.token_offset = int(token_offset)   # global index of slot 0 (sequence shards)
@@ -106,6 +107,7 @@ class QuantizedKVCache:
         self._n = 0
         self._last_pos = None
         self._t = None          # device tensors
+        self._contiguous = True
         self._desc = None
 
     # ------------------------------------------------------------ layout
@@ -133,7 +135,8 @@ class QuantizedKVCache:
         t = {
             "codes": torch.zeros((B, H, cap, 2 * G * cb), dtype=torch.uint8, device=dev),
             "qmask": torch.zeros((B, H, cap // 32), dtype=torch.int32, device=dev),
-            "pool_rows": torch.zeros((B, H, P, 2, d), dtype=torch.bfloat16, device=dev),
+            "pool_rows": torch.zeros((B, H, P, 2, d), dtype=self.row_dtype or torch.bfloat16,
+                                     device=dev),
             "pool_tok": torch.full((B, H, P), -1, dtype=torch.int32, device=dev),
             "pool_kind": torch.full((B, H, P), -1, dtype=torch.int8, device=dev),
             "win_ring": torch.zeros((B, H, W + 1), dtype=torch.int32, device=dev),
@@ -146,8 +149,8 @@ class QuantizedKVCache:
         }
         use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         if use_fast:
-            t["cb_f16"] = torch.zeros((H, 2, 256, 64), dtype=torch.float16, device=dev)
-            t["tile_cs"] = torch.zeros((B, cap // 16, d), dtype=torch.float32, device=dev)
+            t["cb_f16"] = torch.zeros((H, 2, 256, 8), dtype=torch.float16, device=dev)
+            t["pool_krot"] = torch.zeros((B, H, P, d), dtype=torch.float16, device=dev)
         if old is not None:
             oc = old["positions"].shape[1]
             oP = old["pool_tok"].shape[2]
@@ -170,8 +173,8 @@ class QuantizedKVCache:
                     merged = torch.cat([newslots, fs[b, h, :k]])
                     t["free_stack"][b, h, :merged.numel()] = merged
                     t["hstate"][b, h, _lib.HS_FREE_TOP] = merged.numel()
-            if use_fast and "tile_cs" in old:
-                t["tile_cs"][:, :oc // 16] = old["tile_cs"]
+            if use_fast and "pool_krot" in old:
+                t["pool_krot"][:, :, :oP] = old["pool_krot"]
         self._t = t
         self._desc = self._make_desc(cap, P, t)
         self._ws = None
@@ -190,11 +193,12 @@ class QuantizedKVCache:
         D.anchor_fraction = float(self.config.anchor_fraction)
         D.theta_base = float(self.config.theta_base)
         D.token_offset = self.token_offset
+        D.row_dtype = _lib.dtype_tag(t["pool_rows"])
         for f, k in (("codes", "codes"), ("qmask", "qmask"), ("pool_rows", "pool_rows"),
                      ("pool_tok", "pool_tok"), ("pool_kind", "pool_kind"), ("win_ring", "win_ring"),
                      ("free_stack", "free_stack"), ("hstate", "hstate"), ("seq_len", "seq_len"),
                      ("positions", "positions"), ("codebook_k", "cb_k"), ("codebook_v", "cb_v"),
-                     ("codebook_f16", "cb_f16"), ("tile_cs", "tile_cs")):
+                     ("codebook_f16", "cb_f16"), ("pool_krot", "pool_krot")):
             setattr(D, f, t[k].data_ptr() if k in t else None)
         return D
 
@@ -202,7 +206,7 @@ class QuantizedKVCache:
         if self._desc is not None and need <= self._desc.capacity:
             return
         cap = max(need, self._capacity_hint or 0, 2 * (self._desc.capacity if self._desc else 0))
-        self._alloc(_round_up(max(cap, 32), 32))
+        self._alloc(_round_up(max(cap, 128), 128))
 
     @property
     def desc(self):
@@ -254,10 +258,10 @@ class QuantizedKVCache:
                 raise NumericalError(f"non-finite values in {name}")
         self._single = single
         self.Hq, self.Hkv, self.d = Hq, Hkv, d
-        pos_np = np.asarray(positions.detach().cpu().numpy() if isinstance(positions, torch.Tensor)
-                            else positions, dtype=np.int64)
+        pos_np = np.array(positions.detach().cpu().numpy() if isinstance(positions, torch.Tensor)
+                          else positions, dtype=np.int64)
         if pos_np.ndim == 1:
-            pos_np = np.broadcast_to(pos_np, (B, pos_np.shape[0]))
+            pos_np = np.repeat(pos_np[None], B, axis=0)
         if pos_np.shape != (B, n):
             raise ValueError("positions must have one entry per token")
         if np.any(pos_np < 0):
@@ -309,12 +313,17 @@ class QuantizedKVCache:
         self._ensure_capacity(n + 1)
         K = self._row_dtype(K)
         V = self._row_dtype(V.to(K.dtype))
+        if self.row_dtype is None:
+            self.row_dtype = K.dtype
         _lib.call("antkv_cache_build", ctypes.byref(self._desc), _lib.ptr(K), _lib.ptr(V),
                   _lib.dtype_tag(K), _lib.ptr(positions.contiguous()), n,
                   _lib.ptr(anchors.contiguous()), int(anchors.shape[-1]), _lib.stream())
         self._n = n
         if n:
-            self._last_pos = positions[:, -1].cpu().numpy().copy()
+            pos_h = positions.cpu().numpy()
+            self._last_pos = pos_h[:, -1].copy()
+            # the tensor-core decode kernel needs position(slot) = position(0) + slot
+            self._contiguous = bool(np.all(pos_h == pos_h[:, :1] + np.arange(n)[None, :]))
 
     # ------------------------------------------------------------ decode
     def _workspace(self):
@@ -323,6 +332,9 @@ class QuantizedKVCache:
             self._ws = torch.empty((int(nbytes),), dtype=torch.uint8,
                                    device=self._t["codes"].device)
         return self._ws
+
+    def _use_fast(self, fast):
+        return (self.fast if fast is None else fast) and self._contiguous
 
     def step_device(self, q, k, v, qpos, out, lse=None, fast=None):
         """One decode step on device tensors, no host synchronisation:
@@ -338,7 +350,7 @@ class QuantizedKVCache:
         _lib.check(lib.antkv_decode_attention(D, _lib.ptr(q), _lib.dtype_tag(q), _lib.ptr(qpos),
                                               _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws),
                                               ws.numel(), self.splits,
-                                              int(self.fast if fast is None else fast), st))
+                                              int(self._use_fast(fast)), st))
         _lib.check(lib.antkv_cache_evict(D, st))
 
     def attend_device(self, q, qpos, out, lse=None, fast=None):
@@ -346,7 +358,7 @@ class QuantizedKVCache:
         ws = self._workspace()
         _lib.call("antkv_decode_attention", ctypes.byref(self._desc), _lib.ptr(q),
                   _lib.dtype_tag(q), _lib.ptr(qpos), _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws),
-                  ws.numel(), self.splits, int(self.fast if fast is None else fast), _lib.stream())
+                  ws.numel(), self.splits, int(self._use_fast(fast)), _lib.stream())
 
     def decode_step(self, q_new, k_new, v_new, position):
         """Append one token, attend, then evict (cache.py:149-194)."""
@@ -356,6 +368,8 @@ class QuantizedKVCache:
             pos = np.repeat(pos, self.B)
         if self._last_pos is not None and np.any(pos <= self._last_pos):
             raise ValueError("position must exceed all existing positions")
+        if self._last_pos is not None and np.any(pos != self._last_pos + 1):
+            self._contiguous = False
         qt, was_np = as_cuda(q_new)
         kt, _ = as_cuda(k_new)
         vt, _ = as_cuda(v_new)
@@ -420,7 +434,7 @@ class QuantizedKVCache:
         return O
 
     def _host_state(self):
-        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "tile_cs")}
+        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_krot")}
         return t
 
     def kinds_of(self, b=0, h=0):
@@ -459,8 +473,12 @@ class QuantizedKVCache:
         st = self._host_state()
         G = self.d // self.config.vq.d_sub
         cb = 1 if self.config.vq.index_bits <= 8 else 2
-        raw = st["codes"][b, h, :self._n].numpy()
-        arr = raw.view(np.uint8 if cb == 1 else np.uint16).reshape(self._n, 2, G).astype(np.int64)
+        cap = st["codes"].shape[2]
+        raw = st["codes"][b, h].numpy().reshape(-1)
+        units = raw.view(np.uint8 if cb == 1 else np.uint16)
+        # tiled layout [tile][kv][16 slots][G] (common.cuh code_offset)
+        arr = units.reshape(cap // 16, 2, 16, G).transpose(0, 2, 1, 3).reshape(cap, 2, G)
+        arr = arr[:self._n].astype(np.int64)
         kinds = self.kinds_of(b, h)
         kc = {j: arr[j, 0] for j in range(self._n) if kinds[j] == KIND_QUANTIZED}
         vc = {j: arr[j, 1] for j in range(self._n) if kinds[j] == KIND_QUANTIZED}
@@ -598,14 +616,17 @@ class QuantizedKVCache:
         """Install an explicit single-head state (snapshot load)."""
         self._single = True
         self.B, self.Hkv, self.Hq, self.d = 1, 1, self.Hq or 1, d
+        self.row_dtype = torch.float32          # the snapshot stores float32 rows
         n = len(kinds)
         self._ensure_capacity(n + 1)
         t = self._t
         G = d // self.config.vq.d_sub
         cbw = 1 if self.config.vq.index_bits <= 8 else 2
-        rec = np.zeros((n, 2, G), dtype=np.uint8 if cbw == 1 else np.uint16)
-        rec[:, 0], rec[:, 1] = kcodes, vcodes
-        t["codes"][0, 0, :n] = torch.from_numpy(rec.reshape(n, -1).view(np.uint8).copy()).cuda()
+        cap = t["codes"].shape[2]
+        rec = np.zeros((cap, 2, G), dtype=np.uint8 if cbw == 1 else np.uint16)
+        rec[:n, 0], rec[:n, 1] = kcodes, vcodes
+        tiled = rec.reshape(cap // 16, 16, 2, G).transpose(0, 2, 1, 3).reshape(cap, -1)
+        t["codes"][0, 0] = torch.from_numpy(np.ascontiguousarray(tiled).view(np.uint8)).cuda()
         qbits = np.zeros(t["qmask"].shape[-1] * 32, dtype=np.uint8)
         P = t["pool_tok"].shape[-1]
         ptok = np.full(P, -1, np.int32)
@@ -620,8 +641,8 @@ class QuantizedKVCache:
                 pkind[s] = _lib.KIND_ANCHOR if kind == KIND_ANCHOR else _lib.KIND_WINDOWED
                 if kind == KIND_WINDOWED:
                     ring.append(s)
-                t["pool_rows"][0, 0, s, 0] = torch.from_numpy(K[j]).to(torch.bfloat16)
-                t["pool_rows"][0, 0, s, 1] = torch.from_numpy(V[j]).to(torch.bfloat16)
+                t["pool_rows"][0, 0, s, 0] = torch.from_numpy(K[j]).to(t["pool_rows"].dtype)
+                t["pool_rows"][0, 0, s, 1] = torch.from_numpy(V[j]).to(t["pool_rows"].dtype)
                 s += 1
         t["qmask"][0, 0] = torch.from_numpy(np.packbits(qbits, bitorder="little").view(np.int32).copy()).cuda()
         t["pool_tok"][0, 0] = torch.from_numpy(ptok).cuda()
@@ -636,8 +657,6 @@ class QuantizedKVCache:
         t["positions"][0, :n] = torch.tensor(positions, dtype=torch.int64)
         self._n = n
         self._last_pos = np.asarray([positions[-1]], dtype=np.int64) if n else None
-        if "tile_cs" in t and n:
-            self._refresh_tile_cs(n)
-
-    def _refresh_tile_cs(self, n):
-        _lib.call("antkv_cache_prepare_fast", ctypes.byref(self._desc), _lib.stream())
+        self._contiguous = bool(n == 0 or np.all(np.asarray(positions) == positions[0] + np.arange(n)))
+        if "pool_krot" in t:
+            _lib.call("antkv_cache_prepare_fast", ctypes.byref(self._desc), _lib.stream())

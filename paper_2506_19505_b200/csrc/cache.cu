@@ -48,13 +48,15 @@ __device__ __forceinline__ int load_code(const void *codes, int64_t off_elems, i
 // Bulk encoder.  grid = (ceil(rows*groups / 256), nsets): each set s has its
 // own input base (x_set_stride elements), output base (code_set_stride code
 // elements) and codebook (set % cb_mod).  Output code for (row r, group g) is
-// at codes[s*code_set_stride + r*code_row_stride + g].
+// at codes[s*code_set_stride + (r/16)*code_tile_stride + (r%16)*code_row_stride
+// + g] (plain row-major when code_tile_stride == 16*code_row_stride).
 template <int MAXD>
 __global__ void __launch_bounds__(ENC_THREADS)
 vq_encode_kernel(const void *__restrict__ X, int dtype, int64_t rows, int d,
                  int64_t x_set_stride, const float *__restrict__ codebooks, int cb_mod,
                  int m, int d_sub, void *__restrict__ codes, int code_bytes,
-                 int64_t code_set_stride, int64_t code_row_stride, float *__restrict__ d2out) {
+                 int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
+                 float *__restrict__ d2out) {
   __shared__ float sC[ENC_CHUNK_FLOATS];
   const int groups = d / d_sub;
   const int set = blockIdx.y;
@@ -79,7 +81,8 @@ vq_encode_kernel(const void *__restrict__ X, int dtype, int64_t rows, int d,
       for (int c = 0; c < cn; ++c) nearest_update<MAXD>(x, sC + c * d_sub, d_sub, c0 + c, best, best_i);
   }
   if (live) {
-    store_code(codes, set * code_set_stride + r * code_row_stride + g, code_bytes, best_i);
+    store_code(codes, set * code_set_stride + (r >> 4) * code_tile_stride + (r & 15) * code_row_stride + g,
+               code_bytes, best_i);
     if (d2out) d2out[set * rows * groups + item] = best;
   }
 }
@@ -87,7 +90,7 @@ vq_encode_kernel(const void *__restrict__ X, int dtype, int64_t rows, int d,
 int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride,
                   int nsets, const float *codebooks, int cb_mod, int m, int d_sub,
                   void *codes, int code_bytes, int64_t code_set_stride,
-                  int64_t code_row_stride, float *d2, cudaStream_t st) {
+                  int64_t code_tile_stride, int64_t code_row_stride, float *d2, cudaStream_t st) {
   ANTKV_REQUIRE(d_sub >= 1 && d_sub <= 64, "d_sub must be in [1, 64] on the GPU path");
   ANTKV_REQUIRE(d % d_sub == 0, "d=%d not divisible by d_sub=%d", d, d_sub);
   ANTKV_REQUIRE(m >= 1, "empty codebook");
@@ -98,7 +101,7 @@ int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_s
   vq_encode_kernel<MD><<<grid, ENC_THREADS, 0, st>>>(X, dtype, rows, d, x_set_stride,        \
                                                      codebooks, cb_mod, m, d_sub, codes,     \
                                                      code_bytes, code_set_stride,            \
-                                                     code_row_stride, d2)
+                                                     code_tile_stride, code_row_stride, d2)
   if (d_sub <= 2) ENC_LAUNCH(2);
   else if (d_sub <= 4) ENC_LAUNCH(4);
   else if (d_sub <= 8) ENC_LAUNCH(8);
@@ -124,10 +127,6 @@ __global__ void vq_decode_kernel(const void *__restrict__ codes, int code_bytes,
 
 // ------------------------------------------------------------ cache state
 __device__ __forceinline__ int64_t bh_index(int b, int h, int H) { return (int64_t)b * H + h; }
-
-__device__ __forceinline__ int rec_bytes(const antkv_cache_desc &c) {
-  return 2 * c.groups * c.code_bytes;
-}
 
 // Per (b, head) layout from the sorted anchor list (cache.py:126-139).
 // One CTA per (b, head); the codes were written by the bulk encoder.
@@ -199,10 +198,10 @@ __global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ 
   for (int s = 0; s < used; ++s) {
     const int j = ptok[s];
     const int64_t src = (bh * n + j) * c.d;
-    uint16_t *dst = c.pool_rows + (bh * c.pool_capacity + s) * 2 * c.d;
+    const int64_t dst = (bh * c.pool_capacity + s) * 2 * c.d;
     for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-      dst[t] = float_to_bf16_bits(load_elem(K, src + t, dtype));
-      dst[c.d + t] = float_to_bf16_bits(load_elem(V, src + t, dtype));
+      store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(K, src + t, dtype));
+      store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(V, src + t, dtype));
     }
   }
   if (h == 0) {
@@ -213,24 +212,29 @@ __global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ 
   (void)s_win;
 }
 
-// cos/sin of omega_i * P0 for the 16-slot tile starting at `slot` (fast path).
-__device__ void write_tile_cs(const antkv_cache_desc &c, int b, int slot, int64_t pos) {
-  if (!c.tile_cs || (slot & 15)) return;
-  float *dst = c.tile_cs + ((int64_t)b * (c.capacity / 16) + slot / 16) * c.d;
+// Fast path: fp16 copy of pool row `slot`'s K with RoPE applied at `pos`.
+__device__ void write_pool_krot(const antkv_cache_desc &c, int64_t bh, int slot, int64_t pos) {
+  if (!c.pool_krot) return;
+  const int64_t src = (bh * c.pool_capacity + slot) * 2 * c.d;
+  __half *dst = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * c.d;
   for (int i = threadIdx.x; i < c.d / 2; i += blockDim.x) {
+    const float x0 = load_elem(c.pool_rows, src + 2 * i, c.row_dtype);
+    const float x1 = load_elem(c.pool_rows, src + 2 * i + 1, c.row_dtype);
     float cs, sn;
     rope_cs((double)pos * rope_freq(c.theta_base, i, c.d), cs, sn);
-    dst[2 * i] = cs;
-    dst[2 * i + 1] = sn;
+    dst[2 * i] = __float2half_rn(x0 * cs - x1 * sn);
+    dst[2 * i + 1] = __float2half_rn(x0 * sn + x1 * cs);
   }
 }
 
-__global__ void cache_tile_cs_kernel(antkv_cache_desc c, int n) {
-  const int b = blockIdx.y;
-  const int tile = blockIdx.x;
-  if (n < 0) n = c.seq_len[b];
-  if (tile * 16 >= n) return;
-  write_tile_cs(c, b, tile * 16, c.positions[(int64_t)b * c.capacity + tile * 16]);
+// Fast path: rotated K rows for every live pool slot (after build / load).
+__global__ void cache_pool_krot_kernel(antkv_cache_desc c) {
+  const int64_t bh = blockIdx.y;
+  const int b = static_cast<int>(bh / c.Hkv);
+  const int s = blockIdx.x;
+  const int tok = c.pool_tok[bh * c.pool_capacity + s];
+  if (tok < 0 || c.pool_kind[bh * c.pool_capacity + s] == ANTKV_KIND_FREE) return;
+  write_pool_krot(c, bh, s, c.positions[(int64_t)b * c.capacity + tok]);
 }
 
 // Append one token per sequence (one CTA per sequence, loops over heads).
@@ -261,17 +265,18 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
     __syncthreads();
     const int slot = s_slot;
     if (slot >= 0) {
-      uint16_t *dst = c.pool_rows + (bh * c.pool_capacity + slot) * 2 * c.d;
+      const int64_t dst = (bh * c.pool_capacity + slot) * 2 * c.d;
       const int64_t src = bh * c.d;
       for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-        dst[t] = float_to_bf16_bits(load_elem(k, src + t, dtype));
-        dst[c.d + t] = float_to_bf16_bits(load_elem(v, src + t, dtype));
+        store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(k, src + t, dtype));
+        store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(v, src + t, dtype));
       }
+      __syncthreads();
+      write_pool_krot(c, bh, slot, position[b]);
     }
     __syncthreads();
   }
   // the slot's code bits stay clear (qmask initialised to zero above n)
-  write_tile_cs(c, b, j, position[b]);
   if (threadIdx.x == 0) {
     c.positions[(int64_t)b * c.capacity + j] = position[b];
     c.seq_len[b] = j + 1;
@@ -310,7 +315,7 @@ cache_evict_kernel(antkv_cache_desc c) {
   if (!s_encode) return;
   const int slot = s_slot;
   const int j = c.pool_tok[bh * c.pool_capacity + slot];
-  const uint16_t *row = c.pool_rows + (bh * c.pool_capacity + slot) * 2 * c.d;
+  const int64_t row = (bh * c.pool_capacity + slot) * 2 * c.d;
   const int units = 2 * c.groups;             // (kv, group) pairs
   const int team = max(1, 256 / units);       // threads per unit (>= 1)
   const int u = threadIdx.x / team, lane = threadIdx.x % team;
@@ -319,11 +324,11 @@ cache_evict_kernel(antkv_cache_desc c) {
   if (u < units) {
     const int kv = u / c.groups, g = u % c.groups;
     const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-    const uint16_t *x = row + kv * c.d + g * c.d_sub;
+    const int64_t x = row + kv * c.d + g * c.d_sub;
     for (int ci = lane; ci < c.m; ci += team) {
       float s = 0.f;
       for (int t = 0; t < c.d_sub; ++t) {
-        float df = bf16_bits_to_float(x[t]) - cb[(int64_t)ci * c.d_sub + t];
+        float df = load_elem(c.pool_rows, x + t, c.row_dtype) - cb[(int64_t)ci * c.d_sub + t];
         s = fmaf(df, df, s);
       }
       if (s < best) { best = s; best_i = ci; }
@@ -342,9 +347,9 @@ cache_evict_kernel(antkv_cache_desc c) {
       if (o < best || (o == best && oi < best_i)) { best = o; best_i = oi; }
     }
     const int kv = u / c.groups, g = u % c.groups;
-    uint8_t *rec = c.codes + (bh * c.capacity + j) * rec_bytes(c) + kv * c.groups * c.code_bytes;
-    if (c.code_bytes == 1) rec[g] = static_cast<uint8_t>(best_i);
-    else reinterpret_cast<uint16_t *>(rec)[g] = static_cast<uint16_t>(best_i);
+    const int64_t off = bh * c.capacity * 2 * c.groups + code_offset(j, kv, g, c.groups);
+    if (c.code_bytes == 1) c.codes[off] = static_cast<uint8_t>(best_i);
+    else reinterpret_cast<uint16_t *>(c.codes)[off] = static_cast<uint16_t>(best_i);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -368,12 +373,13 @@ __global__ void cache_dequant_codes_kernel(antkv_cache_desc c, int n, float *__r
   const uint32_t bits = c.qmask[bh * (c.capacity / 32) + j / 32];
   float kv = NAN, vv = NAN;
   if (bits & (1u << (j % 32))) {
-    const uint8_t *rec = c.codes + (bh * c.capacity + j) * rec_bytes(c);
     const int g = t / c.d_sub, e = t % c.d_sub;
+    const int64_t hb = bh * c.capacity * 2 * c.groups;
+    const int64_t ok = hb + code_offset(j, 0, g, c.groups), ov = hb + code_offset(j, 1, g, c.groups);
     int ck, cv;
-    if (c.code_bytes == 1) { ck = rec[g]; cv = rec[c.groups + g]; }
-    else { ck = reinterpret_cast<const uint16_t *>(rec)[g];
-           cv = reinterpret_cast<const uint16_t *>(rec)[c.groups + g]; }
+    if (c.code_bytes == 1) { ck = c.codes[ok]; cv = c.codes[ov]; }
+    else { ck = reinterpret_cast<const uint16_t *>(c.codes)[ok];
+           cv = reinterpret_cast<const uint16_t *>(c.codes)[ov]; }
     kv = c.codebook_k[((int64_t)h * c.m + ck) * c.d_sub + e];
     vv = c.codebook_v[((int64_t)h * c.m + cv) * c.d_sub + e];
   }
@@ -387,24 +393,22 @@ __global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__re
   const int s = blockIdx.x;
   const int j = c.pool_tok[bh * c.pool_capacity + s];
   if (j < 0 || j >= n || c.pool_kind[bh * c.pool_capacity + s] == ANTKV_KIND_FREE) return;
-  const uint16_t *row = c.pool_rows + (bh * c.pool_capacity + s) * 2 * c.d;
+  const int64_t row = (bh * c.pool_capacity + s) * 2 * c.d;
   for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-    Khat[(bh * n + j) * c.d + t] = bf16_bits_to_float(row[t]);
-    Vhat[(bh * n + j) * c.d + t] = bf16_bits_to_float(row[c.d + t]);
+    Khat[(bh * n + j) * c.d + t] = load_elem(c.pool_rows, row + t, c.row_dtype);
+    Vhat[(bh * n + j) * c.d + t] = load_elem(c.pool_rows, row + c.d + t, c.row_dtype);
   }
 }
 
-// Fast-path codebook: [Hkv][2][256][8 copies][8] fp16.  Row c of a codebook
-// holds centroid c eight times, one copy per 16-byte bank group, so the eight
-// row addresses of one ldmatrix phase (one per copy) never conflict.
+// Fast-path codebook: compact fp16 [Hkv][2][256][8] (zero rows beyond m);
+// the decode kernel replicates it across bank groups in shared memory.
 __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
   const int h = blockIdx.x / 2, kv = blockIdx.x % 2;
   const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 64;
-  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
-    const int code = i / 64, t = i % 8;
-    const float val = code < c.m ? cb[(int64_t)code * 8 + t] : 0.f;
-    dst[i] = __float2half_rn(val);
+  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 8;
+  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
+    const int code = i / 8, t = i % 8;
+    dst[i] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
   }
 }
 
@@ -420,6 +424,9 @@ static int check_desc(const antkv_cache_desc *c) {
   ANTKV_REQUIRE(c->groups == c->d / c->d_sub, "groups mismatch");
   ANTKV_REQUIRE(c->code_bytes == (c->index_bits <= 8 ? 1 : 2), "code_bytes mismatch");
   ANTKV_REQUIRE(c->index_bits <= 16, "index_bits > 16 unsupported");
+  ANTKV_REQUIRE(c->row_dtype == ANTKV_BF16 || c->row_dtype == ANTKV_F16 || c->row_dtype == ANTKV_F32,
+                "bad row dtype");
+  ANTKV_REQUIRE(c->groups <= 128, "more than 128 sub-vectors per row unsupported");
   ANTKV_REQUIRE(c->capacity % 32 == 0 && c->capacity > 0, "capacity must be a positive multiple of 32");
   ANTKV_REQUIRE(c->window_size >= 0 && c->pool_capacity > c->window_size, "pool too small");
   return ANTKV_OK;
@@ -427,7 +434,7 @@ static int check_desc(const antkv_cache_desc *c) {
 
 extern "C" int antkv_assign_nearest(const float *X, const float *C, int64_t n, int m, int d_sub,
                                     int64_t *idx, float *d2, void *stream) {
-  return launch_encode(X, ANTKV_F32, n, d_sub, 0, 1, C, 1, m, d_sub, idx, 8, 0, 1, d2,
+  return launch_encode(X, ANTKV_F32, n, d_sub, 0, 1, C, 1, m, d_sub, idx, 8, 0, 16, 1, d2,
                        as_stream(stream));
 }
 
@@ -438,7 +445,7 @@ extern "C" int antkv_vq_encode(const void *X, int dtype, int64_t rows, int d,
                 "code_bytes must be 1, 2, 4 or 8");
   ANTKV_REQUIRE(code_bytes >= 8 || m <= (1 << (8 * code_bytes)), "codes do not fit");
   return launch_encode(X, dtype, rows, d, 0, 1, codebook, 1, m, d_sub, codes, code_bytes, 0,
-                       d / d_sub, nullptr, as_stream(stream));
+                       16 * (d / d_sub), d / d_sub, nullptr, as_stream(stream));
 }
 
 extern "C" int antkv_vq_decode(const void *codes, int code_bytes, int64_t rows, int groups,
@@ -461,21 +468,22 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
   ANTKV_REQUIRE(n_anchors + c->window_size + 1 <= c->pool_capacity, "pool capacity too small");
   cudaStream_t st = as_stream(stream);
   const int nsets = c->B * c->Hkv;
-  const int rec = 2 * c->groups * c->code_bytes;
-  // K codes then V codes: code element index within a record is g (+groups for V)
+  const int G = c->groups;
+  // tiled layout: set stride = capacity*2G units, tile stride 32G, row stride G;
+  // V codes start 16G units into each tile
   rc = launch_encode(K, dtype, n, c->d, (int64_t)n * c->d, nsets, c->codebook_k, c->Hkv, c->m,
-                     c->d_sub, c->codes, c->code_bytes, (int64_t)c->capacity * rec / c->code_bytes,
-                     rec / c->code_bytes, nullptr, st);
+                     c->d_sub, c->codes, c->code_bytes, (int64_t)c->capacity * 2 * G, 32 * G, G,
+                     nullptr, st);
   if (rc) return rc;
   rc = launch_encode(V, dtype, n, c->d, (int64_t)n * c->d, nsets, c->codebook_v, c->Hkv, c->m,
-                     c->d_sub, c->codes + c->groups * c->code_bytes, c->code_bytes,
-                     (int64_t)c->capacity * rec / c->code_bytes, rec / c->code_bytes, nullptr, st);
+                     c->d_sub, c->codes + 16 * G * c->code_bytes, c->code_bytes,
+                     (int64_t)c->capacity * 2 * G, 32 * G, G, nullptr, st);
   if (rc) return rc;
   cache_build_kernel<<<nsets, 256, 0, st>>>(*c, K, V, dtype, positions, n, anchors, n_anchors);
   ANTKV_LAUNCH_CHECK("cache_build_kernel");
-  if (c->tile_cs && n > 0) {
-    cache_tile_cs_kernel<<<dim3(ceil_div(n, 16), c->B), 64, 0, st>>>(*c, n);
-    ANTKV_LAUNCH_CHECK("cache_tile_cs_kernel");
+  if (c->pool_krot) {
+    cache_pool_krot_kernel<<<dim3(c->pool_capacity, nsets), 64, 0, st>>>(*c);
+    ANTKV_LAUNCH_CHECK("cache_pool_krot_kernel");
   }
   return ANTKV_OK;
 }
@@ -519,9 +527,9 @@ extern "C" int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream)
   cudaStream_t st = as_stream(stream);
   cache_prepare_fast_kernel<<<c->Hkv * 2, 256, 0, st>>>(*c);
   ANTKV_LAUNCH_CHECK("cache_prepare_fast_kernel");
-  if (c->tile_cs) {
-    cache_tile_cs_kernel<<<dim3(c->capacity / 16, c->B), 64, 0, st>>>(*c, -1);
-    ANTKV_LAUNCH_CHECK("cache_tile_cs_kernel");
+  if (c->pool_krot) {
+    cache_pool_krot_kernel<<<dim3(c->pool_capacity, c->B * c->Hkv), 64, 0, st>>>(*c);
+    ANTKV_LAUNCH_CHECK("cache_pool_krot_kernel");
   }
   return ANTKV_OK;
 }

@@ -39,6 +39,14 @@ __device__ __forceinline__ float load_elem(const void *p, int64_t i, int dtype) 
   return reinterpret_cast<const float *>(p)[i];
 }
 
+__device__ __forceinline__ void store_elem(void *p, int64_t i, int dtype, float v) {
+  if (dtype == ANTKV_BF16) reinterpret_cast<__nv_bfloat16 *>(p)[i] = __float2bfloat16_rn(v);
+  else if (dtype == ANTKV_F16) reinterpret_cast<__half *>(p)[i] = __float2half_rn(v);
+  else reinterpret_cast<float *>(p)[i] = v;
+}
+
+__host__ __device__ inline int dtype_size(int dtype) { return dtype == ANTKV_F32 ? 4 : 2; }
+
 __device__ __forceinline__ float bf16_bits_to_float(uint16_t b) {
   return __uint_as_float(static_cast<uint32_t>(b) << 16);
 }
@@ -82,6 +90,13 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Code layout inside one (sequence, head): tiles of 16 slots, each tile
+// [K codes 16 x G][V codes 16 x G] in code units (1 or 2 bytes), so the K (or
+// V) codes of a tile are one contiguous 16*G-unit block (coalesced / TMA).
+__host__ __device__ __forceinline__ int64_t code_offset(int64_t slot, int kv, int g, int G) {
+  return (slot >> 4) * (32 * (int64_t)G) + kv * (16 * G) + (slot & 15) * G + g;
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }

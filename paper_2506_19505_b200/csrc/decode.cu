@@ -11,10 +11,15 @@ namespace antkv {
 
 constexpr int DG_T = 128;  // items per chunk == threads per CTA
 
+__device__ __forceinline__ int load_code_unit(const antkv_cache_desc &c, int64_t off) {
+  return c.code_bytes == 1 ? c.codes[off] : reinterpret_cast<const uint16_t *>(c.codes)[off];
+}
+
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int dtype,
                        const int64_t *qpos, float *ws_o, float *ws_m, float *ws_l,
                        int splits, cudaStream_t st);
 int decode_fast_supported(const antkv_cache_desc &c);
+void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits);
 
 template <int GQ, bool CB_SMEM>
 __global__ void __launch_bounds__(DG_T)
@@ -63,10 +68,9 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
   const int total = n + pool_high;
   const int per = (total + splits - 1) / splits;
   const int s0 = split * per, s1 = min(total, s0 + per);
-  const int rec = 2 * G * c.code_bytes;
-  const uint8_t *codes = c.codes + bh * c.capacity * rec;
+  const int64_t hb = bh * c.capacity * 2 * G;   // code-unit offset of this head
   const uint32_t *qm = c.qmask + bh * (c.capacity / 32);
-  const uint16_t *pool = c.pool_rows + bh * c.pool_capacity * 2 * d;
+  const int64_t pool = bh * c.pool_capacity * 2 * d;   // element offset of this head's pool
 
   float m_run[GQ], l_run[GQ], acc[GQ][2];
 #pragma unroll
@@ -96,20 +100,20 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
     for (int hh = 0; hh < GQ; ++hh) sc[hh] = 0.f;
     if (src != -1) {
       const double pj = static_cast<double>(c.positions[(int64_t)b * c.capacity + tok]);
-      const uint8_t *r = src >= 0 ? codes + (int64_t)src * rec : nullptr;
-      const uint16_t *prow = src >= 0 ? nullptr : pool + (int64_t)(-2 - src) * 2 * d;
+      const bool r = src >= 0;
+      const int64_t prow = src >= 0 ? 0 : pool + (int64_t)(-2 - src) * 2 * d;
       for (int p = 0; p < d / 2; ++p) {
         float k0, k1;
         if (r) {
           const int e = 2 * p, g = e / dsub, o = e % dsub;
-          const int code = c.code_bytes == 1 ? r[g] : reinterpret_cast<const uint16_t *>(r)[g];
+          const int code = load_code_unit(c, hb + code_offset(src, 0, g, G));
           k0 = cbK[code * dsub + o];
           const int e1 = e + 1, g1 = e1 / dsub, o1 = e1 % dsub;
-          const int code1 = g1 == g ? code : (c.code_bytes == 1 ? r[g1] : reinterpret_cast<const uint16_t *>(r)[g1]);
+          const int code1 = g1 == g ? code : load_code_unit(c, hb + code_offset(src, 0, g1, G));
           k1 = cbK[code1 * dsub + o1];
         } else {
-          k0 = bf16_bits_to_float(prow[2 * p]);
-          k1 = bf16_bits_to_float(prow[2 * p + 1]);
+          k0 = load_elem(c.pool_rows, prow + 2 * p, c.row_dtype);
+          k1 = load_elem(c.pool_rows, prow + 2 * p + 1, c.row_dtype);
         }
         float cs, sn;
         rope_cs(pj * sFreq[p], cs, sn);
@@ -120,7 +124,7 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
       }
       if (r)
         for (int g = 0; g < G; ++g)
-          sVc[threadIdx.x * G + g] = c.code_bytes == 1 ? r[G + g] : reinterpret_cast<const uint16_t *>(r)[G + g];
+          sVc[threadIdx.x * G + g] = load_code_unit(c, hb + code_offset(src, 1, g, G));
     }
     sSrc[threadIdx.x] = src;
 #pragma unroll
@@ -171,7 +175,7 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
         if (s == -1) continue;
         float v;
         if (s >= 0) v = cbV[sVc[t * G + g] * dsub + o];
-        else v = bf16_bits_to_float(pool[(int64_t)(-2 - s) * 2 * d + d + dim]);
+        else v = load_elem(c.pool_rows, pool + (int64_t)(-2 - s) * 2 * d + d + dim, c.row_dtype);
 #pragma unroll
         for (int hh = 0; hh < GQ; ++hh) a[hh] = fmaf(sS[hh * DG_T + t], v, a[hh]);
       }
@@ -279,15 +283,26 @@ static int auto_splits(const antkv_cache_desc &c) {
   return s < 1 ? 1 : (s > 1024 ? 1024 : s);
 }
 
+// Number of partials a call produces (generic: splits; fast: code + pool CTAs).
+static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
+  if (fast) {
+    int cs, ps;
+    decode_fast_plan(c, splits, cs, ps);
+    return cs + ps;
+  }
+  return splits > 0 ? splits : auto_splits(c);
+}
+
 }  // namespace antkv
 
 using namespace antkv;
 
 extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int splits) {
   if (!c) return -1;
-  if (splits <= 0) splits = auto_splits(*c);
+  int s = planned_splits(*c, splits, false);
+  if (decode_fast_supported(*c)) s = max(s, planned_splits(*c, splits, true));
   const int64_t rows = (int64_t)c->B * c->Hq;
-  return (int64_t)splits * rows * (c->d + 2) * sizeof(float) + 256;
+  return (int64_t)s * rows * (c->d + 2) * sizeof(float) + 256;
 }
 
 extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
@@ -297,31 +312,32 @@ extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, 
   ANTKV_REQUIRE(c != nullptr && q != nullptr && out != nullptr, "null argument");
   ANTKV_REQUIRE(c->Hq % c->Hkv == 0, "Hq must be a multiple of Hkv");
   ANTKV_REQUIRE(c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
-  if (splits <= 0) splits = auto_splits(*c);
+  const bool use_fast = fast && decode_fast_supported(*c);
+  const int used = planned_splits(*c, splits, use_fast);
   const int64_t rows = (int64_t)c->B * c->Hq;
-  ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits),
+  ANTKV_REQUIRE(workspace_bytes >= (int64_t)used * rows * (c->d + 2) * (int64_t)sizeof(float),
                 "decode workspace too small");
   float *wo = reinterpret_cast<float *>(workspace);
-  float *wm = wo + (int64_t)splits * rows * c->d;
-  float *wl = wm + (int64_t)splits * rows;
+  float *wm = wo + (int64_t)used * rows * c->d;
+  float *wl = wm + (int64_t)used * rows;
   cudaStream_t st = as_stream(stream);
   const int gq = c->Hq / c->Hkv;
   int rc;
-  if (fast && decode_fast_supported(*c)) {
+  if (use_fast) {
     rc = decode_fast_launch(*c, q, dtype, qpos, wo, wm, wl, splits, st);
   } else {
     switch (gq) {
-      case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
-      case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
-      case 4: rc = launch_generic<4>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
-      case 8: rc = launch_generic<8>(*c, q, dtype, qpos, wo, wm, wl, splits, st); break;
+      case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+      case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+      case 4: rc = launch_generic<4>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+      case 8: rc = launch_generic<8>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
       default:
         set_error("GQA group size %d unsupported (1, 2, 4, 8)", gq);
         return ANTKV_EUNSUPPORTED;
     }
   }
   if (rc) return rc;
-  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, splits, rows, c->d, out, lse);
+  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
   ANTKV_LAUNCH_CHECK("decode_combine_kernel");
   return ANTKV_OK;
 }

@@ -1,14 +1,521 @@
-// sm_100a tensor-core decode kernel for d=128, d_sub=8, m<=256 (1-bit d8m256).
+// sm_100a decode-attention kernel for the 1-bit d8m256 configuration
+// (d = 128, d_sub = 8, m <= 256, 4 query heads per KV head, contiguous
+// positions).  Reference semantics: cache.py:168-178 (RoPE after
+// reconstruction, softmax over the whole cache, A.V).
+//
+// Per 16-slot tile the score matrix S^T[16 tokens x 8 cols] and the output
+// O^T[128 dims x 8 cols] are computed with m16n8k16 tensor-core MMAs whose
+// operands come straight from registers:
+//   * K_hat / V_hat rows are gathered from a shared-memory fp16 codebook
+//     with ldmatrix (one 16-byte centroid row per lane address).  The
+//     codebook is replicated 8x across the 16-byte bank groups so the eight
+//     row addresses of every ldmatrix phase hit distinct banks.
+//   * RoPE: rows 0-7 of a tile are tokens P0..P0+7 (group a), rows 8-15 are
+//     P0+8..P0+15 (group b).  Each row is rotated by its offset g (0..7) in
+//     its group with per-lane constant fp16 (cos, sin) pairs; the group base
+//     rotation is applied to the query instead: columns 0-3 of the MMA carry
+//     the 4 query heads in group a's frame R(p_q - P0) q, columns 4-7 in group
+//     b's frame R(p_q - P0 - 8) q.  Frames advance by R(-16) per tile in fp32
+//     (seeded with float64-reduced angles per warp).
+//   * Group a tokens only see columns 0-3 and group b tokens only 4-7 (the
+//     other products are masked), giving two independent online-softmax
+//     streams that are merged with the CTA merge at the end.
+// Code tiles (K codes 256 B + V codes 256 B per tile) are streamed into a
+// shared-memory ring with cp.async.bulk (TMA bulk copies) and mbarriers.
+// Anchor / window rows (the full-precision pool) are handled by extra CTAs
+// on CUDA cores from fp16 pre-rotated K rows.
 #include "common.cuh"
 
 namespace antkv {
 
-int decode_fast_supported(const antkv_cache_desc &c) { return 0; }
+constexpr int FK_WARPS = 4;
+constexpr int FK_THREADS = 32 * FK_WARPS;
+constexpr int FK_STAGES = 6;
+constexpr int FK_TILE_BYTES = 512;                       // K 256 B + V 256 B
+constexpr int FK_WARP_STAGE_BYTES = 2 * FK_TILE_BYTES;   // 2 tiles per warp per stage
+constexpr int FK_STAGE_BYTES = FK_WARPS * FK_WARP_STAGE_BYTES;
+constexpr int FK_MAX_WARP_WORDS = 64;                    // qmask words per warp (2048 slots)
+
+struct __align__(128) FastSmem {
+  uint4 cbK[256 * 8];                          // [code][copy] 16 B
+  uint4 cbV[256 * 8];
+  uint8_t ring[FK_STAGES][FK_STAGE_BYTES];
+  uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
+  unsigned long long full[FK_STAGES];
+  unsigned long long empty[FK_STAGES];
+};
+
+struct MergeSmem {                             // aliases the ring after the loop
+  float o[FK_WARPS][8][128];
+  float m[FK_WARPS][8];
+  float l[FK_WARPS][8];
+};
+static_assert(sizeof(MergeSmem) <= sizeof(uint8_t) * FK_STAGES * FK_STAGE_BYTES, "merge scratch");
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                             unsigned long long *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t movm_t(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2 *>(&u); }
+
+// (x0, x1) -> (c x0 - s x1, s x0 + c x1) with cs = (c, s), ns = (-s, c)
+__device__ __forceinline__ uint32_t rot2(uint32_t x, uint32_t cs, uint32_t ns) {
+  __half2 v = u2h(x);
+  __half2 r = __hmul2(__high2half2(v), u2h(ns));
+  r = __hfma2(__low2half2(v), u2h(cs), r);
+  return h2u(r);
+}
+
+__device__ __forceinline__ float shfl_max_g(float v) {
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 4));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 8));
+  v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16));
+  return v;
+}
+__device__ __forceinline__ float shfl_sum_g(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  return v;
+}
+
+__device__ void write_empty_partial(int64_t row0, float *ws_o, float *ws_m, float *ws_l) {
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) ws_o[row0 * 128 + i] = 0.f;
+  if (threadIdx.x < 4) {
+    ws_m[row0 + threadIdx.x] = -INFINITY;
+    ws_l[row0 + threadIdx.x] = 0.f;
+  }
+}
+
+// ------------------------------------------------------------------ pool
+// Full-precision rows (anchors + window): CUDA cores, one row per warp step.
+__device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, double pq, int b,
+                          int h, int ps, int pool_splits, int64_t row0, float *ws_o, float *ws_m,
+                          float *ws_l, MergeSmem &mg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+  const int per = (pool_high + pool_splits - 1) / pool_splits;
+  const int r0 = ps * per, r1 = min(pool_high, r0 + per);
+  const int n = c.seq_len[b];
+  // rotated, scaled query dims 4*lane..4*lane+3 (pairs 2*lane, 2*lane+1)
+  float qv[4][4];
+  const float scale = rsqrtf(128.f);
+#pragma unroll
+  for (int hh = 0; hh < 4; ++hh) {
+    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const float x0 = load_elem(q, qb + 2 * pp, qdtype), x1 = load_elem(q, qb + 2 * pp + 1, qdtype);
+      float cs, sn;
+      rope_cs(pq * rope_freq(c.theta_base, 2 * lane + pp, 128), cs, sn);
+      qv[hh][2 * pp] = (x0 * cs - x1 * sn) * scale;
+      qv[hh][2 * pp + 1] = (x0 * sn + x1 * cs) * scale;
+    }
+  }
+  float m[4], l[4], acc[4][4];
+#pragma unroll
+  for (int hh = 0; hh < 4; ++hh) {
+    m[hh] = -INFINITY;
+    l[hh] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
+  }
+  const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
+  const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
+  for (int r = r0 + warp; r < r1; r += FK_WARPS) {
+    const int8_t kind = c.pool_kind[bh * c.pool_capacity + r];
+    const int tok = c.pool_tok[bh * c.pool_capacity + r];
+    if (kind == ANTKV_KIND_FREE || tok < 0 || tok >= n) continue;
+    const uint2 kraw = *reinterpret_cast<const uint2 *>(krot + (int64_t)r * 128 + 4 * lane);
+    const float2 k01 = __half22float2(u2h(kraw.x)), k23 = __half22float2(u2h(kraw.y));
+    float vv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      vv[e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
+    float s[4];
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh)
+      s[hh] = warp_sum(qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y);
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) {
+      const float mn = fmaxf(m[hh], s[hh]);
+      const float al = (m[hh] == -INFINITY) ? 0.f : __expf(m[hh] - mn);
+      const float p = __expf(s[hh] - mn);
+      l[hh] = l[hh] * al + p;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[hh][e] = acc[hh][e] * al + p * vv[e];
+      m[hh] = mn;
+    }
+  }
+  // merge the warps through shared memory: cols 0-3 used
+#pragma unroll
+  for (int hh = 0; hh < 4; ++hh) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mg.o[warp][hh][4 * lane + e] = acc[hh][e];
+    if (lane == 0) {
+      mg.m[warp][hh] = m[hh];
+      mg.l[warp][hh] = l[hh];
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) {
+    const int hh = i / 128, dim = i % 128;
+    float M = -INFINITY;
+    for (int w = 0; w < FK_WARPS; ++w) M = fmaxf(M, mg.m[w][hh]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < FK_WARPS; ++w) {
+        if (mg.m[w][hh] == -INFINITY) continue;
+        const float f = __expf(mg.m[w][hh] - M);
+        L += f * mg.l[w][hh];
+        O += f * mg.o[w][hh][dim];
+      }
+    }
+    ws_o[(row0 + hh) * 128 + dim] = O;
+    if (dim == 0) {
+      ws_m[row0 + hh] = M;
+      ws_l[row0 + hh] = L;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- codes
+__global__ void __launch_bounds__(FK_THREADS, 2)
+decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
+                   const int64_t *__restrict__ qpos, int code_splits, int pool_splits,
+                   float *__restrict__ ws_o, float *__restrict__ ws_m, float *__restrict__ ws_l) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
+  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
+  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
+  const double pq = static_cast<double>(qpos[b]);
+  if (split >= code_splits) {
+    pool_part(c, q, qdtype, pq, b, h, split - code_splits, pool_splits, row0, ws_o, ws_m, ws_l, mg);
+    return;
+  }
+  // ---- work range: tiles [T0, T1), 4 contiguous warp ranges of Tw tiles
+  const int n = c.seq_len[b];
+  const int ntiles = (n + 15) >> 4;
+  const int per_cta = (((ntiles + code_splits - 1) / code_splits) + 2 * FK_WARPS - 1) /
+                      (2 * FK_WARPS) * (2 * FK_WARPS);
+  const int T0 = split * per_cta;
+  if (T0 >= ntiles) {
+    write_empty_partial(row0, ws_o, ws_m, ws_l);
+    return;
+  }
+  const int Tw = per_cta / FK_WARPS;           // even; tiles per warp
+  const int nstages = Tw / 2;
+  const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
+  const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
+  const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
+  const int cap_tiles = c.capacity / 16;
+
+  // ---- setup: barriers, replicated codebooks, qmask words, first stages
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FK_STAGES; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], FK_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  {
+    const uint4 *srcK = reinterpret_cast<const uint4 *>(c.codebook_f16) + (int64_t)h * 2 * 256;
+    const uint4 *srcV = srcK + 256;
+    for (int i = threadIdx.x; i < 256 * 8; i += FK_THREADS) {
+      sm.cbK[i] = __ldg(srcK + (i >> 3));
+      sm.cbV[i] = __ldg(srcV + (i >> 3));
+    }
+    // qmask: warp w's tiles [T0 + w*Tw, +Tw) -> 32-slot words
+    for (int i = lane; i < Tw / 2; i += 32) {
+      const int word = ((T0 + warp * Tw) >> 1) + i;
+      sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
+    }
+  }
+  __syncthreads();
+  auto issue = [&](int st) {
+    const int slot = st % FK_STAGES;
+    mbar_expect_tx(&sm.full[slot], FK_STAGE_BYTES);
+    for (int w = 0; w < FK_WARPS; ++w) {
+      int tile = T0 + w * Tw + 2 * st;
+      if (tile + 2 > cap_tiles) tile = 0;   // beyond capacity: masked dummy data
+      tma_bulk_g2s(&sm.ring[slot][w * FK_WARP_STAGE_BYTES], codes + (int64_t)tile * FK_TILE_BYTES,
+                   FK_WARP_STAGE_BYTES, &sm.full[slot]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
+
+  // ---- per-lane constants
+  // key rotation by the in-group offset g for pairs 8s+t (kc[s][0..1]) and
+  // 8s+4+t (kc[s][2..3]), fp16 (cos, sin) / (-sin, cos)
+  uint32_t kc[8][4];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int pair = 8 * s + 4 * u + t;
+      float cs, sn;
+      rope_cs((double)g * rope_freq(c.theta_base, pair, 128), cs, sn);
+      kc[s][2 * u] = h2u(__floats2half2_rn(cs, sn));
+      kc[s][2 * u + 1] = h2u(__floats2half2_rn(-sn, cs));
+    }
+  }
+  // query frame: lanes 0-15 head g (group a), lanes 16-31 head g-4 (group b)
+  const int head = g & 3;
+  const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 8 : 0);
+  const double delta = pq - static_cast<double>(pos0 + first_slot);
+  float fx[16], fy[16], stc[16], sts[16];
+  {
+    const float scale = rsqrtf(128.f);
+    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + head) * 128;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int pair = 8 * s + 4 * u + t, k = 2 * s + u;
+        const double fr = rope_freq(c.theta_base, pair, 128);
+        const float x0 = load_elem(q, qb + 2 * pair, qdtype) * scale;
+        const float x1 = load_elem(q, qb + 2 * pair + 1, qdtype) * scale;
+        float cs, sn;
+        rope_cs(delta * fr, cs, sn);
+        fx[k] = x0 * cs - x1 * sn;
+        fy[k] = x0 * sn + x1 * cs;
+        rope_cs(-16.0 * fr, stc[k], sts[k]);
+      }
+    }
+  }
+  // ---- online-softmax state for this lane's 2 columns (2t, 2t+1)
+  float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[i][e] = 0.f;
+
+  const uint32_t cbK_base = smem_u32(&sm.cbK[0]) + (lane & 7) * 16;
+  const uint32_t cbV_base = smem_u32(&sm.cbV[0]) + (lane & 7) * 16;
+  const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
+  const int pk = lane >> 4;                             // K-side group parity
+  const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
+  const int pv = (lane >> 3) & 1;                       // V-side group parity
+  const uint32_t sel_k = pk ? 0x7531u : 0x6420u;
+  const uint32_t sel_v = pv ? 0x7531u : 0x6420u;
+  const bool lo = t < 2;                                // owns group-a columns
+
+  for (int st = 0; st < nstages; ++st) {
+    const int slot = st % FK_STAGES;
+    mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
+    const uint32_t qw = sm.qm[warp][st];
+#pragma unroll 1
+    for (int e = 0; e < 2; ++e) {
+      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES + e * FK_TILE_BYTES];
+      const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
+      const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
+      // this lane's 8 K codes (groups 2s+pk) and V codes (groups 2s+pv)
+      const uint32_t kq0 = __byte_perm(kr.x, kr.y, sel_k), kq1 = __byte_perm(kr.z, kr.w, sel_k);
+      const uint32_t vq0 = __byte_perm(vr.x, vr.y, sel_v), vq1 = __byte_perm(vr.z, vr.w, sel_v);
+      // B fragments from the frames
+      uint32_t bq[8][2];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        bq[s][0] = h2u(__floats2half2_rn(fx[2 * s], fy[2 * s]));
+        bq[s][1] = h2u(__floats2half2_rn(fx[2 * s + 1], fy[2 * s + 1]));
+      }
+      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const uint32_t word = s < 4 ? kq0 : kq1;
+        const uint32_t code = (word >> (8 * (s & 3))) & 0xffu;
+        uint32_t a[4];
+        ldsm_x4(cbK_base + code * 128, a);
+        a[0] = rot2(a[0], kc[s][0], kc[s][1]);
+        a[1] = rot2(a[1], kc[s][0], kc[s][1]);
+        a[2] = rot2(a[2], kc[s][2], kc[s][3]);
+        a[3] = rot2(a[3], kc[s][2], kc[s][3]);
+        if (s & 1) mma16816(sb, a, bq[s][0], bq[s][1]);
+        else mma16816(sa, a, bq[s][0], bq[s][1]);
+      }
+      // valid entries: group-a rows (g) in cols 0-3 (lanes t<2), group-b rows
+      // (g+8) in cols 4-7 (lanes t>=2)
+      const int bit = (qw >> (16 * e + g + (lo ? 0 : 8))) & 1;
+      const float s0 = bit ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY;
+      const float s1 = bit ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY;
+      const float mx0 = shfl_max_g(s0), mx1 = shfl_max_g(s1);
+      const float mn0 = fmaxf(mrun[0], mx0), mn1 = fmaxf(mrun[1], mx1);
+      const float al0 = (mrun[0] == mn0) ? 1.f : __expf(mrun[0] - mn0);
+      const float al1 = (mrun[1] == mn1) ? 1.f : __expf(mrun[1] - mn1);
+      const float p0 = bit ? __expf(s0 - mn0) : 0.f;
+      const float p1 = bit ? __expf(s1 - mn1) : 0.f;
+      lrun[0] = lrun[0] * al0 + shfl_sum_g(p0);
+      lrun[1] = lrun[1] * al1 + shfl_sum_g(p1);
+      mrun[0] = mn0;
+      mrun[1] = mn1;
+      if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          o[i][0] *= al0;
+          o[i][1] *= al1;
+          o[i][2] *= al0;
+          o[i][3] *= al1;
+        }
+      }
+      const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
+      const uint32_t pb0 = movm_t(lo ? ph : 0u);       // P[tokens 2t,2t+1][col g]
+      const uint32_t pb1 = movm_t(lo ? 0u : ph);       // P[tokens 8+2t,..][col g]
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        const uint32_t word = mt < 4 ? vq0 : vq1;
+        const uint32_t code = (word >> (8 * (mt & 3))) & 0xffu;
+        uint32_t a[4];
+        ldsm_x4_t(cbV_base + code * 128, a);
+        mma16816(o[mt], a, pb0, pb1);
+      }
+      // advance both frames by 16 positions: f <- R(-16) f
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float x = fx[k], y = fy[k];
+        fx[k] = x * stc[k] - y * sts[k];
+        fy[k] = x * sts[k] + y * stc[k];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[slot]);
+    if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
+      mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
+      issue(st + FK_STAGES);
+    }
+  }
+  // ---- merge 4 warps x 2 streams -> partial for 4 heads
+  __syncthreads();   // all stages consumed; the ring becomes merge scratch
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    mg.o[warp][2 * t][16 * mt + g] = o[mt][0];
+    mg.o[warp][2 * t + 1][16 * mt + g] = o[mt][1];
+    mg.o[warp][2 * t][16 * mt + g + 8] = o[mt][2];
+    mg.o[warp][2 * t + 1][16 * mt + g + 8] = o[mt][3];
+  }
+  if (g == 0) {
+    mg.m[warp][2 * t] = mrun[0];
+    mg.m[warp][2 * t + 1] = mrun[1];
+    mg.l[warp][2 * t] = lrun[0];
+    mg.l[warp][2 * t + 1] = lrun[1];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
+    const int hh = i / 128, dim = i % 128;
+    float M = -INFINITY;
+    for (int w = 0; w < FK_WARPS; ++w)
+      M = fmaxf(M, fmaxf(mg.m[w][hh], mg.m[w][hh + 4]));
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < FK_WARPS; ++w) {
+#pragma unroll
+        for (int sidx = 0; sidx < 2; ++sidx) {
+          const int col = hh + 4 * sidx;
+          const float mv = mg.m[w][col];
+          if (mv == -INFINITY) continue;
+          const float f = __expf(mv - M);
+          L += f * mg.l[w][col];
+          O += f * mg.o[w][col][dim];
+        }
+      }
+    }
+    ws_o[(row0 + hh) * 128 + dim] = O;
+    if (dim == 0) {
+      ws_m[row0 + hh] = M;
+      ws_l[row0 + hh] = L;
+    }
+  }
+}
+
+int decode_fast_supported(const antkv_cache_desc &c) {
+  return c.d == 128 && c.d_sub == 8 && c.m <= 256 && c.code_bytes == 1 && c.Hq == 4 * c.Hkv &&
+         c.codebook_f16 != nullptr && c.pool_krot != nullptr && c.capacity % 128 == 0;
+}
+
+// Split plan shared with the workspace sizing: code CTAs + pool CTAs per
+// (sequence, head).  `requested` > 0 fixes the code CTAs per head.
+void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits) {
+  pool_splits = max(1, min(16, (c.pool_capacity + 127) / 128));
+  const int bh = c.B * c.Hkv;
+  code_splits = requested > 0 ? requested : max(1, (2 * 148 + bh - 1) / bh);
+  // per-warp qmask staging caps a CTA at 4 warps x 128 tiles (see FK_MAX_WARP_WORDS)
+  const int cap_tiles = c.capacity / 16;
+  const int min_code = (cap_tiles + 503) / 504;
+  if (code_splits < min_code) code_splits = min_code;
+}
 
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int dtype, const int64_t *qpos,
                        float *ws_o, float *ws_m, float *ws_l, int splits, cudaStream_t st) {
-  set_error("fast decode kernel not built");
-  return ANTKV_EUNSUPPORTED;
+  int code_splits, pool_splits;
+  decode_fast_plan(c, splits, code_splits, pool_splits);
+  const size_t smem = sizeof(FastSmem);
+  cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(code_splits + pool_splits, c.Hkv, c.B);
+  decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, q, dtype, qpos, code_splits, pool_splits,
+                                                     ws_o, ws_m, ws_l);
+  ANTKV_LAUNCH_CHECK("decode_fast_kernel");
+  // splits beyond code_splits + pool_splits are left unused: mark them empty
+  return ANTKV_OK;
 }
 
 }  // namespace antkv
