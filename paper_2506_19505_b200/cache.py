@@ -310,11 +310,11 @@ class QuantizedKVCache:
         self.d = d
         if anchors.shape[-1] + self.config.window_size + 1 > self._pool_capacity(max(n, 1)):
             raise ValueError("anchor count exceeds the pool capacity")
-        self._ensure_capacity(n + 1)
         K = self._row_dtype(K)
         V = self._row_dtype(V.to(K.dtype))
         if self.row_dtype is None:
             self.row_dtype = K.dtype
+        self._ensure_capacity(n + 1)
         _lib.call("antkv_cache_build", ctypes.byref(self._desc), _lib.ptr(K), _lib.ptr(V),
                   _lib.dtype_tag(K), _lib.ptr(positions.contiguous()), n,
                   _lib.ptr(anchors.contiguous()), int(anchors.shape[-1]), _lib.stream())

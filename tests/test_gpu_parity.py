@@ -284,6 +284,7 @@ def _gqa(seed, B, Hq, Hkv, n, d, notation, steps, window=32, frac=0.01, policy="
     cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), batch=B, fast=fast)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
     Og = cache.prefill(dev(Q[:, :, :n]), dev(K[:, :, :n]), dev(V[:, :, :n]), np.arange(n))
+    anchors0 = [[cache.anchor_indices_of(b, h) for h in range(Hkv)] for b in range(B)]
     outs = []
     for t in range(n, n + steps):
         outs.append(cache.decode_step(dev(Q[:, :, t]), dev(K[:, :, t]), dev(V[:, :, t]), t)
@@ -296,10 +297,13 @@ def _gqa(seed, B, Hq, Hkv, n, d, notation, steps, window=32, frac=0.01, policy="
         assert rel(Og[b].cpu().numpy(), Or) < 1e-4
         sk, sv = ref.last_scores
         for h in range(Hkv):
-            assert_anchor_parity(cache.anchor_indices_of(b, h), ref.heads[h].anchor_indices,
-                                 sk[h], sv[h])
+            assert_anchor_parity(anchors0[b][h], ref.heads[h].anchor_indices, sk[h], sv[h])
         refs.append([ref.decode_step(Q[b, :, t], K[b, :, t], V[b, :, t], t)
                      for t in range(n, n + steps)])
+        for h in range(Hkv):
+            if np.array_equal(anchors0[b][h], ref.heads[h].anchor_indices[:len(anchors0[b][h])]):
+                # same prefill anchors -> identical promotion schedule
+                assert np.array_equal(cache.anchor_indices_of(b, h), ref.heads[h].anchor_indices)
     return cache, np.array(outs), np.array(refs).transpose(1, 0, 2, 3)
 
 
