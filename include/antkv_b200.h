@@ -179,9 +179,12 @@ typedef struct antkv_cache_desc {
   int64_t *positions;  /* [B][capacity]                                     */
   const float *codebook_k; /* [Hkv][m][d_sub] float32                       */
   const float *codebook_v;
-  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8] fp16 centroids     */
+  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8 copies][8] fp16: each
+                              centroid replicated across the 8 16-byte bank
+                              groups of a 128-byte row (64 KB per head)     */
   uint16_t *pool_krot; /* fast path: fp16 [B][Hkv][pool_capacity][d] pool K
                           rows with RoPE applied at their positions          */
+  void *fast_tables;   /* fast path: 8192-byte RoPE constant tables         */
 } antkv_cache_desc;
 
 /* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */

@@ -149,7 +149,8 @@ class QuantizedKVCache:
         }
         use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         if use_fast:
-            t["cb_f16"] = torch.zeros((H, 2, 256, 8), dtype=torch.float16, device=dev)
+            t["cb_f16"] = torch.zeros((H, 2, 256, 64), dtype=torch.float16, device=dev)
+            t["fast_tables"] = torch.zeros((8192,), dtype=torch.uint8, device=dev)
             t["pool_krot"] = torch.zeros((B, H, P, d), dtype=torch.float16, device=dev)
         if old is not None:
             oc = old["positions"].shape[1]
@@ -198,7 +199,8 @@ class QuantizedKVCache:
                      ("pool_tok", "pool_tok"), ("pool_kind", "pool_kind"), ("win_ring", "win_ring"),
                      ("free_stack", "free_stack"), ("hstate", "hstate"), ("seq_len", "seq_len"),
                      ("positions", "positions"), ("codebook_k", "cb_k"), ("codebook_v", "cb_v"),
-                     ("codebook_f16", "cb_f16"), ("pool_krot", "pool_krot")):
+                     ("codebook_f16", "cb_f16"), ("pool_krot", "pool_krot"),
+                     ("fast_tables", "fast_tables")):
             setattr(D, f, t[k].data_ptr() if k in t else None)
         return D
 
@@ -434,7 +436,8 @@ class QuantizedKVCache:
         return O
 
     def _host_state(self):
-        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_krot")}
+        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_krot",
+                                                                  "fast_tables")}
         return t
 
     def kinds_of(self, b=0, h=0):

@@ -400,14 +400,34 @@ __global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__re
   }
 }
 
-// Fast-path codebook: compact fp16 [Hkv][2][256][8] (zero rows beyond m);
-// the decode kernel replicates it across bank groups in shared memory.
+// Fast-path codebook: fp16 [Hkv][2][256][8 copies][8] (zero rows beyond m).
+// Row `code` holds the centroid in each of the 8 16-byte bank groups, so the
+// eight ldmatrix row addresses of a phase (copy = lane & 7) never conflict.
+// Block (Hkv*2) also writes the RoPE constant tables (FastTables).
 __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
+  if (blockIdx.x == gridDim.x - 1) {
+    FastTables *tab = reinterpret_cast<FastTables *>(c.fast_tables);
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+      const double om = rope_freq(c.theta_base, i, 128);
+      tab->omega[i] = om;
+      float cs, sn;
+      rope_cs(-16.0 * om, cs, sn);
+      tab->step[i][0] = cs;
+      tab->step[i][1] = sn;
+      for (int g = 0; g < 8; ++g) {
+        rope_cs((double)g * om, cs, sn);
+        __half2 a = __floats2half2_rn(cs, sn), b = __floats2half2_rn(-sn, cs);
+        tab->kc[g][i][0] = *reinterpret_cast<uint32_t *>(&a);
+        tab->kc[g][i][1] = *reinterpret_cast<uint32_t *>(&b);
+      }
+    }
+    return;
+  }
   const int h = blockIdx.x / 2, kv = blockIdx.x % 2;
   const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 8;
-  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
-    const int code = i / 8, t = i % 8;
+  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 64;
+  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
+    const int code = i / 64, t = i % 8;
     dst[i] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
   }
 }
@@ -523,9 +543,10 @@ extern "C" int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *K
 extern "C" int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
-  ANTKV_REQUIRE(c->d_sub == 8 && c->m <= 256 && c->codebook_f16, "fast path needs d_sub=8, m<=256");
+  ANTKV_REQUIRE(c->d == 128 && c->d_sub == 8 && c->m <= 256 && c->codebook_f16 && c->fast_tables,
+                "fast path needs d=128, d_sub=8, m<=256");
   cudaStream_t st = as_stream(stream);
-  cache_prepare_fast_kernel<<<c->Hkv * 2, 256, 0, st>>>(*c);
+  cache_prepare_fast_kernel<<<c->Hkv * 2 + 1, 256, 0, st>>>(*c);
   ANTKV_LAUNCH_CHECK("cache_prepare_fast_kernel");
   if (c->pool_krot) {
     cache_pool_krot_kernel<<<dim3(c->pool_capacity, c->B * c->Hkv), 64, 0, st>>>(*c);

@@ -43,6 +43,7 @@ struct __align__(128) FastSmem {
   uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
   unsigned long long full[FK_STAGES];
   unsigned long long empty[FK_STAGES];
+  unsigned long long cbbar;
 };
 
 struct MergeSmem {                             // aliases the ring after the loop
@@ -142,7 +143,8 @@ __device__ void write_empty_partial(int64_t row0, float *ws_o, float *ws_m, floa
 }
 
 // ------------------------------------------------------------------ pool
-// Full-precision rows (anchors + window): CUDA cores, one row per warp step.
+// Full-precision rows (anchors + window) on CUDA cores: a warp handles 4 rows
+// per step (32 lanes x 4 dims), all loads of the 4 rows in flight together.
 __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, double pq, int b,
                           int h, int ps, int pool_splits, int64_t row0, float *ws_o, float *ws_m,
                           float *ws_l, MergeSmem &mg) {
@@ -152,6 +154,7 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
   const int per = (pool_high + pool_splits - 1) / pool_splits;
   const int r0 = ps * per, r1 = min(pool_high, r0 + per);
   const int n = c.seq_len[b];
+  const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
   // rotated, scaled query dims 4*lane..4*lane+3 (pairs 2*lane, 2*lane+1)
   float qv[4][4];
   const float scale = rsqrtf(128.f);
@@ -162,7 +165,7 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
     for (int pp = 0; pp < 2; ++pp) {
       const float x0 = load_elem(q, qb + 2 * pp, qdtype), x1 = load_elem(q, qb + 2 * pp + 1, qdtype);
       float cs, sn;
-      rope_cs(pq * rope_freq(c.theta_base, 2 * lane + pp, 128), cs, sn);
+      rope_cs(pq * tab->omega[2 * lane + pp], cs, sn);
       qv[hh][2 * pp] = (x0 * cs - x1 * sn) * scale;
       qv[hh][2 * pp + 1] = (x0 * sn + x1 * cs) * scale;
     }
@@ -177,29 +180,52 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
   }
   const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
   const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
-  for (int r = r0 + warp; r < r1; r += FK_WARPS) {
-    const int8_t kind = c.pool_kind[bh * c.pool_capacity + r];
-    const int tok = c.pool_tok[bh * c.pool_capacity + r];
-    if (kind == ANTKV_KIND_FREE || tok < 0 || tok >= n) continue;
-    const uint2 kraw = *reinterpret_cast<const uint2 *>(krot + (int64_t)r * 128 + 4 * lane);
-    const float2 k01 = __half22float2(u2h(kraw.x)), k23 = __half22float2(u2h(kraw.y));
-    float vv[4];
+  for (int rb = r0 + 4 * warp; rb < r1; rb += 4 * FK_WARPS) {
+    bool ok[4];
+    uint2 kraw[4];
+    float vv[4][4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      vv[e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
-    float s[4];
+    for (int u = 0; u < 4; ++u) {
+      const int r = min(rb + u, r1 - 1);
+      const int8_t kind = c.pool_kind[bh * c.pool_capacity + r];
+      const int tok = c.pool_tok[bh * c.pool_capacity + r];
+      ok[u] = (rb + u < r1) && kind != ANTKV_KIND_FREE && tok >= 0 && tok < n;
+      kraw[u] = *reinterpret_cast<const uint2 *>(krot + (int64_t)r * 128 + 4 * lane);
 #pragma unroll
-    for (int hh = 0; hh < 4; ++hh)
-      s[hh] = warp_sum(qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y);
+      for (int e = 0; e < 4; ++e)
+        vv[u][e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
+    }
+    float s[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float2 k01 = __half22float2(u2h(kraw[u].x)), k23 = __half22float2(u2h(kraw[u].y));
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh)
+        s[u][hh] = qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) s[u][hh] += __shfl_xor_sync(0xffffffffu, s[u][hh], o);
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh) {
-      const float mn = fmaxf(m[hh], s[hh]);
-      const float al = (m[hh] == -INFINITY) ? 0.f : __expf(m[hh] - mn);
-      const float p = __expf(s[hh] - mn);
-      l[hh] = l[hh] * al + p;
+      float mx = m[hh];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[hh][e] = acc[hh][e] * al + p * vv[e];
-      m[hh] = mn;
+      for (int u = 0; u < 4; ++u) if (ok[u]) mx = fmaxf(mx, s[u][hh]);
+      const float al = (m[hh] == mx) ? 1.f : __expf(m[hh] - mx);
+      l[hh] *= al;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[hh][e] *= al;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float p = ok[u] ? __expf(s[u][hh] - mx) : 0.f;
+        l[hh] += p;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[hh][e] = fmaf(p, vv[u][e], acc[hh][e]);
+      }
+      m[hh] = mx;
     }
   }
   // merge the warps through shared memory: cols 0-3 used
@@ -234,6 +260,90 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
   }
 }
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Per-warp streaming state for the code tiles.
+struct WarpState {
+  uint32_t kc[8][4];      // key rotation constants for offset g
+  float fx[16], fy[16];   // query frame pairs (log2-scaled)
+  float stc[16], sts[16]; // R(-16) per pair
+  float mrun[2], lrun[2]; // online softmax of this lane's 2 columns (log2 units)
+  float o[8][4];          // O^T accumulators
+};
+
+// One 16-slot code tile: S^T = rot(K_hat) . frame (8 HMMA), masked online
+// softmax over the lane's 2 columns, O^T += V_hat^T . P (8 HMMA).
+__device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint32_t mbits,
+                                          uint32_t cbK_base, uint32_t cbV_base, int tk, int tv,
+                                          uint32_t sel_k, uint32_t sel_v, bool lo) {
+  const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
+  const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
+  const uint32_t kq0 = __byte_perm(kr.x, kr.y, sel_k), kq1 = __byte_perm(kr.z, kr.w, sel_k);
+  const uint32_t vq0 = __byte_perm(vr.x, vr.y, sel_v), vq1 = __byte_perm(vr.z, vr.w, sel_v);
+  float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const uint32_t word = s < 4 ? kq0 : kq1;
+    const uint32_t code = (word >> (8 * (s & 3))) & 0xffu;
+    uint32_t a[4];
+    ldsm_x4(cbK_base + code * 128, a);
+    a[0] = rot2(a[0], w.kc[s][0], w.kc[s][1]);
+    a[1] = rot2(a[1], w.kc[s][0], w.kc[s][1]);
+    a[2] = rot2(a[2], w.kc[s][2], w.kc[s][3]);
+    a[3] = rot2(a[3], w.kc[s][2], w.kc[s][3]);
+    const uint32_t b0 = h2u(__floats2half2_rn(w.fx[2 * s], w.fy[2 * s]));
+    const uint32_t b1 = h2u(__floats2half2_rn(w.fx[2 * s + 1], w.fy[2 * s + 1]));
+    if (s & 1) mma16816(sb, a, b0, b1);
+    else mma16816(sa, a, b0, b1);
+  }
+  // lanes t<2 own group-a rows (g) in cols 0-3, lanes t>=2 group-b rows (g+8)
+  const bool valid = mbits & 1u;
+  const float s0 = valid ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY;
+  const float s1 = valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY;
+  const float mn0 = fmaxf(w.mrun[0], shfl_max_g(s0));
+  const float mn1 = fmaxf(w.mrun[1], shfl_max_g(s1));
+  const float al0 = ex2(w.mrun[0] - mn0);     // -inf - -inf guarded below
+  const float al1 = ex2(w.mrun[1] - mn1);
+  const float a0 = (w.mrun[0] == mn0) ? 1.f : al0;
+  const float a1 = (w.mrun[1] == mn1) ? 1.f : al1;
+  const float p0 = valid ? ex2(s0 - mn0) : 0.f;
+  const float p1 = valid ? ex2(s1 - mn1) : 0.f;
+  w.lrun[0] = w.lrun[0] * a0 + shfl_sum_g(p0);
+  w.lrun[1] = w.lrun[1] * a1 + shfl_sum_g(p1);
+  w.mrun[0] = mn0;
+  w.mrun[1] = mn1;
+  if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w.o[i][0] *= a0;
+      w.o[i][1] *= a1;
+      w.o[i][2] *= a0;
+      w.o[i][3] *= a1;
+    }
+  }
+  const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
+  const uint32_t pb0 = movm_t(lo ? ph : 0u);
+  const uint32_t pb1 = movm_t(lo ? 0u : ph);
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const uint32_t word = mt < 4 ? vq0 : vq1;
+    const uint32_t code = (word >> (8 * (mt & 3))) & 0xffu;
+    uint32_t a[4];
+    ldsm_x4_t(cbV_base + code * 128, a);
+    mma16816(w.o[mt], a, pb0, pb1);
+  }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const float x = w.fx[k], y = w.fy[k];
+    w.fx[k] = x * w.stc[k] - y * w.sts[k];
+    w.fy[k] = x * w.sts[k] + y * w.stc[k];
+  }
+}
+
 // ----------------------------------------------------------------- codes
 __global__ void __launch_bounds__(FK_THREADS, 2)
 decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
@@ -252,7 +362,7 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
     pool_part(c, q, qdtype, pq, b, h, split - code_splits, pool_splits, row0, ws_o, ws_m, ws_l, mg);
     return;
   }
-  // ---- work range: tiles [T0, T1), 4 contiguous warp ranges of Tw tiles
+  // ---- work range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
   const int n = c.seq_len[b];
   const int ntiles = (n + 15) >> 4;
   const int per_cta = (((ntiles + code_splits - 1) / code_splits) + 2 * FK_WARPS - 1) /
@@ -268,27 +378,16 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
   const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
   const int cap_tiles = c.capacity / 16;
+  const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
 
-  // ---- setup: barriers, replicated codebooks, qmask words, first stages
+  // ---- setup: barriers; TMA: replicated codebooks + first code stages
   if (threadIdx.x == 0) {
     for (int s = 0; s < FK_STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
       mbar_init(&sm.empty[s], FK_WARPS);
     }
+    mbar_init(&sm.cbbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  {
-    const uint4 *srcK = reinterpret_cast<const uint4 *>(c.codebook_f16) + (int64_t)h * 2 * 256;
-    const uint4 *srcV = srcK + 256;
-    for (int i = threadIdx.x; i < 256 * 8; i += FK_THREADS) {
-      sm.cbK[i] = __ldg(srcK + (i >> 3));
-      sm.cbV[i] = __ldg(srcV + (i >> 3));
-    }
-    // qmask: warp w's tiles [T0 + w*Tw, +Tw) -> 32-slot words
-    for (int i = lane; i < Tw / 2; i += 32) {
-      const int word = ((T0 + warp * Tw) >> 1) + i;
-      sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
-    }
   }
   __syncthreads();
   auto issue = [&](int st) {
@@ -301,142 +400,78 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
                    FK_WARP_STAGE_BYTES, &sm.full[slot]);
     }
   };
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    const uint8_t *cbsrc = reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * 65536;
+    mbar_expect_tx(&sm.cbbar, 65536);
+    tma_bulk_g2s(&sm.cbK[0], cbsrc, 32768, &sm.cbbar);
+    tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
-
-  // ---- per-lane constants
-  // key rotation by the in-group offset g for pairs 8s+t (kc[s][0..1]) and
-  // 8s+4+t (kc[s][2..3]), fp16 (cos, sin) / (-sin, cos)
-  uint32_t kc[8][4];
+  }
+  // qmask words of this warp's range: tiles [T0 + w*Tw, +Tw) -> Tw/2 32-slot words
+  for (int i = lane; i < Tw / 2; i += 32) {
+    const int word = ((T0 + warp * Tw) >> 1) + i;
+    sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
+  }
+  // ---- per-lane constants (tables prepared once per cache)
+  WarpState w;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int pair = 8 * s + 4 * u + t;
-      float cs, sn;
-      rope_cs((double)g * rope_freq(c.theta_base, pair, 128), cs, sn);
-      kc[s][2 * u] = h2u(__floats2half2_rn(cs, sn));
-      kc[s][2 * u + 1] = h2u(__floats2half2_rn(-sn, cs));
+      w.kc[s][2 * u] = tab->kc[g][pair][0];
+      w.kc[s][2 * u + 1] = tab->kc[g][pair][1];
     }
   }
-  // query frame: lanes 0-15 head g (group a), lanes 16-31 head g-4 (group b)
-  const int head = g & 3;
-  const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 8 : 0);
-  const double delta = pq - static_cast<double>(pos0 + first_slot);
-  float fx[16], fy[16], stc[16], sts[16];
   {
-    const float scale = rsqrtf(128.f);
+    // query frame: lanes 0-15 head g in group a's frame, 16-31 head g-4 in b's
+    const int head = g & 3;
+    const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 8 : 0);
+    const double delta = pq - static_cast<double>(pos0 + first_slot);
+    const float scale = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
     const int64_t qb = ((int64_t)b * c.Hq + h * 4 + head) * 128;
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int pair = 8 * s + 4 * u + t, k = 2 * s + u;
-        const double fr = rope_freq(c.theta_base, pair, 128);
         const float x0 = load_elem(q, qb + 2 * pair, qdtype) * scale;
         const float x1 = load_elem(q, qb + 2 * pair + 1, qdtype) * scale;
         float cs, sn;
-        rope_cs(delta * fr, cs, sn);
-        fx[k] = x0 * cs - x1 * sn;
-        fy[k] = x0 * sn + x1 * cs;
-        rope_cs(-16.0 * fr, stc[k], sts[k]);
+        rope_cs(delta * tab->omega[pair], cs, sn);
+        w.fx[k] = x0 * cs - x1 * sn;
+        w.fy[k] = x0 * sn + x1 * cs;
+        w.stc[k] = tab->step[pair][0];
+        w.sts[k] = tab->step[pair][1];
       }
     }
   }
-  // ---- online-softmax state for this lane's 2 columns (2t, 2t+1)
-  float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};
-  float o[8][4];
+  w.mrun[0] = w.mrun[1] = -INFINITY;
+  w.lrun[0] = w.lrun[1] = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) o[i][e] = 0.f;
+    for (int e = 0; e < 4; ++e) w.o[i][e] = 0.f;
 
   const uint32_t cbK_base = smem_u32(&sm.cbK[0]) + (lane & 7) * 16;
   const uint32_t cbV_base = smem_u32(&sm.cbV[0]) + (lane & 7) * 16;
   const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
-  const int pk = lane >> 4;                             // K-side group parity
   const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
-  const int pv = (lane >> 3) & 1;                       // V-side group parity
-  const uint32_t sel_k = pk ? 0x7531u : 0x6420u;
-  const uint32_t sel_v = pv ? 0x7531u : 0x6420u;
+  const uint32_t sel_k = (lane >> 4) ? 0x7531u : 0x6420u;
+  const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
   const bool lo = t < 2;                                // owns group-a columns
+  const int rowbit = g + (lo ? 0 : 8);
+  __syncwarp();
+  mbar_wait(&sm.cbbar, 0);
 
   for (int st = 0; st < nstages; ++st) {
     const int slot = st % FK_STAGES;
     mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
     const uint32_t qw = sm.qm[warp][st];
-#pragma unroll 1
-    for (int e = 0; e < 2; ++e) {
-      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES + e * FK_TILE_BYTES];
-      const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
-      const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
-      // this lane's 8 K codes (groups 2s+pk) and V codes (groups 2s+pv)
-      const uint32_t kq0 = __byte_perm(kr.x, kr.y, sel_k), kq1 = __byte_perm(kr.z, kr.w, sel_k);
-      const uint32_t vq0 = __byte_perm(vr.x, vr.y, sel_v), vq1 = __byte_perm(vr.z, vr.w, sel_v);
-      // B fragments from the frames
-      uint32_t bq[8][2];
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        bq[s][0] = h2u(__floats2half2_rn(fx[2 * s], fy[2 * s]));
-        bq[s][1] = h2u(__floats2half2_rn(fx[2 * s + 1], fy[2 * s + 1]));
-      }
-      float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int s = 0; s < 8; ++s) {
-        const uint32_t word = s < 4 ? kq0 : kq1;
-        const uint32_t code = (word >> (8 * (s & 3))) & 0xffu;
-        uint32_t a[4];
-        ldsm_x4(cbK_base + code * 128, a);
-        a[0] = rot2(a[0], kc[s][0], kc[s][1]);
-        a[1] = rot2(a[1], kc[s][0], kc[s][1]);
-        a[2] = rot2(a[2], kc[s][2], kc[s][3]);
-        a[3] = rot2(a[3], kc[s][2], kc[s][3]);
-        if (s & 1) mma16816(sb, a, bq[s][0], bq[s][1]);
-        else mma16816(sa, a, bq[s][0], bq[s][1]);
-      }
-      // valid entries: group-a rows (g) in cols 0-3 (lanes t<2), group-b rows
-      // (g+8) in cols 4-7 (lanes t>=2)
-      const int bit = (qw >> (16 * e + g + (lo ? 0 : 8))) & 1;
-      const float s0 = bit ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY;
-      const float s1 = bit ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY;
-      const float mx0 = shfl_max_g(s0), mx1 = shfl_max_g(s1);
-      const float mn0 = fmaxf(mrun[0], mx0), mn1 = fmaxf(mrun[1], mx1);
-      const float al0 = (mrun[0] == mn0) ? 1.f : __expf(mrun[0] - mn0);
-      const float al1 = (mrun[1] == mn1) ? 1.f : __expf(mrun[1] - mn1);
-      const float p0 = bit ? __expf(s0 - mn0) : 0.f;
-      const float p1 = bit ? __expf(s1 - mn1) : 0.f;
-      lrun[0] = lrun[0] * al0 + shfl_sum_g(p0);
-      lrun[1] = lrun[1] * al1 + shfl_sum_g(p1);
-      mrun[0] = mn0;
-      mrun[1] = mn1;
-      if (__any_sync(0xffffffffu, al0 != 1.f || al1 != 1.f)) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          o[i][0] *= al0;
-          o[i][1] *= al1;
-          o[i][2] *= al0;
-          o[i][3] *= al1;
-        }
-      }
-      const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
-      const uint32_t pb0 = movm_t(lo ? ph : 0u);       // P[tokens 2t,2t+1][col g]
-      const uint32_t pb1 = movm_t(lo ? 0u : ph);       // P[tokens 8+2t,..][col g]
-#pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
-        const uint32_t word = mt < 4 ? vq0 : vq1;
-        const uint32_t code = (word >> (8 * (mt & 3))) & 0xffu;
-        uint32_t a[4];
-        ldsm_x4_t(cbV_base + code * 128, a);
-        mma16816(o[mt], a, pb0, pb1);
-      }
-      // advance both frames by 16 positions: f <- R(-16) f
-#pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float x = fx[k], y = fy[k];
-        fx[k] = x * stc[k] - y * sts[k];
-        fy[k] = x * sts[k] + y * stc[k];
-      }
-    }
+    const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
+    code_tile(w, tb, qw >> rowbit, cbK_base, cbV_base, tk, tv, sel_k, sel_v, lo);
+    code_tile(w, tb + FK_TILE_BYTES, qw >> (16 + rowbit), cbK_base, cbV_base, tk, tv, sel_k,
+              sel_v, lo);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[slot]);
     if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
@@ -444,38 +479,39 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
       issue(st + FK_STAGES);
     }
   }
-  // ---- merge 4 warps x 2 streams -> partial for 4 heads
+  // ---- merge 4 warps x 2 streams -> partial for 4 heads (natural-log units)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
+  const float ln2 = 0.6931471805599453f;
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
-    mg.o[warp][2 * t][16 * mt + g] = o[mt][0];
-    mg.o[warp][2 * t + 1][16 * mt + g] = o[mt][1];
-    mg.o[warp][2 * t][16 * mt + g + 8] = o[mt][2];
-    mg.o[warp][2 * t + 1][16 * mt + g + 8] = o[mt][3];
+    mg.o[warp][2 * t][16 * mt + g] = w.o[mt][0];
+    mg.o[warp][2 * t + 1][16 * mt + g] = w.o[mt][1];
+    mg.o[warp][2 * t][16 * mt + g + 8] = w.o[mt][2];
+    mg.o[warp][2 * t + 1][16 * mt + g + 8] = w.o[mt][3];
   }
   if (g == 0) {
-    mg.m[warp][2 * t] = mrun[0];
-    mg.m[warp][2 * t + 1] = mrun[1];
-    mg.l[warp][2 * t] = lrun[0];
-    mg.l[warp][2 * t + 1] = lrun[1];
+    mg.m[warp][2 * t] = w.mrun[0] * ln2;
+    mg.m[warp][2 * t + 1] = w.mrun[1] * ln2;
+    mg.l[warp][2 * t] = w.lrun[0];
+    mg.l[warp][2 * t + 1] = w.lrun[1];
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
     const int hh = i / 128, dim = i % 128;
     float M = -INFINITY;
-    for (int w = 0; w < FK_WARPS; ++w)
-      M = fmaxf(M, fmaxf(mg.m[w][hh], mg.m[w][hh + 4]));
+    for (int ww = 0; ww < FK_WARPS; ++ww)
+      M = fmaxf(M, fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]));
     float L = 0.f, O = 0.f;
     if (M != -INFINITY) {
-      for (int w = 0; w < FK_WARPS; ++w) {
+      for (int ww = 0; ww < FK_WARPS; ++ww) {
 #pragma unroll
         for (int sidx = 0; sidx < 2; ++sidx) {
           const int col = hh + 4 * sidx;
-          const float mv = mg.m[w][col];
+          const float mv = mg.m[ww][col];
           if (mv == -INFINITY) continue;
           const float f = __expf(mv - M);
-          L += f * mg.l[w][col];
-          O += f * mg.o[w][col][dim];
+          L += f * mg.l[ww][col];
+          O += f * mg.o[ww][col][dim];
         }
       }
     }
@@ -489,15 +525,18 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
 
 int decode_fast_supported(const antkv_cache_desc &c) {
   return c.d == 128 && c.d_sub == 8 && c.m <= 256 && c.code_bytes == 1 && c.Hq == 4 * c.Hkv &&
-         c.codebook_f16 != nullptr && c.pool_krot != nullptr && c.capacity % 128 == 0;
+         c.codebook_f16 != nullptr && c.pool_krot != nullptr && c.fast_tables != nullptr &&
+         c.capacity % 128 == 0;
 }
 
 // Split plan shared with the workspace sizing: code CTAs + pool CTAs per
 // (sequence, head).  `requested` > 0 fixes the code CTAs per head.
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits) {
-  pool_splits = max(1, min(16, (c.pool_capacity + 127) / 128));
+  // ~2 resident CTAs per SM in total; pool rows are ~1-2 % of the tokens but
+  // ~15 % of the bytes, so they get a few CTAs of their own
+  pool_splits = max(1, min(8, (c.pool_capacity + 319) / 320));
   const int bh = c.B * c.Hkv;
-  code_splits = requested > 0 ? requested : max(1, (2 * 148 + bh - 1) / bh);
+  code_splits = requested > 0 ? requested : max(1, (2 * 148 + bh - 1) / bh - pool_splits);
   // per-warp qmask staging caps a CTA at 4 warps x 128 tiles (see FK_MAX_WARP_WORDS)
   const int cap_tiles = c.capacity / 16;
   const int min_code = (cap_tiles + 503) / 504;
