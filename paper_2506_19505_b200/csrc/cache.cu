@@ -237,44 +237,58 @@ __global__ void cache_pool_krot_kernel(antkv_cache_desc c) {
   write_pool_krot(c, bh, s, c.positions[(int64_t)b * c.capacity + tok]);
 }
 
-// Append one token per sequence (one CTA per sequence, loops over heads).
+// Append one token per sequence (cache.py:157-166).  One CTA per sequence;
+// threads 0..Hkv-1 update the per-head state in parallel, then all threads
+// copy the K/V rows of every head and (fast path) write the rotated K rows.
 __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__ k,
                                     const void *__restrict__ v, int dtype,
                                     const int64_t *__restrict__ position) {
   const int b = blockIdx.x;
   const int j = c.seq_len[b];
-  __shared__ int s_slot;
-  for (int h = 0; h < c.Hkv; ++h) {
+  __shared__ int s_slot[256];
+  for (int h = threadIdx.x; h < c.Hkv; h += blockDim.x) {
     const int64_t bh = bh_index(b, h, c.Hkv);
     int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
-    if (threadIdx.x == 0) {
-      int top = hs[ANTKV_HS_FREE_TOP] - 1;
-      int slot = top >= 0 ? c.free_stack[bh * c.pool_capacity + top] : -1;
-      if (slot >= 0) {
-        hs[ANTKV_HS_FREE_TOP] = top;
-        c.pool_tok[bh * c.pool_capacity + slot] = j;
-        c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_WINDOWED;
-        int32_t *ring = c.win_ring + bh * (c.window_size + 1);
-        int pos = (hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % (c.window_size + 1);
-        ring[pos] = slot;
-        hs[ANTKV_HS_WIN_COUNT] += 1;
-        if (slot + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot + 1;
-      }
-      s_slot = slot;
-    }
-    __syncthreads();
-    const int slot = s_slot;
+    const int top = hs[ANTKV_HS_FREE_TOP] - 1;
+    const int slot = top >= 0 ? c.free_stack[bh * c.pool_capacity + top] : -1;
     if (slot >= 0) {
-      const int64_t dst = (bh * c.pool_capacity + slot) * 2 * c.d;
-      const int64_t src = bh * c.d;
-      for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-        store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(k, src + t, dtype));
-        store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(v, src + t, dtype));
-      }
-      __syncthreads();
-      write_pool_krot(c, bh, slot, position[b]);
+      hs[ANTKV_HS_FREE_TOP] = top;
+      c.pool_tok[bh * c.pool_capacity + slot] = j;
+      c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_WINDOWED;
+      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+      ring[(hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % (c.window_size + 1)] = slot;
+      hs[ANTKV_HS_WIN_COUNT] += 1;
+      if (slot + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot + 1;
     }
+    s_slot[h] = slot;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < c.Hkv * c.d; i += blockDim.x) {
+    const int h = i / c.d, t = i % c.d;
+    const int slot = s_slot[h];
+    if (slot < 0) continue;
+    const int64_t bh = bh_index(b, h, c.Hkv);
+    const int64_t dst = (bh * c.pool_capacity + slot) * 2 * c.d;
+    store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(k, bh * c.d + t, dtype));
+    store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(v, bh * c.d + t, dtype));
+  }
+  if (c.pool_krot) {
     __syncthreads();
+    const double pos = static_cast<double>(position[b]);
+    for (int i = threadIdx.x; i < c.Hkv * (c.d / 2); i += blockDim.x) {
+      const int h = i / (c.d / 2), p = i % (c.d / 2);
+      const int slot = s_slot[h];
+      if (slot < 0) continue;
+      const int64_t bh = bh_index(b, h, c.Hkv);
+      const int64_t src = (bh * c.pool_capacity + slot) * 2 * c.d;
+      const float x0 = load_elem(c.pool_rows, src + 2 * p, c.row_dtype);
+      const float x1 = load_elem(c.pool_rows, src + 2 * p + 1, c.row_dtype);
+      float cs, sn;
+      rope_cs(pos * rope_freq(c.theta_base, p, c.d), cs, sn);
+      __half *dst = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * c.d;
+      dst[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
+      dst[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
+    }
   }
   // the slot's code bits stay clear (qmask initialised to zero above n)
   if (threadIdx.x == 0) {
@@ -284,10 +298,12 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
 }
 
 // Evict (cache.py:180-193).  One CTA (256 threads) per (b, head).  Encoding
+// stages the row and (when they fit) both codebooks in shared memory, then
 // splits each (K/V, group) over a team of threads that scans a slice of the
-// codebook, then reduces (distance, index) with the lowest index on ties.
+// codebook, reducing (distance, index) with the lowest index on ties.
 __global__ void __launch_bounds__(256)
-cache_evict_kernel(antkv_cache_desc c) {
+cache_evict_kernel(antkv_cache_desc c, int cb_in_smem) {
+  extern __shared__ float ev_sm[];
   const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
   const int64_t bh = bh_index(b, h, c.Hkv);
   int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
@@ -316,6 +332,18 @@ cache_evict_kernel(antkv_cache_desc c) {
   const int slot = s_slot;
   const int j = c.pool_tok[bh * c.pool_capacity + slot];
   const int64_t row = (bh * c.pool_capacity + slot) * 2 * c.d;
+  const int cbn = c.m * c.d_sub;
+  float *sx = ev_sm;                       // [2][d]
+  float *scb = ev_sm + 2 * c.d;            // [2][m][d_sub] when cb_in_smem
+  for (int i = threadIdx.x; i < 2 * c.d; i += blockDim.x) sx[i] = load_elem(c.pool_rows, row + i, c.row_dtype);
+  if (cb_in_smem) {
+    const float *gk = c.codebook_k + (int64_t)h * cbn, *gv = c.codebook_v + (int64_t)h * cbn;
+    for (int i = threadIdx.x; i < cbn; i += blockDim.x) {
+      scb[i] = gk[i];
+      scb[cbn + i] = gv[i];
+    }
+  }
+  __syncthreads();
   const int units = 2 * c.groups;             // (kv, group) pairs
   const int team = max(1, 256 / units);       // threads per unit (>= 1)
   const int u = threadIdx.x / team, lane = threadIdx.x % team;
@@ -323,12 +351,13 @@ cache_evict_kernel(antkv_cache_desc c) {
   int best_i = 0x7fffffff;
   if (u < units) {
     const int kv = u / c.groups, g = u % c.groups;
-    const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-    const int64_t x = row + kv * c.d + g * c.d_sub;
+    const float *cb = cb_in_smem ? scb + kv * cbn
+                                 : (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * cbn;
+    const float *x = sx + kv * c.d + g * c.d_sub;
     for (int ci = lane; ci < c.m; ci += team) {
       float s = 0.f;
       for (int t = 0; t < c.d_sub; ++t) {
-        float df = load_elem(c.pool_rows, x + t, c.row_dtype) - cb[(int64_t)ci * c.d_sub + t];
+        const float df = x[t] - cb[(int64_t)ci * c.d_sub + t];
         s = fmaf(df, df, s);
       }
       if (s < best) { best = s; best_i = ci; }
@@ -512,7 +541,8 @@ extern "C" int antkv_cache_append(const antkv_cache_desc *c, const void *k, cons
                                   int dtype, const int64_t *position, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
-  cache_append_kernel<<<c->B, 128, 0, as_stream(stream)>>>(*c, k, v, dtype, position);
+  ANTKV_REQUIRE(c->Hkv <= 256, "at most 256 KV heads");
+  cache_append_kernel<<<c->B, 256, 0, as_stream(stream)>>>(*c, k, v, dtype, position);
   ANTKV_LAUNCH_CHECK("cache_append_kernel");
   return ANTKV_OK;
 }
@@ -520,7 +550,11 @@ extern "C" int antkv_cache_append(const antkv_cache_desc *c, const void *k, cons
 extern "C" int antkv_cache_evict(const antkv_cache_desc *c, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
-  cache_evict_kernel<<<c->B * c->Hkv, 256, 0, as_stream(stream)>>>(*c);
+  const size_t cbn = (size_t)c->m * c->d_sub;
+  const int cb_in_smem = cbn * 2 * sizeof(float) <= 64 * 1024;
+  const size_t smem = sizeof(float) * (2 * c->d + (cb_in_smem ? 2 * cbn : 0));
+  cudaFuncSetAttribute(cache_evict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cache_evict_kernel<<<c->B * c->Hkv, 256, smem, as_stream(stream)>>>(*c, cb_in_smem);
   ANTKV_LAUNCH_CHECK("cache_evict_kernel");
   return ANTKV_OK;
 }

@@ -30,7 +30,7 @@ namespace antkv {
 
 constexpr int FK_WARPS = 4;
 constexpr int FK_THREADS = 32 * FK_WARPS;
-constexpr int FK_STAGES = 6;
+constexpr int FK_STAGES = 10;
 constexpr int FK_TILE_BYTES = 512;                       // K 256 B + V 256 B
 constexpr int FK_WARP_STAGE_BYTES = 2 * FK_TILE_BYTES;   // 2 tiles per warp per stage
 constexpr int FK_STAGE_BYTES = FK_WARPS * FK_WARP_STAGE_BYTES;
