@@ -368,7 +368,8 @@ def run_ours(args):
             "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
                     "h2d_bytes_per_step": L * (qh[0, 0].numel() + 2 * kh[0, 0].numel()) * 2 + 8,
                     "d2h_bytes_per_step": L * B * HQ * D * 4, "ms_per_step": e2e_ms},
-            "gpu_launches": args.steps * L * (4 if world == 1 else 3),
+            "gpu_launches": args.steps * L * ((1 if args.kernel == "fast" else 4) if world == 1
+                                              else (3 if args.kernel == "fast" else 4)),
             "clocks": clk.summary(),
             "encode": enc,
         }

@@ -216,6 +216,19 @@ ANTKV_API int antkv_decode_attention(const antkv_cache_desc *c, const void *q, i
                            void *workspace, int64_t workspace_bytes, int splits,
                            int fast, void *stream);
 
+/* One full decode step (cache.py:149-194): append (k, v) [B][Hkv][d] as
+ * windowed, attend q [B][Hq][d] over the cache (output before eviction),
+ * then evict/promote/encode the oldest window row.  With `fast` and a
+ * d8m256 cache this is ONE kernel launch (attention + split combine + cache
+ * update in the last CTA of every (sequence, head)); otherwise append,
+ * attention, combine and evict run as separate kernels.  The workspace
+ * (antkv_decode_workspace_bytes) must be zero-filled before its first use;
+ * the kernels leave its ticket counters at zero. */
+ANTKV_API int antkv_decode_step(const antkv_cache_desc *c, const void *q, const void *k,
+                                const void *v, int dtype, const int64_t *qpos, float *out,
+                                float *lse, void *workspace, int64_t workspace_bytes,
+                                int splits, int fast, void *stream);
+
 /* Evict the oldest windowed row of every (b, head) whose window exceeds
  * window_size: promote to anchor while the budget has headroom, otherwise
  * encode it into the code slots (cache.py:180-193). */

@@ -62,6 +62,7 @@ _SIGS = {
     "antkv_cache_append": (_i, [ctypes.POINTER(CacheDesc), _vp, _vp, _i, _vp, _vp]),
     "antkv_decode_attention": (_i, [ctypes.POINTER(CacheDesc), _vp, _i, _vp, _vp, _vp, _vp, _i64, _i, _i, _vp]),
     "antkv_cache_evict": (_i, [ctypes.POINTER(CacheDesc), _vp]),
+    "antkv_decode_step": (_i, [ctypes.POINTER(CacheDesc), _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _i, _i, _vp]),
     "antkv_cache_dequantize": (_i, [ctypes.POINTER(CacheDesc), _i, _vp, _vp, _vp]),
     "antkv_lse_combine": (_i, [_vp, _vp, _i, _i64, _i, _vp, _vp, _vp]),
     "antkv_cache_prepare_fast": (_i, [ctypes.POINTER(CacheDesc), _vp]),

@@ -331,7 +331,8 @@ class QuantizedKVCache:
     def _workspace(self):
         if self._ws is None:
             nbytes = _lib.load().antkv_decode_workspace_bytes(ctypes.byref(self._desc), self.splits)
-            self._ws = torch.empty((int(nbytes),), dtype=torch.uint8,
+            # zero-filled once: the kernels keep its ticket counters at zero
+            self._ws = torch.zeros((int(nbytes),), dtype=torch.uint8,
                                    device=self._t["codes"].device)
         return self._ws
 
@@ -340,20 +341,16 @@ class QuantizedKVCache:
 
     def step_device(self, q, k, v, qpos, out, lse=None, fast=None):
         """One decode step on device tensors, no host synchronisation:
-        append (k, v) as windowed, attend q over the cache, evict.
-        q [B, Hq, d], k/v [B, Hkv, d] (bf16/fp16/fp32), qpos int64 [B],
-        out float32 [B, Hq, d].  The caller maintains capacity."""
-        D = ctypes.byref(self._desc)
-        st = _lib.stream()
+        append (k, v) as windowed, attend q over the cache, evict
+        (antkv_decode_step: a single fused kernel on the d8m256 fast path).
+        q [B, Hq, d], k/v [B, Hkv, d] (one dtype: bf16/fp16/fp32), qpos int64
+        [B], out float32 [B, Hq, d].  The caller maintains capacity."""
         ws = self._workspace()
         lib = _lib.load(check_device=False)
-        _lib.check(lib.antkv_cache_append(D, _lib.ptr(k), _lib.ptr(v), _lib.dtype_tag(k),
-                                          _lib.ptr(qpos), st))
-        _lib.check(lib.antkv_decode_attention(D, _lib.ptr(q), _lib.dtype_tag(q), _lib.ptr(qpos),
-                                              _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws),
-                                              ws.numel(), self.splits,
-                                              int(self._use_fast(fast)), st))
-        _lib.check(lib.antkv_cache_evict(D, st))
+        _lib.check(lib.antkv_decode_step(ctypes.byref(self._desc), _lib.ptr(q), _lib.ptr(k),
+                                         _lib.ptr(v), _lib.dtype_tag(q), _lib.ptr(qpos),
+                                         _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws), ws.numel(),
+                                         self.splits, int(self._use_fast(fast)), _lib.stream()))
 
     def attend_device(self, q, qpos, out, lse=None, fast=None):
         """Attention only (no append/evict): used by sequence shards."""
@@ -382,6 +379,7 @@ class QuantizedKVCache:
             raise ValueError("decode_step before prefill is not supported on the GPU cache")
         self._ensure_capacity(self._n + 2)
         qt, kt, vt = self._row_dtype(qt), self._row_dtype(kt), self._row_dtype(vt.to(kt.dtype))
+        qt = qt.to(kt.dtype)
         qp = torch.from_numpy(pos).to(qt.device)
         out = torch.empty((self.B, self.Hq, self.d), dtype=torch.float32, device=qt.device)
         self.step_device(qt, kt, vt, qp, out)

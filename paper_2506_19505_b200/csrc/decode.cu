@@ -15,9 +15,10 @@ __device__ __forceinline__ int load_code_unit(const antkv_cache_desc &c, int64_t
   return c.code_bytes == 1 ? c.codes[off] : reinterpret_cast<const uint16_t *>(c.codes)[off];
 }
 
-int decode_fast_launch(const antkv_cache_desc &c, const void *q, int dtype,
-                       const int64_t *qpos, float *ws_o, float *ws_m, float *ws_l,
-                       int splits, cudaStream_t st);
+int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
+                       const void *vnew, int kvdtype, const int64_t *qpos, float *out, float *lse,
+                       float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
+                       cudaStream_t st);
 int decode_fast_supported(const antkv_cache_desc &c);
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits);
 
@@ -297,49 +298,85 @@ static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
 
 using namespace antkv;
 
+static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
+  return (int64_t)used * c.B * c.Hq * (c.d + 2) * (int64_t)sizeof(float);
+}
+
+// Workspace = split partials (o, m, l) + self-resetting CTA tickets
+// [B*Hkv + B] int32 at the end.  Zero it once before the first call.
 extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int splits) {
   if (!c) return -1;
   int s = planned_splits(*c, splits, false);
   if (decode_fast_supported(*c)) s = max(s, planned_splits(*c, splits, true));
+  return partial_bytes(*c, s) + (int64_t)(c->B * c->Hkv + c->B) * 4 + 256;
+}
+
+static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, const void *knew,
+                          const void *vnew, int kvdtype, const int64_t *qpos, float *out,
+                          float *lse, void *workspace, int64_t workspace_bytes, int splits,
+                          bool use_fast, cudaStream_t st) {
+  const int used = planned_splits(*c, splits, use_fast);
   const int64_t rows = (int64_t)c->B * c->Hq;
-  return (int64_t)s * rows * (c->d + 2) * sizeof(float) + 256;
+  ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits), "decode workspace too small");
+  float *wo = reinterpret_cast<float *>(workspace);
+  float *wm = wo + (int64_t)used * rows * c->d;
+  float *wl = wm + (int64_t)used * rows;
+  int *cnt = reinterpret_cast<int *>(reinterpret_cast<char *>(workspace) + workspace_bytes -
+                                     256 - (int64_t)(c->B * c->Hkv + c->B) * 4);
+  if (use_fast)
+    return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
+                              splits, st);
+  const int gq = c->Hq / c->Hkv;
+  int rc;
+  switch (gq) {
+    case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+    case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+    case 4: rc = launch_generic<4>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+    case 8: rc = launch_generic<8>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
+    default:
+      set_error("GQA group size %d unsupported (1, 2, 4, 8)", gq);
+      return ANTKV_EUNSUPPORTED;
+  }
+  if (rc) return rc;
+  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
+  ANTKV_LAUNCH_CHECK("decode_combine_kernel");
+  return ANTKV_OK;
+}
+
+static int check_decode_args(const antkv_cache_desc *c, const void *q, float *out) {
+  ANTKV_REQUIRE(c != nullptr && q != nullptr && out != nullptr, "null argument");
+  ANTKV_REQUIRE(c->Hq % c->Hkv == 0, "Hq must be a multiple of Hkv");
+  ANTKV_REQUIRE(c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
+  return ANTKV_OK;
 }
 
 extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
                                       const int64_t *qpos, float *out, float *lse,
                                       void *workspace, int64_t workspace_bytes, int splits,
                                       int fast, void *stream) {
-  ANTKV_REQUIRE(c != nullptr && q != nullptr && out != nullptr, "null argument");
-  ANTKV_REQUIRE(c->Hq % c->Hkv == 0, "Hq must be a multiple of Hkv");
-  ANTKV_REQUIRE(c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
-  const bool use_fast = fast && decode_fast_supported(*c);
-  const int used = planned_splits(*c, splits, use_fast);
-  const int64_t rows = (int64_t)c->B * c->Hq;
-  ANTKV_REQUIRE(workspace_bytes >= (int64_t)used * rows * (c->d + 2) * (int64_t)sizeof(float),
-                "decode workspace too small");
-  float *wo = reinterpret_cast<float *>(workspace);
-  float *wm = wo + (int64_t)used * rows * c->d;
-  float *wl = wm + (int64_t)used * rows;
-  cudaStream_t st = as_stream(stream);
-  const int gq = c->Hq / c->Hkv;
-  int rc;
-  if (use_fast) {
-    rc = decode_fast_launch(*c, q, dtype, qpos, wo, wm, wl, splits, st);
-  } else {
-    switch (gq) {
-      case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
-      case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
-      case 4: rc = launch_generic<4>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
-      case 8: rc = launch_generic<8>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
-      default:
-        set_error("GQA group size %d unsupported (1, 2, 4, 8)", gq);
-        return ANTKV_EUNSUPPORTED;
-    }
-  }
+  int rc = check_decode_args(c, q, out);
   if (rc) return rc;
-  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
-  ANTKV_LAUNCH_CHECK("decode_combine_kernel");
-  return ANTKV_OK;
+  return attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
+                        workspace_bytes, splits, fast && decode_fast_supported(*c), as_stream(stream));
+}
+
+extern "C" int antkv_decode_step(const antkv_cache_desc *c, const void *q, const void *k,
+                                 const void *v, int dtype, const int64_t *qpos, float *out,
+                                 float *lse, void *workspace, int64_t workspace_bytes, int splits,
+                                 int fast, void *stream) {
+  int rc = check_decode_args(c, q, out);
+  if (rc) return rc;
+  ANTKV_REQUIRE(k != nullptr && v != nullptr, "null k/v");
+  cudaStream_t st = as_stream(stream);
+  if (fast && decode_fast_supported(*c))   // one fused launch
+    return attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes,
+                          splits, true, st);
+  rc = antkv_cache_append(c, k, v, dtype, qpos, stream);
+  if (rc) return rc;
+  rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
+                      workspace_bytes, splits, false, st);
+  if (rc) return rc;
+  return antkv_cache_evict(c, stream);
 }
 
 extern "C" int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows, int d,

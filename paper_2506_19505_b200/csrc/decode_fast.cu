@@ -44,6 +44,8 @@ struct __align__(128) FastSmem {
   unsigned long long full[FK_STAGES];
   unsigned long long empty[FK_STAGES];
   unsigned long long cbbar;
+  int ticket;
+  int ev_slot, ev_encode, app_slot;
 };
 
 struct MergeSmem {                             // aliases the ring after the loop
@@ -134,40 +136,92 @@ __device__ __forceinline__ float shfl_sum_g(float v) {
   return v;
 }
 
-__device__ void write_empty_partial(int64_t row0, float *ws_o, float *ws_m, float *ws_l) {
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) ws_o[row0 * 128 + i] = 0.f;
+// Arguments of one decode step / attention call.
+struct StepArgs {
+  const void *q;           // [B][Hq][128]
+  const void *knew;        // [B][Hkv][128] token appended this step (NULL: attend only)
+  const void *vnew;
+  int qdtype, kvdtype;
+  const int64_t *qpos;     // [B]
+  float *out;              // [B][Hq][128]
+  float *lse;              // [B][Hq] or NULL
+  float *ws_o, *ws_m, *ws_l;
+  int *cnt;                // [B*Hkv] CTA tickets + [B] head tickets (self-resetting)
+  int code_splits, pool_splits;
+};
+
+__device__ __forceinline__ float round_to(int dtype, float x) {
+  if (dtype == ANTKV_BF16) return __bfloat162float(__float2bfloat16_rn(x));
+  if (dtype == ANTKV_F16) return __half2float(__float2half_rn(x));
+  return x;
+}
+
+__device__ void write_partial_empty(int64_t row0, const StepArgs &a) {
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) a.ws_o[row0 * 128 + i] = 0.f;
   if (threadIdx.x < 4) {
-    ws_m[row0 + threadIdx.x] = -INFINITY;
-    ws_l[row0 + threadIdx.x] = 0.f;
+    a.ws_m[row0 + threadIdx.x] = -INFINITY;
+    a.ws_l[row0 + threadIdx.x] = 0.f;
+  }
+}
+
+// Merge per-warp (m, l, o) states (natural-log units) of `cols_per_head`
+// columns per head into this CTA's partial rows.
+__device__ void write_partial_merged(const MergeSmem &mg, int ncol_sets, int64_t row0,
+                                     const StepArgs &a) {
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) {
+    const int hh = i / 128, dim = i % 128;
+    float M = -INFINITY;
+    for (int w = 0; w < FK_WARPS; ++w)
+      for (int sidx = 0; sidx < ncol_sets; ++sidx) M = fmaxf(M, mg.m[w][hh + 4 * sidx]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < FK_WARPS; ++w) {
+        for (int sidx = 0; sidx < ncol_sets; ++sidx) {
+          const int col = hh + 4 * sidx;
+          const float mv = mg.m[w][col];
+          if (mv == -INFINITY) continue;
+          const float f = __expf(mv - M);
+          L += f * mg.l[w][col];
+          O += f * mg.o[w][col][dim];
+        }
+      }
+    }
+    a.ws_o[(row0 + hh) * 128 + dim] = O;
+    if (dim == 0) {
+      a.ws_m[row0 + hh] = M;
+      a.ws_l[row0 + hh] = L;
+    }
   }
 }
 
 // ------------------------------------------------------------------ pool
 // Full-precision rows (anchors + window) on CUDA cores: a warp handles 4 rows
 // per step (32 lanes x 4 dims), all loads of the 4 rows in flight together.
-__device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, double pq, int b,
-                          int h, int ps, int pool_splits, int64_t row0, float *ws_o, float *ws_m,
-                          float *ws_l, MergeSmem &mg) {
+// Pool CTA 0 also attends the token being appended this step (its row has
+// not entered the pool yet: the reference appends before attending,
+// cache.py:162-178).
+__device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double pq, int b, int h,
+                          int ps, int64_t row0, MergeSmem &mg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bh = (int64_t)b * c.Hkv + h;
   const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-  const int per = (pool_high + pool_splits - 1) / pool_splits;
+  const int per = (pool_high + a.pool_splits - 1) / a.pool_splits;
   const int r0 = ps * per, r1 = min(pool_high, r0 + per);
   const int n = c.seq_len[b];
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
   // rotated, scaled query dims 4*lane..4*lane+3 (pairs 2*lane, 2*lane+1)
-  float qv[4][4];
+  float qv[4][4], qcs[2], qsn[2];
   const float scale = rsqrtf(128.f);
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
 #pragma unroll
   for (int hh = 0; hh < 4; ++hh) {
     const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
-      const float x0 = load_elem(q, qb + 2 * pp, qdtype), x1 = load_elem(q, qb + 2 * pp + 1, qdtype);
-      float cs, sn;
-      rope_cs(pq * tab->omega[2 * lane + pp], cs, sn);
-      qv[hh][2 * pp] = (x0 * cs - x1 * sn) * scale;
-      qv[hh][2 * pp + 1] = (x0 * sn + x1 * cs) * scale;
+      const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
+      qv[hh][2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
+      qv[hh][2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
     }
   }
   float m[4], l[4], acc[4][4];
@@ -177,6 +231,29 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
     l[hh] = 0.f;
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
+  }
+  if (ps == 0 && warp == 0 && a.knew) {
+    // the appended token at position p_q: K rotated in fp32 then rounded to
+    // fp16 like every pool K row; V rounded to the pool dtype
+    float kk[4], vv[4];
+    const int64_t kb = bh * 128 + 4 * lane;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const float x0 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp, a.kvdtype));
+      const float x1 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp + 1, a.kvdtype));
+      kk[2 * pp] = __half2float(__float2half_rn(x0 * qcs[pp] - x1 * qsn[pp]));
+      kk[2 * pp + 1] = __half2float(__float2half_rn(x0 * qsn[pp] + x1 * qcs[pp]));
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) vv[e] = round_to(c.row_dtype, load_elem(a.vnew, kb + e, a.kvdtype));
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) {
+      const float s = warp_sum(qv[hh][0] * kk[0] + qv[hh][1] * kk[1] + qv[hh][2] * kk[2] + qv[hh][3] * kk[3]);
+      m[hh] = s;
+      l[hh] = 1.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[hh][e] = vv[e];
+    }
   }
   const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
   const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
@@ -228,7 +305,6 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
       m[hh] = mx;
     }
   }
-  // merge the warps through shared memory: cols 0-3 used
 #pragma unroll
   for (int hh = 0; hh < 4; ++hh) {
 #pragma unroll
@@ -239,25 +315,7 @@ __device__ void pool_part(const antkv_cache_desc &c, const void *q, int qdtype, 
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) {
-    const int hh = i / 128, dim = i % 128;
-    float M = -INFINITY;
-    for (int w = 0; w < FK_WARPS; ++w) M = fmaxf(M, mg.m[w][hh]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      for (int w = 0; w < FK_WARPS; ++w) {
-        if (mg.m[w][hh] == -INFINITY) continue;
-        const float f = __expf(mg.m[w][hh] - M);
-        L += f * mg.l[w][hh];
-        O += f * mg.o[w][hh][dim];
-      }
-    }
-    ws_o[(row0 + hh) * 128 + dim] = O;
-    if (dim == 0) {
-      ws_m[row0 + hh] = M;
-      ws_l[row0 + hh] = L;
-    }
-  }
+  write_partial_merged(mg, 1, row0, a);
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -306,10 +364,8 @@ __device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint3
   const float s1 = valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY;
   const float mn0 = fmaxf(w.mrun[0], shfl_max_g(s0));
   const float mn1 = fmaxf(w.mrun[1], shfl_max_g(s1));
-  const float al0 = ex2(w.mrun[0] - mn0);     // -inf - -inf guarded below
-  const float al1 = ex2(w.mrun[1] - mn1);
-  const float a0 = (w.mrun[0] == mn0) ? 1.f : al0;
-  const float a1 = (w.mrun[1] == mn1) ? 1.f : al1;
+  const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
+  const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
   const float p0 = valid ? ex2(s0 - mn0) : 0.f;
   const float p1 = valid ? ex2(s1 - mn1) : 0.f;
   w.lrun[0] = w.lrun[0] * a0 + shfl_sum_g(p0);
@@ -344,32 +400,19 @@ __device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint3
   }
 }
 
-// ----------------------------------------------------------------- codes
-__global__ void __launch_bounds__(FK_THREADS, 2)
-decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
-                   const int64_t *__restrict__ qpos, int code_splits, int pool_splits,
-                   float *__restrict__ ws_o, float *__restrict__ ws_m, float *__restrict__ ws_l) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
-  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
-  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
+__device__ void code_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm,
+                          MergeSmem &mg, double pq, int b, int h, int split, int64_t row0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t bh = (int64_t)b * c.Hkv + h;
-  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
-  const double pq = static_cast<double>(qpos[b]);
-  if (split >= code_splits) {
-    pool_part(c, q, qdtype, pq, b, h, split - code_splits, pool_splits, row0, ws_o, ws_m, ws_l, mg);
-    return;
-  }
-  // ---- work range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
+  // work range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
   const int n = c.seq_len[b];
   const int ntiles = (n + 15) >> 4;
-  const int per_cta = (((ntiles + code_splits - 1) / code_splits) + 2 * FK_WARPS - 1) /
+  const int per_cta = (((ntiles + a.code_splits - 1) / a.code_splits) + 2 * FK_WARPS - 1) /
                       (2 * FK_WARPS) * (2 * FK_WARPS);
   const int T0 = split * per_cta;
   if (T0 >= ntiles) {
-    write_empty_partial(row0, ws_o, ws_m, ws_l);
+    write_partial_empty(row0, a);
     return;
   }
   const int Tw = per_cta / FK_WARPS;           // even; tiles per warp
@@ -380,7 +423,7 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
   const int cap_tiles = c.capacity / 16;
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
 
-  // ---- setup: barriers; TMA: replicated codebooks + first code stages
+  // barriers; TMA: replicated codebooks + first code stages
   if (threadIdx.x == 0) {
     for (int s = 0; s < FK_STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -412,7 +455,7 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
   }
-  // ---- per-lane constants (tables prepared once per cache)
+  // per-lane constants (tables prepared once per cache)
   WarpState w;
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
@@ -435,8 +478,8 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int pair = 8 * s + 4 * u + t, k = 2 * s + u;
-        const float x0 = load_elem(q, qb + 2 * pair, qdtype) * scale;
-        const float x1 = load_elem(q, qb + 2 * pair + 1, qdtype) * scale;
+        const float x0 = load_elem(a.q, qb + 2 * pair, a.qdtype) * scale;
+        const float x1 = load_elem(a.q, qb + 2 * pair + 1, a.qdtype) * scale;
         float cs, sn;
         rope_cs(delta * tab->omega[pair], cs, sn);
         w.fx[k] = x0 * cs - x1 * sn;
@@ -479,7 +522,7 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
       issue(st + FK_STAGES);
     }
   }
-  // ---- merge 4 warps x 2 streams -> partial for 4 heads (natural-log units)
+  // merge 4 warps x 2 streams (natural-log units)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
   const float ln2 = 0.6931471805599453f;
 #pragma unroll
@@ -496,29 +539,193 @@ decode_fast_kernel(antkv_cache_desc c, const void *__restrict__ q, int qdtype,
     mg.l[warp][2 * t + 1] = w.lrun[1];
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
-    const int hh = i / 128, dim = i % 128;
-    float M = -INFINITY;
-    for (int ww = 0; ww < FK_WARPS; ++ww)
-      M = fmaxf(M, fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]));
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      for (int ww = 0; ww < FK_WARPS; ++ww) {
-#pragma unroll
-        for (int sidx = 0; sidx < 2; ++sidx) {
-          const int col = hh + 4 * sidx;
-          const float mv = mg.m[ww][col];
-          if (mv == -INFINITY) continue;
-          const float f = __expf(mv - M);
-          L += f * mg.l[ww][col];
-          O += f * mg.o[ww][col][dim];
-        }
+  write_partial_merged(mg, 2, row0, a);
+}
+
+// Append the step's token to head (b, h) and evict the oldest window row
+// (cache.py:162-166, 180-193).  Runs in the last CTA of (b, h), after every
+// CTA of that head has finished reading the cache.
+__device__ void append_evict(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm, int b,
+                             int h, int n, double pq) {
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  if (threadIdx.x == 0) {
+    const int top = hs[ANTKV_HS_FREE_TOP] - 1;
+    const int slot = top >= 0 ? c.free_stack[bh * c.pool_capacity + top] : -1;
+    if (slot >= 0) {
+      hs[ANTKV_HS_FREE_TOP] = top;
+      c.pool_tok[bh * c.pool_capacity + slot] = n;
+      c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_WINDOWED;
+      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+      ring[(hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % (c.window_size + 1)] = slot;
+      hs[ANTKV_HS_WIN_COUNT] += 1;
+      if (slot + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot + 1;
+    }
+    sm.app_slot = slot;
+  }
+  __syncthreads();
+  const int slot = sm.app_slot;
+  if (slot >= 0) {
+    const int64_t dst = (bh * c.pool_capacity + slot) * 256;
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+      const float kx = load_elem(a.knew, bh * 128 + t, a.kvdtype);
+      store_elem(c.pool_rows, dst + t, c.row_dtype, kx);
+      store_elem(c.pool_rows, dst + 128 + t, c.row_dtype, load_elem(a.vnew, bh * 128 + t, a.kvdtype));
+    }
+    const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
+    for (int p = threadIdx.x; p < 64; p += blockDim.x) {
+      const float x0 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p, a.kvdtype));
+      const float x1 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p + 1, a.kvdtype));
+      float cs, sn;
+      rope_cs(pq * tab->omega[p], cs, sn);
+      __half *kr = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * 128;
+      kr[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
+      kr[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
+    }
+  }
+  // eviction decision
+  if (threadIdx.x == 0) {
+    sm.ev_encode = 0;
+    if (hs[ANTKV_HS_WIN_COUNT] > c.window_size) {
+      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+      const int es = ring[hs[ANTKV_HS_WIN_HEAD]];
+      hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % (c.window_size + 1);
+      hs[ANTKV_HS_WIN_COUNT] -= 1;
+      const int budget = budget_for((int64_t)n + 1 + c.token_offset, c.anchor_count, c.anchor_fraction);
+      if (hs[ANTKV_HS_ANCHORS] < budget) {
+        c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_ANCHOR;
+        hs[ANTKV_HS_ANCHORS] += 1;
+      } else {
+        sm.ev_slot = es;
+        sm.ev_encode = 1;
       }
     }
-    ws_o[(row0 + hh) * 128 + dim] = O;
-    if (dim == 0) {
-      ws_m[row0 + hh] = M;
-      ws_l[row0 + hh] = L;
+  }
+  __syncthreads();
+  if (!sm.ev_encode) return;
+  const int es = sm.ev_slot;
+  const int j = c.pool_tok[bh * c.pool_capacity + es];
+  float *sx = reinterpret_cast<float *>(&sm.ring[0][0]);   // [2][128]
+  float *scb = sx + 256;                                     // [2][256][8] fp32
+  const int64_t row = (bh * c.pool_capacity + es) * 256;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sx[i] = load_elem(c.pool_rows, row + i, c.row_dtype);
+  const float *gk = c.codebook_k + (int64_t)h * c.m * 8, *gv = c.codebook_v + (int64_t)h * c.m * 8;
+  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
+    scb[i] = i < c.m * 8 ? gk[i] : INFINITY;
+    scb[2048 + i] = i < c.m * 8 ? gv[i] : INFINITY;
+  }
+  __syncthreads();
+  // 32 units (kv, group) x 4 threads, each scanning 64 centroids in order
+  const int u = threadIdx.x >> 2, part = threadIdx.x & 3;
+  const int kv = u >> 4, grp = u & 15;
+  const float *x = sx + kv * 128 + grp * 8;
+  const float *cb = scb + kv * 2048;
+  float best = INFINITY;
+  int best_i = 0x7fffffff;
+  for (int ci = part * 64; ci < part * 64 + 64 && ci < c.m; ++ci) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float df = x[e] - cb[ci * 8 + e];
+      s = fmaf(df, df, s);
+    }
+    if (s < best) { best = s; best_i = ci; }
+  }
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+    if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
+  }
+  if (part == 0)
+    c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
+    c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_FREE;
+    c.pool_tok[bh * c.pool_capacity + es] = -1;
+    c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = es;
+    hs[ANTKV_HS_FREE_TOP] += 1;
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+__global__ void __launch_bounds__(FK_THREADS, 2)
+decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
+  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
+  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  const int S = a.code_splits + a.pool_splits;
+  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
+  const double pq = static_cast<double>(a.qpos[b]);
+  const int n = c.seq_len[b];
+  if (split >= a.code_splits) pool_part(c, a, pq, b, h, split - a.code_splits, row0, mg);
+  else code_part(c, a, sm, mg, pq, b, h, split, row0);
+
+  // ---- ticket: the last CTA of (b, h) combines the partials and updates the cache
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
+  __syncthreads();
+  if (sm.ticket != S - 1) return;
+  __threadfence();
+  const int64_t rows = (int64_t)c.B * c.Hq;
+  float *wts = reinterpret_cast<float *>(&sm.ring[0][0]);      // [S][4] weights
+  float *hdr = wts + 4 * S;                                    // [4] M, [4] L
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  {
+    // warp hh: max / normaliser over splits for head hh
+    const int hh = warp;
+    const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
+    float M = -INFINITY;
+    for (int s = lane; s < S; s += 32) M = fmaxf(M, __ldcg(a.ws_m + s * rows + row));
+    M = warp_max(M);
+    float L = 0.f;
+    for (int s = lane; s < S; s += 32) {
+      const float ms = __ldcg(a.ws_m + s * rows + row);
+      const float wv = (ms == -INFINITY) ? 0.f : __expf(ms - M);
+      wts[s * 4 + hh] = wv;
+      L += wv * __ldcg(a.ws_l + s * rows + row);
+    }
+    L = warp_sum(L);
+    if (lane == 0) {
+      hdr[hh] = M;
+      hdr[4 + hh] = L;
+      if (a.lse) a.lse[row] = M + logf(L);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
+    const int hh = i / 128, dim = i % 128;
+    const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int s = 0;
+    for (; s + 4 <= S; s += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        acc[u] = fmaf(wts[(s + u) * 4 + hh], __ldcg(a.ws_o + ((s + u) * rows + row) * 128 + dim), acc[u]);
+    }
+    for (; s < S; ++s) acc[0] = fmaf(wts[s * 4 + hh], __ldcg(a.ws_o + (s * rows + row) * 128 + dim), acc[0]);
+    a.out[row * 128 + dim] = (acc[0] + acc[1] + acc[2] + acc[3]) / hdr[4 + hh];
+  }
+  __syncthreads();
+  if (a.knew) append_evict(c, a, sm, b, h, n, pq);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.cnt[bh] = 0;
+    if (a.knew) {
+      // the last head of sequence b publishes the new length / position
+      int *cb = a.cnt + (int64_t)c.B * c.Hkv + b;
+      if (atomicAdd(cb, 1) == c.Hkv - 1) {
+        c.positions[(int64_t)b * c.capacity + n] = a.qpos[b];
+        __threadfence();
+        c.seq_len[b] = n + 1;
+        *cb = 0;
+      }
     }
   }
 }
@@ -543,17 +750,31 @@ void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits
   if (code_splits < min_code) code_splits = min_code;
 }
 
-int decode_fast_launch(const antkv_cache_desc &c, const void *q, int dtype, const int64_t *qpos,
-                       float *ws_o, float *ws_m, float *ws_l, int splits, cudaStream_t st) {
-  int code_splits, pool_splits;
-  decode_fast_plan(c, splits, code_splits, pool_splits);
+// One fused launch: attention over the cache (+ the appended token), LSE
+// combine of the splits, and (when knew != NULL) append + evict.
+int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
+                       const void *vnew, int kvdtype, const int64_t *qpos, float *out, float *lse,
+                       float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
+                       cudaStream_t st) {
+  StepArgs a;
+  a.q = q;
+  a.knew = knew;
+  a.vnew = vnew;
+  a.qdtype = qdtype;
+  a.kvdtype = kvdtype;
+  a.qpos = qpos;
+  a.out = out;
+  a.lse = lse;
+  a.ws_o = ws_o;
+  a.ws_m = ws_m;
+  a.ws_l = ws_l;
+  a.cnt = cnt;
+  decode_fast_plan(c, splits, a.code_splits, a.pool_splits);
   const size_t smem = sizeof(FastSmem);
   cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid(code_splits + pool_splits, c.Hkv, c.B);
-  decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, q, dtype, qpos, code_splits, pool_splits,
-                                                     ws_o, ws_m, ws_l);
+  dim3 grid(a.code_splits + a.pool_splits, c.Hkv, c.B);
+  decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, a);
   ANTKV_LAUNCH_CHECK("decode_fast_kernel");
-  // splits beyond code_splits + pool_splits are left unused: mark them empty
   return ANTKV_OK;
 }
 
