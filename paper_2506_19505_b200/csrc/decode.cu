@@ -298,6 +298,11 @@ static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
 
 using namespace antkv;
 
+// tickets [B*Hkv] + [B] and the per-head cache-update plan [B*Hkv][4]
+static int64_t counter_bytes(const antkv_cache_desc &c) {
+  return (int64_t)(c.B * c.Hkv + c.B + 4 * c.B * c.Hkv) * 4;
+}
+
 static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
   return (int64_t)used * c.B * c.Hq * (c.d + 2) * (int64_t)sizeof(float);
 }
@@ -308,7 +313,7 @@ extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int s
   if (!c) return -1;
   int s = planned_splits(*c, splits, false);
   if (decode_fast_supported(*c)) s = max(s, planned_splits(*c, splits, true));
-  return partial_bytes(*c, s) + (int64_t)(c->B * c->Hkv + c->B) * 4 + 256;
+  return partial_bytes(*c, s) + counter_bytes(*c) + 256;
 }
 
 static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, const void *knew,
@@ -322,7 +327,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   float *wm = wo + (int64_t)used * rows * c->d;
   float *wl = wm + (int64_t)used * rows;
   int *cnt = reinterpret_cast<int *>(reinterpret_cast<char *>(workspace) + workspace_bytes -
-                                     256 - (int64_t)(c->B * c->Hkv + c->B) * 4);
+                                     256 - counter_bytes(*c));
   if (use_fast)
     return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
                               splits, st);

@@ -30,7 +30,7 @@ namespace antkv {
 
 constexpr int FK_WARPS = 4;
 constexpr int FK_THREADS = 32 * FK_WARPS;
-constexpr int FK_STAGES = 10;
+constexpr int FK_STAGES = 8;
 constexpr int FK_TILE_BYTES = 512;                       // K 256 B + V 256 B
 constexpr int FK_WARP_STAGE_BYTES = 2 * FK_TILE_BYTES;   // 2 tiles per warp per stage
 constexpr int FK_STAGE_BYTES = FK_WARPS * FK_WARP_STAGE_BYTES;
@@ -41,11 +41,13 @@ struct __align__(128) FastSmem {
   uint4 cbV[256 * 8];
   uint8_t ring[FK_STAGES][FK_STAGE_BYTES];
   uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
+  float po[FK_WARPS][4][128];                  // pool-row partials per warp (4 heads)
+  float pm[FK_WARPS][4], pl[FK_WARPS][4];
   unsigned long long full[FK_STAGES];
   unsigned long long empty[FK_STAGES];
   unsigned long long cbbar;
   int ticket;
-  int ev_slot, ev_encode, app_slot;
+  int upd[4];
 };
 
 struct MergeSmem {                             // aliases the ring after the loop
@@ -146,8 +148,9 @@ struct StepArgs {
   float *out;              // [B][Hq][128]
   float *lse;              // [B][Hq] or NULL
   float *ws_o, *ws_m, *ws_l;
-  int *cnt;                // [B*Hkv] CTA tickets + [B] head tickets (self-resetting)
-  int code_splits, pool_splits;
+  int *cnt;                // [B*Hkv] CTA tickets, [B] head tickets (self-resetting),
+                           // [B*Hkv][4] cache-update plan
+  int splits;              // CTAs per (b, head)
 };
 
 __device__ __forceinline__ float round_to(int dtype, float x) {
@@ -156,60 +159,24 @@ __device__ __forceinline__ float round_to(int dtype, float x) {
   return x;
 }
 
-__device__ void write_partial_empty(int64_t row0, const StepArgs &a) {
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) a.ws_o[row0 * 128 + i] = 0.f;
-  if (threadIdx.x < 4) {
-    a.ws_m[row0 + threadIdx.x] = -INFINITY;
-    a.ws_l[row0 + threadIdx.x] = 0.f;
-  }
-}
-
-// Merge per-warp (m, l, o) states (natural-log units) of `cols_per_head`
-// columns per head into this CTA's partial rows.
-__device__ void write_partial_merged(const MergeSmem &mg, int ncol_sets, int64_t row0,
-                                     const StepArgs &a) {
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) {
-    const int hh = i / 128, dim = i % 128;
-    float M = -INFINITY;
-    for (int w = 0; w < FK_WARPS; ++w)
-      for (int sidx = 0; sidx < ncol_sets; ++sidx) M = fmaxf(M, mg.m[w][hh + 4 * sidx]);
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      for (int w = 0; w < FK_WARPS; ++w) {
-        for (int sidx = 0; sidx < ncol_sets; ++sidx) {
-          const int col = hh + 4 * sidx;
-          const float mv = mg.m[w][col];
-          if (mv == -INFINITY) continue;
-          const float f = __expf(mv - M);
-          L += f * mg.l[w][col];
-          O += f * mg.o[w][col][dim];
-        }
-      }
-    }
-    a.ws_o[(row0 + hh) * 128 + dim] = O;
-    if (dim == 0) {
-      a.ws_m[row0 + hh] = M;
-      a.ws_l[row0 + hh] = L;
-    }
-  }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // ------------------------------------------------------------------ pool
-// Full-precision rows (anchors + window) on CUDA cores: a warp handles 4 rows
-// per step (32 lanes x 4 dims), all loads of the 4 rows in flight together.
-// Pool CTA 0 also attends the token being appended this step (its row has
-// not entered the pool yet: the reference appends before attending,
-// cache.py:162-178).
-__device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double pq, int b, int h,
-                          int ps, int64_t row0, MergeSmem &mg) {
+// Full-precision rows [r0, r1) of the pool (anchors + window) on CUDA cores:
+// a warp handles 4 rows per step (32 lanes x 4 dims), all loads of the 4
+// rows in flight together.  With `with_new` the token appended this step is
+// attended too (the reference appends before attending, cache.py:162-178).
+// Results (natural-log units) go to the per-warp pool area of shared memory.
+__device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm,
+                               double pq, int b, int h, int r0, int r1, bool with_new) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bh = (int64_t)b * c.Hkv + h;
-  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-  const int per = (pool_high + a.pool_splits - 1) / a.pool_splits;
-  const int r0 = ps * per, r1 = min(pool_high, r0 + per);
   const int n = c.seq_len[b];
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
-  // rotated, scaled query dims 4*lane..4*lane+3 (pairs 2*lane, 2*lane+1)
   float qv[4][4], qcs[2], qsn[2];
   const float scale = rsqrtf(128.f);
 #pragma unroll
@@ -232,9 +199,8 @@ __device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double p
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
   }
-  if (ps == 0 && warp == 0 && a.knew) {
-    // the appended token at position p_q: K rotated in fp32 then rounded to
-    // fp16 like every pool K row; V rounded to the pool dtype
+  if (with_new && warp == 0) {
+    // K rotated in fp32 then rounded to fp16 like every pool K row; V in the pool dtype
     float kk[4], vv[4];
     const int64_t kb = bh * 128 + 4 * lane;
 #pragma unroll
@@ -248,8 +214,7 @@ __device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double p
     for (int e = 0; e < 4; ++e) vv[e] = round_to(c.row_dtype, load_elem(a.vnew, kb + e, a.kvdtype));
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh) {
-      const float s = warp_sum(qv[hh][0] * kk[0] + qv[hh][1] * kk[1] + qv[hh][2] * kk[2] + qv[hh][3] * kk[3]);
-      m[hh] = s;
+      m[hh] = warp_sum(qv[hh][0] * kk[0] + qv[hh][1] * kk[1] + qv[hh][2] * kk[2] + qv[hh][3] * kk[3]);
       l[hh] = 1.f;
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[hh][e] = vv[e];
@@ -272,32 +237,32 @@ __device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double p
       for (int e = 0; e < 4; ++e)
         vv[u][e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
     }
-    float s[4][4];
+    float sc[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const float2 k01 = __half22float2(u2h(kraw[u].x)), k23 = __half22float2(u2h(kraw[u].y));
 #pragma unroll
       for (int hh = 0; hh < 4; ++hh)
-        s[u][hh] = qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y;
+        sc[u][hh] = qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int hh = 0; hh < 4; ++hh) s[u][hh] += __shfl_xor_sync(0xffffffffu, s[u][hh], o);
+        for (int hh = 0; hh < 4; ++hh) sc[u][hh] += __shfl_xor_sync(0xffffffffu, sc[u][hh], o);
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh) {
       float mx = m[hh];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) if (ok[u]) mx = fmaxf(mx, s[u][hh]);
+      for (int u = 0; u < 4; ++u) if (ok[u]) mx = fmaxf(mx, sc[u][hh]);
       const float al = (m[hh] == mx) ? 1.f : __expf(m[hh] - mx);
       l[hh] *= al;
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[hh][e] *= al;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float p = ok[u] ? __expf(s[u][hh] - mx) : 0.f;
+        const float p = ok[u] ? __expf(sc[u][hh] - mx) : 0.f;
         l[hh] += p;
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[hh][e] = fmaf(p, vv[u][e], acc[hh][e]);
@@ -307,21 +272,132 @@ __device__ void pool_part(const antkv_cache_desc &c, const StepArgs &a, double p
   }
 #pragma unroll
   for (int hh = 0; hh < 4; ++hh) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) mg.o[warp][hh][4 * lane + e] = acc[hh][e];
+    *reinterpret_cast<float4 *>(&sm.po[warp][hh][4 * lane]) =
+        make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
     if (lane == 0) {
-      mg.m[warp][hh] = m[hh];
-      mg.l[warp][hh] = l[hh];
+      sm.pm[warp][hh] = m[hh];
+      sm.pl[warp][hh] = l[hh];
     }
   }
-  __syncthreads();
-  write_partial_merged(mg, 1, row0, a);
 }
 
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
+// Cache-update plan of this step for head (b, h), prepared early by one CTA
+// while the others still read the cache (cache.py:162-166, 180-193):
+// the new token's rows go into the next free pool slot (still marked FREE,
+// so readers skip it) and, if the window overflows and the anchor budget is
+// exhausted, the oldest window row is encoded into its (still masked) code
+// slot.  plan = {new slot, evicted slot, action 0 none / 1 promote / 2 encode,
+// evicted token}; the last CTA of (b, h) commits it.
+__device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, int b, int h, int n,
+                               double pq) {
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  const int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  const int top = hs[ANTKV_HS_FREE_TOP];
+  const int slot_new = top > 0 ? c.free_stack[bh * c.pool_capacity + top - 1] : -1;
+  const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
+  if (slot_new >= 0) {
+    const int64_t dst = (bh * c.pool_capacity + slot_new) * 256;
+    __half *kr = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot_new) * 128;
+    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
+      store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(a.knew, bh * 128 + t, a.kvdtype));
+      store_elem(c.pool_rows, dst + 128 + t, c.row_dtype, load_elem(a.vnew, bh * 128 + t, a.kvdtype));
+    }
+    for (int p = threadIdx.x; p < 64; p += blockDim.x) {
+      const float x0 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p, a.kvdtype));
+      const float x1 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p + 1, a.kvdtype));
+      float cs, sn;
+      rope_cs(pq * tab->omega[p], cs, sn);
+      kr[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
+      kr[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
+    }
+  }
+  int es = -1, action = 0, j = -1;
+  if (slot_new >= 0 && hs[ANTKV_HS_WIN_COUNT] + 1 > c.window_size) {
+    es = hs[ANTKV_HS_WIN_COUNT] > 0 ? c.win_ring[bh * (c.window_size + 1) + hs[ANTKV_HS_WIN_HEAD]]
+                                     : slot_new;
+    j = es == slot_new ? n : c.pool_tok[bh * c.pool_capacity + es];
+    const int budget = budget_for((int64_t)n + 1 + c.token_offset, c.anchor_count, c.anchor_fraction);
+    action = hs[ANTKV_HS_ANCHORS] < budget ? 1 : 2;
+  }
+  if (action == 2) {
+    __syncthreads();   // the new row (if evicted itself) is visible to the block
+    // 32 units (kv, group) x 4 threads, each scanning 64 centroids in order;
+    // float32 distances, lowest index on ties (_ckernels.pyx:150-162)
+    const int64_t row = (bh * c.pool_capacity + es) * 256;
+    for (int base = 0; base < 32 * 4; base += blockDim.x) {
+      const int tid = base + threadIdx.x;
+      const int u = tid >> 2, part = tid & 3;
+      const int kv = u >> 4, grp = u & 15;
+      const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * 8;
+      float x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = load_elem(c.pool_rows, row + kv * 128 + grp * 8 + e, c.row_dtype);
+      float best = INFINITY;
+      int best_i = 0x7fffffff;
+      const int lo_c = part * 64, hi_c = min(c.m, lo_c + 64);
+      for (int ci = lo_c; ci < hi_c; ++ci) {
+        const float4 c0 = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8));
+        const float4 c1 = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8 + 4));
+        float s = 0.f, df;
+        df = x[0] - c0.x; s = fmaf(df, df, s);
+        df = x[1] - c0.y; s = fmaf(df, df, s);
+        df = x[2] - c0.z; s = fmaf(df, df, s);
+        df = x[3] - c0.w; s = fmaf(df, df, s);
+        df = x[4] - c1.x; s = fmaf(df, df, s);
+        df = x[5] - c1.y; s = fmaf(df, df, s);
+        df = x[6] - c1.z; s = fmaf(df, df, s);
+        df = x[7] - c1.w; s = fmaf(df, df, s);
+        if (s < best) { best = s; best_i = ci; }
+      }
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+        if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
+      }
+      if (part == 0)
+        c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * 4;
+    plan[0] = slot_new;
+    plan[1] = es;
+    plan[2] = action;
+    plan[3] = j;
+  }
+}
+
+// Commit the plan (last CTA of (b, h), every reader of the head is done).
+__device__ void commit_update(const antkv_cache_desc &c, const StepArgs &a, int b, int h, int n) {
+  const int64_t bh = (int64_t)b * c.Hkv + h;
+  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  const int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * 4;
+  const int slot_new = __ldcg(plan), es = __ldcg(plan + 1), action = __ldcg(plan + 2), j = __ldcg(plan + 3);
+  const int W1 = c.window_size + 1;
+  int32_t *ring = c.win_ring + bh * W1;
+  if (slot_new >= 0) {
+    hs[ANTKV_HS_FREE_TOP] -= 1;
+    c.pool_tok[bh * c.pool_capacity + slot_new] = n;
+    c.pool_kind[bh * c.pool_capacity + slot_new] = ANTKV_KIND_WINDOWED;
+    ring[(hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % W1] = slot_new;
+    hs[ANTKV_HS_WIN_COUNT] += 1;
+    if (slot_new + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot_new + 1;
+  }
+  if (action != 0) {
+    hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % W1;
+    hs[ANTKV_HS_WIN_COUNT] -= 1;
+    if (action == 1) {
+      c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_ANCHOR;
+      hs[ANTKV_HS_ANCHORS] += 1;
+    } else {
+      atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
+      c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_FREE;
+      c.pool_tok[bh * c.pool_capacity + es] = -1;
+      c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = es;
+      hs[ANTKV_HS_FREE_TOP] += 1;
+    }
+  }
 }
 
 // Per-warp streaming state for the code tiles.
@@ -400,30 +476,37 @@ __device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint3
   }
 }
 
-__device__ void code_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm,
-                          MergeSmem &mg, double pq, int b, int h, int split, int64_t row0) {
+// ---------------------------------------------------------------- kernel
+// Every CTA of (b, h) handles an equal share of the code tiles and of the
+// pool rows; the last split also attends the appended token and prepares the
+// cache update; the last CTA to finish combines the partials and commits.
+__global__ void __launch_bounds__(FK_THREADS, 2)
+decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
+  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
+  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
+  const int S = a.splits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t bh = (int64_t)b * c.Hkv + h;
-  // work range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
+  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
+  const double pq = static_cast<double>(a.qpos[b]);
   const int n = c.seq_len[b];
+  const bool last_split = split == S - 1;
+
+  // ---- code range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
   const int ntiles = (n + 15) >> 4;
-  const int per_cta = (((ntiles + a.code_splits - 1) / a.code_splits) + 2 * FK_WARPS - 1) /
-                      (2 * FK_WARPS) * (2 * FK_WARPS);
+  const int per_cta = (((ntiles + S - 1) / S) + 2 * FK_WARPS - 1) / (2 * FK_WARPS) * (2 * FK_WARPS);
   const int T0 = split * per_cta;
-  if (T0 >= ntiles) {
-    write_partial_empty(row0, a);
-    return;
-  }
   const int Tw = per_cta / FK_WARPS;           // even; tiles per warp
-  const int nstages = Tw / 2;
+  const int nstages = T0 < ntiles ? Tw / 2 : 0;
   const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
   const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
   const int cap_tiles = c.capacity / 16;
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
 
-  // barriers; TMA: replicated codebooks + first code stages
   if (threadIdx.x == 0) {
     for (int s = 0; s < FK_STAGES; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -443,30 +526,42 @@ __device__ void code_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem
                    FK_WARP_STAGE_BYTES, &sm.full[slot]);
     }
   };
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && nstages > 0) {
     const uint8_t *cbsrc = reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * 65536;
     mbar_expect_tx(&sm.cbbar, 65536);
     tma_bulk_g2s(&sm.cbK[0], cbsrc, 32768, &sm.cbbar);
     tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
   }
-  // qmask words of this warp's range: tiles [T0 + w*Tw, +Tw) -> Tw/2 32-slot words
+  // ---- while the first stages stream in: pool rows and the cache-update plan
+  {
+    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+    const int per = (pool_high + S - 1) / S;
+    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
+    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
+    if (last_split && a.knew) prepare_update(c, a, b, h, n, pq);
+  }
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
   }
-  // per-lane constants (tables prepared once per cache)
   WarpState w;
+  w.mrun[0] = w.mrun[1] = -INFINITY;
+  w.lrun[0] = w.lrun[1] = 0.f;
 #pragma unroll
-  for (int s = 0; s < 8; ++s) {
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int pair = 8 * s + 4 * u + t;
-      w.kc[s][2 * u] = tab->kc[g][pair][0];
-      w.kc[s][2 * u + 1] = tab->kc[g][pair][1];
+    for (int e = 0; e < 4; ++e) w.o[i][e] = 0.f;
+  if (nstages > 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int pair = 8 * s + 4 * u + t;
+        w.kc[s][2 * u] = tab->kc[g][pair][0];
+        w.kc[s][2 * u + 1] = tab->kc[g][pair][1];
+      }
     }
-  }
-  {
     // query frame: lanes 0-15 head g in group a's frame, 16-31 head g-4 in b's
     const int head = g & 3;
     const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 8 : 0);
@@ -488,41 +583,33 @@ __device__ void code_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem
         w.sts[k] = tab->step[pair][1];
       }
     }
-  }
-  w.mrun[0] = w.mrun[1] = -INFINITY;
-  w.lrun[0] = w.lrun[1] = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) w.o[i][e] = 0.f;
-
-  const uint32_t cbK_base = smem_u32(&sm.cbK[0]) + (lane & 7) * 16;
-  const uint32_t cbV_base = smem_u32(&sm.cbV[0]) + (lane & 7) * 16;
-  const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
-  const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
-  const uint32_t sel_k = (lane >> 4) ? 0x7531u : 0x6420u;
-  const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
-  const bool lo = t < 2;                                // owns group-a columns
-  const int rowbit = g + (lo ? 0 : 8);
-  __syncwarp();
-  mbar_wait(&sm.cbbar, 0);
-
-  for (int st = 0; st < nstages; ++st) {
-    const int slot = st % FK_STAGES;
-    mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
-    const uint32_t qw = sm.qm[warp][st];
-    const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
-    code_tile(w, tb, qw >> rowbit, cbK_base, cbV_base, tk, tv, sel_k, sel_v, lo);
-    code_tile(w, tb + FK_TILE_BYTES, qw >> (16 + rowbit), cbK_base, cbV_base, tk, tv, sel_k,
-              sel_v, lo);
+    const uint32_t cbK_base = smem_u32(&sm.cbK[0]) + (lane & 7) * 16;
+    const uint32_t cbV_base = smem_u32(&sm.cbV[0]) + (lane & 7) * 16;
+    const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
+    const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
+    const uint32_t sel_k = (lane >> 4) ? 0x7531u : 0x6420u;
+    const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
+    const bool lo = t < 2;                                // owns group-a columns
+    const int rowbit = g + (lo ? 0 : 8);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[slot]);
-    if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
-      mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
-      issue(st + FK_STAGES);
+    mbar_wait(&sm.cbbar, 0);
+    for (int st = 0; st < nstages; ++st) {
+      const int slot = st % FK_STAGES;
+      mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
+      const uint32_t qw = sm.qm[warp][st];
+      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
+      code_tile(w, tb, qw >> rowbit, cbK_base, cbV_base, tk, tv, sel_k, sel_v, lo);
+      code_tile(w, tb + FK_TILE_BYTES, qw >> (16 + rowbit), cbK_base, cbV_base, tk, tv, sel_k,
+                sel_v, lo);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[slot]);
+      if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
+        mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
+        issue(st + FK_STAGES);
+      }
     }
   }
-  // merge 4 warps x 2 streams (natural-log units)
+  // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
   const float ln2 = 0.6931471805599453f;
 #pragma unroll
@@ -539,133 +626,32 @@ __device__ void code_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem
     mg.l[warp][2 * t + 1] = w.lrun[1];
   }
   __syncthreads();
-  write_partial_merged(mg, 2, row0, a);
-}
-
-// Append the step's token to head (b, h) and evict the oldest window row
-// (cache.py:162-166, 180-193).  Runs in the last CTA of (b, h), after every
-// CTA of that head has finished reading the cache.
-__device__ void append_evict(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm, int b,
-                             int h, int n, double pq) {
-  const int64_t bh = (int64_t)b * c.Hkv + h;
-  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
-  if (threadIdx.x == 0) {
-    const int top = hs[ANTKV_HS_FREE_TOP] - 1;
-    const int slot = top >= 0 ? c.free_stack[bh * c.pool_capacity + top] : -1;
-    if (slot >= 0) {
-      hs[ANTKV_HS_FREE_TOP] = top;
-      c.pool_tok[bh * c.pool_capacity + slot] = n;
-      c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_WINDOWED;
-      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
-      ring[(hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % (c.window_size + 1)] = slot;
-      hs[ANTKV_HS_WIN_COUNT] += 1;
-      if (slot + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot + 1;
-    }
-    sm.app_slot = slot;
-  }
-  __syncthreads();
-  const int slot = sm.app_slot;
-  if (slot >= 0) {
-    const int64_t dst = (bh * c.pool_capacity + slot) * 256;
-    for (int t = threadIdx.x; t < 128; t += blockDim.x) {
-      const float kx = load_elem(a.knew, bh * 128 + t, a.kvdtype);
-      store_elem(c.pool_rows, dst + t, c.row_dtype, kx);
-      store_elem(c.pool_rows, dst + 128 + t, c.row_dtype, load_elem(a.vnew, bh * 128 + t, a.kvdtype));
-    }
-    const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
-    for (int p = threadIdx.x; p < 64; p += blockDim.x) {
-      const float x0 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p, a.kvdtype));
-      const float x1 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p + 1, a.kvdtype));
-      float cs, sn;
-      rope_cs(pq * tab->omega[p], cs, sn);
-      __half *kr = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * 128;
-      kr[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
-      kr[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
-    }
-  }
-  // eviction decision
-  if (threadIdx.x == 0) {
-    sm.ev_encode = 0;
-    if (hs[ANTKV_HS_WIN_COUNT] > c.window_size) {
-      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
-      const int es = ring[hs[ANTKV_HS_WIN_HEAD]];
-      hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % (c.window_size + 1);
-      hs[ANTKV_HS_WIN_COUNT] -= 1;
-      const int budget = budget_for((int64_t)n + 1 + c.token_offset, c.anchor_count, c.anchor_fraction);
-      if (hs[ANTKV_HS_ANCHORS] < budget) {
-        c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_ANCHOR;
-        hs[ANTKV_HS_ANCHORS] += 1;
-      } else {
-        sm.ev_slot = es;
-        sm.ev_encode = 1;
+  for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
+    const int hh = i / 128, dim = i % 128;
+    float M = -INFINITY;
+    for (int ww = 0; ww < FK_WARPS; ++ww)
+      M = fmaxf(M, fmaxf(fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]), sm.pm[ww][hh]));
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int ww = 0; ww < FK_WARPS; ++ww) {
+#pragma unroll
+        for (int src = 0; src < 3; ++src) {
+          const float mv = src < 2 ? mg.m[ww][hh + 4 * src] : sm.pm[ww][hh];
+          if (mv == -INFINITY) continue;
+          const float f = __expf(mv - M);
+          L += f * (src < 2 ? mg.l[ww][hh + 4 * src] : sm.pl[ww][hh]);
+          O += f * (src < 2 ? mg.o[ww][hh + 4 * src][dim] : sm.po[ww][hh][dim]);
+        }
       }
     }
-  }
-  __syncthreads();
-  if (!sm.ev_encode) return;
-  const int es = sm.ev_slot;
-  const int j = c.pool_tok[bh * c.pool_capacity + es];
-  float *sx = reinterpret_cast<float *>(&sm.ring[0][0]);   // [2][128]
-  float *scb = sx + 256;                                     // [2][256][8] fp32
-  const int64_t row = (bh * c.pool_capacity + es) * 256;
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) sx[i] = load_elem(c.pool_rows, row + i, c.row_dtype);
-  const float *gk = c.codebook_k + (int64_t)h * c.m * 8, *gv = c.codebook_v + (int64_t)h * c.m * 8;
-  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
-    scb[i] = i < c.m * 8 ? gk[i] : INFINITY;
-    scb[2048 + i] = i < c.m * 8 ? gv[i] : INFINITY;
-  }
-  __syncthreads();
-  // 32 units (kv, group) x 4 threads, each scanning 64 centroids in order
-  const int u = threadIdx.x >> 2, part = threadIdx.x & 3;
-  const int kv = u >> 4, grp = u & 15;
-  const float *x = sx + kv * 128 + grp * 8;
-  const float *cb = scb + kv * 2048;
-  float best = INFINITY;
-  int best_i = 0x7fffffff;
-  for (int ci = part * 64; ci < part * 64 + 64 && ci < c.m; ++ci) {
-    float s = 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float df = x[e] - cb[ci * 8 + e];
-      s = fmaf(df, df, s);
+    a.ws_o[(row0 + hh) * 128 + dim] = O;
+    if (dim == 0) {
+      a.ws_m[row0 + hh] = M;
+      a.ws_l[row0 + hh] = L;
     }
-    if (s < best) { best = s; best_i = ci; }
   }
-#pragma unroll
-  for (int o = 1; o < 4; o <<= 1) {
-    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-    if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
-  }
-  if (part == 0)
-    c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
-    c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_FREE;
-    c.pool_tok[bh * c.pool_capacity + es] = -1;
-    c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = es;
-    hs[ANTKV_HS_FREE_TOP] += 1;
-  }
-}
 
-// ---------------------------------------------------------------- kernel
-__global__ void __launch_bounds__(FK_THREADS, 2)
-decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
-  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
-  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
-  const int64_t bh = (int64_t)b * c.Hkv + h;
-  const int S = a.code_splits + a.pool_splits;
-  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
-  const double pq = static_cast<double>(a.qpos[b]);
-  const int n = c.seq_len[b];
-  if (split >= a.code_splits) pool_part(c, a, pq, b, h, split - a.code_splits, row0, mg);
-  else code_part(c, a, sm, mg, pq, b, h, split, row0);
-
-  // ---- ticket: the last CTA of (b, h) combines the partials and updates the cache
+  // ---- ticket: the last CTA of (b, h) combines the partials and commits
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
@@ -673,22 +659,20 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   if (sm.ticket != S - 1) return;
   __threadfence();
   const int64_t rows = (int64_t)c.B * c.Hq;
-  float *wts = reinterpret_cast<float *>(&sm.ring[0][0]);      // [S][4] weights
-  float *hdr = wts + 4 * S;                                    // [4] M, [4] L
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float *wts = reinterpret_cast<float *>(&sm.ring[0][0]);   // [S][4] (merge data consumed)
+  float *hdr = wts + 4 * S;                                       // [4] M, [4] L
   {
-    // warp hh: max / normaliser over splits for head hh
-    const int hh = warp;
+    const int hh = warp;   // warp hh: max / normaliser over splits for head hh
     const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
     float M = -INFINITY;
-    for (int s = lane; s < S; s += 32) M = fmaxf(M, __ldcg(a.ws_m + s * rows + row));
+    for (int s2 = lane; s2 < S; s2 += 32) M = fmaxf(M, __ldcg(a.ws_m + s2 * rows + row));
     M = warp_max(M);
     float L = 0.f;
-    for (int s = lane; s < S; s += 32) {
-      const float ms = __ldcg(a.ws_m + s * rows + row);
+    for (int s2 = lane; s2 < S; s2 += 32) {
+      const float ms = __ldcg(a.ws_m + s2 * rows + row);
       const float wv = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-      wts[s * 4 + hh] = wv;
-      L += wv * __ldcg(a.ws_l + s * rows + row);
+      wts[s2 * 4 + hh] = wv;
+      L += wv * __ldcg(a.ws_l + s2 * rows + row);
     }
     L = warp_sum(L);
     if (lane == 0) {
@@ -702,20 +686,18 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int hh = i / 128, dim = i % 128;
     const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int s = 0;
-    for (; s + 4 <= S; s += 4) {
+    int s2 = 0;
+    for (; s2 + 4 <= S; s2 += 4) {
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        acc[u] = fmaf(wts[(s + u) * 4 + hh], __ldcg(a.ws_o + ((s + u) * rows + row) * 128 + dim), acc[u]);
+        acc[u] = fmaf(wts[(s2 + u) * 4 + hh], __ldcg(a.ws_o + ((s2 + u) * rows + row) * 128 + dim), acc[u]);
     }
-    for (; s < S; ++s) acc[0] = fmaf(wts[s * 4 + hh], __ldcg(a.ws_o + (s * rows + row) * 128 + dim), acc[0]);
+    for (; s2 < S; ++s2) acc[0] = fmaf(wts[s2 * 4 + hh], __ldcg(a.ws_o + (s2 * rows + row) * 128 + dim), acc[0]);
     a.out[row * 128 + dim] = (acc[0] + acc[1] + acc[2] + acc[3]) / hdr[4 + hh];
   }
-  __syncthreads();
-  if (a.knew) append_evict(c, a, sm, b, h, n, pq);
-  __threadfence();
-  __syncthreads();
   if (threadIdx.x == 0) {
+    if (a.knew) commit_update(c, a, b, h, n);
+    __threadfence();
     a.cnt[bh] = 0;
     if (a.knew) {
       // the last head of sequence b publishes the new length / position
@@ -736,18 +718,15 @@ int decode_fast_supported(const antkv_cache_desc &c) {
          c.capacity % 128 == 0;
 }
 
-// Split plan shared with the workspace sizing: code CTAs + pool CTAs per
-// (sequence, head).  `requested` > 0 fixes the code CTAs per head.
+// CTAs per (sequence, head): ~2 resident CTAs per SM in total.
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits) {
-  // ~2 resident CTAs per SM in total; pool rows are ~1-2 % of the tokens but
-  // ~15 % of the bytes, so they get a few CTAs of their own
-  pool_splits = max(1, min(8, (c.pool_capacity + 319) / 320));
   const int bh = c.B * c.Hkv;
-  code_splits = requested > 0 ? requested : max(1, (2 * 148 + bh - 1) / bh - pool_splits);
-  // per-warp qmask staging caps a CTA at 4 warps x 128 tiles (see FK_MAX_WARP_WORDS)
+  code_splits = requested > 0 ? requested : max(1, (2 * 148) / bh);
+  // per-warp qmask staging caps a CTA at 4 warps x 128 tiles (FK_MAX_WARP_WORDS)
   const int cap_tiles = c.capacity / 16;
   const int min_code = (cap_tiles + 503) / 504;
   if (code_splits < min_code) code_splits = min_code;
+  pool_splits = 0;
 }
 
 // One fused launch: attention over the cache (+ the appended token), LSE
@@ -769,10 +748,12 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   a.ws_m = ws_m;
   a.ws_l = ws_l;
   a.cnt = cnt;
-  decode_fast_plan(c, splits, a.code_splits, a.pool_splits);
+  int cs, ps;
+  decode_fast_plan(c, splits, cs, ps);
+  a.splits = cs + ps;
   const size_t smem = sizeof(FastSmem);
   cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid(a.code_splits + a.pool_splits, c.Hkv, c.B);
+  dim3 grid(a.splits, c.Hkv, c.B);
   decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, a);
   ANTKV_LAUNCH_CHECK("decode_fast_kernel");
   return ANTKV_OK;
