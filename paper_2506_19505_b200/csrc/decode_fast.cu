@@ -222,12 +222,13 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
   }
   const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
   const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
-  for (int rb = r0 + 4 * warp; rb < r1; rb += 4 * FK_WARPS) {
-    bool ok[4];
-    uint2 kraw[4];
-    float vv[4][4];
+  constexpr int RB = 8;   // rows per warp per round (all loads in flight together)
+  for (int rb = r0 + RB * warp; rb < r1; rb += RB * FK_WARPS) {
+    bool ok[RB];
+    uint2 kraw[RB];
+    float vv[RB][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < RB; ++u) {
       const int r = min(rb + u, r1 - 1);
       const int8_t kind = c.pool_kind[bh * c.pool_capacity + r];
       const int tok = c.pool_tok[bh * c.pool_capacity + r];
@@ -237,9 +238,9 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
       for (int e = 0; e < 4; ++e)
         vv[u][e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
     }
-    float sc[4][4];
+    float sc[RB][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < RB; ++u) {
       const float2 k01 = __half22float2(u2h(kraw[u].x)), k23 = __half22float2(u2h(kraw[u].y));
 #pragma unroll
       for (int hh = 0; hh < 4; ++hh)
@@ -248,20 +249,20 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < RB; ++u)
 #pragma unroll
         for (int hh = 0; hh < 4; ++hh) sc[u][hh] += __shfl_xor_sync(0xffffffffu, sc[u][hh], o);
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh) {
       float mx = m[hh];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) if (ok[u]) mx = fmaxf(mx, sc[u][hh]);
+      for (int u = 0; u < RB; ++u) if (ok[u]) mx = fmaxf(mx, sc[u][hh]);
       const float al = (m[hh] == mx) ? 1.f : __expf(m[hh] - mx);
       l[hh] *= al;
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[hh][e] *= al;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < RB; ++u) {
         const float p = ok[u] ? __expf(sc[u][hh] - mx) : 0.f;
         l[hh] += p;
 #pragma unroll
@@ -409,19 +410,33 @@ struct WarpState {
   float o[8][4];          // O^T accumulators
 };
 
-// One 16-slot code tile: S^T = rot(K_hat) . frame (8 HMMA), masked online
-// softmax over the lane's 2 columns, O^T += V_hat^T . P (8 HMMA).
-__device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint32_t mbits,
-                                          uint32_t cbK_base, uint32_t cbV_base, int tk, int tv,
-                                          uint32_t sel_k, uint32_t sel_v, bool lo) {
+// Code records of one 16-slot tile for this lane: 8 K codes (groups 2s+pk)
+// and 8 V codes (groups 2mt+pv), packed 4 per word.
+struct TileCodes {
+  uint32_t k0, k1, v0, v1, mbits;
+};
+
+__device__ __forceinline__ TileCodes tile_codes(const uint8_t *tb, uint32_t mbits, int tk, int tv,
+                                                uint32_t sel_k, uint32_t sel_v) {
   const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
   const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
-  const uint32_t kq0 = __byte_perm(kr.x, kr.y, sel_k), kq1 = __byte_perm(kr.z, kr.w, sel_k);
-  const uint32_t vq0 = __byte_perm(vr.x, vr.y, sel_v), vq1 = __byte_perm(vr.z, vr.w, sel_v);
+  TileCodes tc;
+  tc.k0 = __byte_perm(kr.x, kr.y, sel_k);
+  tc.k1 = __byte_perm(kr.z, kr.w, sel_k);
+  tc.v0 = __byte_perm(vr.x, vr.y, sel_v);
+  tc.v1 = __byte_perm(vr.z, vr.w, sel_v);
+  tc.mbits = mbits;
+  return tc;
+}
+
+// S^T = rot(K_hat) . frame (8 HMMA in two chains); advances the frame.
+// Returns this lane's 2 scores (log2 units; -inf when masked).
+__device__ __forceinline__ float2 qk_tile(WarpState &w, const TileCodes &tc, uint32_t cbK_base,
+                                          bool lo) {
   float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const uint32_t word = s < 4 ? kq0 : kq1;
+    const uint32_t word = s < 4 ? tc.k0 : tc.k1;
     const uint32_t code = (word >> (8 * (s & 3))) & 0xffu;
     uint32_t a[4];
     ldsm_x4(cbK_base + code * 128, a);
@@ -434,16 +449,27 @@ __device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint3
     if (s & 1) mma16816(sb, a, b0, b1);
     else mma16816(sa, a, b0, b1);
   }
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const float x = w.fx[k], y = w.fy[k];
+    w.fx[k] = x * w.stc[k] - y * w.sts[k];
+    w.fy[k] = x * w.sts[k] + y * w.stc[k];
+  }
   // lanes t<2 own group-a rows (g) in cols 0-3, lanes t>=2 group-b rows (g+8)
-  const bool valid = mbits & 1u;
-  const float s0 = valid ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY;
-  const float s1 = valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY;
-  const float mn0 = fmaxf(w.mrun[0], shfl_max_g(s0));
-  const float mn1 = fmaxf(w.mrun[1], shfl_max_g(s1));
+  const bool valid = tc.mbits & 1u;
+  return make_float2(valid ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY,
+                     valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY);
+}
+
+// Online softmax over the lane's 2 columns; rescales O^T; returns the P
+// B-fragments (P[tokens][col g]) for the PV MMA.
+__device__ __forceinline__ uint2 softmax_tile(WarpState &w, float2 sc, bool lo) {
+  const float mn0 = fmaxf(w.mrun[0], shfl_max_g(sc.x));
+  const float mn1 = fmaxf(w.mrun[1], shfl_max_g(sc.y));
   const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
   const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
-  const float p0 = valid ? ex2(s0 - mn0) : 0.f;
-  const float p1 = valid ? ex2(s1 - mn1) : 0.f;
+  const float p0 = sc.x == -INFINITY ? 0.f : ex2(sc.x - mn0);
+  const float p1 = sc.y == -INFINITY ? 0.f : ex2(sc.y - mn1);
   w.lrun[0] = w.lrun[0] * a0 + shfl_sum_g(p0);
   w.lrun[1] = w.lrun[1] * a1 + shfl_sum_g(p1);
   w.mrun[0] = mn0;
@@ -458,21 +484,19 @@ __device__ __forceinline__ void code_tile(WarpState &w, const uint8_t *tb, uint3
     }
   }
   const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
-  const uint32_t pb0 = movm_t(lo ? ph : 0u);
-  const uint32_t pb1 = movm_t(lo ? 0u : ph);
+  return make_uint2(movm_t(lo ? ph : 0u), movm_t(lo ? 0u : ph));
+}
+
+// O^T += V_hat^T . P (8 independent HMMA).
+__device__ __forceinline__ void pv_tile(WarpState &w, uint32_t v0, uint32_t v1, uint2 pb,
+                                        uint32_t cbV_base) {
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
-    const uint32_t word = mt < 4 ? vq0 : vq1;
+    const uint32_t word = mt < 4 ? v0 : v1;
     const uint32_t code = (word >> (8 * (mt & 3))) & 0xffu;
     uint32_t a[4];
     ldsm_x4_t(cbV_base + code * 128, a);
-    mma16816(w.o[mt], a, pb0, pb1);
-  }
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const float x = w.fx[k], y = w.fy[k];
-    w.fx[k] = x * w.stc[k] - y * w.sts[k];
-    w.fy[k] = x * w.sts[k] + y * w.stc[k];
+    mma16816(w.o[mt], a, pb.x, pb.y);
   }
 }
 
@@ -593,21 +617,37 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int rowbit = g + (lo ? 0 : 8);
     __syncwarp();
     mbar_wait(&sm.cbbar, 0);
-    for (int st = 0; st < nstages; ++st) {
-      const int slot = st % FK_STAGES;
-      mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
+    // tiles i = 0 .. 2*nstages-1 of this warp; stage st = i/2 holds tiles 2st, 2st+1.
+    // Software pipeline: PV of tile i-1 is issued together with QK of tile i.
+    auto fetch = [&](int i) -> TileCodes {
+      const int st = i >> 1, slot = st % FK_STAGES;
+      if ((i & 1) == 0) mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
       const uint32_t qw = sm.qm[warp][st];
-      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
-      code_tile(w, tb, qw >> rowbit, cbK_base, cbV_base, tk, tv, sel_k, sel_v, lo);
-      code_tile(w, tb + FK_TILE_BYTES, qw >> (16 + rowbit), cbK_base, cbV_base, tk, tv, sel_k,
-                sel_v, lo);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[slot]);
-      if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
-        mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
-        issue(st + FK_STAGES);
+      const TileCodes tc = tile_codes(&sm.ring[slot][warp * FK_WARP_STAGE_BYTES + (i & 1) * FK_TILE_BYTES],
+                                      qw >> (16 * (i & 1) + rowbit), tk, tv, sel_k, sel_v);
+      if (i & 1) {   // both tiles' codes are in registers: release the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[slot]);
+        if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
+          mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
+          issue(st + FK_STAGES);
+        }
       }
+      return tc;
+    };
+    const int ntile = 2 * nstages;
+    TileCodes cur = fetch(0);
+    uint2 pb = softmax_tile(w, qk_tile(w, cur, cbK_base, lo), lo);
+    uint32_t pv0 = cur.v0, pv1 = cur.v1;
+    for (int i = 1; i < ntile; ++i) {
+      cur = fetch(i);
+      pv_tile(w, pv0, pv1, pb, cbV_base);
+      const float2 sc = qk_tile(w, cur, cbK_base, lo);
+      pb = softmax_tile(w, sc, lo);
+      pv0 = cur.v0;
+      pv1 = cur.v1;
     }
+    pv_tile(w, pv0, pv1, pb, cbV_base);
   }
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
