@@ -461,20 +461,23 @@ __device__ __forceinline__ float2 qk_tile(WarpState &w, const TileCodes &tc, uin
                      valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY);
 }
 
-// Online softmax over the lane's 2 columns; rescales O^T; returns the P
+// Online softmax over the lane's 2 columns with a lazily updated reference
+// max: P = 2^(s - mref) is exact for any mref; mref only has to be raised
+// (with an exact column max + rescale of O and l) when a score exceeds it by
+// more than 2^8, which keeps P <= 256 (well inside fp16).  The column sums
+// stay per lane and are reduced once at the end.  Returns the P
 // B-fragments (P[tokens][col g]) for the PV MMA.
 __device__ __forceinline__ uint2 softmax_tile(WarpState &w, float2 sc, bool lo) {
-  const float mn0 = fmaxf(w.mrun[0], shfl_max_g(sc.x));
-  const float mn1 = fmaxf(w.mrun[1], shfl_max_g(sc.y));
-  const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
-  const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
-  const float p0 = sc.x == -INFINITY ? 0.f : ex2(sc.x - mn0);
-  const float p1 = sc.y == -INFINITY ? 0.f : ex2(sc.y - mn1);
-  w.lrun[0] = w.lrun[0] * a0 + shfl_sum_g(p0);
-  w.lrun[1] = w.lrun[1] * a1 + shfl_sum_g(p1);
-  w.mrun[0] = mn0;
-  w.mrun[1] = mn1;
-  if (__any_sync(0xffffffffu, a0 != 1.f || a1 != 1.f)) {
+  const bool up = (sc.x > w.mrun[0] + 8.f) || (sc.y > w.mrun[1] + 8.f);
+  if (__any_sync(0xffffffffu, up)) {
+    const float mn0 = fmaxf(w.mrun[0], shfl_max_g(sc.x));
+    const float mn1 = fmaxf(w.mrun[1], shfl_max_g(sc.y));
+    const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
+    const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
+    w.lrun[0] *= a0;
+    w.lrun[1] *= a1;
+    w.mrun[0] = mn0;
+    w.mrun[1] = mn1;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       w.o[i][0] *= a0;
@@ -483,6 +486,10 @@ __device__ __forceinline__ uint2 softmax_tile(WarpState &w, float2 sc, bool lo) 
       w.o[i][3] *= a1;
     }
   }
+  const float p0 = sc.x == -INFINITY ? 0.f : ex2(sc.x - w.mrun[0]);
+  const float p1 = sc.y == -INFINITY ? 0.f : ex2(sc.y - w.mrun[1]);
+  w.lrun[0] += p0;     // per-lane partial column sums
+  w.lrun[1] += p1;
   const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
   return make_uint2(movm_t(lo ? ph : 0u), movm_t(lo ? 0u : ph));
 }
@@ -659,11 +666,12 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     mg.o[warp][2 * t][16 * mt + g + 8] = w.o[mt][2];
     mg.o[warp][2 * t + 1][16 * mt + g + 8] = w.o[mt][3];
   }
+  const float lsum0 = shfl_sum_g(w.lrun[0]), lsum1 = shfl_sum_g(w.lrun[1]);
   if (g == 0) {
     mg.m[warp][2 * t] = w.mrun[0] * ln2;
     mg.m[warp][2 * t + 1] = w.mrun[1] * ln2;
-    mg.l[warp][2 * t] = w.lrun[0];
-    mg.l[warp][2 * t + 1] = w.lrun[1];
+    mg.l[warp][2 * t] = lsum0;
+    mg.l[warp][2 * t + 1] = lsum1;
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
