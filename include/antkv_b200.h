@@ -184,7 +184,7 @@ typedef struct antkv_cache_desc {
                               groups of a 128-byte row (64 KB per head)     */
   uint16_t *pool_krot; /* fast path: fp16 [B][Hkv][pool_capacity][d] pool K
                           rows with RoPE applied at their positions          */
-  void *fast_tables;   /* fast path: 8192-byte RoPE constant tables         */
+  void *fast_tables;   /* fast path: 16384-byte RoPE constant tables        */
 } antkv_cache_desc;
 
 /* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */

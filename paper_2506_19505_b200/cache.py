@@ -150,7 +150,7 @@ class QuantizedKVCache:
         use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         if use_fast:
             t["cb_f16"] = torch.zeros((H, 2, 256, 64), dtype=torch.float16, device=dev)
-            t["fast_tables"] = torch.zeros((8192,), dtype=torch.uint8, device=dev)
+            t["fast_tables"] = torch.zeros((16384,), dtype=torch.uint8, device=dev)
             t["pool_krot"] = torch.zeros((B, H, P, d), dtype=torch.float16, device=dev)
         if old is not None:
             oc = old["positions"].shape[1]

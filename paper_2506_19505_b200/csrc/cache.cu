@@ -440,10 +440,10 @@ __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
       const double om = rope_freq(c.theta_base, i, 128);
       tab->omega[i] = om;
       float cs, sn;
-      rope_cs(-16.0 * om, cs, sn);
+      rope_cs(-32.0 * om, cs, sn);
       tab->step[i][0] = cs;
       tab->step[i][1] = sn;
-      for (int g = 0; g < 8; ++g) {
+      for (int g = 0; g < 16; ++g) {
         rope_cs((double)g * om, cs, sn);
         __half2 a = __floats2half2_rn(cs, sn), b = __floats2half2_rn(-sn, cs);
         tab->kc[g][i][0] = *reinterpret_cast<uint32_t *>(&a);

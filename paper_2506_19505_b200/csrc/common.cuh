@@ -102,11 +102,11 @@ __host__ __device__ __forceinline__ int64_t code_offset(int64_t slot, int kv, in
 
 // Fast-path RoPE constants for d = 128 (antkv_cache_desc::fast_tables).
 struct FastTables {
-  uint32_t kc[8][64][2];   // fp16x2 (cos, sin), (-sin, cos) of g*omega_i, g = 0..7
-  float step[64][2];       // cos, sin of -16*omega_i
+  uint32_t kc[16][64][2];  // fp16x2 (cos, sin), (-sin, cos) of r*omega_i, r = 0..15
+  float step[64][2];       // cos, sin of -32*omega_i (frame advance per tile pair)
   double omega[64];        // theta^(-2i/128)
 };
-static_assert(sizeof(FastTables) <= 8192, "fast tables");
+static_assert(sizeof(FastTables) <= 16384, "fast tables");
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 

@@ -401,23 +401,29 @@ __device__ void commit_update(const antkv_cache_desc &c, const StepArgs &a, int 
   }
 }
 
-// Per-warp streaming state for the code tiles.
+// Per-warp streaming state for the code tiles.  A stage holds an even and an
+// odd 16-slot tile; both are multiplied with ONE B fragment: columns 0-3 are
+// the 4 query heads in the even tile's frame R(p_q - P0) q (lanes 0-15),
+// columns 4-7 in the odd tile's frame R(p_q - P0 - 16) q (lanes 16-31).  Row r
+// of a tile is rotated by R(r), r = g or g + 8.  Even-tile scores are read
+// from columns 0-3 and odd-tile scores from 4-7, so the O^T columns 0-3 / 4-7
+// accumulate two independent streams merged at the end.
 struct WarpState {
-  uint32_t kc[8][4];      // key rotation constants for offset g
+  uint32_t kc[8][8];      // key rotation (cos,sin)/(-sin,cos) for rows g, g+8
   float fx[16], fy[16];   // query frame pairs (log2-scaled)
-  float stc[16], sts[16]; // R(-16) per pair
-  float mrun[2], lrun[2]; // online softmax of this lane's 2 columns (log2 units)
+  float stc[16], sts[16]; // R(-32) per pair
+  float mrun[2], lrun[2]; // softmax of this lane's 2 columns (log2 units; lrun per lane)
   float o[8][4];          // O^T accumulators
 };
 
 // Code records of one 16-slot tile for this lane: 8 K codes (groups 2s+pk)
 // and 8 V codes (groups 2mt+pv), packed 4 per word.
 struct TileCodes {
-  uint32_t k0, k1, v0, v1, mbits;
+  uint32_t k0, k1, v0, v1;
 };
 
-__device__ __forceinline__ TileCodes tile_codes(const uint8_t *tb, uint32_t mbits, int tk, int tv,
-                                                uint32_t sel_k, uint32_t sel_v) {
+__device__ __forceinline__ TileCodes tile_codes(const uint8_t *tb, int tk, int tv, uint32_t sel_k,
+                                                uint32_t sel_v) {
   const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
   const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
   TileCodes tc;
@@ -425,53 +431,75 @@ __device__ __forceinline__ TileCodes tile_codes(const uint8_t *tb, uint32_t mbit
   tc.k1 = __byte_perm(kr.z, kr.w, sel_k);
   tc.v0 = __byte_perm(vr.x, vr.y, sel_v);
   tc.v1 = __byte_perm(vr.z, vr.w, sel_v);
-  tc.mbits = mbits;
   return tc;
 }
 
-// S^T = rot(K_hat) . frame (8 HMMA in two chains); advances the frame.
-// Returns this lane's 2 scores (log2 units; -inf when masked).
-__device__ __forceinline__ float2 qk_tile(WarpState &w, const TileCodes &tc, uint32_t cbK_base,
-                                          bool lo) {
+// Shared-memory address of centroid `byte k of word` in a replicated codebook.
+__device__ __forceinline__ uint32_t cb_addr(uint32_t word, int k, uint32_t base) {
+  uint32_t code, addr;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(code) : "r"(word), "r"(0x4440 + k));
+  asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(addr) : "r"(code), "r"(base));
+  return addr;
+}
+
+// S^T = rot(K_hat) . B (8 HMMA in two chains); returns the 4 accumulators.
+__device__ __forceinline__ float4 qk_tile(const WarpState &w, const TileCodes &tc,
+                                          const uint32_t (&bq)[8][2], uint32_t cbK_base) {
   float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
-    const uint32_t word = s < 4 ? tc.k0 : tc.k1;
-    const uint32_t code = (word >> (8 * (s & 3))) & 0xffu;
     uint32_t a[4];
-    ldsm_x4(cbK_base + code * 128, a);
+    ldsm_x4(cb_addr(s < 4 ? tc.k0 : tc.k1, s & 3, cbK_base), a);
     a[0] = rot2(a[0], w.kc[s][0], w.kc[s][1]);
-    a[1] = rot2(a[1], w.kc[s][0], w.kc[s][1]);
-    a[2] = rot2(a[2], w.kc[s][2], w.kc[s][3]);
-    a[3] = rot2(a[3], w.kc[s][2], w.kc[s][3]);
-    const uint32_t b0 = h2u(__floats2half2_rn(w.fx[2 * s], w.fy[2 * s]));
-    const uint32_t b1 = h2u(__floats2half2_rn(w.fx[2 * s + 1], w.fy[2 * s + 1]));
-    if (s & 1) mma16816(sb, a, b0, b1);
-    else mma16816(sa, a, b0, b1);
+    a[1] = rot2(a[1], w.kc[s][2], w.kc[s][3]);
+    a[2] = rot2(a[2], w.kc[s][4], w.kc[s][5]);
+    a[3] = rot2(a[3], w.kc[s][6], w.kc[s][7]);
+    if (s & 1) mma16816(sb, a, bq[s][0], bq[s][1]);
+    else mma16816(sa, a, bq[s][0], bq[s][1]);
   }
+  return make_float4(sa[0] + sb[0], sa[1] + sb[1], sa[2] + sb[2], sa[3] + sb[3]);
+}
+
+// O^T += V_hat^T . P (8 independent HMMA).
+__device__ __forceinline__ void pv_tile(WarpState &w, const TileCodes &tc, uint32_t pb0,
+                                        uint32_t pb1, uint32_t cbV_base) {
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    uint32_t a[4];
+    ldsm_x4_t(cb_addr(mt < 4 ? tc.v0 : tc.v1, mt & 3, cbV_base), a);
+    mma16816(w.o[mt], a, pb0, pb1);
+  }
+}
+
+// One stage = even + odd tile.  `mrow` holds this lane's two row-valid bits
+// (row g in bit 0, row g+8 in bit 1) of the tile whose columns it owns.
+__device__ __forceinline__ void stage_tiles(WarpState &w, const TileCodes &te, const TileCodes &to,
+                                            uint32_t mrow, uint32_t cbK_base, uint32_t cbV_base,
+                                            bool lo) {
+  uint32_t bq[8][2];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    bq[s][0] = h2u(__floats2half2_rn(w.fx[2 * s], w.fy[2 * s]));
+    bq[s][1] = h2u(__floats2half2_rn(w.fx[2 * s + 1], w.fy[2 * s + 1]));
+  }
+  const float4 se = qk_tile(w, te, bq, cbK_base);
+  const float4 so = qk_tile(w, to, bq, cbK_base);
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const float x = w.fx[k], y = w.fy[k];
     w.fx[k] = x * w.stc[k] - y * w.sts[k];
     w.fy[k] = x * w.sts[k] + y * w.stc[k];
   }
-  // lanes t<2 own group-a rows (g) in cols 0-3, lanes t>=2 group-b rows (g+8)
-  const bool valid = tc.mbits & 1u;
-  return make_float2(valid ? (lo ? sa[0] + sb[0] : sa[2] + sb[2]) : -INFINITY,
-                     valid ? (lo ? sa[1] + sb[1] : sa[3] + sb[3]) : -INFINITY);
-}
-
-// Online softmax over the lane's 2 columns with a lazily updated reference
-// max: P = 2^(s - mref) is exact for any mref; mref only has to be raised
-// (with an exact column max + rescale of O and l) when a score exceeds it by
-// more than 2^8, which keeps P <= 256 (well inside fp16).  The column sums
-// stay per lane and are reduced once at the end.  Returns the P
-// B-fragments (P[tokens][col g]) for the PV MMA.
-__device__ __forceinline__ uint2 softmax_tile(WarpState &w, float2 sc, bool lo) {
-  const bool up = (sc.x > w.mrun[0] + 8.f) || (sc.y > w.mrun[1] + 8.f);
+  // this lane's scores: (row g, col 2t), (row g, 2t+1), (row g+8, 2t), (row g+8, 2t+1)
+  const float4 sv = lo ? se : so;
+  const bool v0 = mrow & 1u, v1 = mrow & 2u;
+  const float s00 = v0 ? sv.x : -INFINITY, s01 = v0 ? sv.y : -INFINITY;
+  const float s10 = v1 ? sv.z : -INFINITY, s11 = v1 ? sv.w : -INFINITY;
+  // lazily updated reference max (P <= 2^8 keeps fp16 safe); exact max + rescale on raise
+  const bool up = fmaxf(s00, s10) > w.mrun[0] + 8.f || fmaxf(s01, s11) > w.mrun[1] + 8.f;
   if (__any_sync(0xffffffffu, up)) {
-    const float mn0 = fmaxf(w.mrun[0], shfl_max_g(sc.x));
-    const float mn1 = fmaxf(w.mrun[1], shfl_max_g(sc.y));
+    const float mn0 = fmaxf(w.mrun[0], shfl_max_g(fmaxf(s00, s10)));
+    const float mn1 = fmaxf(w.mrun[1], shfl_max_g(fmaxf(s01, s11)));
     const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
     const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
     w.lrun[0] *= a0;
@@ -486,25 +514,14 @@ __device__ __forceinline__ uint2 softmax_tile(WarpState &w, float2 sc, bool lo) 
       w.o[i][3] *= a1;
     }
   }
-  const float p0 = sc.x == -INFINITY ? 0.f : ex2(sc.x - w.mrun[0]);
-  const float p1 = sc.y == -INFINITY ? 0.f : ex2(sc.y - w.mrun[1]);
-  w.lrun[0] += p0;     // per-lane partial column sums
-  w.lrun[1] += p1;
-  const uint32_t ph = h2u(__floats2half2_rn(p0, p1));
-  return make_uint2(movm_t(lo ? ph : 0u), movm_t(lo ? 0u : ph));
-}
-
-// O^T += V_hat^T . P (8 independent HMMA).
-__device__ __forceinline__ void pv_tile(WarpState &w, uint32_t v0, uint32_t v1, uint2 pb,
-                                        uint32_t cbV_base) {
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const uint32_t word = mt < 4 ? v0 : v1;
-    const uint32_t code = (word >> (8 * (mt & 3))) & 0xffu;
-    uint32_t a[4];
-    ldsm_x4_t(cbV_base + code * 128, a);
-    mma16816(w.o[mt], a, pb.x, pb.y);
-  }
+  const float p00 = v0 ? ex2(s00 - w.mrun[0]) : 0.f, p01 = v0 ? ex2(s01 - w.mrun[1]) : 0.f;
+  const float p10 = v1 ? ex2(s10 - w.mrun[0]) : 0.f, p11 = v1 ? ex2(s11 - w.mrun[1]) : 0.f;
+  w.lrun[0] += p00 + p10;
+  w.lrun[1] += p01 + p11;
+  const uint32_t x0 = h2u(__floats2half2_rn(p00, p01));   // P[row g][cols 2t, 2t+1]
+  const uint32_t x1 = h2u(__floats2half2_rn(p10, p11));   // P[row g+8][...]
+  pv_tile(w, te, movm_t(lo ? x0 : 0u), movm_t(lo ? x1 : 0u), cbV_base);
+  pv_tile(w, to, movm_t(lo ? 0u : x0), movm_t(lo ? 0u : x1), cbV_base);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -589,13 +606,15 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int pair = 8 * s + 4 * u + t;
-        w.kc[s][2 * u] = tab->kc[g][pair][0];
-        w.kc[s][2 * u + 1] = tab->kc[g][pair][1];
+        w.kc[s][4 * u] = tab->kc[g][pair][0];
+        w.kc[s][4 * u + 1] = tab->kc[g][pair][1];
+        w.kc[s][4 * u + 2] = tab->kc[g + 8][pair][0];
+        w.kc[s][4 * u + 3] = tab->kc[g + 8][pair][1];
       }
     }
-    // query frame: lanes 0-15 head g in group a's frame, 16-31 head g-4 in b's
+    // query frame: lanes 0-15 head g in the even tile's frame, 16-31 head g-4 in the odd's
     const int head = g & 3;
-    const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 8 : 0);
+    const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 16 : 0);
     const double delta = pq - static_cast<double>(pos0 + first_slot);
     const float scale = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
     const int64_t qb = ((int64_t)b * c.Hq + h * 4 + head) * 128;
@@ -620,41 +639,25 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
     const uint32_t sel_k = (lane >> 4) ? 0x7531u : 0x6420u;
     const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
-    const bool lo = t < 2;                                // owns group-a columns
-    const int rowbit = g + (lo ? 0 : 8);
+    const bool lo = t < 2;                                // owns the even tile's columns
+    const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >>7 above)
     __syncwarp();
     mbar_wait(&sm.cbbar, 0);
-    // tiles i = 0 .. 2*nstages-1 of this warp; stage st = i/2 holds tiles 2st, 2st+1.
-    // Software pipeline: PV of tile i-1 is issued together with QK of tile i.
-    auto fetch = [&](int i) -> TileCodes {
-      const int st = i >> 1, slot = st % FK_STAGES;
-      if ((i & 1) == 0) mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
-      const uint32_t qw = sm.qm[warp][st];
-      const TileCodes tc = tile_codes(&sm.ring[slot][warp * FK_WARP_STAGE_BYTES + (i & 1) * FK_TILE_BYTES],
-                                      qw >> (16 * (i & 1) + rowbit), tk, tv, sel_k, sel_v);
-      if (i & 1) {   // both tiles' codes are in registers: release the stage
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.empty[slot]);
-        if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
-          mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
-          issue(st + FK_STAGES);
-        }
+    for (int st = 0; st < nstages; ++st) {
+      const int slot = st % FK_STAGES;
+      mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
+      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
+      const TileCodes te = tile_codes(tb, tk, tv, sel_k, sel_v);
+      const TileCodes to = tile_codes(tb + FK_TILE_BYTES, tk, tv, sel_k, sel_v);
+      const uint32_t qw = sm.qm[warp][st] >> rowbit;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.empty[slot]);   // codes are in registers
+      if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
+        mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
+        issue(st + FK_STAGES);
       }
-      return tc;
-    };
-    const int ntile = 2 * nstages;
-    TileCodes cur = fetch(0);
-    uint2 pb = softmax_tile(w, qk_tile(w, cur, cbK_base, lo), lo);
-    uint32_t pv0 = cur.v0, pv1 = cur.v1;
-    for (int i = 1; i < ntile; ++i) {
-      cur = fetch(i);
-      pv_tile(w, pv0, pv1, pb, cbV_base);
-      const float2 sc = qk_tile(w, cur, cbK_base, lo);
-      pb = softmax_tile(w, sc, lo);
-      pv0 = cur.v0;
-      pv1 = cur.v1;
+      stage_tiles(w, te, to, (qw & 1u) | ((qw >> 7) & 2u), cbK_base, cbV_base, lo);
     }
-    pv_tile(w, pv0, pv1, pb, cbV_base);
   }
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
