@@ -336,19 +336,28 @@ __device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, int
       float best = INFINITY;
       int best_i = 0x7fffffff;
       const int lo_c = part * 64, hi_c = min(c.m, lo_c + 64);
-      for (int ci = lo_c; ci < hi_c; ++ci) {
-        const float4 c0 = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8));
-        const float4 c1 = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8 + 4));
-        float s = 0.f, df;
-        df = x[0] - c0.x; s = fmaf(df, df, s);
-        df = x[1] - c0.y; s = fmaf(df, df, s);
-        df = x[2] - c0.z; s = fmaf(df, df, s);
-        df = x[3] - c0.w; s = fmaf(df, df, s);
-        df = x[4] - c1.x; s = fmaf(df, df, s);
-        df = x[5] - c1.y; s = fmaf(df, df, s);
-        df = x[6] - c1.z; s = fmaf(df, df, s);
-        df = x[7] - c1.w; s = fmaf(df, df, s);
-        if (s < best) { best = s; best_i = ci; }
+      for (int c8 = lo_c; c8 < hi_c; c8 += 8) {
+        float4 cv[8][2];   // 8 centroids in flight per round
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ci = min(c8 + u, c.m - 1);
+          cv[u][0] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8));
+          cv[u][1] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8 + 4));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (c8 + u >= hi_c) break;
+          float s = 0.f, df;
+          df = x[0] - cv[u][0].x; s = fmaf(df, df, s);
+          df = x[1] - cv[u][0].y; s = fmaf(df, df, s);
+          df = x[2] - cv[u][0].z; s = fmaf(df, df, s);
+          df = x[3] - cv[u][0].w; s = fmaf(df, df, s);
+          df = x[4] - cv[u][1].x; s = fmaf(df, df, s);
+          df = x[5] - cv[u][1].y; s = fmaf(df, df, s);
+          df = x[6] - cv[u][1].z; s = fmaf(df, df, s);
+          df = x[7] - cv[u][1].w; s = fmaf(df, df, s);
+          if (s < best) { best = s; best_i = c8 + u; }
+        }
       }
 #pragma unroll
       for (int o = 1; o < 4; o <<= 1) {
@@ -581,14 +590,9 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
   }
-  // ---- while the first stages stream in: pool rows and the cache-update plan
-  {
-    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-    const int per = (pool_high + S - 1) / S;
-    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
-    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
-    if (last_split && a.knew) prepare_update(c, a, b, h, n, pq);
-  }
+  // the last split (smallest code share) prepares the cache update while the
+  // first stages stream in
+  if (last_split && a.knew) prepare_update(c, a, b, h, n, pq);
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
@@ -658,6 +662,13 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       }
       stage_tiles(w, te, to, (qw & 1u) | ((qw >> 7) & 2u), cbK_base, cbV_base, lo);
     }
+  }
+  // ---- pool rows (anchors + window) of this CTA's share
+  {
+    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+    const int per = (pool_high + S - 1) / S;
+    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
+    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
   }
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
