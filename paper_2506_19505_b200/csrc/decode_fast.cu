@@ -744,18 +744,30 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
-    const int hh = i / 128, dim = i % 128;
+  {
+    // thread = (head warp, 4 consecutive dims); 8 split rows in flight per round
+    const int hh = warp, d4 = 4 * lane;
     const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int s2 = 0;
-    for (; s2 + 4 <= S; s2 += 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s0 = 0; s0 < S; s0 += 8) {
+      float4 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        acc[u] = fmaf(wts[(s2 + u) * 4 + hh], __ldcg(a.ws_o + ((s2 + u) * rows + row) * 128 + dim), acc[u]);
+      for (int u = 0; u < 8; ++u) {
+        const int s2 = min(s0 + u, S - 1);
+        v[u] = __ldcg(reinterpret_cast<const float4 *>(a.ws_o + (s2 * rows + row) * 128 + d4));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float wv = (s0 + u < S) ? wts[(s0 + u) * 4 + hh] : 0.f;
+        acc.x = fmaf(wv, v[u].x, acc.x);
+        acc.y = fmaf(wv, v[u].y, acc.y);
+        acc.z = fmaf(wv, v[u].z, acc.z);
+        acc.w = fmaf(wv, v[u].w, acc.w);
+      }
     }
-    for (; s2 < S; ++s2) acc[0] = fmaf(wts[s2 * 4 + hh], __ldcg(a.ws_o + (s2 * rows + row) * 128 + dim), acc[0]);
-    a.out[row * 128 + dim] = (acc[0] + acc[1] + acc[2] + acc[3]) / hdr[4 + hh];
+    const float inv = 1.f / hdr[4 + hh];
+    *reinterpret_cast<float4 *>(a.out + row * 128 + d4) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   }
   if (threadIdx.x == 0) {
     if (a.knew) commit_update(c, a, b, h, n);
