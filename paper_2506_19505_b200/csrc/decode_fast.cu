@@ -24,6 +24,8 @@
 // shared-memory ring with cp.async.bulk (TMA bulk copies) and mbarriers.
 // Anchor / window rows (the full-precision pool) are handled by extra CTAs
 // on CUDA cores from fp16 pre-rotated K rows.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace antkv {
@@ -151,7 +153,19 @@ struct StepArgs {
   int *cnt;                // [B*Hkv] CTA tickets, [B] head tickets (self-resetting),
                            // [B*Hkv][4] cache-update plan
   int splits;              // CTAs per (b, head)
+  unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 __device__ __forceinline__ float round_to(int dtype, float x) {
   if (dtype == ANTKV_BF16) return __bfloat162float(__float2bfloat16_rn(x));
@@ -551,6 +565,8 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   const double pq = static_cast<double>(a.qpos[b]);
   const int n = c.seq_len[b];
   const bool last_split = split == S - 1;
+  unsigned long long tr[6];
+  if (a.trace && threadIdx.x == 0) tr[0] = gtimer();
 
   // ---- code range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
   const int ntiles = (n + 15) >> 4;
@@ -647,6 +663,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >>7 above)
     __syncwarp();
     mbar_wait(&sm.cbbar, 0);
+    if (a.trace && threadIdx.x == 0) tr[1] = gtimer();
     for (int st = 0; st < nstages; ++st) {
       const int slot = st % FK_STAGES;
       mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
@@ -664,6 +681,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   // ---- pool rows (anchors + window) of this CTA's share
+  if (a.trace && threadIdx.x == 0) tr[2] = gtimer();
   {
     const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
     const int per = (pool_high + S - 1) / S;
@@ -718,6 +736,16 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
   __syncthreads();
+  if (a.trace && threadIdx.x == 0) {
+    tr[3] = gtimer();
+    unsigned long long *o = a.trace + 8 * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    o[0] = smid() | ((unsigned long long)sm.ticket << 32);
+    o[1] = tr[0];
+    o[2] = tr[1];
+    o[3] = tr[2];
+    o[4] = tr[3];
+    o[5] = 0;
+  }
   if (sm.ticket != S - 1) return;
   __threadfence();
   const int64_t rows = (int64_t)c.B * c.Hq;
@@ -771,6 +799,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
   if (threadIdx.x == 0) {
     if (a.knew) commit_update(c, a, b, h, n);
+    if (a.trace) a.trace[8 * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) + 5] = gtimer();
     __threadfence();
     a.cnt[bh] = 0;
     if (a.knew) {
@@ -803,6 +832,36 @@ void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits
   pool_splits = 0;
 }
 
+static unsigned long long *g_trace = nullptr;
+static int g_trace_n = 0;
+static unsigned long long *debug_trace_buffer() {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char *e = getenv("ANTKV_TRACE");
+    enabled = e && e[0] == '1';
+    if (enabled) {
+      g_trace_n = 8 * 65536;
+      if (cudaMalloc(&g_trace, sizeof(unsigned long long) * g_trace_n) != cudaSuccess) g_trace = nullptr;
+    }
+  }
+  return g_trace;
+}
+
+}  // namespace antkv
+
+// Debug: copy the per-CTA timeline of the last traced fast-decode launch
+// (8 words per CTA: smid | ticket << 32, t_start, t_loop, t_pool, t_done,
+// t_committed) to host memory.  Returns the number of words copied.
+extern "C" int antkv_debug_trace(unsigned long long *host, int max_words) {
+  if (!antkv::g_trace) return 0;
+  const int n = max_words < antkv::g_trace_n ? max_words : antkv::g_trace_n;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, antkv::g_trace, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost);
+  return n;
+}
+
+namespace antkv {
+
 // One fused launch: attention over the cache (+ the appended token), LSE
 // combine of the splits, and (when knew != NULL) append + evict.
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
@@ -825,6 +884,7 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   int cs, ps;
   decode_fast_plan(c, splits, cs, ps);
   a.splits = cs + ps;
+  a.trace = debug_trace_buffer();
   const size_t smem = sizeof(FastSmem);
   cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(a.splits, c.Hkv, c.B);
