@@ -243,6 +243,10 @@ ANTKV_API int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *Kh
 ANTKV_API int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows,
                       int d, float *out, float *lse_out, void *stream);
 
+/* Debug: per-CTA timeline of the last fast-decode launch when the process
+ * runs with ANTKV_TRACE=1 (8 words per CTA); returns words copied. */
+ANTKV_API int antkv_debug_trace(unsigned long long *host, int max_words);
+
 /* Build the fast-path fp16 codebooks from codebook_k/v and the rotated
  * pool K rows for the rows currently held. */
 ANTKV_API int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream);

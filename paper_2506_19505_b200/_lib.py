@@ -66,6 +66,7 @@ _SIGS = {
     "antkv_cache_dequantize": (_i, [ctypes.POINTER(CacheDesc), _i, _vp, _vp, _vp]),
     "antkv_lse_combine": (_i, [_vp, _vp, _i, _i64, _i, _vp, _vp, _vp]),
     "antkv_cache_prepare_fast": (_i, [ctypes.POINTER(CacheDesc), _vp]),
+    "antkv_debug_trace": (_i, [_vp, _i]),
 }
 
 EXPORTED = tuple(_SIGS)
