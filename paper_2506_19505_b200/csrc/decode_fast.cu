@@ -236,7 +236,7 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
   }
   const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
   const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
-  constexpr int RB = 8;   // rows per warp per round (all loads in flight together)
+  constexpr int RB = 10;  // rows per warp per round (all loads in flight together)
   for (int rb = r0 + RB * warp; rb < r1; rb += RB * FK_WARPS) {
     bool ok[RB];
     uint2 kraw[RB];
@@ -303,8 +303,8 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
 // exhausted, the oldest window row is encoded into its (still masked) code
 // slot.  plan = {new slot, evicted slot, action 0 none / 1 promote / 2 encode,
 // evicted token}; the last CTA of (b, h) commits it.
-__device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, int b, int h, int n,
-                               double pq) {
+__device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm, int b,
+                               int h, int n, double pq) {
   const int64_t bh = (int64_t)b * c.Hkv + h;
   const int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
   const int top = hs[ANTKV_HS_FREE_TOP];
@@ -336,52 +336,78 @@ __device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, int
   }
   if (action == 2) {
     __syncthreads();   // the new row (if evicted itself) is visible to the block
-    // 32 units (kv, group) x 4 threads, each scanning 64 centroids in order;
-    // float32 distances, lowest index on ties (_ckernels.pyx:150-162)
+    // 32 units (kv, group) x 4 threads, each scanning 64 centroids of the fp16
+    // shared-memory codebook for a top-4 shortlist, then rescoring it with the
+    // float32 centroids: float32 distances, lowest index on ties
+    // (_ckernels.pyx:150-162; SURVEY.md §7 hard part 2: shortlist + exact
+    // rescore).
     const int64_t row = (bh * c.pool_capacity + es) * 256;
-    for (int base = 0; base < 32 * 4; base += blockDim.x) {
-      const int tid = base + threadIdx.x;
-      const int u = tid >> 2, part = tid & 3;
-      const int kv = u >> 4, grp = u & 15;
-      const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * 8;
-      float x[8];
+    const int u = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int kv = u >> 4, grp = u & 15;
+    float x[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = load_elem(c.pool_rows, row + kv * 128 + grp * 8 + e, c.row_dtype);
-      float best = INFINITY;
-      int best_i = 0x7fffffff;
-      const int lo_c = part * 64, hi_c = min(c.m, lo_c + 64);
-      for (int c8 = lo_c; c8 < hi_c; c8 += 8) {
-        float4 cv[8][2];   // 8 centroids in flight per round
+    for (int e = 0; e < 8; ++e) x[e] = load_elem(c.pool_rows, row + kv * 128 + grp * 8 + e, c.row_dtype);
+    const uint4 *cb16 = kv ? sm.cbV : sm.cbK;
+    float sd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
+    int si[4] = {0, 0, 0, 0};
+    const int lo_c = part * 64, hi_c = min(c.m, lo_c + 64);
+    for (int ci = lo_c; ci < hi_c; ++ci) {
+      const uint4 raw = cb16[ci * 8 + (threadIdx.x & 7)];
+      const float2 c01 = __half22float2(u2h(raw.x)), c23 = __half22float2(u2h(raw.y));
+      const float2 c45 = __half22float2(u2h(raw.z)), c67 = __half22float2(u2h(raw.w));
+      float d = 0.f, df;
+      df = x[0] - c01.x; d = fmaf(df, df, d);
+      df = x[1] - c01.y; d = fmaf(df, df, d);
+      df = x[2] - c23.x; d = fmaf(df, df, d);
+      df = x[3] - c23.y; d = fmaf(df, df, d);
+      df = x[4] - c45.x; d = fmaf(df, df, d);
+      df = x[5] - c45.y; d = fmaf(df, df, d);
+      df = x[6] - c67.x; d = fmaf(df, df, d);
+      df = x[7] - c67.y; d = fmaf(df, df, d);
+      if (d < sd[3]) {   // insert into the sorted top-4 (earlier index first on ties)
+        sd[3] = d;
+        si[3] = ci;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int ci = min(c8 + u, c.m - 1);
-          cv[u][0] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8));
-          cv[u][1] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8 + 4));
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          if (c8 + u >= hi_c) break;
-          float s = 0.f, df;
-          df = x[0] - cv[u][0].x; s = fmaf(df, df, s);
-          df = x[1] - cv[u][0].y; s = fmaf(df, df, s);
-          df = x[2] - cv[u][0].z; s = fmaf(df, df, s);
-          df = x[3] - cv[u][0].w; s = fmaf(df, df, s);
-          df = x[4] - cv[u][1].x; s = fmaf(df, df, s);
-          df = x[5] - cv[u][1].y; s = fmaf(df, df, s);
-          df = x[6] - cv[u][1].z; s = fmaf(df, df, s);
-          df = x[7] - cv[u][1].w; s = fmaf(df, df, s);
-          if (s < best) { best = s; best_i = c8 + u; }
+        for (int k = 3; k > 0; --k) {
+          if (sd[k] < sd[k - 1]) {
+            const float td = sd[k]; sd[k] = sd[k - 1]; sd[k - 1] = td;
+            const int ti = si[k]; si[k] = si[k - 1]; si[k - 1] = ti;
+          }
         }
       }
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-        if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
-      }
-      if (part == 0)
-        c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
     }
+    const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * 8;
+    float4 cv[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ci = si[k];
+      cv[k][0] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8));
+      cv[k][1] = __ldg(reinterpret_cast<const float4 *>(cb + ci * 8 + 4));
+    }
+    float best = INFINITY;
+    int best_i = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (sd[k] == INFINITY) continue;
+      float d = 0.f, df;
+      df = x[0] - cv[k][0].x; d = fmaf(df, df, d);
+      df = x[1] - cv[k][0].y; d = fmaf(df, df, d);
+      df = x[2] - cv[k][0].z; d = fmaf(df, df, d);
+      df = x[3] - cv[k][0].w; d = fmaf(df, df, d);
+      df = x[4] - cv[k][1].x; d = fmaf(df, df, d);
+      df = x[5] - cv[k][1].y; d = fmaf(df, df, d);
+      df = x[6] - cv[k][1].z; d = fmaf(df, df, d);
+      df = x[7] - cv[k][1].w; d = fmaf(df, df, d);
+      if (d < best || (d == best && si[k] < best_i)) { best = d; best_i = si[k]; }
+    }
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
+      if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
+    }
+    if (part == 0)
+      c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
   }
   if (threadIdx.x == 0) {
     int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * 4;
@@ -599,16 +625,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
                    FK_WARP_STAGE_BYTES, &sm.full[slot]);
     }
   };
-  if (threadIdx.x == 0 && nstages > 0) {
+  const bool prep = last_split && a.knew;
+  if (threadIdx.x == 0 && (nstages > 0 || prep)) {
     const uint8_t *cbsrc = reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * 65536;
     mbar_expect_tx(&sm.cbbar, 65536);
     tma_bulk_g2s(&sm.cbK[0], cbsrc, 32768, &sm.cbbar);
     tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
   }
-  // the last split (smallest code share) prepares the cache update while the
-  // first stages stream in
-  if (last_split && a.knew) prepare_update(c, a, b, h, n, pq);
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
@@ -663,6 +687,8 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >>7 above)
     __syncwarp();
     mbar_wait(&sm.cbbar, 0);
+    // the last split (smallest code share) prepares the cache update
+    if (prep) prepare_update(c, a, sm, b, h, n, pq);
     if (a.trace && threadIdx.x == 0) tr[1] = gtimer();
     for (int st = 0; st < nstages; ++st) {
       const int slot = st % FK_STAGES;
@@ -679,6 +705,10 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       }
       stage_tiles(w, te, to, (qw & 1u) | ((qw >> 7) & 2u), cbK_base, cbV_base, lo);
     }
+  }
+  if (nstages == 0 && prep) {
+    mbar_wait(&sm.cbbar, 0);
+    prepare_update(c, a, sm, b, h, n, pq);
   }
   // ---- pool rows (anchors + window) of this CTA's share
   if (a.trace && threadIdx.x == 0) tr[2] = gtimer();
