@@ -45,9 +45,11 @@ struct __align__(128) FastSmem {
   uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
   float po[FK_WARPS][4][128];                  // pool-row partials per warp (4 heads)
   float pm[FK_WARPS][4], pl[FK_WARPS][4];
+  float pq[32][20];                            // pool-path query per lane: qv[4][4], cos[2], sin[2]
   unsigned long long full[FK_STAGES];
   unsigned long long empty[FK_STAGES];
   unsigned long long cbbar;
+  unsigned long long pqbar;
   int ticket;
   int upd[4];
 };
@@ -192,18 +194,15 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
   const int n = c.seq_len[b];
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
   float qv[4][4], qcs[2], qsn[2];
-  const float scale = rsqrtf(128.f);
+  (void)tab;
 #pragma unroll
-  for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
+  for (int hh = 0; hh < 4; ++hh)
 #pragma unroll
-  for (int hh = 0; hh < 4; ++hh) {
-    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
+    for (int e = 0; e < 4; ++e) qv[hh][e] = sm.pq[lane][4 * hh + e];
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
-      qv[hh][2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
-      qv[hh][2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
-    }
+  for (int pp = 0; pp < 2; ++pp) {
+    qcs[pp] = sm.pq[lane][16 + pp];
+    qsn[pp] = sm.pq[lane][18 + pp];
   }
   float m[4], l[4], acc[4][4];
 #pragma unroll
@@ -248,9 +247,20 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
       const int tok = c.pool_tok[bh * c.pool_capacity + r];
       ok[u] = (rb + u < r1) && kind != ANTKV_KIND_FREE && tok >= 0 && tok < n;
       kraw[u] = *reinterpret_cast<const uint2 *>(krot + (int64_t)r * 128 + 4 * lane);
+      if (c.row_dtype == ANTKV_F32) {
+        const float4 f = *reinterpret_cast<const float4 *>(
+            reinterpret_cast<const float *>(c.pool_rows) + vbase + (int64_t)r * 256 + 4 * lane);
+        vv[u][0] = f.x; vv[u][1] = f.y; vv[u][2] = f.z; vv[u][3] = f.w;
+      } else {
+        const uint2 raw = *reinterpret_cast<const uint2 *>(
+            reinterpret_cast<const uint16_t *>(c.pool_rows) + vbase + (int64_t)r * 256 + 4 * lane);
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        vv[u][e] = load_elem(c.pool_rows, vbase + (int64_t)r * 256 + 4 * lane + e, c.row_dtype);
+        for (int e = 0; e < 4; ++e) {
+          const uint16_t hb = static_cast<uint16_t>((e < 2 ? raw.x : raw.y) >> (16 * (e & 1)));
+          vv[u][e] = c.row_dtype == ANTKV_BF16 ? bf16_bits_to_float(hb)
+                                               : __half2float(__ushort_as_half(hb));
+        }
+      }
     }
     float sc[RB][4];
 #pragma unroll
@@ -595,11 +605,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   if (a.trace && threadIdx.x == 0) tr[0] = gtimer();
 
   // ---- code range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
+  // the last split also prepares the cache update, so it gets half a share
   const int ntiles = (n + 15) >> 4;
-  const int per_cta = (((ntiles + S - 1) / S) + 2 * FK_WARPS - 1) / (2 * FK_WARPS) * (2 * FK_WARPS);
+  const float shares = (a.knew && S > 1) ? S - 0.5f : (float)S;
+  const int per_cta = ((int)ceilf(ntiles / shares) + 2 * FK_WARPS - 1) / (2 * FK_WARPS) * (2 * FK_WARPS);
   const int T0 = split * per_cta;
-  const int Tw = per_cta / FK_WARPS;           // even; tiles per warp
-  const int nstages = T0 < ntiles ? Tw / 2 : 0;
+  const int mine = max(0, min(per_cta, ntiles - T0));           // valid tiles of this CTA
+  const int Tw = ((mine + FK_WARPS - 1) / FK_WARPS + 1) & ~1;   // even; tiles per warp
+  const int nstages = Tw / 2;
   const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
   const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
@@ -612,6 +625,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       mbar_init(&sm.empty[s], FK_WARPS);
     }
     mbar_init(&sm.cbbar, 1);
+    mbar_init(&sm.pqbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -632,6 +646,30 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     tma_bulk_g2s(&sm.cbK[0], cbsrc, 32768, &sm.cbbar);
     tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
+  }
+  if (warp == 0) {
+    // pool-path query: rotated at p_q, scaled; dims 4*lane..4*lane+3 of the 4 heads
+    float qcs[2], qsn[2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
+    const float scale = rsqrtf(128.f);
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh) {
+      const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
+        sm.pq[lane][4 * hh + 2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
+        sm.pq[lane][4 * hh + 2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
+      }
+    }
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      sm.pq[lane][16 + pp] = qcs[pp];
+      sm.pq[lane][18 + pp] = qsn[pp];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.pqbar);   // release: the pool part waits on it
   }
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
@@ -716,6 +754,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
     const int per = (pool_high + S - 1) / S;
     const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
+    mbar_wait(&sm.pqbar, 0);
     pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
   }
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
