@@ -45,11 +45,9 @@ struct __align__(128) FastSmem {
   uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
   float po[FK_WARPS][4][128];                  // pool-row partials per warp (4 heads)
   float pm[FK_WARPS][4], pl[FK_WARPS][4];
-  float pq[32][20];                            // pool-path query per lane: qv[4][4], cos[2], sin[2]
   unsigned long long full[FK_STAGES];
   unsigned long long empty[FK_STAGES];
   unsigned long long cbbar;
-  unsigned long long pqbar;
   int ticket;
   int upd[4];
 };
@@ -194,15 +192,18 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
   const int n = c.seq_len[b];
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
   float qv[4][4], qcs[2], qsn[2];
-  (void)tab;
+  const float scale = rsqrtf(128.f);
 #pragma unroll
-  for (int hh = 0; hh < 4; ++hh)
+  for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) qv[hh][e] = sm.pq[lane][4 * hh + e];
+  for (int hh = 0; hh < 4; ++hh) {
+    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
 #pragma unroll
-  for (int pp = 0; pp < 2; ++pp) {
-    qcs[pp] = sm.pq[lane][16 + pp];
-    qsn[pp] = sm.pq[lane][18 + pp];
+    for (int pp = 0; pp < 2; ++pp) {
+      const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
+      qv[hh][2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
+      qv[hh][2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
+    }
   }
   float m[4], l[4], acc[4][4];
 #pragma unroll
@@ -625,7 +626,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       mbar_init(&sm.empty[s], FK_WARPS);
     }
     mbar_init(&sm.cbbar, 1);
-    mbar_init(&sm.pqbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -647,29 +647,13 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
     for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
   }
-  if (warp == 0) {
-    // pool-path query: rotated at p_q, scaled; dims 4*lane..4*lane+3 of the 4 heads
-    float qcs[2], qsn[2];
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
-    const float scale = rsqrtf(128.f);
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh) {
-      const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
-        sm.pq[lane][4 * hh + 2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
-        sm.pq[lane][4 * hh + 2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
-      }
-    }
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      sm.pq[lane][16 + pp] = qcs[pp];
-      sm.pq[lane][18 + pp] = qsn[pp];
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.pqbar);   // release: the pool part waits on it
+  // ---- pool rows (anchors + window) of this CTA's share, while the
+  // codebooks and the first code stages stream in
+  {
+    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+    const int per = (pool_high + S - 1) / S;
+    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
+    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
   }
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
@@ -748,15 +732,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     mbar_wait(&sm.cbbar, 0);
     prepare_update(c, a, sm, b, h, n, pq);
   }
-  // ---- pool rows (anchors + window) of this CTA's share
   if (a.trace && threadIdx.x == 0) tr[2] = gtimer();
-  {
-    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-    const int per = (pool_high + S - 1) / S;
-    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
-    mbar_wait(&sm.pqbar, 0);
-    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
-  }
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
   const float ln2 = 0.6931471805599453f;

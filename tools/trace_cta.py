@@ -41,14 +41,15 @@ def main():
     cnt = np.bincount(sm, minlength=148)
     print("CTAs per SM histogram", np.bincount(cnt))
     print(f"start  min {st.min():.1f} max {st.max():.1f} us")
-    print(f"loop0  min {lp.min():.1f} med {np.median(lp):.1f} max {lp.max():.1f}")
-    print(f"pool0  min {pl.min():.1f} med {np.median(pl):.1f} max {pl.max():.1f}")
+    lp = np.where(lp > 1e6, np.nan, lp); lp = np.where(lp < -1e6, np.nan, lp)
+    print(f"loop0  min {np.nanmin(lp):.1f} med {np.nanmedian(lp):.1f} max {np.nanmax(lp):.1f}")
+    print(f"loop1  min {pl.min():.1f} med {np.median(pl):.1f} max {pl.max():.1f}")
     print(f"done   min {dn.min():.1f} med {np.median(dn):.1f} max {dn.max():.1f}")
     last = a[:, 5] > 0
     print("commit (last CTAs):", np.round(cm[last], 1))
     order = np.argsort(-dn)[:8]
     for i in order:
-        print(f"  cta {i:3d} split {i % 37:2d} head {i // 37} sm {sm[i]:3d} start {st[i]:6.1f} loop {lp[i]:6.1f} pool {pl[i]:6.1f} done {dn[i]:6.1f}")
+        print(f"  cta {i:3d} split {i % 37:2d} head {i // 37} sm {sm[i]:3d} start {st[i]:6.1f} loop {lp[i]:6.1f} loopend {pl[i]:6.1f} done {dn[i]:6.1f}")
 
 
 if __name__ == "__main__":
