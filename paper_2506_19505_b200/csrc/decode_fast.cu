@@ -185,8 +185,10 @@ __device__ __forceinline__ float ex2(float x) {
 // rows in flight together.  With `with_new` the token appended this step is
 // attended too (the reference appends before attending, cache.py:162-178).
 // Results (natural-log units) go to the per-warp pool area of shared memory.
+template <typename AfterLoads>
 __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm,
-                               double pq, int b, int h, int r0, int r1, bool with_new) {
+                               double pq, int b, int h, int r0, int r1, bool with_new,
+                               AfterLoads after_loads) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t bh = (int64_t)b * c.Hkv + h;
   const int n = c.seq_len[b];
@@ -237,7 +239,12 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
   const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
   const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
   constexpr int RB = 10;  // rows per warp per round (all loads in flight together)
-  for (int rb = r0 + RB * warp; rb < r1; rb += RB * FK_WARPS) {
+  bool first = true;
+  for (int rb = r0 + RB * warp; first || rb < r1; rb += RB * FK_WARPS) {
+    if (rb >= r1) {   // no rows for this warp: still run the hook once
+      after_loads();
+      break;
+    }
     bool ok[RB];
     uint2 kraw[RB];
     float vv[RB][4];
@@ -262,6 +269,10 @@ __device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, Fas
                                                : __half2float(__ushort_as_half(hb));
         }
       }
+    }
+    if (first) {
+      after_loads();   // rows requested: now queue the bulk copies behind them
+      first = false;
     }
     float sc[RB][4];
 #pragma unroll
@@ -640,21 +651,39 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   };
   const bool prep = last_split && a.knew;
-  if (threadIdx.x == 0 && (nstages > 0 || prep)) {
-    const uint8_t *cbsrc = reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * 65536;
-    mbar_expect_tx(&sm.cbbar, 65536);
-    tma_bulk_g2s(&sm.cbK[0], cbsrc, 32768, &sm.cbbar);
-    tma_bulk_g2s(&sm.cbV[0], cbsrc + 32768, 32768, &sm.cbbar);
-    for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
-  }
-  // ---- pool rows (anchors + window) of this CTA's share, while the
-  // codebooks and the first code stages stream in
+  // ---- pool rows (anchors + window) of this CTA's share first: their loads
+  // are issued before the code-tile bulk copies that follow in the hook
   {
     const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
     const int per = (pool_high + S - 1) / S;
     const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
-    pool_rows_part(c, a, sm, pq, b, h, r0, r1, last_split && a.knew);
+    pool_rows_part(c, a, sm, pq, b, h, r0, r1, prep, [&]() {
+      if (threadIdx.x == 0)
+        for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
+    });
   }
+  // ---- replicated fp16 codebooks: row `code` holds the centroid in all 8
+  // 16-byte bank groups (copy 0 of the prepared global layout is read)
+  if (nstages > 0 || prep) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(c.codebook_f16) + (int64_t)h * 4096;
+    uint4 vk[2], vv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int code = threadIdx.x + u * FK_THREADS;
+      vk[u] = __ldg(src + code * 8);
+      vv[u] = __ldg(src + 2048 + code * 8);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int code = threadIdx.x + u * FK_THREADS;
+#pragma unroll
+      for (int cp = 0; cp < 8; ++cp) {
+        sm.cbK[code * 8 + ((cp + threadIdx.x) & 7)] = vk[u];
+        sm.cbV[code * 8 + ((cp + threadIdx.x) & 7)] = vv[u];
+      }
+    }
+  }
+  __syncthreads();
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
@@ -707,8 +736,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
     const bool lo = t < 2;                                // owns the even tile's columns
     const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >>7 above)
-    __syncwarp();
-    mbar_wait(&sm.cbbar, 0);
     // the last split (smallest code share) prepares the cache update
     if (prep) prepare_update(c, a, sm, b, h, n, pq);
     if (a.trace && threadIdx.x == 0) tr[1] = gtimer();
@@ -728,10 +755,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       stage_tiles(w, te, to, (qw & 1u) | ((qw >> 7) & 2u), cbK_base, cbV_base, lo);
     }
   }
-  if (nstages == 0 && prep) {
-    mbar_wait(&sm.cbbar, 0);
-    prepare_update(c, a, sm, b, h, n, pq);
-  }
+  if (nstages == 0 && prep) prepare_update(c, a, sm, b, h, n, pq);
   if (a.trace && threadIdx.x == 0) tr[2] = gtimer();
   // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
   __syncthreads();   // all stages consumed; the ring becomes merge scratch
