@@ -613,7 +613,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   const double pq = static_cast<double>(a.qpos[b]);
   const int n = c.seq_len[b];
   const bool last_split = split == S - 1;
-  unsigned long long tr[6];
+  unsigned long long tr[8];
   if (a.trace && threadIdx.x == 0) tr[0] = gtimer();
 
   // ---- code range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
@@ -662,6 +662,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
         for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
     });
   }
+  if (a.trace && threadIdx.x == 0) tr[4] = gtimer();
   // ---- replicated fp16 codebooks: row `code` holds the centroid in all 8
   // 16-byte bank groups (copy 0 of the prepared global layout is read)
   if (nstages > 0 || prep) {
@@ -684,6 +685,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   __syncthreads();
+  if (a.trace && threadIdx.x == 0) tr[5] = gtimer();
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
@@ -814,6 +816,8 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     o[3] = tr[2];
     o[4] = tr[3];
     o[5] = 0;
+    o[6] = tr[4];
+    o[7] = tr[5];
   }
   if (sm.ticket != S - 1) return;
   __threadfence();

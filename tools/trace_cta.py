@@ -45,6 +45,9 @@ def main():
     print(f"loop0  min {np.nanmin(lp):.1f} med {np.nanmedian(lp):.1f} max {np.nanmax(lp):.1f}")
     print(f"loop1  min {pl.min():.1f} med {np.median(pl):.1f} max {pl.max():.1f}")
     print(f"done   min {dn.min():.1f} med {np.median(dn):.1f} max {dn.max():.1f}")
+    pdone, cbdone = (a[:, 6] - t0) / 1e3, (a[:, 7] - t0) / 1e3
+    print(f"pool done min {pdone.min():.1f} med {np.median(pdone):.1f} max {pdone.max():.1f}")
+    print(f"cb done   min {cbdone.min():.1f} med {np.median(cbdone):.1f} max {cbdone.max():.1f}")
     last = a[:, 5] > 0
     print("commit (last CTAs):", np.round(cm[last], 1))
     order = np.argsort(-dn)[:8]
