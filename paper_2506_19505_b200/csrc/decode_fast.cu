@@ -154,6 +154,7 @@ struct StepArgs {
                            // [B*Hkv][4] cache-update plan
   int splits;              // CTAs per (b, head)
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
+  int debug_mode;              // ANTKV_DEBUG_MODE: 1 skip pool rows, 2 stop after setup
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -657,7 +658,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
     const int per = (pool_high + S - 1) / S;
     const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
-    pool_rows_part(c, a, sm, pq, b, h, r0, r1, prep, [&]() {
+    pool_rows_part(c, a, sm, pq, b, h, r0, (a.debug_mode & 1) ? r0 : r1, prep, [&]() {
       if (threadIdx.x == 0)
         for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
     });
@@ -686,6 +687,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
   __syncthreads();
   if (a.trace && threadIdx.x == 0) tr[5] = gtimer();
+  if (a.debug_mode & 2) return;
   for (int i = lane; i < Tw / 2; i += 32) {
     const int word = ((T0 + warp * Tw) >> 1) + i;
     sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
@@ -958,6 +960,14 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   decode_fast_plan(c, splits, cs, ps);
   a.splits = cs + ps;
   a.trace = debug_trace_buffer();
+  {
+    static int dm = -1;
+    if (dm < 0) {
+      const char *e = getenv("ANTKV_DEBUG_MODE");
+      dm = e ? atoi(e) : 0;
+    }
+    a.debug_mode = dm;
+  }
   const size_t smem = sizeof(FastSmem);
   cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(a.splits, c.Hkv, c.B);
