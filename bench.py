@@ -39,7 +39,7 @@ METRIC = "decode attn tok/s & HBM GB/s at 128K ctx, 1-bit VQ KV; encode tok/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--ctx", type=int, default=131072, help="context tokens per GPU")
@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--kernel", default="fast", choices=["fast", "generic"])
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     return p.parse_args()
 
@@ -106,7 +107,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.01)
 
     def __exit__(self, *a):
         self._stop.set()
@@ -138,7 +139,7 @@ def build_layers(args, rank, world, torch):
         cv = rng.standard_normal((HKV, vq.m, vq.d_sub)).astype(np.float32)
         cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), batch=args.batch,
                                  q_heads=HQ, fast=(args.kernel == "fast"), splits=args.splits,
-                                 capacity=n + args.steps + args.warmup + 64, token_offset=offset)
+                                 capacity=n + args.steps + args.warmup + 96, token_offset=offset)
         K = torch.randn((args.batch, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
         V = torch.randn((args.batch, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
         # anchors: the real top-k kernel on synthetic anchor scores; this
@@ -255,17 +256,41 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    use_graph = world == 1 and not args.no_graph
+    if use_graph:
+        # CUDA graphs: one step = the 32 per-layer decode kernels, replayed so
+        # host launch overhead is outside the measurement
+        q_st, k_st, v_st = qs[0].clone(), ks[0].clone(), vs[0].clone()
+        qpos_st = qpos[0].clone()
+        out_st = torch.empty((L, B, HQ, D), dtype=torch.float32, device="cuda")
+
+        def body():
+            for l in range(L):
+                caches[l].step_device(q_st[l], k_st[l], v_st[l], qpos_st, out_st[l])
+            qpos_st.add_(1)
+
+        body()                       # eager warm-up (lazy init), advances the caches by 1
+        torch.cuda.synchronize()
+        step_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(step_graph):
+            body()
+        run_step = step_graph.replay
+        advanced = 1
+    else:
+        def run_step_s(s):
+            for l in range(L):
+                layer_step(s, l, caches[l])
+        advanced = 0
+
     for s in range(args.warmup):
-        for l in range(L):
-            layer_step(s, l, caches[l])
+        run_step() if use_graph else run_step_s(s)
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         e0.record()
         for s in range(args.warmup, total_steps):
-            for l in range(L):
-                layer_step(s, l, caches[l])
+            run_step() if use_graph else run_step_s(s)
         e1.record()
         barrier()
     ms = e0.elapsed_time(e1) / args.steps
@@ -274,56 +299,80 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     for c in caches:
-        c._n += args.warmup + args.steps if is_tail else 0
+        c._n += (args.warmup + args.steps + advanced) if is_tail else 0
 
-    # attention-kernel-only timing on the same caches (no append/evict)
+    # attention-kernel-only timing on the same caches (no append/evict),
+    # graph-captured: per-launch device time of the decode-attention kernel
     reps = max(3, min(args.steps, 10))
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    qlast = qpos[-1]
+    qlast = (qpos_st if use_graph else qpos[-1]).clone()
     for l in range(L):
         caches[l].attend_device(qs[0, l], qlast, out)
     torch.cuda.synchronize()
+    if use_graph:
+        att_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(att_graph):
+            for l in range(L):
+                caches[l].attend_device(qs[0, l], qlast, out)
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record()
     for r in range(reps):
-        for l in range(L):
-            caches[l].attend_device(qs[r % total_steps, l], qlast, out)
+        if use_graph:
+            att_graph.replay()
+        else:
+            for l in range(L):
+                caches[l].attend_device(qs[r % total_steps, l], qlast, out)
     a1.record()
     torch.cuda.synchronize()
     attn_ms = a0.elapsed_time(a1) / (reps * L)
     alg_bytes = algorithmic_bytes(caches[0], torch)
 
-    # e2e through the public step API with pinned host buffers
-    qh = qs[: min(total_steps, 4)].cpu().pin_memory()
-    kh = ks[: min(total_steps, 4)].cpu().pin_memory()
-    vh = vs[: min(total_steps, 4)].cpu().pin_memory()
+    # e2e through the public step API with pinned host buffers: every step
+    # copies q/k/v of every layer host->device and the outputs device->host
+    qh = qs[0].cpu().pin_memory()
+    kh = ks[0].cpu().pin_memory()
+    vh = vs[0].cpu().pin_memory()
     outh = torch.empty((L, B, HQ, D), dtype=torch.float32).pin_memory()
-    dq = torch.empty_like(qs[0, 0])
-    dk = torch.empty_like(ks[0, 0])
-    dv = torch.empty_like(vs[0, 0])
     e2e_steps = max(3, min(args.steps, 8))
-    base = total_steps
-    cap_left = min(c.capacity for c in caches) - caches[0].token_count - 2
-    e2e_steps = min(e2e_steps, max(1, cap_left))
+    cap_left = min(c.capacity for c in caches) - caches[0].token_count - 4
+    e2e_steps = min(e2e_steps, max(1, cap_left - 1))
+    if use_graph:
+        dq, dk, dv, p_dev, o_dev = q_st, k_st, v_st, qpos_st, out_st
+    else:
+        dq, dk, dv = torch.empty_like(qs[0]), torch.empty_like(ks[0]), torch.empty_like(vs[0])
+        p_dev = qpos[-1] + 1
+        o_dev = torch.empty((L, B, HQ, D), dtype=torch.float32, device="cuda")
+
+    def e2e_body():
+        dq.copy_(qh, non_blocking=True)
+        dk.copy_(kh, non_blocking=True)
+        dv.copy_(vh, non_blocking=True)
+        for l in range(L):
+            if world == 1:
+                caches[l].step_device(dq[l], dk[l], dv[l], p_dev, o_dev[l])
+            else:
+                caches[l].attend_device(dq[l], p_dev, out, lse)
+                o_all, l_all = gather_partials(out, lse)
+                o_dev[l].copy_(lse_merge(o_all, l_all, merged))
+        outh.copy_(o_dev, non_blocking=True)
+        p_dev.add_(1)
+
+    if use_graph:
+        e2e_body()
+        torch.cuda.synchronize()
+        e2e_graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(e2e_graph):
+            e2e_body()
+        for c in caches:
+            c._n += 1
     barrier()
-    h0 = time.perf_counter()
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record()
     for s in range(e2e_steps):
-        p = torch.full((B,), gpos0 + base + s, dtype=torch.int64).pin_memory().cuda(non_blocking=True)
-        for l in range(L):
-            i = s % qh.shape[0]
-            dq.copy_(qh[i, l], non_blocking=True)
-            dk.copy_(kh[i, l], non_blocking=True)
-            dv.copy_(vh[i, l], non_blocking=True)
-            if world == 1:
-                caches[l].step_device(dq, dk, dv, p, out)
-                outh[l].copy_(out, non_blocking=True)
-            else:
-                caches[l].attend_device(dq, p, out, lse)
-                o_all, l_all = gather_partials(out, lse)
-                outh[l].copy_(lse_merge(o_all, l_all, merged), non_blocking=True)
+        e2e_graph.replay() if use_graph else e2e_body()
     x1.record()
     torch.cuda.synchronize()
+    for c in caches:
+        c._n += e2e_steps if (world == 1) else 0
     e2e_ms = x0.elapsed_time(x1) / e2e_steps
     t = torch.tensor([e2e_ms], device="cuda")
     if world > 1:
@@ -358,6 +407,7 @@ def run_ours(args):
                 "tok_s_definition": "batch * layers / step time (BASELINE.md: batch / one layer's "
                                     "decode-attention call) x GPUs (weak scaling)",
                 "model_tok_s": B / (ms / 1e3),
+                "launch": "CUDA graph per step" if use_graph else "eager",
             },
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "kernel": "decode attention (split-KV + combine)",
@@ -366,8 +416,11 @@ def run_ours(args):
                          "traffic": None, "algorithmic_bytes_per_launch": alg_bytes,
                          "launch_ms": attn_ms},
             "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
-                    "h2d_bytes_per_step": L * (qh[0, 0].numel() + 2 * kh[0, 0].numel()) * 2 + 8,
-                    "d2h_bytes_per_step": L * B * HQ * D * 4, "ms_per_step": e2e_ms},
+                    "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,
+                    "d2h_bytes_per_step": outh.numel() * 4, "ms_per_step": e2e_ms,
+                    "path": "QuantizedKVCache.step_device per layer (antkv_decode_step) with "
+                            "pinned-host q/k/v H2D and output D2H inside the timed region"
+                            + (", CUDA-graph replay" if use_graph else "")},
             "gpu_launches": args.steps * L * ((1 if args.kernel == "fast" else 4) if world == 1
                                               else (3 if args.kernel == "fast" else 4)),
             "clocks": clk.summary(),
