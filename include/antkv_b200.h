@@ -18,8 +18,8 @@
  *                             kernels/__init__.py:37)
  *   antkv_prefill_attention <- attention.flash_attention_aux (attention.py:146-169)
  *                             with RoPE (attention.py:89-106) fused, GQA-batched
- *   antkv_prefill_anchor_scores <- anchors.anchor_scores_blocked (anchors.py:235-256)
- *   antkv_select_anchors   <- anchors.select_anchors  (anchors.py:265-301)
+ *   antkv_prefill_anchor_scores <- anchors.anchor_scores_blocked (anchors.py:66-87)
+ *   antkv_select_anchors   <- anchors.select_anchors  (anchors.py:96-132)
  *   antkv_cache_build      <- QuantizedKVCache.prefill layout step (cache.py:122-139)
  *   antkv_cache_append     <- QuantizedKVCache.decode_step append (cache.py:157-166)
  *   antkv_decode_attention <- QuantizedKVCache.decode_step math (cache.py:168-178)
@@ -136,7 +136,7 @@ ANTKV_API int antkv_prefill_anchor_scores(const void *Q, const void *K, int dtyp
 
 /* Top-budget selection per (b, kv head) under `policy`, ties to the lower
  * index, result sorted ascending: anchors int32 [B][Hkv][budget].
- * budget is clipped to [0, n] by the caller (anchors.py:273). */
+ * budget is clipped to [0, n] by the caller (anchors.py:104). */
 ANTKV_API int antkv_select_anchors(const float *ans_k, const float *ans_v, int B, int Hkv,
                          int n, int budget, int policy, int32_t *anchors,
                          void *stream);
@@ -179,11 +179,14 @@ typedef struct antkv_cache_desc {
   int64_t *positions;  /* [B][capacity]                                     */
   const float *codebook_k; /* [Hkv][m][d_sub] float32                       */
   const float *codebook_v;
-  uint16_t *codebook_f16;  /* fast path: [Hkv][2][256][8 copies][8] fp16: each
-                              centroid replicated across the 8 16-byte bank
-                              groups of a 128-byte row (64 KB per head)     */
-  uint16_t *pool_krot; /* fast path: fp16 [B][Hkv][pool_capacity][d] pool K
-                          rows with RoPE applied at their positions          */
+  uint16_t *codebook_f16;  /* fast path: [Hkv][256 codes][2 (K,V)][8 copies][8]
+                              fp16: each centroid replicated across the 8
+                              16-byte bank groups of a 128-byte row (64 KB per
+                              head, one contiguous bulk copy)                */
+  uint16_t *pool_f16;  /* fast path: fp16 [B][Hkv][pool_capacity/16] tiles of
+                          [2 (K rotated at its position, V)][16 slots][128]
+                          with the 16-byte chunks of slot r XOR-swizzled by
+                          r & 7; pool_capacity is a multiple of 16          */
   void *fast_tables;   /* fast path: 16384-byte RoPE constant tables        */
 } antkv_cache_desc;
 

@@ -16,7 +16,7 @@ reference's compiled Cython kernels built from the reference sources by
 Extension beyond the single-head reference (GQA): the reference is
 single-head.  ``OracleCache`` keeps one cache state per KV head
 and selects that head's anchors from the anchor scores summed over the Q heads
-of its group.  AnS is a sum over query rows (anchors.py:230-231), so for a
+of its group.  AnS is a sum over query rows (anchors.py:61-62), so for a
 group size of 1 this is exactly the reference; the tests check that
 bit-for-bit against ``QuantizedKVCache``.
 """
@@ -33,7 +33,7 @@ __all__ = [
     "KIND_WINDOWED", "POLICIES",
 ]
 
-POLICIES = ("by_k", "by_v", "by_sum")          # anchors.py:198
+POLICIES = ("by_k", "by_v", "by_sum")          # anchors.py:29
 KIND_ANCHOR = "anchor"                         # cache.py:24-26
 KIND_QUANTIZED = "quantized"
 KIND_WINDOWED = "windowed"
@@ -171,7 +171,7 @@ def flash_attention_aux(Q, K, V, block_q, block_k, positions=None, theta_base=10
 
 def anchor_scores_blocked(Q, K, M, L, q_norms, block_q, block_k, positions=None,
                           theta_base=10000.0, causal=False):
-    """anchors.py:235-256."""
+    """anchors.py:66-87."""
     Q = np.asarray(Q, dtype=np.float64)
     K = np.asarray(K, dtype=np.float64)
     if positions is not None:
@@ -271,13 +271,13 @@ def unpack_indices(data, bits, count):
 
 # ---------------------------------------------------------------- anchors
 def ranked(scores):
-    """Descending score, ties to the lower index (anchors.py:259-262)."""
+    """Descending score, ties to the lower index (anchors.py:90-93)."""
     n = len(scores)
     return np.lexsort((np.arange(n), -np.asarray(scores, dtype=np.float64)))
 
 
 def select_anchors(ans_k, ans_v, budget, policy="by_sum"):
-    """anchors.py:265-301.  Returns sorted int64 indices."""
+    """anchors.py:96-132.  Returns sorted int64 indices."""
     if policy not in POLICIES:
         raise ValueError(f"unknown policy {policy!r}")
     n = len(ans_v)

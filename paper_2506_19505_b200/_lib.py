@@ -40,7 +40,7 @@ class CacheDesc(ctypes.Structure):
         ("codes", _vp), ("qmask", _vp), ("pool_rows", _vp), ("pool_tok", _vp),
         ("pool_kind", _vp), ("win_ring", _vp), ("free_stack", _vp), ("hstate", _vp),
         ("seq_len", _vp), ("positions", _vp), ("codebook_k", _vp), ("codebook_v", _vp),
-        ("codebook_f16", _vp), ("pool_krot", _vp), ("fast_tables", _vp),
+        ("codebook_f16", _vp), ("pool_f16", _vp), ("fast_tables", _vp),
     ]
 
 

@@ -1,4 +1,4 @@
-"""Anchor scores and selection, mirroring antkv.anchors (anchors.py:201-301).
+"""Anchor scores and selection, mirroring antkv.anchors (anchors.py:32-132).
 
 anchor_scores_blocked reconstructs A = exp(S - M)/L blockwise on the GPU
 (antkv_ans_blocked); select_anchors runs the radix top-k selection kernel
@@ -34,7 +34,7 @@ class AnchorSelection:
 
 def anchor_scores_blocked(Q, K, V, aux: AttentionAux, block_q, block_k, rope=None,
                           causal=False):
-    """Blockwise AnS from the attention auxiliaries (anchors.py:235-256)."""
+    """Blockwise AnS from the attention auxiliaries (anchors.py:66-87)."""
     Qt, was_np = _check(Q, "Q")
     Kt, _ = _check(K, "K")
     H, n_q, d = Qt.shape
@@ -76,7 +76,7 @@ def select_anchors_device(ans_k, ans_v, budget, policy="by_sum"):
 
 def select_anchors(scores: AnchorScores, budget, policy="by_sum"):
     """Top-budget tokens under the policy, ties to the lower index
-    (anchors.py:265-301).  Scores are compared in float32 on the GPU."""
+    (anchors.py:96-132).  Scores are compared in float32 on the GPU."""
     if policy not in POLICIES:
         raise ValueError(f"unknown policy {policy!r}")
     k, was_np = as_cuda(scores.ans_k, torch.float32)

@@ -120,7 +120,8 @@ class QuantizedKVCache:
         return self._desc.capacity if self._desc is not None else 0
 
     def _pool_capacity(self, cap):
-        return self.config.budget_for(cap) + self.config.window_size + 2
+        # a multiple of 16: the fast decode kernel streams the pool in 16-slot tiles
+        return _round_up(self.config.budget_for(cap) + self.config.window_size + 2, 16)
 
     def _alloc(self, cap):
         """(Re)allocate device state for `cap` token slots, keeping contents."""
@@ -149,9 +150,9 @@ class QuantizedKVCache:
         }
         use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         if use_fast:
-            t["cb_f16"] = torch.zeros((H, 2, 256, 64), dtype=torch.float16, device=dev)
+            t["cb_f16"] = torch.zeros((H, 256, 2, 64), dtype=torch.float16, device=dev)
             t["fast_tables"] = torch.zeros((16384,), dtype=torch.uint8, device=dev)
-            t["pool_krot"] = torch.zeros((B, H, P, d), dtype=torch.float16, device=dev)
+            t["pool_f16"] = torch.zeros((B, H, P, 2, d), dtype=torch.float16, device=dev)
         if old is not None:
             oc = old["positions"].shape[1]
             oP = old["pool_tok"].shape[2]
@@ -174,8 +175,8 @@ class QuantizedKVCache:
                     merged = torch.cat([newslots, fs[b, h, :k]])
                     t["free_stack"][b, h, :merged.numel()] = merged
                     t["hstate"][b, h, _lib.HS_FREE_TOP] = merged.numel()
-            if use_fast and "pool_krot" in old:
-                t["pool_krot"][:, :, :oP] = old["pool_krot"]
+            if use_fast and "pool_f16" in old:
+                t["pool_f16"][:, :, :oP] = old["pool_f16"]   # whole 16-slot tiles
         self._t = t
         self._desc = self._make_desc(cap, P, t)
         self._ws = None
@@ -199,7 +200,7 @@ class QuantizedKVCache:
                      ("pool_tok", "pool_tok"), ("pool_kind", "pool_kind"), ("win_ring", "win_ring"),
                      ("free_stack", "free_stack"), ("hstate", "hstate"), ("seq_len", "seq_len"),
                      ("positions", "positions"), ("codebook_k", "cb_k"), ("codebook_v", "cb_v"),
-                     ("codebook_f16", "cb_f16"), ("pool_krot", "pool_krot"),
+                     ("codebook_f16", "cb_f16"), ("pool_f16", "pool_f16"),
                      ("fast_tables", "fast_tables")):
             setattr(D, f, t[k].data_ptr() if k in t else None)
         return D
@@ -434,7 +435,7 @@ class QuantizedKVCache:
         return O
 
     def _host_state(self):
-        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_krot",
+        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_f16",
                                                                   "fast_tables")}
         return t
 
@@ -659,5 +660,5 @@ class QuantizedKVCache:
         self._n = n
         self._last_pos = np.asarray([positions[-1]], dtype=np.int64) if n else None
         self._contiguous = bool(n == 0 or np.all(np.asarray(positions) == positions[0] + np.arange(n)))
-        if "pool_krot" in t:
+        if "pool_f16" in t:
             _lib.call("antkv_cache_prepare_fast", ctypes.byref(self._desc), _lib.stream())

@@ -212,29 +212,32 @@ __global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ 
   (void)s_win;
 }
 
-// Fast path: fp16 copy of pool row `slot`'s K with RoPE applied at `pos`.
-__device__ void write_pool_krot(const antkv_cache_desc &c, int64_t bh, int slot, int64_t pos) {
-  if (!c.pool_krot) return;
+// Fast path: fp16 copy of pool row `slot` (K with RoPE applied at `pos`, V)
+// in the tiled pool_f16 layout.
+__device__ void write_pool_f16(const antkv_cache_desc &c, int64_t bh, int slot, int64_t pos) {
+  if (!c.pool_f16) return;
   const int64_t src = (bh * c.pool_capacity + slot) * 2 * c.d;
-  __half *dst = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * c.d;
+  __half *dst = reinterpret_cast<__half *>(c.pool_f16) + bh * c.pool_capacity * 2 * c.d;
   for (int i = threadIdx.x; i < c.d / 2; i += blockDim.x) {
     const float x0 = load_elem(c.pool_rows, src + 2 * i, c.row_dtype);
     const float x1 = load_elem(c.pool_rows, src + 2 * i + 1, c.row_dtype);
     float cs, sn;
     rope_cs((double)pos * rope_freq(c.theta_base, i, c.d), cs, sn);
-    dst[2 * i] = __float2half_rn(x0 * cs - x1 * sn);
-    dst[2 * i + 1] = __float2half_rn(x0 * sn + x1 * cs);
+    dst[pool_f16_offset(slot, 0, 2 * i)] = __float2half_rn(x0 * cs - x1 * sn);
+    dst[pool_f16_offset(slot, 0, 2 * i + 1)] = __float2half_rn(x0 * sn + x1 * cs);
   }
+  for (int i = threadIdx.x; i < c.d; i += blockDim.x)
+    dst[pool_f16_offset(slot, 1, i)] = __float2half_rn(load_elem(c.pool_rows, src + c.d + i, c.row_dtype));
 }
 
-// Fast path: rotated K rows for every live pool slot (after build / load).
-__global__ void cache_pool_krot_kernel(antkv_cache_desc c) {
+// Fast path: pool_f16 rows for every live pool slot (after build / load).
+__global__ void cache_pool_f16_kernel(antkv_cache_desc c) {
   const int64_t bh = blockIdx.y;
   const int b = static_cast<int>(bh / c.Hkv);
   const int s = blockIdx.x;
   const int tok = c.pool_tok[bh * c.pool_capacity + s];
   if (tok < 0 || c.pool_kind[bh * c.pool_capacity + s] == ANTKV_KIND_FREE) return;
-  write_pool_krot(c, bh, s, c.positions[(int64_t)b * c.capacity + tok]);
+  write_pool_f16(c, bh, s, c.positions[(int64_t)b * c.capacity + tok]);
 }
 
 // Append one token per sequence (cache.py:157-166).  One CTA per sequence;
@@ -272,7 +275,7 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
     store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(k, bh * c.d + t, dtype));
     store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(v, bh * c.d + t, dtype));
   }
-  if (c.pool_krot) {
+  if (c.pool_f16) {
     __syncthreads();
     const double pos = static_cast<double>(position[b]);
     for (int i = threadIdx.x; i < c.Hkv * (c.d / 2); i += blockDim.x) {
@@ -285,9 +288,13 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
       const float x1 = load_elem(c.pool_rows, src + 2 * p + 1, c.row_dtype);
       float cs, sn;
       rope_cs(pos * rope_freq(c.theta_base, p, c.d), cs, sn);
-      __half *dst = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot) * c.d;
-      dst[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
-      dst[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
+      __half *dst = reinterpret_cast<__half *>(c.pool_f16) + bh * c.pool_capacity * 2 * c.d;
+      dst[pool_f16_offset(slot, 0, 2 * p)] = __float2half_rn(x0 * cs - x1 * sn);
+      dst[pool_f16_offset(slot, 0, 2 * p + 1)] = __float2half_rn(x0 * sn + x1 * cs);
+      dst[pool_f16_offset(slot, 1, 2 * p)] =
+          __float2half_rn(load_elem(c.pool_rows, src + c.d + 2 * p, c.row_dtype));
+      dst[pool_f16_offset(slot, 1, 2 * p + 1)] =
+          __float2half_rn(load_elem(c.pool_rows, src + c.d + 2 * p + 1, c.row_dtype));
     }
   }
   // the slot's code bits stay clear (qmask initialised to zero above n)
@@ -429,7 +436,7 @@ __global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__re
   }
 }
 
-// Fast-path codebook: fp16 [Hkv][2][256][8 copies][8] (zero rows beyond m).
+// Fast-path codebook: fp16 [Hkv][256][2 (K,V)][8 copies][8] (zero rows beyond m).
 // Row `code` holds the centroid in each of the 8 16-byte bank groups, so the
 // eight ldmatrix row addresses of a phase (copy = lane & 7) never conflict.
 // Block (Hkv*2) also writes the RoPE constant tables (FastTables).
@@ -454,10 +461,10 @@ __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
   }
   const int h = blockIdx.x / 2, kv = blockIdx.x % 2;
   const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + ((int64_t)h * 2 + kv) * 256 * 64;
+  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + (int64_t)h * 256 * 128 + kv * 64;
   for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
     const int code = i / 64, t = i % 8;
-    dst[i] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
+    dst[code * 128 + i % 64] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
   }
 }
 
@@ -530,9 +537,9 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
   if (rc) return rc;
   cache_build_kernel<<<nsets, 256, 0, st>>>(*c, K, V, dtype, positions, n, anchors, n_anchors);
   ANTKV_LAUNCH_CHECK("cache_build_kernel");
-  if (c->pool_krot) {
-    cache_pool_krot_kernel<<<dim3(c->pool_capacity, nsets), 64, 0, st>>>(*c);
-    ANTKV_LAUNCH_CHECK("cache_pool_krot_kernel");
+  if (c->pool_f16) {
+    cache_pool_f16_kernel<<<dim3(c->pool_capacity, nsets), 64, 0, st>>>(*c);
+    ANTKV_LAUNCH_CHECK("cache_pool_f16_kernel");
   }
   return ANTKV_OK;
 }
@@ -582,9 +589,10 @@ extern "C" int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream)
   cudaStream_t st = as_stream(stream);
   cache_prepare_fast_kernel<<<c->Hkv * 2 + 1, 256, 0, st>>>(*c);
   ANTKV_LAUNCH_CHECK("cache_prepare_fast_kernel");
-  if (c->pool_krot) {
-    cache_pool_krot_kernel<<<dim3(c->pool_capacity, c->B * c->Hkv), 64, 0, st>>>(*c);
-    ANTKV_LAUNCH_CHECK("cache_pool_krot_kernel");
+  if (c->pool_f16) {
+    ANTKV_REQUIRE(c->pool_capacity % 16 == 0, "pool_capacity must be a multiple of 16");
+    cache_pool_f16_kernel<<<dim3(c->pool_capacity, c->B * c->Hkv), 64, 0, st>>>(*c);
+    ANTKV_LAUNCH_CHECK("cache_pool_f16_kernel");
   }
   return ANTKV_OK;
 }

@@ -100,6 +100,16 @@ __host__ __device__ __forceinline__ int64_t code_offset(int64_t slot, int kv, in
   return (slot >> 4) * (32 * (int64_t)G) + kv * (16 * G) + (slot & 15) * G + g;
 }
 
+// Fast-path pool tile layout (antkv_cache_desc::pool_f16), in halves from the
+// (sequence, head) base: 16-slot tiles of [K rotated | V][16 slots][128], the
+// 16-byte chunk c of slot r stored at chunk c ^ (r & 7) so the eight row
+// addresses of an ldmatrix phase fall into distinct bank groups.
+__host__ __device__ __forceinline__ int64_t pool_f16_offset(int slot, int kv, int dim) {
+  const int r = slot & 15;
+  return (int64_t)(slot >> 4) * 4096 + kv * 2048 + r * 128 + ((((dim >> 3) ^ (r & 7))) << 3) +
+         (dim & 7);
+}
+
 // Fast-path RoPE constants for d = 128 (antkv_cache_desc::fast_tables).
 struct FastTables {
   uint32_t kc[16][64][2];  // fp16x2 (cos, sin), (-sin, cos) of r*omega_i, r = 0..15
@@ -107,6 +117,10 @@ struct FastTables {
   double omega[64];        // theta^(-2i/128)
 };
 static_assert(sizeof(FastTables) <= 16384, "fast tables");
+
+// Ints per (sequence, head) of the fused decode kernel's cache-update plan
+// (decode workspace, after the CTA / sequence tickets).
+constexpr int kPlanWords = 12;
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 

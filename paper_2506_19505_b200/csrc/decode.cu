@@ -300,7 +300,7 @@ using namespace antkv;
 
 // tickets [B*Hkv] + [B] and the per-head cache-update plan [B*Hkv][4]
 static int64_t counter_bytes(const antkv_cache_desc &c) {
-  return (int64_t)(c.B * c.Hkv + c.B + 4 * c.B * c.Hkv) * 4;
+  return (int64_t)(c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv) * 4;
 }
 
 static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
@@ -355,6 +355,12 @@ static int check_decode_args(const antkv_cache_desc *c, const void *q, float *ou
   return ANTKV_OK;
 }
 
+// The fused kernel bulk-copies the 4 query rows of a head: q must be 16-byte
+// aligned (any contiguous tensor is); otherwise the generic kernels run.
+static bool fast_ok(const antkv_cache_desc *c, const void *q, int fast) {
+  return fast && decode_fast_supported(*c) && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+}
+
 extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
                                       const int64_t *qpos, float *out, float *lse,
                                       void *workspace, int64_t workspace_bytes, int splits,
@@ -362,7 +368,7 @@ extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, 
   int rc = check_decode_args(c, q, out);
   if (rc) return rc;
   return attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
-                        workspace_bytes, splits, fast && decode_fast_supported(*c), as_stream(stream));
+                        workspace_bytes, splits, fast_ok(c, q, fast), as_stream(stream));
 }
 
 extern "C" int antkv_decode_step(const antkv_cache_desc *c, const void *q, const void *k,
@@ -373,7 +379,7 @@ extern "C" int antkv_decode_step(const antkv_cache_desc *c, const void *q, const
   if (rc) return rc;
   ANTKV_REQUIRE(k != nullptr && v != nullptr, "null k/v");
   cudaStream_t st = as_stream(stream);
-  if (fast && decode_fast_supported(*c))   // one fused launch
+  if (fast_ok(c, q, fast))   // one fused launch
     return attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes,
                           splits, true, st);
   rc = antkv_cache_append(c, k, v, dtype, qpos, stream);

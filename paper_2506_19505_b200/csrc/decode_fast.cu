@@ -1,63 +1,84 @@
 // sm_100a decode-attention kernel for the 1-bit d8m256 configuration
 // (d = 128, d_sub = 8, m <= 256, 4 query heads per KV head, contiguous
-// positions).  Reference semantics: cache.py:168-178 (RoPE after
-// reconstruction, softmax over the whole cache, A.V).
+// positions).  Reference semantics: cache.py:149-194 (append the new token,
+// RoPE after reconstruction, softmax over the whole cache, A.V, then evict).
 //
-// Per 16-slot tile the score matrix S^T[16 tokens x 8 cols] and the output
-// O^T[128 dims x 8 cols] are computed with m16n8k16 tensor-core MMAs whose
-// operands come straight from registers:
-//   * K_hat / V_hat rows are gathered from a shared-memory fp16 codebook
-//     with ldmatrix (one 16-byte centroid row per lane address).  The
-//     codebook is replicated 8x across the 16-byte bank groups so the eight
-//     row addresses of every ldmatrix phase hit distinct banks.
-//   * RoPE: rows 0-7 of a tile are tokens P0..P0+7 (group a), rows 8-15 are
-//     P0+8..P0+15 (group b).  Each row is rotated by its offset g (0..7) in
-//     its group with per-lane constant fp16 (cos, sin) pairs; the group base
-//     rotation is applied to the query instead: columns 0-3 of the MMA carry
-//     the 4 query heads in group a's frame R(p_q - P0) q, columns 4-7 in group
-//     b's frame R(p_q - P0 - 8) q.  Frames advance by R(-16) per tile in fp32
-//     (seeded with float64-reduced angles per warp).
-//   * Group a tokens only see columns 0-3 and group b tokens only 4-7 (the
-//     other products are masked), giving two independent online-softmax
-//     streams that are merged with the CTA merge at the end.
-// Code tiles (K codes 256 B + V codes 256 B per tile) are streamed into a
-// shared-memory ring with cp.async.bulk (TMA bulk copies) and mbarriers.
-// Anchor / window rows (the full-precision pool) are handled by extra CTAs
-// on CUDA cores from fp16 pre-rotated K rows.
+// One launch does the whole decode step for every (sequence, KV head):
+//   * CTAs: `splits` per (sequence, head), one CTA of 8 warps per SM.  Each
+//     CTA owns a contiguous range of 16-slot code tiles (split into 8
+//     contiguous warp ranges) and a share of the full-precision pool tiles.
+//   * Codebooks: one 64 KB bulk copy per CTA of the prepared fp16 layout
+//     [code][K 8 copies | V 8 copies]: a centroid row sits in all eight
+//     16-byte bank groups, so the eight row addresses of an ldmatrix phase
+//     (copy = lane & 7) never conflict, and an address is ONE prmt:
+//     (code << 8) | lane_offset, with the codebook base folded into the
+//     ldmatrix uniform operand.
+//   * Code tiles (K codes 256 B + V codes 256 B per tile) stream through a
+//     private 8-stage ring per warp (cp.async.bulk + mbarrier); the warp
+//     refills its own slots, so warps never wait on each other.
+//   * Per stage (an even and an odd tile) S^T[16 x 8] = rot(K_hat) . B and
+//     O^T[128 x 8] += V_hat^T . P with m16n8k16 tensor-core MMAs on register
+//     operands.  RoPE: row r of a tile is rotated by R(r) with per-lane fp16
+//     (cos, sin) constants; the tile base rotation lives in the query
+//     frames: B columns 0-3 hold the 4 query heads in the even tile's frame,
+//     columns 4-7 in the odd tile's frame.  Frames advance by R(-32) per
+//     stage in packed fp32 (FFMA2), seeded from float64-reduced angles.
+//   * Pool tiles (anchors + window: K rotated at its own position and V, in
+//     fp16, pre-swizzled) are bulk-copied per warp and multiplied with the
+//     query in the absolute frame (no per-row rotation).
+//   * Online softmax in log2 units with a lazily raised reference max (P <=
+//     2^8 keeps fp16 P exact enough); CTA merge in shared memory; the last
+//     CTA of each (sequence, head) (atomic ticket) combines the splits and
+//     commits the cache-update plan that one CTA prepared while the others
+//     were reading (new row into a free pool slot, oldest window row
+//     promoted or encoded).
 #include <stdlib.h>
 
 #include "common.cuh"
 
 namespace antkv {
 
-constexpr int FK_WARPS = 4;
+constexpr int FK_WARPS = 8;
 constexpr int FK_THREADS = 32 * FK_WARPS;
-constexpr int FK_STAGES = 8;
+constexpr int FK_NS = 4;                                 // ring slots per warp
 constexpr int FK_TILE_BYTES = 512;                       // K 256 B + V 256 B
-constexpr int FK_WARP_STAGE_BYTES = 2 * FK_TILE_BYTES;   // 2 tiles per warp per stage
-constexpr int FK_STAGE_BYTES = FK_WARPS * FK_WARP_STAGE_BYTES;
+constexpr int FK_STAGE_BYTES = 2 * FK_TILE_BYTES;        // even + odd tile
+constexpr int FK_SLOT_BYTES = 2 * FK_STAGE_BYTES;        // two stages per ring slot
+// The codebook sits at offset 0 of dynamic shared memory, whose shared-window
+// address is 0x400 on sm_100 (the 1 KB reserved block; probed once on the
+// host, decode_fast_smem_base_ok): gathers use it as an ldmatrix immediate.
+constexpr uint32_t FK_SMEM_BASE = 0x400;
+// ANTKV_TRACE=1: per-CTA timeline words: 0 smid | ticket << 32, then global
+// timer stamps 1 start, 2 barriers ready, 3 prologue loads issued, 4 frames,
+// 5 pool wait, 6 pool done, 7 prepare done, 8 loop start, 9 loop end,
+// 10 partial written, 11 committed (last CTA only).
+constexpr int FK_TRACE_WORDS = 16;
+constexpr int FK_POOL_TILE_BYTES = 8192;                 // [K|V][16 slots][128] fp16
 constexpr int FK_MAX_WARP_WORDS = 64;                    // qmask words per warp (2048 slots)
+constexpr int FK_CB_BYTES = 256 * 256;                   // [code][K 128 B | V 128 B]
 
 struct __align__(128) FastSmem {
-  uint4 cbK[256 * 8];                          // [code][copy] 16 B
-  uint4 cbV[256 * 8];
-  uint8_t ring[FK_STAGES][FK_STAGE_BYTES];
+  uint8_t cb[FK_CB_BYTES];
+  uint8_t ring[FK_WARPS][FK_NS][FK_SLOT_BYTES];
+  uint8_t pool[FK_WARPS][FK_POOL_TILE_BYTES];
   uint32_t qm[FK_WARPS][FK_MAX_WARP_WORDS];
-  float po[FK_WARPS][4][128];                  // pool-row partials per warp (4 heads)
-  float pm[FK_WARPS][4], pl[FK_WARPS][4];
-  unsigned long long full[FK_STAGES];
-  unsigned long long empty[FK_STAGES];
-  unsigned long long cbbar;
-  int ticket;
-  int upd[4];
+  float xo[4][128];                          // the appended token's row (prep CTA)
+  float xm[4];                               // its scaled logits (log2 units)
+  FastTables tab;                            // RoPE constants (bulk copy)
+  uint8_t qraw[4 * 128 * 4];                 // the 4 query rows of the head (input dtype)
+  float2 ang[2 * FK_WARPS + 1][64];          // (cos, sin) per query frame and pair
+  unsigned long long full[FK_WARPS][FK_NS];
+  unsigned long long pfull[FK_WARPS];
+  unsigned long long cbbar, tbar;
+  int ticket, gticket;
 };
 
-struct MergeSmem {                             // aliases the ring after the loop
+struct MergeSmem {                             // aliases the pool area after the loops
   float o[FK_WARPS][8][128];
   float m[FK_WARPS][8];
   float l[FK_WARPS][8];
 };
-static_assert(sizeof(MergeSmem) <= sizeof(uint8_t) * FK_STAGES * FK_STAGE_BYTES, "merge scratch");
+static_assert(sizeof(MergeSmem) <= sizeof(uint8_t) * FK_WARPS * FK_POOL_TILE_BYTES, "merge scratch");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -69,9 +90,6 @@ __device__ __forceinline__ void mbar_init(unsigned long long *bar, int count) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long *bar, uint32_t parity) {
   uint32_t done;
@@ -92,6 +110,9 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -103,6 +124,18 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
+// Gathers from the codebook: `off` = (code << 8) | copy offset (| 128 for V).
+__device__ __forceinline__ void ldsm_cb(uint32_t off, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4+1024];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(off));
+}
+__device__ __forceinline__ void ldsm_cb_t(uint32_t off, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4+1024];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(off));
+}
+static_assert(FK_SMEM_BASE == 1024, "ldsm_cb immediates");
 __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
                                          uint32_t b1) {
   asm volatile(
@@ -116,8 +149,14 @@ __device__ __forceinline__ uint32_t movm_t(uint32_t x) {
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
   return y;
 }
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t *>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2 *>(&u); }
+__device__ __forceinline__ uint32_t pack_h2(float x, float y) { return h2u(__floats2half2_rn(x, y)); }
 
 // (x0, x1) -> (c x0 - s x1, s x0 + c x1) with cs = (c, s), ns = (-s, c)
 __device__ __forceinline__ uint32_t rot2(uint32_t x, uint32_t cs, uint32_t ns) {
@@ -150,11 +189,10 @@ struct StepArgs {
   float *out;              // [B][Hq][128]
   float *lse;              // [B][Hq] or NULL
   float *ws_o, *ws_m, *ws_l;
-  int *cnt;                // [B*Hkv] CTA tickets, [B] head tickets (self-resetting),
-                           // [B*Hkv][4] cache-update plan
+  int *cnt;                // [B*Hkv] CTA tickets, [B] sequence tickets (self-resetting),
+                           // [B*Hkv][kPlanWords] cache-update plans
   int splits;              // CTAs per (b, head)
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
-  int debug_mode;              // ANTKV_DEBUG_MODE: 1 skip pool rows, 2 stop after setup
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -180,202 +218,86 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// ------------------------------------------------------------------ pool
-// Full-precision rows [r0, r1) of the pool (anchors + window) on CUDA cores:
-// a warp handles 4 rows per step (32 lanes x 4 dims), all loads of the 4
-// rows in flight together.  With `with_new` the token appended this step is
-// attended too (the reference appends before attending, cache.py:162-178).
-// Results (natural-log units) go to the per-warp pool area of shared memory.
-template <typename AfterLoads>
-__device__ void pool_rows_part(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm,
-                               double pq, int b, int h, int r0, int r1, bool with_new,
-                               AfterLoads after_loads) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t bh = (int64_t)b * c.Hkv + h;
-  const int n = c.seq_len[b];
-  const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
-  float qv[4][4], qcs[2], qsn[2];
-  const float scale = rsqrtf(128.f);
-#pragma unroll
-  for (int pp = 0; pp < 2; ++pp) rope_cs(pq * tab->omega[2 * lane + pp], qcs[pp], qsn[pp]);
-#pragma unroll
-  for (int hh = 0; hh < 4; ++hh) {
-    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + hh) * 128 + 4 * lane;
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const float x0 = load_elem(a.q, qb + 2 * pp, a.qdtype), x1 = load_elem(a.q, qb + 2 * pp + 1, a.qdtype);
-      qv[hh][2 * pp] = (x0 * qcs[pp] - x1 * qsn[pp]) * scale;
-      qv[hh][2 * pp + 1] = (x0 * qsn[pp] + x1 * qcs[pp]) * scale;
-    }
-  }
-  float m[4], l[4], acc[4][4];
-#pragma unroll
-  for (int hh = 0; hh < 4; ++hh) {
-    m[hh] = -INFINITY;
-    l[hh] = 0.f;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
-  }
-  if (with_new && warp == 0) {
-    // K rotated in fp32 then rounded to fp16 like every pool K row; V in the pool dtype
-    float kk[4], vv[4];
-    const int64_t kb = bh * 128 + 4 * lane;
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const float x0 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp, a.kvdtype));
-      const float x1 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp + 1, a.kvdtype));
-      kk[2 * pp] = __half2float(__float2half_rn(x0 * qcs[pp] - x1 * qsn[pp]));
-      kk[2 * pp + 1] = __half2float(__float2half_rn(x0 * qsn[pp] + x1 * qcs[pp]));
-    }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) vv[e] = round_to(c.row_dtype, load_elem(a.vnew, kb + e, a.kvdtype));
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh) {
-      m[hh] = warp_sum(qv[hh][0] * kk[0] + qv[hh][1] * kk[1] + qv[hh][2] * kk[2] + qv[hh][3] * kk[3]);
-      l[hh] = 1.f;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[hh][e] = vv[e];
-    }
-  }
-  const __half *krot = reinterpret_cast<const __half *>(c.pool_krot) + bh * c.pool_capacity * 128;
-  const int64_t vbase = bh * c.pool_capacity * 2 * 128 + 128;
-  constexpr int RB = 10;  // rows per warp per round (all loads in flight together)
-  bool first = true;
-  for (int rb = r0 + RB * warp; first || rb < r1; rb += RB * FK_WARPS) {
-    if (rb >= r1) {   // no rows for this warp: still run the hook once
-      after_loads();
-      break;
-    }
-    bool ok[RB];
-    uint2 kraw[RB];
-    float vv[RB][4];
-#pragma unroll
-    for (int u = 0; u < RB; ++u) {
-      const int r = min(rb + u, r1 - 1);
-      const int8_t kind = c.pool_kind[bh * c.pool_capacity + r];
-      const int tok = c.pool_tok[bh * c.pool_capacity + r];
-      ok[u] = (rb + u < r1) && kind != ANTKV_KIND_FREE && tok >= 0 && tok < n;
-      kraw[u] = *reinterpret_cast<const uint2 *>(krot + (int64_t)r * 128 + 4 * lane);
-      if (c.row_dtype == ANTKV_F32) {
-        const float4 f = *reinterpret_cast<const float4 *>(
-            reinterpret_cast<const float *>(c.pool_rows) + vbase + (int64_t)r * 256 + 4 * lane);
-        vv[u][0] = f.x; vv[u][1] = f.y; vv[u][2] = f.z; vv[u][3] = f.w;
-      } else {
-        const uint2 raw = *reinterpret_cast<const uint2 *>(
-            reinterpret_cast<const uint16_t *>(c.pool_rows) + vbase + (int64_t)r * 256 + 4 * lane);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint16_t hb = static_cast<uint16_t>((e < 2 ? raw.x : raw.y) >> (16 * (e & 1)));
-          vv[u][e] = c.row_dtype == ANTKV_BF16 ? bf16_bits_to_float(hb)
-                                               : __half2float(__ushort_as_half(hb));
-        }
-      }
-    }
-    if (first) {
-      after_loads();   // rows requested: now queue the bulk copies behind them
-      first = false;
-    }
-    float sc[RB][4];
-#pragma unroll
-    for (int u = 0; u < RB; ++u) {
-      const float2 k01 = __half22float2(u2h(kraw[u].x)), k23 = __half22float2(u2h(kraw[u].y));
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh)
-        sc[u][hh] = qv[hh][0] * k01.x + qv[hh][1] * k01.y + qv[hh][2] * k23.x + qv[hh][3] * k23.y;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < RB; ++u)
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) sc[u][hh] += __shfl_xor_sync(0xffffffffu, sc[u][hh], o);
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh) {
-      float mx = m[hh];
-#pragma unroll
-      for (int u = 0; u < RB; ++u) if (ok[u]) mx = fmaxf(mx, sc[u][hh]);
-      const float al = (m[hh] == mx) ? 1.f : __expf(m[hh] - mx);
-      l[hh] *= al;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) acc[hh][e] *= al;
-#pragma unroll
-      for (int u = 0; u < RB; ++u) {
-        const float p = ok[u] ? __expf(sc[u][hh] - mx) : 0.f;
-        l[hh] += p;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[hh][e] = fmaf(p, vv[u][e], acc[hh][e]);
-      }
-      m[hh] = mx;
-    }
-  }
-#pragma unroll
-  for (int hh = 0; hh < 4; ++hh) {
-    *reinterpret_cast<float4 *>(&sm.po[warp][hh][4 * lane]) =
-        make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
-    if (lane == 0) {
-      sm.pm[warp][hh] = m[hh];
-      sm.pl[warp][hh] = l[hh];
-    }
-  }
-}
-
-// Cache-update plan of this step for head (b, h), prepared early by one CTA
-// while the others still read the cache (cache.py:162-166, 180-193):
-// the new token's rows go into the next free pool slot (still marked FREE,
-// so readers skip it) and, if the window overflows and the anchor budget is
-// exhausted, the oldest window row is encoded into its (still masked) code
-// slot.  plan = {new slot, evicted slot, action 0 none / 1 promote / 2 encode,
-// evicted token}; the last CTA of (b, h) commits it.
+// ------------------------------------------------------------ cache update
+// Plan of this step's cache update for head (b, h), prepared by the last
+// split while the other CTAs still read the cache (cache.py:157-166,
+// 180-193): the new token's rows go into the next free pool slot (still
+// marked FREE, so readers skip it) and, if the window overflows and the
+// anchor budget is exhausted, the oldest window row is encoded into its
+// (still masked) code slot.  All new state words are computed here, so the
+// commit in the last CTA is a batch of independent stores.
+// plan: 0 slot_new, 1 evicted slot, 2 action (0 none / 1 promote / 2 encode),
+// 3 evicted token, 4 ring position of slot_new, 5..9 new hstate words 0..4,
+// 10 free-stack index receiving the evicted slot.
 __device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, FastSmem &sm, int b,
                                int h, int n, double pq) {
   const int64_t bh = (int64_t)b * c.Hkv + h;
   const int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
-  const int top = hs[ANTKV_HS_FREE_TOP];
-  const int slot_new = top > 0 ? c.free_stack[bh * c.pool_capacity + top - 1] : -1;
+  const int A0 = hs[ANTKV_HS_ANCHORS], H0 = hs[ANTKV_HS_WIN_HEAD], C0 = hs[ANTKV_HS_WIN_COUNT];
+  const int F0 = hs[ANTKV_HS_FREE_TOP], PH0 = hs[ANTKV_HS_POOL_HIGH];
+  const int W1 = c.window_size + 1;
+  const int slot_new = F0 > 0 ? c.free_stack[bh * c.pool_capacity + F0 - 1] : -1;
   const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
   if (slot_new >= 0) {
     const int64_t dst = (bh * c.pool_capacity + slot_new) * 256;
-    __half *kr = reinterpret_cast<__half *>(c.pool_krot) + (bh * c.pool_capacity + slot_new) * 128;
+    __half *pf = reinterpret_cast<__half *>(c.pool_f16) + bh * c.pool_capacity * 256;
     for (int t = threadIdx.x; t < 128; t += blockDim.x) {
-      store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(a.knew, bh * 128 + t, a.kvdtype));
-      store_elem(c.pool_rows, dst + 128 + t, c.row_dtype, load_elem(a.vnew, bh * 128 + t, a.kvdtype));
+      const float vk = load_elem(a.knew, bh * 128 + t, a.kvdtype);
+      const float vv = load_elem(a.vnew, bh * 128 + t, a.kvdtype);
+      store_elem(c.pool_rows, dst + t, c.row_dtype, vk);
+      store_elem(c.pool_rows, dst + 128 + t, c.row_dtype, vv);
+      pf[pool_f16_offset(slot_new, 1, t)] = __float2half_rn(round_to(c.row_dtype, vv));
     }
     for (int p = threadIdx.x; p < 64; p += blockDim.x) {
       const float x0 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p, a.kvdtype));
       const float x1 = round_to(c.row_dtype, load_elem(a.knew, bh * 128 + 2 * p + 1, a.kvdtype));
       float cs, sn;
       rope_cs(pq * tab->omega[p], cs, sn);
-      kr[2 * p] = __float2half_rn(x0 * cs - x1 * sn);
-      kr[2 * p + 1] = __float2half_rn(x0 * sn + x1 * cs);
+      pf[pool_f16_offset(slot_new, 0, 2 * p)] = __float2half_rn(x0 * cs - x1 * sn);
+      pf[pool_f16_offset(slot_new, 0, 2 * p + 1)] = __float2half_rn(x0 * sn + x1 * cs);
     }
   }
-  int es = -1, action = 0, j = -1;
-  if (slot_new >= 0 && hs[ANTKV_HS_WIN_COUNT] + 1 > c.window_size) {
-    es = hs[ANTKV_HS_WIN_COUNT] > 0 ? c.win_ring[bh * (c.window_size + 1) + hs[ANTKV_HS_WIN_HEAD]]
-                                     : slot_new;
+  int F1 = F0, C1 = C0, PH1 = PH0, ring_pos = -1;
+  if (slot_new >= 0) {
+    F1 = F0 - 1;
+    ring_pos = (H0 + C0) % W1;
+    C1 = C0 + 1;
+    PH1 = max(PH0, slot_new + 1);
+  }
+  int es = -1, action = 0, j = -1, A1 = A0, H1 = H0, C2 = C1, F2 = F1, push = -1;
+  if (slot_new >= 0 && C1 > c.window_size) {
+    es = C0 > 0 ? c.win_ring[bh * W1 + H0] : slot_new;
     j = es == slot_new ? n : c.pool_tok[bh * c.pool_capacity + es];
     const int budget = budget_for((int64_t)n + 1 + c.token_offset, c.anchor_count, c.anchor_fraction);
-    action = hs[ANTKV_HS_ANCHORS] < budget ? 1 : 2;
+    action = A0 < budget ? 1 : 2;
+    H1 = (H0 + 1) % W1;
+    C2 = C1 - 1;
+    if (action == 1) {
+      A1 = A0 + 1;
+    } else {
+      push = F1;
+      F2 = F1 + 1;
+    }
   }
   if (action == 2) {
     __syncthreads();   // the new row (if evicted itself) is visible to the block
-    // 32 units (kv, group) x 4 threads, each scanning 64 centroids of the fp16
-    // shared-memory codebook for a top-4 shortlist, then rescoring it with the
-    // float32 centroids: float32 distances, lowest index on ties
+    // 32 units (kv, group) x 8 threads, each scanning 32 centroids of the
+    // fp16 shared-memory codebook for a top-4 shortlist, then rescoring it
+    // with the float32 centroids: float32 distances, lowest index on ties
     // (_ckernels.pyx:150-162; SURVEY.md §7 hard part 2: shortlist + exact
     // rescore).
     const int64_t row = (bh * c.pool_capacity + es) * 256;
-    const int u = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int u = threadIdx.x >> 3, part = threadIdx.x & 7;
     const int kv = u >> 4, grp = u & 15;
     float x[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) x[e] = load_elem(c.pool_rows, row + kv * 128 + grp * 8 + e, c.row_dtype);
-    const uint4 *cb16 = kv ? sm.cbV : sm.cbK;
     float sd[4] = {INFINITY, INFINITY, INFINITY, INFINITY};
     int si[4] = {0, 0, 0, 0};
-    const int lo_c = part * 64, hi_c = min(c.m, lo_c + 64);
+    const int lo_c = part * 32, hi_c = min(c.m, lo_c + 32);
     for (int ci = lo_c; ci < hi_c; ++ci) {
-      const uint4 raw = cb16[ci * 8 + (threadIdx.x & 7)];
+      const uint4 raw =
+          *reinterpret_cast<const uint4 *>(&sm.cb[ci * 256 + kv * 128 + (threadIdx.x & 7) * 16]);
       const float2 c01 = __half22float2(u2h(raw.x)), c23 = __half22float2(u2h(raw.y));
       const float2 c45 = __half22float2(u2h(raw.z)), c67 = __half22float2(u2h(raw.w));
       float d = 0.f, df;
@@ -424,7 +346,7 @@ __device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, Fas
       if (d < best || (d == best && si[k] < best_i)) { best = d; best_i = si[k]; }
     }
 #pragma unroll
-    for (int o = 1; o < 4; o <<= 1) {
+    for (int o = 1; o < 8; o <<= 1) {
       const float ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
       if (ob < best || (ob == best && oi < best_i)) { best = ob; best_i = oi; }
@@ -433,95 +355,81 @@ __device__ void prepare_update(const antkv_cache_desc &c, const StepArgs &a, Fas
       c.codes[bh * c.capacity * 32 + code_offset(j, kv, grp, 16)] = static_cast<uint8_t>(best_i);
   }
   if (threadIdx.x == 0) {
-    int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * 4;
+    int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * kPlanWords;
     plan[0] = slot_new;
     plan[1] = es;
     plan[2] = action;
     plan[3] = j;
+    plan[4] = ring_pos;
+    plan[5 + ANTKV_HS_ANCHORS] = A1;
+    plan[5 + ANTKV_HS_WIN_HEAD] = H1;
+    plan[5 + ANTKV_HS_WIN_COUNT] = C2;
+    plan[5 + ANTKV_HS_FREE_TOP] = F2;
+    plan[5 + ANTKV_HS_POOL_HIGH] = PH1;
+    plan[10] = push;
+    if (h == 0) c.positions[(int64_t)b * c.capacity + n] = a.qpos[b];   // read by nobody this step
   }
 }
 
-// Commit the plan (last CTA of (b, h), every reader of the head is done).
+// Commit the plan (last CTA of (b, h): every reader of the head is done).
+// All values were computed by prepare_update; these are independent stores
+// (program order keeps slot_new == evicted slot, window_size == 0, right).
 __device__ void commit_update(const antkv_cache_desc &c, const StepArgs &a, int b, int h, int n) {
   const int64_t bh = (int64_t)b * c.Hkv + h;
+  const int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * kPlanWords;
+  int p[11];
+#pragma unroll
+  for (int i = 0; i < 11; ++i) p[i] = __ldcg(plan + i);
+  const int slot_new = p[0], es = p[1], action = p[2], j = p[3];
   int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
-  const int *plan = a.cnt + (int64_t)c.B * c.Hkv + c.B + bh * 4;
-  const int slot_new = __ldcg(plan), es = __ldcg(plan + 1), action = __ldcg(plan + 2), j = __ldcg(plan + 3);
-  const int W1 = c.window_size + 1;
-  int32_t *ring = c.win_ring + bh * W1;
   if (slot_new >= 0) {
-    hs[ANTKV_HS_FREE_TOP] -= 1;
     c.pool_tok[bh * c.pool_capacity + slot_new] = n;
     c.pool_kind[bh * c.pool_capacity + slot_new] = ANTKV_KIND_WINDOWED;
-    ring[(hs[ANTKV_HS_WIN_HEAD] + hs[ANTKV_HS_WIN_COUNT]) % W1] = slot_new;
-    hs[ANTKV_HS_WIN_COUNT] += 1;
-    if (slot_new + 1 > hs[ANTKV_HS_POOL_HIGH]) hs[ANTKV_HS_POOL_HIGH] = slot_new + 1;
+    c.win_ring[bh * (c.window_size + 1) + p[4]] = slot_new;
   }
-  if (action != 0) {
-    hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % W1;
-    hs[ANTKV_HS_WIN_COUNT] -= 1;
-    if (action == 1) {
-      c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_ANCHOR;
-      hs[ANTKV_HS_ANCHORS] += 1;
-    } else {
-      atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
-      c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_FREE;
-      c.pool_tok[bh * c.pool_capacity + es] = -1;
-      c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = es;
-      hs[ANTKV_HS_FREE_TOP] += 1;
-    }
+  if (action == 1) {
+    c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_ANCHOR;
+  } else if (action == 2) {
+    atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
+    c.pool_kind[bh * c.pool_capacity + es] = ANTKV_KIND_FREE;
+    c.pool_tok[bh * c.pool_capacity + es] = -1;
+    c.free_stack[bh * c.pool_capacity + p[10]] = es;
   }
+#pragma unroll
+  for (int i = 0; i < 5; ++i) hs[i] = p[5 + i];
 }
 
-// Per-warp streaming state for the code tiles.  A stage holds an even and an
-// odd 16-slot tile; both are multiplied with ONE B fragment: columns 0-3 are
-// the 4 query heads in the even tile's frame R(p_q - P0) q (lanes 0-15),
-// columns 4-7 in the odd tile's frame R(p_q - P0 - 16) q (lanes 16-31).  Row r
-// of a tile is rotated by R(r), r = g or g + 8.  Even-tile scores are read
-// from columns 0-3 and odd-tile scores from 4-7, so the O^T columns 0-3 / 4-7
-// accumulate two independent streams merged at the end.
+// ------------------------------------------------------------ streaming
+// Per-warp state.  Lane (g = lane / 4, t = lane % 4) holds, per k-step s,
+// the query-frame pairs 8s + t (u = 0) and 8s + 4 + t (u = 1) of column g.
 struct WarpState {
   uint32_t kc[8][8];      // key rotation (cos,sin)/(-sin,cos) for rows g, g+8
-  float fx[16], fy[16];   // query frame pairs (log2-scaled)
-  float stc[16], sts[16]; // R(-32) per pair
+  float2 fx[8], fy[8];    // frame pairs k = 2s + u, planar: fx[s] = (x_{2s}, x_{2s+1})
+  float2 sc[8], ss[8];    // cos / sin of -32 omega for the same pairs
   float mrun[2], lrun[2]; // softmax of this lane's 2 columns (log2 units; lrun per lane)
   float o[8][4];          // O^T accumulators
 };
 
-// Code records of one 16-slot tile for this lane: 8 K codes (groups 2s+pk)
-// and 8 V codes (groups 2mt+pv), packed 4 per word.
-struct TileCodes {
-  uint32_t k0, k1, v0, v1;
+// Per-lane constants of the code-tile addressing.
+struct LaneAddr {
+  uint32_t lcK, lcV;      // copy offset (lane & 7) * 16 (+128 for V) in byte 0
+  uint32_t sK0, sK1;      // prmt selectors: byte 2(s&1) + (lane >> 4) of a K code word -> byte 1
+  uint32_t sV0, sV1;      // byte 2(mt&1) + ((lane >> 3) & 1) of a V code word -> byte 1
 };
 
-__device__ __forceinline__ TileCodes tile_codes(const uint8_t *tb, int tk, int tv, uint32_t sel_k,
-                                                uint32_t sel_v) {
-  const uint4 kr = *reinterpret_cast<const uint4 *>(tb + tk * 16);
-  const uint4 vr = *reinterpret_cast<const uint4 *>(tb + 256 + tv * 16);
-  TileCodes tc;
-  tc.k0 = __byte_perm(kr.x, kr.y, sel_k);
-  tc.k1 = __byte_perm(kr.z, kr.w, sel_k);
-  tc.v0 = __byte_perm(vr.x, vr.y, sel_v);
-  tc.v1 = __byte_perm(vr.z, vr.w, sel_v);
-  return tc;
+__device__ __forceinline__ uint32_t word_of(const uint4 &v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
-// Shared-memory address of centroid `byte k of word` in a replicated codebook.
-__device__ __forceinline__ uint32_t cb_addr(uint32_t word, int k, uint32_t base) {
-  uint32_t code, addr;
-  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(code) : "r"(word), "r"(0x4440 + k));
-  asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(addr) : "r"(code), "r"(base));
-  return addr;
-}
-
-// S^T = rot(K_hat) . B (8 HMMA in two chains); returns the 4 accumulators.
-__device__ __forceinline__ float4 qk_tile(const WarpState &w, const TileCodes &tc,
-                                          const uint32_t (&bq)[8][2], uint32_t cbK_base) {
+// S^T = rot(K_hat) . B (8 HMMA in two chains) for one tile whose 16 K codes
+// of this lane's ldmatrix row are `kr`.
+__device__ __forceinline__ float4 qk_tile(const WarpState &w, const uint4 &kr,
+                                          const uint32_t (&bq)[8][2], const LaneAddr &la) {
   float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     uint32_t a[4];
-    ldsm_x4(cb_addr(s < 4 ? tc.k0 : tc.k1, s & 3, cbK_base), a);
+    ldsm_cb(prmt(word_of(kr, s >> 1), la.lcK, (s & 1) ? la.sK1 : la.sK0), a);
     a[0] = rot2(a[0], w.kc[s][0], w.kc[s][1]);
     a[1] = rot2(a[1], w.kc[s][2], w.kc[s][3]);
     a[2] = rot2(a[2], w.kc[s][4], w.kc[s][5]);
@@ -533,37 +441,21 @@ __device__ __forceinline__ float4 qk_tile(const WarpState &w, const TileCodes &t
 }
 
 // O^T += V_hat^T . P (8 independent HMMA).
-__device__ __forceinline__ void pv_tile(WarpState &w, const TileCodes &tc, uint32_t pb0,
-                                        uint32_t pb1, uint32_t cbV_base) {
+__device__ __forceinline__ void pv_tile(WarpState &w, const uint4 &vr, uint32_t pb0, uint32_t pb1,
+                                        const LaneAddr &la) {
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
     uint32_t a[4];
-    ldsm_x4_t(cb_addr(mt < 4 ? tc.v0 : tc.v1, mt & 3, cbV_base), a);
+    ldsm_cb_t(prmt(word_of(vr, mt >> 1), la.lcV, (mt & 1) ? la.sV1 : la.sV0), a);
     mma16816(w.o[mt], a, pb0, pb1);
   }
 }
 
-// One stage = even + odd tile.  `mrow` holds this lane's two row-valid bits
-// (row g in bit 0, row g+8 in bit 1) of the tile whose columns it owns.
-__device__ __forceinline__ void stage_tiles(WarpState &w, const TileCodes &te, const TileCodes &to,
-                                            uint32_t mrow, uint32_t cbK_base, uint32_t cbV_base,
-                                            bool lo) {
-  uint32_t bq[8][2];
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    bq[s][0] = h2u(__floats2half2_rn(w.fx[2 * s], w.fy[2 * s]));
-    bq[s][1] = h2u(__floats2half2_rn(w.fx[2 * s + 1], w.fy[2 * s + 1]));
-  }
-  const float4 se = qk_tile(w, te, bq, cbK_base);
-  const float4 so = qk_tile(w, to, bq, cbK_base);
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const float x = w.fx[k], y = w.fy[k];
-    w.fx[k] = x * w.stc[k] - y * w.sts[k];
-    w.fy[k] = x * w.sts[k] + y * w.stc[k];
-  }
-  // this lane's scores: (row g, col 2t), (row g, 2t+1), (row g+8, 2t), (row g+8, 2t+1)
-  const float4 sv = lo ? se : so;
+// Online softmax of this lane's 4 scores (rows g / g+8, columns 2t / 2t+1;
+// `mrow` bit 0 = row g valid, bit 1 = row g+8).  Returns P packed as the
+// C-fragment half2 pairs of rows g and g+8.
+__device__ __forceinline__ void softmax_p(WarpState &w, const float4 &sv, uint32_t mrow,
+                                          uint32_t &x0, uint32_t &x1) {
   const bool v0 = mrow & 1u, v1 = mrow & 2u;
   const float s00 = v0 ? sv.x : -INFINITY, s01 = v0 ? sv.y : -INFINITY;
   const float s10 = v1 ? sv.z : -INFINITY, s11 = v1 ? sv.w : -INFINITY;
@@ -590,179 +482,415 @@ __device__ __forceinline__ void stage_tiles(WarpState &w, const TileCodes &te, c
   const float p10 = v1 ? ex2(s10 - w.mrun[0]) : 0.f, p11 = v1 ? ex2(s11 - w.mrun[1]) : 0.f;
   w.lrun[0] += p00 + p10;
   w.lrun[1] += p01 + p11;
-  const uint32_t x0 = h2u(__floats2half2_rn(p00, p01));   // P[row g][cols 2t, 2t+1]
-  const uint32_t x1 = h2u(__floats2half2_rn(p10, p11));   // P[row g+8][...]
-  pv_tile(w, te, movm_t(lo ? x0 : 0u), movm_t(lo ? x1 : 0u), cbV_base);
-  pv_tile(w, to, movm_t(lo ? 0u : x0), movm_t(lo ? 0u : x1), cbV_base);
+  x0 = pack_h2(p00, p01);   // P[row g][cols 2t, 2t+1]
+  x1 = pack_h2(p10, p11);   // P[row g+8][...]
+}
+
+// One code stage = even + odd tile.  `mrow` holds this lane's two row-valid
+// bits of the tile whose columns it owns.
+__device__ __forceinline__ void stage_tiles(WarpState &w, const uint4 &kre, const uint4 &vre,
+                                            const uint4 &kro, const uint4 &vro, uint32_t mrow,
+                                            const LaneAddr &la, bool lo) {
+  uint32_t bq[8][2];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    bq[s][0] = pack_h2(w.fx[s].x, w.fy[s].x);
+    bq[s][1] = pack_h2(w.fx[s].y, w.fy[s].y);
+  }
+  const float4 se = qk_tile(w, kre, bq, la);
+  const float4 so = qk_tile(w, kro, bq, la);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {   // frames advance by R(-32): packed fp32 complex multiply
+    const float2 x = w.fx[s], y = w.fy[s];
+    w.fx[s] = __ffma2_rn(make_float2(-y.x, -y.y), w.ss[s], __fmul2_rn(x, w.sc[s]));
+    w.fy[s] = __ffma2_rn(y, w.sc[s], __fmul2_rn(x, w.ss[s]));
+  }
+  uint32_t x0, x1;
+  softmax_p(w, lo ? se : so, mrow, x0, x1);
+  pv_tile(w, vre, movm_t(lo ? x0 : 0u), movm_t(lo ? x1 : 0u), la);
+  pv_tile(w, vro, movm_t(lo ? 0u : x0), movm_t(lo ? 0u : x1), la);
+}
+
+// Online softmax over two stages at once (one lazy-max check): sA / sB are
+// this lane's scores of stage A / B, mA / mB their row-valid bits.
+__device__ __forceinline__ void softmax_p2(WarpState &w, const float4 &sA, uint32_t mA,
+                                           const float4 &sB, uint32_t mB, uint32_t (&x)[4]) {
+  float v[8];
+  v[0] = (mA & 1u) ? sA.x : -INFINITY;
+  v[1] = (mA & 1u) ? sA.y : -INFINITY;
+  v[2] = (mA & 2u) ? sA.z : -INFINITY;
+  v[3] = (mA & 2u) ? sA.w : -INFINITY;
+  v[4] = (mB & 1u) ? sB.x : -INFINITY;
+  v[5] = (mB & 1u) ? sB.y : -INFINITY;
+  v[6] = (mB & 2u) ? sB.z : -INFINITY;
+  v[7] = (mB & 2u) ? sB.w : -INFINITY;
+  const float c0 = fmaxf(fmaxf(v[0], v[2]), fmaxf(v[4], v[6]));   // column 2t
+  const float c1 = fmaxf(fmaxf(v[1], v[3]), fmaxf(v[5], v[7]));   // column 2t+1
+  if (__any_sync(0xffffffffu, c0 > w.mrun[0] + 8.f || c1 > w.mrun[1] + 8.f)) {
+    const float mn0 = fmaxf(w.mrun[0], shfl_max_g(c0));
+    const float mn1 = fmaxf(w.mrun[1], shfl_max_g(c1));
+    const float a0 = (w.mrun[0] == mn0) ? 1.f : ex2(w.mrun[0] - mn0);
+    const float a1 = (w.mrun[1] == mn1) ? 1.f : ex2(w.mrun[1] - mn1);
+    w.lrun[0] *= a0;
+    w.lrun[1] *= a1;
+    w.mrun[0] = mn0;
+    w.mrun[1] = mn1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      w.o[i][0] *= a0;
+      w.o[i][1] *= a1;
+      w.o[i][2] *= a0;
+      w.o[i][3] *= a1;
+    }
+  }
+  // a column with no valid score yet keeps mrun = -inf: subtract 0 instead
+  const float m0 = w.mrun[0] == -INFINITY ? 0.f : w.mrun[0];
+  const float m1 = w.mrun[1] == -INFINITY ? 0.f : w.mrun[1];
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = ex2(v[i] - ((i & 1) ? m1 : m0));   // ex2(-inf) = 0
+  w.lrun[0] += (p[0] + p[2]) + (p[4] + p[6]);
+  w.lrun[1] += (p[1] + p[3]) + (p[5] + p[7]);
+  x[0] = pack_h2(p[0], p[1]);   // stage A, row g
+  x[1] = pack_h2(p[2], p[3]);   // stage A, row g+8
+  x[2] = pack_h2(p[4], p[5]);
+  x[3] = pack_h2(p[6], p[7]);
+}
+
+__device__ __forceinline__ void advance_frames(WarpState &w) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {   // frames advance by R(-32): packed fp32 complex multiply
+    const float2 x = w.fx[s], y = w.fy[s];
+    w.fx[s] = __ffma2_rn(make_float2(-y.x, -y.y), w.ss[s], __fmul2_rn(x, w.sc[s]));
+    w.fy[s] = __ffma2_rn(y, w.sc[s], __fmul2_rn(x, w.ss[s]));
+  }
+}
+
+// One ring slot = two stages = tiles 0..3 (stage A: 0 even / 1 odd, stage B:
+// 2 / 3).  All QK products first (8 independent HMMA chains), one softmax,
+// then all PV products, so each phase is one long basic block.
+__device__ __forceinline__ void slot_tiles(WarpState &w, const uint8_t *tb, int tk, int tv,
+                                           uint32_t qwA, uint32_t qwB, const LaneAddr &la,
+                                           bool lo) {
+  const uint4 k0 = *reinterpret_cast<const uint4 *>(tb + 0 * FK_TILE_BYTES + tk * 16);
+  const uint4 k1 = *reinterpret_cast<const uint4 *>(tb + 1 * FK_TILE_BYTES + tk * 16);
+  const uint4 k2 = *reinterpret_cast<const uint4 *>(tb + 2 * FK_TILE_BYTES + tk * 16);
+  const uint4 k3 = *reinterpret_cast<const uint4 *>(tb + 3 * FK_TILE_BYTES + tk * 16);
+  float4 sA, sB;
+  {
+    uint32_t bq[8][2];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      bq[s][0] = pack_h2(w.fx[s].x, w.fy[s].x);
+      bq[s][1] = pack_h2(w.fx[s].y, w.fy[s].y);
+    }
+    const float4 s0 = qk_tile(w, k0, bq, la);
+    const float4 s1 = qk_tile(w, k1, bq, la);
+    sA = lo ? s0 : s1;
+  }
+  advance_frames(w);
+  {
+    uint32_t bq[8][2];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      bq[s][0] = pack_h2(w.fx[s].x, w.fy[s].x);
+      bq[s][1] = pack_h2(w.fx[s].y, w.fy[s].y);
+    }
+    const float4 s2 = qk_tile(w, k2, bq, la);
+    const float4 s3 = qk_tile(w, k3, bq, la);
+    sB = lo ? s2 : s3;
+  }
+  advance_frames(w);
+  const uint4 v0 = *reinterpret_cast<const uint4 *>(tb + 0 * FK_TILE_BYTES + 256 + tv * 16);
+  const uint4 v1 = *reinterpret_cast<const uint4 *>(tb + 1 * FK_TILE_BYTES + 256 + tv * 16);
+  const uint4 v2 = *reinterpret_cast<const uint4 *>(tb + 2 * FK_TILE_BYTES + 256 + tv * 16);
+  const uint4 v3 = *reinterpret_cast<const uint4 *>(tb + 3 * FK_TILE_BYTES + 256 + tv * 16);
+  uint32_t x[4];
+  softmax_p2(w, sA, (qwA & 1u) | ((qwA >> 7) & 2u), sB, (qwB & 1u) | ((qwB >> 7) & 2u), x);
+  pv_tile(w, v0, movm_t(lo ? x[0] : 0u), movm_t(lo ? x[1] : 0u), la);
+  pv_tile(w, v1, movm_t(lo ? 0u : x[0]), movm_t(lo ? 0u : x[1]), la);
+  pv_tile(w, v2, movm_t(lo ? x[2] : 0u), movm_t(lo ? x[3] : 0u), la);
+  pv_tile(w, v3, movm_t(lo ? 0u : x[2]), movm_t(lo ? 0u : x[3]), la);
+}
+
+// One pool tile (16 full-precision slots) in the absolute frame `bqa`
+// (columns 4-7 zero; only the lanes owning columns 0-3 keep scores).
+__device__ __forceinline__ void pool_tile(WarpState &w, uint32_t base, const uint32_t (&bqa)[8][2],
+                                          uint32_t mrow, bool lo) {
+  const int lane = threadIdx.x & 31;
+  const int tk = (lane & 7) + 8 * ((lane >> 3) & 1), hk = lane >> 4;
+  const int tv = (lane & 7) + 8 * (lane >> 4), pv = (lane >> 3) & 1;
+  float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    uint32_t a[4];
+    ldsm_x4(base + tk * 256 + ((((2 * s + hk) ^ (lane & 7))) << 4), a);
+    if (s & 1) mma16816(sb, a, bqa[s][0], bqa[s][1]);
+    else mma16816(sa, a, bqa[s][0], bqa[s][1]);
+  }
+  const float4 sv = make_float4(sa[0] + sb[0], sa[1] + sb[1], sa[2] + sb[2], sa[3] + sb[3]);
+  uint32_t x0, x1;
+  softmax_p(w, sv, lo ? mrow : 0u, x0, x1);
+  const uint32_t p0 = movm_t(lo ? x0 : 0u), p1 = movm_t(lo ? x1 : 0u);
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    uint32_t a[4];
+    ldsm_x4_t(base + 4096 + tv * 256 + ((((2 * mt + pv) ^ (lane & 7))) << 4), a);
+    mma16816(w.o[mt], a, p0, p1);
+  }
 }
 
 // ---------------------------------------------------------------- kernel
-// Every CTA of (b, h) handles an equal share of the code tiles and of the
-// pool rows; the last split also attends the appended token and prepares the
-// cache update; the last CTA to finish combines the partials and commits.
-__global__ void __launch_bounds__(FK_THREADS, 2)
+__global__ void __launch_bounds__(FK_THREADS, 1)
 decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
-  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.ring[0][0]);
+  MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.pool[0][0]);
   const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
   const int S = a.splits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int64_t bh = (int64_t)b * c.Hkv + h;
-  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
+  const bool last_split = split == S - 1;
+  const bool prep = last_split && a.knew;
+  unsigned long long tr[FK_TRACE_WORDS];
+#define FK_TR(i) \
+  if (a.trace && threadIdx.x == 0) tr[i] = gtimer();
+  FK_TR(1);
+
+  // ---- prologue.  Phase 0: scalar loads (not used until phase 1), barrier
+  // setup, then bulk copies of the codebook, the RoPE tables and the 4 query
+  // rows -- nothing waits on a global load before every copy is in flight.
   const double pq = static_cast<double>(a.qpos[b]);
   const int n = c.seq_len[b];
-  const bool last_split = split == S - 1;
-  unsigned long long tr[8];
-  if (a.trace && threadIdx.x == 0) tr[0] = gtimer();
-
-  // ---- code range: tiles [T0, T0 + per_cta), 4 contiguous warp ranges of Tw tiles
-  // the last split also prepares the cache update, so it gets half a share
-  const int ntiles = (n + 15) >> 4;
-  const float shares = (a.knew && S > 1) ? S - 0.5f : (float)S;
-  const int per_cta = ((int)ceilf(ntiles / shares) + 2 * FK_WARPS - 1) / (2 * FK_WARPS) * (2 * FK_WARPS);
-  const int T0 = split * per_cta;
-  const int mine = max(0, min(per_cta, ntiles - T0));           // valid tiles of this CTA
-  const int Tw = ((mine + FK_WARPS - 1) / FK_WARPS + 1) & ~1;   // even; tiles per warp
-  const int nstages = Tw / 2;
+  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
   const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
-  const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
-  const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
-  const int cap_tiles = c.capacity / 16;
-  const FastTables *tab = reinterpret_cast<const FastTables *>(c.fast_tables);
-
+  const int qbytes = 4 * 128 * dtype_size(a.qdtype);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < FK_STAGES; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], FK_WARPS);
+    for (int ww = 0; ww < FK_WARPS; ++ww) {
+      for (int s = 0; s < FK_NS; ++s) mbar_init(&sm.full[ww][s], 1);
+      mbar_init(&sm.pfull[ww], 1);
     }
     mbar_init(&sm.cbbar, 1);
+    mbar_init(&sm.tbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int st) {
-    const int slot = st % FK_STAGES;
-    mbar_expect_tx(&sm.full[slot], FK_STAGE_BYTES);
-    for (int w = 0; w < FK_WARPS; ++w) {
-      int tile = T0 + w * Tw + 2 * st;
-      if (tile + 2 > cap_tiles) tile = 0;   // beyond capacity: masked dummy data
-      tma_bulk_g2s(&sm.ring[slot][w * FK_WARP_STAGE_BYTES], codes + (int64_t)tile * FK_TILE_BYTES,
-                   FK_WARP_STAGE_BYTES, &sm.full[slot]);
-    }
-  };
-  const bool prep = last_split && a.knew;
-  // ---- pool rows (anchors + window) of this CTA's share first: their loads
-  // are issued before the code-tile bulk copies that follow in the hook
-  {
-    const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-    const int per = (pool_high + S - 1) / S;
-    const int r0 = min(pool_high, split * per), r1 = min(pool_high, r0 + per);
-    pool_rows_part(c, a, sm, pq, b, h, r0, (a.debug_mode & 1) ? r0 : r1, prep, [&]() {
-      if (threadIdx.x == 0)
-        for (int st = 0; st < min(nstages, FK_STAGES); ++st) issue(st);
-    });
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&sm.tbar, sizeof(FastTables) + qbytes);
+    tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
+    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
+                 qbytes, &sm.tbar);   // rows h*4 .. h*4+3 of sequence b
+    mbar_expect_tx(&sm.cbbar, FK_CB_BYTES);
+    tma_bulk_g2s(sm.cb, reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * FK_CB_BYTES,
+                 FK_CB_BYTES, &sm.cbbar);
   }
-  if (a.trace && threadIdx.x == 0) tr[4] = gtimer();
-  // ---- replicated fp16 codebooks: row `code` holds the centroid in all 8
-  // 16-byte bank groups (copy 0 of the prepared global layout is read)
-  if (nstages > 0 || prep) {
-    const uint4 *src = reinterpret_cast<const uint4 *>(c.codebook_f16) + (int64_t)h * 4096;
-    uint4 vk[2], vv[2];
+  FK_TR(2);
+
+  // ---- phase 1 (needs n / pool_high): work split, bulk copies of the code
+  // and pool tiles, qmask words, pool-tile kinds.  Code tiles: the last
+  // split also prepares the cache update, so it gets half a share; each warp
+  // streams Tw contiguous tiles.
+  const int ntiles = (n + 15) >> 4;
+  const float shares = (a.knew && S > 1) ? S - 0.5f : (float)S;
+  const int per_cta = ((int)ceilf(ntiles / shares) + 4 * FK_WARPS - 1) / (4 * FK_WARPS) * (4 * FK_WARPS);
+  const int T0 = split * per_cta;
+  const int mine = max(0, min(per_cta, ntiles - T0));
+  const int Tw = ((mine + FK_WARPS - 1) / FK_WARPS + 3) & ~3;   // a multiple of 4 tiles
+  const int nstages = Tw / 2;                                    // even
+  const int nslots = nstages / 2;
+  const int wt0 = T0 + warp * Tw;
+  const int cap_tiles = c.capacity / 16;
+  const uint8_t *codes = c.codes + bh * c.capacity * 32;   // 32 code bytes per slot
+  // pool tiles: an equal share per CTA, one tile per warp per round
+  const int ptiles = (pool_high + 15) >> 4;
+  const int pper = (ptiles + S - 1) / S;
+  const int pt0 = min(ptiles, split * pper), pt1 = min(ptiles, pt0 + pper);
+  const uint8_t *pool_g = reinterpret_cast<const uint8_t *>(c.pool_f16) + bh * c.pool_capacity * 512;
+  auto issue_code = [&](int it) {   // ring slot it % FK_NS <- tiles wt0 + 4 it .. + 3
+    const int slot = it % FK_NS;
+    int tile = wt0 + 4 * it;
+    if (tile + 4 > cap_tiles) tile = 0;   // beyond capacity: masked dummy data
+    mbar_expect_tx(&sm.full[warp][slot], FK_SLOT_BYTES);
+    tma_bulk_g2s(&sm.ring[warp][slot][0], codes + (int64_t)tile * FK_TILE_BYTES, FK_SLOT_BYTES,
+                 &sm.full[warp][slot]);
+  };
+  auto issue_pool = [&](int tile) {
+    mbar_expect_tx(&sm.pfull[warp], FK_POOL_TILE_BYTES);
+    tma_bulk_g2s(&sm.pool[warp][0], pool_g + (int64_t)tile * FK_POOL_TILE_BYTES, FK_POOL_TILE_BYTES,
+                 &sm.pfull[warp]);
+  };
+  if (lane == 0) {
+    if (pt0 + warp < pt1) issue_pool(pt0 + warp);
+    for (int it = 0; it < min(nslots, FK_NS); ++it) issue_code(it);
+  }
+  // qmask words of this warp's range (one word per stage), up to 2 per lane
+  const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
+  uint32_t qmv[2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int code = threadIdx.x + u * FK_THREADS;
-      vk[u] = __ldg(src + code * 8);
-      vv[u] = __ldg(src + 2048 + code * 8);
-    }
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int code = threadIdx.x + u * FK_THREADS;
-#pragma unroll
-      for (int cp = 0; cp < 8; ++cp) {
-        sm.cbK[code * 8 + ((cp + threadIdx.x) & 7)] = vk[u];
-        sm.cbV[code * 8 + ((cp + threadIdx.x) & 7)] = vv[u];
-      }
-    }
+  for (int u = 0; u < 2; ++u) {
+    const int i = lane + 32 * u, word = (wt0 >> 1) + i;
+    qmv[u] = (i < nstages && word * 32 < c.capacity) ? __ldcs(qmg + word) : 0u;
+  }
+  const int8_t *kinds = c.pool_kind + bh * c.pool_capacity;
+  int8_t kd0 = ANTKV_KIND_FREE, kd1 = ANTKV_KIND_FREE;
+  if (pt0 + warp < pt1) {
+    kd0 = kinds[(pt0 + warp) * 16 + g];
+    kd1 = kinds[(pt0 + warp) * 16 + g + 8];
+  }
+  FK_TR(3);
+
+  // ---- phase 2: (cos, sin) of every query frame of the CTA, cooperatively
+  // from float64-reduced angles (frame 2w + e: warp w's even / odd tile
+  // frame; frame 16: the absolute frame p_q of the pool rows)
+  mbar_wait(&sm.tbar, 0);
+  for (int e = threadIdx.x; e < (2 * FK_WARPS + 1) * 64; e += FK_THREADS) {
+    const int f = e >> 6, p = e & 63;
+    const double delta = f < 2 * FK_WARPS
+        ? pq - static_cast<double>(pos0 + (int64_t)(T0 + (f >> 1) * Tw) * 16 + (f & 1) * 16)
+        : pq;
+    float cs, sn;
+    rope_cs(delta * sm.tab.omega[p], cs, sn);
+    sm.ang[f][p] = make_float2(cs, sn);
   }
   __syncthreads();
-  if (a.trace && threadIdx.x == 0) tr[5] = gtimer();
-  if (a.debug_mode & 2) return;
-  for (int i = lane; i < Tw / 2; i += 32) {
-    const int word = ((T0 + warp * Tw) >> 1) + i;
-    sm.qm[warp][i] = (word * 32 < c.capacity) ? qmg[word] : 0u;
-  }
+  const float scale = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
   WarpState w;
+  uint32_t bqa[8][2];
+  {
+    const int qo = (g & 3) * 128;
+    const int fr = 2 * warp + (g >= 4 ? 1 : 0);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      float fxv[2], fyv[2], scv[2], ssv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int pair = 8 * s + 4 * u + t;
+        const uint2 k0 = *reinterpret_cast<const uint2 *>(&sm.tab.kc[g][pair][0]);
+        const uint2 k1 = *reinterpret_cast<const uint2 *>(&sm.tab.kc[g + 8][pair][0]);
+        w.kc[s][4 * u] = k0.x;
+        w.kc[s][4 * u + 1] = k0.y;
+        w.kc[s][4 * u + 2] = k1.x;
+        w.kc[s][4 * u + 3] = k1.y;
+        scv[u] = sm.tab.step[pair][0];
+        ssv[u] = sm.tab.step[pair][1];
+        const float x0 = load_elem(sm.qraw, qo + 2 * pair, a.qdtype) * scale;
+        const float x1 = load_elem(sm.qraw, qo + 2 * pair + 1, a.qdtype) * scale;
+        const float2 cf = sm.ang[fr][pair], ca = sm.ang[2 * FK_WARPS][pair];
+        fxv[u] = x0 * cf.x - x1 * cf.y;
+        fyv[u] = x0 * cf.y + x1 * cf.x;
+        bqa[s][u] = g < 4 ? pack_h2(x0 * ca.x - x1 * ca.y, x0 * ca.y + x1 * ca.x) : 0u;
+      }
+      w.fx[s] = make_float2(fxv[0], fxv[1]);
+      w.fy[s] = make_float2(fyv[0], fyv[1]);
+      w.sc[s] = make_float2(scv[0], scv[1]);
+      w.ss[s] = make_float2(ssv[0], ssv[1]);
+    }
+  }
   w.mrun[0] = w.mrun[1] = -INFINITY;
   w.lrun[0] = w.lrun[1] = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) w.o[i][e] = 0.f;
-  if (nstages > 0) {
+  FK_TR(4);
+  // ---- the appended token (prep CTA, warp 0): attended like a pool row
+  if (prep && warp == 0) {
+    const int64_t kb = bh * 128 + 4 * lane;
+    float kk[4], vv[4], cs[2], sn[2];
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int pair = 8 * s + 4 * u + t;
-        w.kc[s][4 * u] = tab->kc[g][pair][0];
-        w.kc[s][4 * u + 1] = tab->kc[g][pair][1];
-        w.kc[s][4 * u + 2] = tab->kc[g + 8][pair][0];
-        w.kc[s][4 * u + 3] = tab->kc[g + 8][pair][1];
-      }
+    for (int pp = 0; pp < 2; ++pp) {
+      const float2 ca = sm.ang[2 * FK_WARPS][2 * lane + pp];
+      cs[pp] = ca.x;
+      sn[pp] = ca.y;
+      const float x0 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp, a.kvdtype));
+      const float x1 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp + 1, a.kvdtype));
+      kk[2 * pp] = __half2float(__float2half_rn(x0 * cs[pp] - x1 * sn[pp]));
+      kk[2 * pp + 1] = __half2float(__float2half_rn(x0 * sn[pp] + x1 * cs[pp]));
     }
-    // query frame: lanes 0-15 head g in the even tile's frame, 16-31 head g-4 in the odd's
-    const int head = g & 3;
-    const int64_t first_slot = (int64_t)(T0 + warp * Tw) * 16 + (g >= 4 ? 16 : 0);
-    const double delta = pq - static_cast<double>(pos0 + first_slot);
-    const float scale = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
-    const int64_t qb = ((int64_t)b * c.Hq + h * 4 + head) * 128;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
+    for (int e = 0; e < 4; ++e)
+      vv[e] = __half2float(__float2half_rn(round_to(c.row_dtype, load_elem(a.vnew, kb + e, a.kvdtype))));
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int pair = 8 * s + 4 * u + t, k = 2 * s + u;
-        const float x0 = load_elem(a.q, qb + 2 * pair, a.qdtype) * scale;
-        const float x1 = load_elem(a.q, qb + 2 * pair + 1, a.qdtype) * scale;
-        float cs, sn;
-        rope_cs(delta * tab->omega[pair], cs, sn);
-        w.fx[k] = x0 * cs - x1 * sn;
-        w.fy[k] = x0 * sn + x1 * cs;
-        w.stc[k] = tab->step[pair][0];
-        w.sts[k] = tab->step[pair][1];
+    for (int hh = 0; hh < 4; ++hh) {
+      const int qh = hh * 128 + 4 * lane;
+      float sdot = 0.f;
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const float x0 = load_elem(sm.qraw, qh + 2 * pp, a.qdtype) * scale;
+        const float x1 = load_elem(sm.qraw, qh + 2 * pp + 1, a.qdtype) * scale;
+        sdot += (x0 * cs[pp] - x1 * sn[pp]) * kk[2 * pp] + (x0 * sn[pp] + x1 * cs[pp]) * kk[2 * pp + 1];
       }
+      sdot = warp_sum(sdot);
+      *reinterpret_cast<float4 *>(&sm.xo[hh][4 * lane]) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+      if (lane == 0) sm.xm[hh] = sdot;
     }
-    const uint32_t cbK_base = smem_u32(&sm.cbK[0]) + (lane & 7) * 16;
-    const uint32_t cbV_base = smem_u32(&sm.cbV[0]) + (lane & 7) * 16;
-    const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
-    const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
-    const uint32_t sel_k = (lane >> 4) ? 0x7531u : 0x6420u;
-    const uint32_t sel_v = ((lane >> 3) & 1) ? 0x7531u : 0x6420u;
-    const bool lo = t < 2;                                // owns the even tile's columns
-    const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >>7 above)
-    // the last split (smallest code share) prepares the cache update
-    if (prep) prepare_update(c, a, sm, b, h, n, pq);
-    if (a.trace && threadIdx.x == 0) tr[1] = gtimer();
-    for (int st = 0; st < nstages; ++st) {
-      const int slot = st % FK_STAGES;
-      mbar_wait(&sm.full[slot], (st / FK_STAGES) & 1);
-      const uint8_t *tb = &sm.ring[slot][warp * FK_WARP_STAGE_BYTES];
-      const TileCodes te = tile_codes(tb, tk, tv, sel_k, sel_v);
-      const TileCodes to = tile_codes(tb + FK_TILE_BYTES, tk, tv, sel_k, sel_v);
-      const uint32_t qw = sm.qm[warp][st] >> rowbit;
+  } else if (warp == 0 && lane < 4) {
+    sm.xm[lane] = -INFINITY;
+  }
+
+  const bool lo = t < 2;   // owns columns 0-3 (even tile / pool)
+  // ---- pool tiles (absolute frame: R(p_q) q, columns 4-7 zero)
+  if (pt0 + warp < pt1) {
+    int r = 0;
+    for (int tile = pt0 + warp; tile < pt1; tile += FK_WARPS, ++r) {
+      if (r > 0) {
+        kd0 = kinds[tile * 16 + g];
+        kd1 = kinds[tile * 16 + g + 8];
+      }
+      const uint32_t mrow = (kd0 != ANTKV_KIND_FREE ? 1u : 0u) | (kd1 != ANTKV_KIND_FREE ? 2u : 0u);
+      if (r == 0) FK_TR(5);
+      mbar_wait(&sm.pfull[warp], r & 1);
+      pool_tile(w, smem_u32(&sm.pool[warp][0]), bqa, mrow, lo);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.empty[slot]);   // codes are in registers
-      if (threadIdx.x == 0 && st + FK_STAGES < nstages) {
-        mbar_wait(&sm.empty[slot], (st / FK_STAGES) & 1);
-        issue(st + FK_STAGES);
+      if (lane == 0 && tile + FK_WARPS < pt1) {
+        fence_proxy_async();
+        issue_pool(tile + FK_WARPS);
       }
-      stage_tiles(w, te, to, (qw & 1u) | ((qw >> 7) & 2u), cbK_base, cbV_base, lo);
     }
   }
-  if (nstages == 0 && prep) prepare_update(c, a, sm, b, h, n, pq);
-  if (a.trace && threadIdx.x == 0) tr[2] = gtimer();
-  // ---- merge 4 warps x (2 code streams + pool rows) -> partial (natural log)
-  __syncthreads();   // all stages consumed; the ring becomes merge scratch
+  FK_TR(6);
+  if (prep) {
+    mbar_wait(&sm.cbbar, 0);
+    prepare_update(c, a, sm, b, h, n, pq);
+  }
+  FK_TR(7);
+
+  // ---- code tiles
+  if (nstages > 0) {
+    LaneAddr la;
+    la.lcK = (lane & 7) * 16;
+    la.lcV = la.lcK + 128;
+    la.sK0 = 0x5504u | ((0u + (lane >> 4)) << 4);
+    la.sK1 = 0x5504u | ((2u + (lane >> 4)) << 4);
+    la.sV0 = 0x5504u | ((0u + ((lane >> 3) & 1)) << 4);
+    la.sV1 = 0x5504u | ((2u + ((lane >> 3) & 1)) << 4);
+    const int tk = (lane & 7) + 8 * ((lane >> 3) & 1);     // K-side token row
+    const int tv = (lane & 7) + 8 * (lane >> 4);          // V-side token row
+    const int rowbit = g + (lo ? 0 : 16);                 // rows g (+8 via >> 7 below)
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (lane + 32 * u < nstages) sm.qm[warp][lane + 32 * u] = qmv[u];
+    __syncwarp();                                         // qm words visible to the warp
+    mbar_wait(&sm.cbbar, 0);
+    FK_TR(8);
+    for (int it = 0; it < nslots; ++it) {
+      const int slot = it % FK_NS;
+      mbar_wait(&sm.full[warp][slot], (it / FK_NS) & 1);
+      const uint32_t qwA = sm.qm[warp][2 * it] >> rowbit, qwB = sm.qm[warp][2 * it + 1] >> rowbit;
+      slot_tiles(w, &sm.ring[warp][slot][0], tk, tv, qwA, qwB, la, lo);
+      __syncwarp();
+      if (lane == 0 && it + FK_NS < nslots) {   // every lane has read the slot: refill it
+        fence_proxy_async();
+        issue_code(it + FK_NS);
+      }
+    }
+  }
+  FK_TR(9);
+  mbar_wait(&sm.cbbar, 0);   // no bulk copy may still be in flight at exit
+
+  // ---- merge 8 warps x 2 streams (+ the appended token) -> partial (natural log)
+  __syncthreads();   // pool tiles consumed: the pool area becomes merge scratch
   const float ln2 = 0.6931471805599453f;
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -773,136 +901,150 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
   const float lsum0 = shfl_sum_g(w.lrun[0]), lsum1 = shfl_sum_g(w.lrun[1]);
   if (g == 0) {
-    mg.m[warp][2 * t] = w.mrun[0] * ln2;
-    mg.m[warp][2 * t + 1] = w.mrun[1] * ln2;
+    mg.m[warp][2 * t] = w.mrun[0];
+    mg.m[warp][2 * t + 1] = w.mrun[1];
     mg.l[warp][2 * t] = lsum0;
     mg.l[warp][2 * t + 1] = lsum1;
   }
   __syncthreads();
+  const int64_t rows = (int64_t)c.B * c.Hq;
+  const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
   for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
-    const int hh = i / 128, dim = i % 128;
-    float M = -INFINITY;
-    for (int ww = 0; ww < FK_WARPS; ++ww)
-      M = fmaxf(M, fmaxf(fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]), sm.pm[ww][hh]));
+    const int hh = i >> 7, dim = i & 127;
+    float M = sm.xm[hh];
+#pragma unroll
+    for (int ww = 0; ww < FK_WARPS; ++ww) M = fmaxf(M, fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]));
     float L = 0.f, O = 0.f;
     if (M != -INFINITY) {
+      if (sm.xm[hh] != -INFINITY) {
+        const float f = ex2(sm.xm[hh] - M);
+        L = f;
+        O = f * sm.xo[hh][dim];
+      }
+#pragma unroll
       for (int ww = 0; ww < FK_WARPS; ++ww) {
 #pragma unroll
-        for (int src = 0; src < 3; ++src) {
-          const float mv = src < 2 ? mg.m[ww][hh + 4 * src] : sm.pm[ww][hh];
+        for (int src = 0; src < 2; ++src) {
+          const float mv = mg.m[ww][hh + 4 * src];
           if (mv == -INFINITY) continue;
-          const float f = __expf(mv - M);
-          L += f * (src < 2 ? mg.l[ww][hh + 4 * src] : sm.pl[ww][hh]);
-          O += f * (src < 2 ? mg.o[ww][hh + 4 * src][dim] : sm.po[ww][hh][dim]);
+          const float f = ex2(mv - M);
+          L += f * mg.l[ww][hh + 4 * src];
+          O += f * mg.o[ww][hh + 4 * src][dim];
         }
       }
     }
     a.ws_o[(row0 + hh) * 128 + dim] = O;
     if (dim == 0) {
-      a.ws_m[row0 + hh] = M;
+      a.ws_m[row0 + hh] = M * ln2;
       a.ws_l[row0 + hh] = L;
     }
   }
 
-  // ---- ticket: the last CTA of (b, h) combines the partials and commits
+  // ---- tickets: the last CTA of (b, h) combines and commits; the last CTA
+  // of sequence b publishes its new length
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
+  if (threadIdx.x == 0) {
+    sm.ticket = atomicAdd(&a.cnt[bh], 1);
+    sm.gticket = a.knew ? atomicAdd(&a.cnt[(int64_t)c.B * c.Hkv + b], 1) : -1;
+  }
   __syncthreads();
   if (a.trace && threadIdx.x == 0) {
-    tr[3] = gtimer();
-    unsigned long long *o = a.trace + 8 * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    tr[10] = gtimer();
+    unsigned long long *o =
+        a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
     o[0] = smid() | ((unsigned long long)sm.ticket << 32);
-    o[1] = tr[0];
-    o[2] = tr[1];
-    o[3] = tr[2];
-    o[4] = tr[3];
-    o[5] = 0;
-    o[6] = tr[4];
-    o[7] = tr[5];
+    for (int i = 1; i <= 10; ++i) o[i] = tr[i];
+    o[11] = 0;
+  }
+  if (threadIdx.x == 0 && sm.gticket == c.Hkv * S - 1) {
+    // every CTA of sequence b has read seq_len: publish the appended token
+    c.seq_len[b] = n + 1;
+    a.cnt[(int64_t)c.B * c.Hkv + b] = 0;
   }
   if (sm.ticket != S - 1) return;
   __threadfence();
-  const int64_t rows = (int64_t)c.B * c.Hq;
-  float *wts = reinterpret_cast<float *>(&sm.ring[0][0]);   // [S][4] (merge data consumed)
-  float *hdr = wts + 4 * S;                                       // [4] M, [4] L
-  {
-    const int hh = warp;   // warp hh: max / normaliser over splits for head hh
-    const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
-    float M = -INFINITY;
-    for (int s2 = lane; s2 < S; s2 += 32) M = fmaxf(M, __ldcg(a.ws_m + s2 * rows + row));
-    M = warp_max(M);
-    float L = 0.f;
-    for (int s2 = lane; s2 < S; s2 += 32) {
-      const float ms = __ldcg(a.ws_m + s2 * rows + row);
-      const float wv = (ms == -INFINITY) ? 0.f : __expf(ms - M);
-      wts[s2 * 4 + hh] = wv;
-      L += wv * __ldcg(a.ws_l + s2 * rows + row);
-    }
-    L = warp_sum(L);
-    if (lane == 0) {
-      hdr[hh] = M;
-      hdr[4 + hh] = L;
-      if (a.lse) a.lse[row] = M + logf(L);
-    }
-  }
-  __syncthreads();
-  {
-    // thread = (head warp, 4 consecutive dims); 8 split rows in flight per round
+  if (warp < 4) {
+    // warp hh combines head hh: lane = 4 dims; one pass over the splits with
+    // a running max (all loads of a chunk of 8 splits in flight together)
     const int hh = warp, d4 = 4 * lane;
     const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
+    float M = -INFINITY, L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s0 = 0; s0 < S; s0 += 8) {
+      float ms[8], ls[8];
       float4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int s2 = min(s0 + u, S - 1);
+        ms[u] = (s0 + u < S) ? __ldcg(a.ws_m + s2 * rows + row) : -INFINITY;
+        ls[u] = __ldcg(a.ws_l + s2 * rows + row);
         v[u] = __ldcg(reinterpret_cast<const float4 *>(a.ws_o + (s2 * rows + row) * 128 + d4));
       }
+      float mc = M;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mc = fmaxf(mc, ms[u]);
+      if (mc == -INFINITY) continue;
+      const float al = (M == -INFINITY) ? 0.f : __expf(M - mc);
+      L *= al;
+      acc.x *= al; acc.y *= al; acc.z *= al; acc.w *= al;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const float wv = (s0 + u < S) ? wts[(s0 + u) * 4 + hh] : 0.f;
+        const float wv = (ms[u] == -INFINITY) ? 0.f : __expf(ms[u] - mc);
+        L = fmaf(wv, ls[u], L);
         acc.x = fmaf(wv, v[u].x, acc.x);
         acc.y = fmaf(wv, v[u].y, acc.y);
         acc.z = fmaf(wv, v[u].z, acc.z);
         acc.w = fmaf(wv, v[u].w, acc.w);
       }
+      M = mc;
     }
-    const float inv = 1.f / hdr[4 + hh];
+    const float inv = 1.f / L;
     *reinterpret_cast<float4 *>(a.out + row * 128 + d4) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-  }
-  if (threadIdx.x == 0) {
-    if (a.knew) commit_update(c, a, b, h, n);
-    if (a.trace) a.trace[8 * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) + 5] = gtimer();
-    __threadfence();
+    if (lane == 0 && a.lse) a.lse[row] = M + logf(L);
+  } else if (threadIdx.x == 128) {
+    if (a.knew) commit_update(c, a, b, h, n);   // overlaps the combine
+    if (a.trace)
+      a.trace[FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) + 11] = gtimer();
     a.cnt[bh] = 0;
-    if (a.knew) {
-      // the last head of sequence b publishes the new length / position
-      int *cb = a.cnt + (int64_t)c.B * c.Hkv + b;
-      if (atomicAdd(cb, 1) == c.Hkv - 1) {
-        c.positions[(int64_t)b * c.capacity + n] = a.qpos[b];
-        __threadfence();
-        c.seq_len[b] = n + 1;
-        *cb = 0;
-      }
-    }
   }
+}
+
+__global__ void smem_base_probe_kernel(uint32_t *out) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  *out = smem_u32(smraw);
+}
+
+// The kernel's gathers assume dynamic shared memory starts at 0x400.
+int decode_fast_smem_base_ok() {
+  static int ok = -1;
+  if (ok < 0) {
+    uint32_t *d = nullptr, h = 0;
+    ok = 0;
+    if (cudaMalloc(&d, 4) == cudaSuccess) {
+      smem_base_probe_kernel<<<1, 1, 1024>>>(d);
+      if (cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost) == cudaSuccess) ok = (h == FK_SMEM_BASE);
+      cudaFree(d);
+    }
+    cudaGetLastError();
+  }
+  return ok;
 }
 
 int decode_fast_supported(const antkv_cache_desc &c) {
-  return c.d == 128 && c.d_sub == 8 && c.m <= 256 && c.code_bytes == 1 && c.Hq == 4 * c.Hkv &&
-         c.codebook_f16 != nullptr && c.pool_krot != nullptr && c.fast_tables != nullptr &&
-         c.capacity % 128 == 0;
+  return decode_fast_smem_base_ok() && c.d == 128 && c.d_sub == 8 && c.m <= 256 && c.code_bytes == 1 && c.Hq == 4 * c.Hkv &&
+         c.codebook_f16 != nullptr && c.pool_f16 != nullptr && c.fast_tables != nullptr &&
+         c.capacity % 128 == 0 && c.pool_capacity % 16 == 0;
 }
 
-// CTAs per (sequence, head): ~2 resident CTAs per SM in total.
+// CTAs per (sequence, head): one resident CTA per SM in total.
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits) {
   const int bh = c.B * c.Hkv;
-  code_splits = requested > 0 ? requested : max(1, (2 * 148) / bh);
-  // per-warp qmask staging caps a CTA at 4 warps x 128 tiles (FK_MAX_WARP_WORDS)
-  const int cap_tiles = c.capacity / 16;
-  const int min_code = (cap_tiles + 503) / 504;
+  code_splits = requested > 0 ? requested : max(1, 148 / bh);
+  // per-warp qmask staging caps a CTA at 8 warps x 128 tiles (FK_MAX_WARP_WORDS)
+  // (per_cta <= 1008 tiles once splits >= cap_tiles / 1000 + 1)
+  const int min_code = c.capacity / 16 / 1000 + 1;
   if (code_splits < min_code) code_splits = min_code;
   pool_splits = 0;
 }
@@ -915,7 +1057,7 @@ static unsigned long long *debug_trace_buffer() {
     const char *e = getenv("ANTKV_TRACE");
     enabled = e && e[0] == '1';
     if (enabled) {
-      g_trace_n = 8 * 65536;
+      g_trace_n = FK_TRACE_WORDS * 65536;
       if (cudaMalloc(&g_trace, sizeof(unsigned long long) * g_trace_n) != cudaSuccess) g_trace = nullptr;
     }
   }
@@ -925,8 +1067,8 @@ static unsigned long long *debug_trace_buffer() {
 }  // namespace antkv
 
 // Debug: copy the per-CTA timeline of the last traced fast-decode launch
-// (8 words per CTA: smid | ticket << 32, t_start, t_loop, t_pool, t_done,
-// t_committed) to host memory.  Returns the number of words copied.
+// (FK_TRACE_WORDS = 16 words per CTA, see FK_TRACE_WORDS) to host memory.
+// Returns the number of words copied.
 extern "C" int antkv_debug_trace(unsigned long long *host, int max_words) {
   if (!antkv::g_trace) return 0;
   const int n = max_words < antkv::g_trace_n ? max_words : antkv::g_trace_n;
@@ -960,16 +1102,12 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   decode_fast_plan(c, splits, cs, ps);
   a.splits = cs + ps;
   a.trace = debug_trace_buffer();
-  {
-    static int dm = -1;
-    if (dm < 0) {
-      const char *e = getenv("ANTKV_DEBUG_MODE");
-      dm = e ? atoi(e) : 0;
-    }
-    a.debug_mode = dm;
-  }
   const size_t smem = sizeof(FastSmem);
-  cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
   dim3 grid(a.splits, c.Hkv, c.B);
   decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, a);
   ANTKV_LAUNCH_CHECK("decode_fast_kernel");

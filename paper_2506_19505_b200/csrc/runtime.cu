@@ -29,6 +29,8 @@ extern "C" const char *antkv_last_error(void) { return g_err; }
 
 extern "C" int antkv_version(void) { return 1; }
 
+namespace antkv { int decode_fast_smem_base_ok(); }
+
 extern "C" int antkv_device_check(int device) {
   cudaDeviceProp p;
   cudaError_t e = cudaGetDeviceProperties(&p, device);
@@ -43,5 +45,6 @@ extern "C" int antkv_device_check(int device) {
     cuda_status(e, "kernel image");
     return 0;
   }
+  antkv::decode_fast_smem_base_ok();   // one-time probe, outside any stream capture
   return 1;
 }

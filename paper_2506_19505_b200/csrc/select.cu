@@ -1,18 +1,18 @@
-// Anchor selection (anchors.py:259-301) on the GPU.
+// Anchor selection (anchors.py:90-132) on the GPU.
 //
 // The reference ranks by lexsort((index, -score)) and takes prefixes.  Every
 // policy reduces to "top-k SET" queries with ties to the lower index:
 //   by_k   = topk(ans_k, B)
 //   by_v   = topk(ans_v, B)
 //   by_sum = S_K := topk(ans_k, B/2);  S_V := topk(ans_v restricted to the
-//            complement of S_K, B - B/2)   (the V fill of anchors.py:281-288
+//            complement of S_K, B - B/2)   (the V fill of anchors.py:112-119
 //            walks the V ranking skipping S_K, which is exactly that set);
-//            the K top-off (anchors.py:290-295) can never fire once the budget
+//            the K top-off (anchors.py:121-126) can never fire once the budget
 //            is clipped to n.
 // A top-k set is {key > T} plus the lowest-index elements with key == T,
 // where T is found by an 8-bit radix select over the order-preserving
 // uint32 image of the float scores.  The result is compacted in index order,
-// i.e. already sorted (anchors.py:298).  One 1024-thread CTA per (b, head).
+// i.e. already sorted (anchors.py:129).  One 1024-thread CTA per (b, head).
 #include "common.cuh"
 
 namespace antkv {
