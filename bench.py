@@ -160,6 +160,20 @@ def build_layers(args, rank, world, torch):
     return caches, cfg
 
 
+def measured_traffic(args):
+    """DRAM bytes per decode launch from the committed ncu --set full capture
+    (profiles/decode_fast_traffic.json) when it was taken on this workload."""
+    f = ROOT / "profiles" / "decode_fast_traffic.json"
+    try:
+        t = json.loads(f.read_text())
+    except (OSError, ValueError):
+        return None
+    if (t.get("ctx"), t.get("notation"), t.get("batch")) == (args.ctx, args.notation, args.batch) \
+            and args.kernel == "fast":
+        return t["dram_bytes_per_launch"]
+    return None
+
+
 def algorithmic_bytes(cache, torch):
     """Bytes one decode-attention call must move (SURVEY.md §8d formula):
     H_kv*[n_q*(code bytes/token) + n_fp*2*d*2] + 2*H_q*d*2 + codebooks."""
@@ -413,7 +427,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "decode attention (split-KV + combine)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "traffic": None, "algorithmic_bytes_per_launch": alg_bytes,
+                         "traffic": measured_traffic(args), "algorithmic_bytes_per_launch": alg_bytes,
                          "launch_ms": attn_ms},
             "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,

@@ -173,3 +173,16 @@ def test_sequence_sharded_merge_gloo_world2():
         assert p.exitcode == 0
     A = O.softmax_rows((q[None] @ K.T) / np.sqrt(16))
     assert np.abs(merged[0] - (A @ V)[0]).max() < 1e-5
+
+
+def test_package_never_imports_the_oracle():
+    """The product path has no CPU fallback: nothing in the package (Python or
+    CUDA sources) refers to oracle/ or numpy re-implementations of the path."""
+    import re
+    from pathlib import Path
+    pkg = Path(__file__).resolve().parent.parent / "paper_2506_19505_b200"
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
+        src = f.read_text()
+        assert not re.search(r"^\s*(import|from)\s+\S*oracle", src, re.M), f
+        assert "antkv_oracle" not in src, f
+        assert "/root/reference" not in src, f
