@@ -13,7 +13,9 @@ import torch
 
 from .errors import UnsupportedError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libantkv_b200.so"
+# ANTKV_LIB overrides the library path (kernel experiments); there is no fallback
+LIB_PATH = Path(os.environ.get("ANTKV_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libantkv_b200.so")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 F32, BF16, F16 = 0, 1, 2

@@ -74,6 +74,19 @@ class MemoryReport:
     fp_baseline_bits: int
 
 
+_FAST_TABLES = {}
+
+
+def _shared_fast_tables(dev, theta):
+    """RoPE constant tables of the fast decode kernel.  They depend only on
+    theta (d = 128), so every cache of the process shares one copy, which
+    stays L2-resident across the layers of a decode step."""
+    key = (dev.index, theta)
+    if key not in _FAST_TABLES:
+        _FAST_TABLES[key] = torch.zeros((16384,), dtype=torch.uint8, device=dev)
+    return _FAST_TABLES[key]
+
+
 def _round_up(x, m):
     return (x + m - 1) // m * m
 
@@ -151,7 +164,7 @@ class QuantizedKVCache:
         use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         if use_fast:
             t["cb_f16"] = torch.zeros((H, 256, 2, 64), dtype=torch.float16, device=dev)
-            t["fast_tables"] = torch.zeros((16384,), dtype=torch.uint8, device=dev)
+            t["fast_tables"] = _shared_fast_tables(dev, float(self.config.theta_base))
             t["pool_f16"] = torch.zeros((B, H, P, 2, d), dtype=torch.float16, device=dev)
         if old is not None:
             oc = old["positions"].shape[1]

@@ -112,15 +112,37 @@ __host__ __device__ __forceinline__ int64_t pool_f16_offset(int slot, int kv, in
 
 // Fast-path RoPE constants for d = 128 (antkv_cache_desc::fast_tables).
 struct FastTables {
-  uint32_t kc[16][64][2];  // fp16x2 (cos, sin), (-sin, cos) of r*omega_i, r = 0..15
-  float step[64][2];       // cos, sin of -32*omega_i (frame advance per tile pair)
+  // fp16x2 {(cos, sin), (-sin, cos)} of r * omega_p for rows r = g and g + 8
+  // and pair p = 8 s + 4 u + t, laid out [s][u][t][g] as one 16-byte record
+  // {row g: (c,s), (-s,c); row g+8: (c,s), (-s,c)}: the 32 lanes (g = lane / 4,
+  // t = lane % 4) of a warp read 512 consecutive bytes with one LDS.128
+  uint4 kc[8][2][4][8];
+  // cos, sin of -32 * omega_p (frame advance per stage) for pairs p = 8 s + 4 u + t:
+  // step[s][t] = (c_{u=0}, s_{u=0}, c_{u=1}, s_{u=1})
+  float4 step[8][4];
   double omega[64];        // theta^(-2i/128)
+  uint64_t turns[64];      // omega_i / (2 pi) in units of 2^-64 turns
 };
+
+// cos/sin of delta * omega for an integer position difference, reduced
+// exactly in integer arithmetic: delta * turns mod 2^64 is the fractional
+// number of turns (error ~ |delta| * 2^-53 relative turns, < 1e-9 rad).
+__device__ __forceinline__ void turns_cs(int64_t delta, uint64_t turns, float &c, float &s) {
+  const uint64_t p = static_cast<uint64_t>(delta) * turns;
+  const float a = static_cast<float>(static_cast<int64_t>(p)) * 3.4061215800865545e-19f;  // 2pi/2^64
+  __sincosf(a, &s, &c);
+}
 static_assert(sizeof(FastTables) <= 16384, "fast tables");
 
 // Ints per (sequence, head) of the fused decode kernel's cache-update plan
 // (decode workspace, after the CTA / sequence tickets).
 constexpr int kPlanWords = 12;
+
+// Position of pair p = 8 s + 4 u + t in the fast kernel's lane order
+// ((s, t) major, u minor): a lane's two pairs of k-step s are adjacent.
+__host__ __device__ __forceinline__ int lane_pair_pos(int p) {
+  return ((p >> 3) * 4 + (p & 3)) * 2 + ((p >> 2) & 1);
+}
 
 inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 

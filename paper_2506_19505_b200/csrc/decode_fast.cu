@@ -51,7 +51,8 @@ constexpr uint32_t FK_SMEM_BASE = 0x400;
 // ANTKV_TRACE=1: per-CTA timeline words: 0 smid | ticket << 32, then global
 // timer stamps 1 start, 2 barriers ready, 3 prologue loads issued, 4 frames,
 // 5 pool wait, 6 pool done, 7 prepare done, 8 loop start, 9 loop end,
-// 10 partial written, 11 committed (last CTA only).
+// 10 after the tickets, 11 committed (last CTA only), 12 all warps done,
+// 13 partial written, 15 combine done (last CTA only).
 constexpr int FK_TRACE_WORDS = 16;
 constexpr int FK_POOL_TILE_BYTES = 8192;                 // [K|V][16 slots][128] fp16
 constexpr int FK_MAX_WARP_WORDS = 64;                    // qmask words per warp (2048 slots)
@@ -66,11 +67,14 @@ struct __align__(128) FastSmem {
   float xm[4];                               // its scaled logits (log2 units)
   FastTables tab;                            // RoPE constants (bulk copy)
   uint8_t qraw[4 * 128 * 4];                 // the 4 query rows of the head (input dtype)
-  float2 ang[2 * FK_WARPS + 1][64];          // (cos, sin) per query frame and pair
+  float2 qf[4][64];                          // the same, float32 pairs in lane order, scaled
+                                             // by log2(e)/sqrt(d)
+  float2 ang[2 * FK_WARPS + 1][64];          // (cos, sin) per query frame, pairs in lane order
   unsigned long long full[FK_WARPS][FK_NS];
   unsigned long long pfull[FK_WARPS];
-  unsigned long long cbbar, tbar;
+  unsigned long long cbbar, tbar, qbar;
   int ticket, gticket;
+  unsigned long long t0clk;                  // trace: start clock of the CTA
 };
 
 struct MergeSmem {                             // aliases the pool area after the loops
@@ -430,12 +434,18 @@ __device__ __forceinline__ float4 qk_tile(const WarpState &w, const uint4 &kr,
   for (int s = 0; s < 8; ++s) {
     uint32_t a[4];
     ldsm_cb(prmt(word_of(kr, s >> 1), la.lcK, (s & 1) ? la.sK1 : la.sK0), a);
+#ifndef FK_EXP_NOROT
     a[0] = rot2(a[0], w.kc[s][0], w.kc[s][1]);
     a[1] = rot2(a[1], w.kc[s][2], w.kc[s][3]);
     a[2] = rot2(a[2], w.kc[s][4], w.kc[s][5]);
     a[3] = rot2(a[3], w.kc[s][6], w.kc[s][7]);
+#endif
+#ifdef FK_EXP_NOQKMMA
+    sa[s & 3] += __uint_as_float((a[0] ^ a[1] ^ a[2] ^ a[3] ^ bq[s][0]) & 0x3fffffffu);
+#else
     if (s & 1) mma16816(sb, a, bq[s][0], bq[s][1]);
     else mma16816(sa, a, bq[s][0], bq[s][1]);
+#endif
   }
   return make_float4(sa[0] + sb[0], sa[1] + sb[1], sa[2] + sb[2], sa[3] + sb[3]);
 }
@@ -607,10 +617,14 @@ __device__ __forceinline__ void slot_tiles(WarpState &w, const uint8_t *tb, int 
   const uint4 v3 = *reinterpret_cast<const uint4 *>(tb + 3 * FK_TILE_BYTES + 256 + tv * 16);
   uint32_t x[4];
   softmax_p2(w, sA, (qwA & 1u) | ((qwA >> 7) & 2u), sB, (qwB & 1u) | ((qwB >> 7) & 2u), x);
+#ifndef FK_EXP_NOPV
   pv_tile(w, v0, movm_t(lo ? x[0] : 0u), movm_t(lo ? x[1] : 0u), la);
   pv_tile(w, v1, movm_t(lo ? 0u : x[0]), movm_t(lo ? 0u : x[1]), la);
   pv_tile(w, v2, movm_t(lo ? x[2] : 0u), movm_t(lo ? x[3] : 0u), la);
   pv_tile(w, v3, movm_t(lo ? 0u : x[2]), movm_t(lo ? 0u : x[3]), la);
+#else
+  w.o[0][0] += __uint_as_float(x[0] ^ x[1] ^ x[2] ^ x[3] ^ v0.x ^ v1.x ^ v2.x ^ v3.x);
+#endif
 }
 
 // One pool tile (16 full-precision slots) in the absolute frame `bqa`
@@ -654,18 +668,20 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   const bool last_split = split == S - 1;
   const bool prep = last_split && a.knew;
   unsigned long long tr[FK_TRACE_WORDS];
+  // stamps: SM cycle counter (clock64) relative to the start, plus the
+  // global timer at the start to align CTAs (globaltimer ticks too coarsely
+  // for sub-microsecond phases)
 #define FK_TR(i) \
-  if (a.trace && threadIdx.x == 0) tr[i] = gtimer();
+  if (a.trace && threadIdx.x == 0) tr[i] = clock64();
   FK_TR(1);
+  unsigned long long g0 = 0;
+  if (a.trace && threadIdx.x == 0) g0 = gtimer();
 
-  // ---- prologue.  Phase 0: scalar loads (not used until phase 1), barrier
-  // setup, then bulk copies of the codebook, the RoPE tables and the 4 query
-  // rows -- nothing waits on a global load before every copy is in flight.
-  const double pq = static_cast<double>(a.qpos[b]);
-  const int n = c.seq_len[b];
-  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-  const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
-  const int qbytes = 4 * 128 * dtype_size(a.qdtype);
+  // ---- prologue.  Phase 0 touches only data no kernel writes during
+  // decoding (the prepared codebook and RoPE tables), so with programmatic
+  // dependent launch it overlaps the tail of the previous kernel in the
+  // stream; griddepcontrol.wait then orders everything else (cache state, q)
+  // after that kernel has completed.
   if (threadIdx.x == 0) {
     for (int ww = 0; ww < FK_WARPS; ++ww) {
       for (int s = 0; s < FK_NS; ++s) mbar_init(&sm.full[ww][s], 1);
@@ -673,17 +689,46 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
     mbar_init(&sm.cbbar, 1);
     mbar_init(&sm.tbar, 1);
+    mbar_init(&sm.qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int qbytes = 4 * 128 * dtype_size(a.qdtype);
   if (threadIdx.x == 0) {
-    mbar_expect_tx(&sm.tbar, sizeof(FastTables) + qbytes);
-    tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
-    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
-                 qbytes, &sm.tbar);   // rows h*4 .. h*4+3 of sequence b
     mbar_expect_tx(&sm.cbbar, FK_CB_BYTES);
     tma_bulk_g2s(sm.cb, reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * FK_CB_BYTES,
                  FK_CB_BYTES, &sm.cbbar);
+    mbar_expect_tx(&sm.tbar, sizeof(FastTables));
+    tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // key-rotation constants and frame steps into registers (tables only)
+  WarpState w;
+  mbar_wait(&sm.tbar, 0);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const float4 st = sm.tab.step[s][t];
+    w.sc[s] = make_float2(st.x, st.z);
+    w.ss[s] = make_float2(st.y, st.w);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint4 k = sm.tab.kc[s][u][t][g];
+      w.kc[s][4 * u] = k.x;
+      w.kc[s][4 * u + 1] = k.y;
+      w.kc[s][4 * u + 2] = k.z;
+      w.kc[s][4 * u + 3] = k.w;
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // scalar loads (not used until phase 1) and the 4 query rows
+  const int64_t qp = a.qpos[b];
+  const int n = c.seq_len[b];
+  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+  const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&sm.qbar, qbytes);
+    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
+                 qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
   }
   FK_TR(2);
 
@@ -743,48 +788,38 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   // ---- phase 2: (cos, sin) of every query frame of the CTA, cooperatively
   // from float64-reduced angles (frame 2w + e: warp w's even / odd tile
   // frame; frame 16: the absolute frame p_q of the pool rows)
-  mbar_wait(&sm.tbar, 0);
-  for (int e = threadIdx.x; e < (2 * FK_WARPS + 1) * 64; e += FK_THREADS) {
-    const int f = e >> 6, p = e & 63;
-    const double delta = f < 2 * FK_WARPS
-        ? pq - static_cast<double>(pos0 + (int64_t)(T0 + (f >> 1) * Tw) * 16 + (f & 1) * 16)
-        : pq;
-    float cs, sn;
-    rope_cs(delta * sm.tab.omega[p], cs, sn);
-    sm.ang[f][p] = make_float2(cs, sn);
+  mbar_wait(&sm.qbar, 0);
+  const double pq = static_cast<double>(qp);
+  {
+    for (int e = threadIdx.x; e < (2 * FK_WARPS + 1) * 64; e += FK_THREADS) {
+      const int f = e >> 6, p = e & 63;
+      const int64_t delta = f < 2 * FK_WARPS
+          ? qp - (pos0 + (int64_t)(T0 + (f >> 1) * Tw) * 16 + (f & 1) * 16)
+          : qp;
+      float cs, sn;
+      turns_cs(delta, sm.tab.turns[p], cs, sn);
+      sm.ang[f][lane_pair_pos(p)] = make_float2(cs, sn);
+    }
+    const float sc = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
+    for (int e = threadIdx.x; e < 256; e += FK_THREADS)
+      sm.qf[e >> 6][lane_pair_pos(e & 63)] =
+          make_float2(load_elem(sm.qraw, 2 * e, a.qdtype) * sc, load_elem(sm.qraw, 2 * e + 1, a.qdtype) * sc);
   }
   __syncthreads();
-  const float scale = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
-  WarpState w;
+  FK_TR(14);
   uint32_t bqa[8][2];
   {
-    const int qo = (g & 3) * 128;
     const int fr = 2 * warp + (g >= 4 ? 1 : 0);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
-      float fxv[2], fyv[2], scv[2], ssv[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int pair = 8 * s + 4 * u + t;
-        const uint2 k0 = *reinterpret_cast<const uint2 *>(&sm.tab.kc[g][pair][0]);
-        const uint2 k1 = *reinterpret_cast<const uint2 *>(&sm.tab.kc[g + 8][pair][0]);
-        w.kc[s][4 * u] = k0.x;
-        w.kc[s][4 * u + 1] = k0.y;
-        w.kc[s][4 * u + 2] = k1.x;
-        w.kc[s][4 * u + 3] = k1.y;
-        scv[u] = sm.tab.step[pair][0];
-        ssv[u] = sm.tab.step[pair][1];
-        const float x0 = load_elem(sm.qraw, qo + 2 * pair, a.qdtype) * scale;
-        const float x1 = load_elem(sm.qraw, qo + 2 * pair + 1, a.qdtype) * scale;
-        const float2 cf = sm.ang[fr][pair], ca = sm.ang[2 * FK_WARPS][pair];
-        fxv[u] = x0 * cf.x - x1 * cf.y;
-        fyv[u] = x0 * cf.y + x1 * cf.x;
-        bqa[s][u] = g < 4 ? pack_h2(x0 * ca.x - x1 * ca.y, x0 * ca.y + x1 * ca.x) : 0u;
-      }
-      w.fx[s] = make_float2(fxv[0], fxv[1]);
-      w.fy[s] = make_float2(fyv[0], fyv[1]);
-      w.sc[s] = make_float2(scv[0], scv[1]);
-      w.ss[s] = make_float2(ssv[0], ssv[1]);
+      const float4 xq = *reinterpret_cast<const float4 *>(&sm.qf[g & 3][(s * 4 + t) * 2]);
+      const float4 cf = *reinterpret_cast<const float4 *>(&sm.ang[fr][(s * 4 + t) * 2]);
+      const float4 ca = *reinterpret_cast<const float4 *>(&sm.ang[2 * FK_WARPS][(s * 4 + t) * 2]);
+      // pair u = 0: (xq.x, xq.y) rotated by (cf.x, cf.y); u = 1: (xq.z, xq.w) by (cf.z, cf.w)
+      w.fx[s] = make_float2(xq.x * cf.x - xq.y * cf.y, xq.z * cf.z - xq.w * cf.w);
+      w.fy[s] = make_float2(xq.x * cf.y + xq.y * cf.x, xq.z * cf.w + xq.w * cf.z);
+      bqa[s][0] = g < 4 ? pack_h2(xq.x * ca.x - xq.y * ca.y, xq.x * ca.y + xq.y * ca.x) : 0u;
+      bqa[s][1] = g < 4 ? pack_h2(xq.z * ca.z - xq.w * ca.w, xq.z * ca.w + xq.w * ca.z) : 0u;
     }
   }
   w.mrun[0] = w.mrun[1] = -INFINITY;
@@ -800,7 +835,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     float kk[4], vv[4], cs[2], sn[2];
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
-      const float2 ca = sm.ang[2 * FK_WARPS][2 * lane + pp];
+      const float2 ca = sm.ang[2 * FK_WARPS][lane_pair_pos(2 * lane + pp)];
       cs[pp] = ca.x;
       sn[pp] = ca.y;
       const float x0 = round_to(c.row_dtype, load_elem(a.knew, kb + 2 * pp, a.kvdtype));
@@ -813,12 +848,11 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       vv[e] = __half2float(__float2half_rn(round_to(c.row_dtype, load_elem(a.vnew, kb + e, a.kvdtype))));
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh) {
-      const int qh = hh * 128 + 4 * lane;
       float sdot = 0.f;
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
-        const float x0 = load_elem(sm.qraw, qh + 2 * pp, a.qdtype) * scale;
-        const float x1 = load_elem(sm.qraw, qh + 2 * pp + 1, a.qdtype) * scale;
+        const float2 xq = sm.qf[hh][lane_pair_pos(2 * lane + pp)];
+        const float x0 = xq.x, x1 = xq.y;
         sdot += (x0 * cs[pp] - x1 * sn[pp]) * kk[2 * pp] + (x0 * sn[pp] + x1 * cs[pp]) * kk[2 * pp + 1];
       }
       sdot = warp_sum(sdot);
@@ -878,7 +912,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       const int slot = it % FK_NS;
       mbar_wait(&sm.full[warp][slot], (it / FK_NS) & 1);
       const uint32_t qwA = sm.qm[warp][2 * it] >> rowbit, qwB = sm.qm[warp][2 * it + 1] >> rowbit;
+#ifdef FK_EXP_STREAM
+      {
+        const uint4 k0 = *reinterpret_cast<const uint4 *>(&sm.ring[warp][slot][tk * 16]);
+        w.o[0][0] += __uint_as_float((k0.x ^ qwA ^ qwB) & 0x3fffffffu) * 1e-30f;
+      }
+#else
       slot_tiles(w, &sm.ring[warp][slot][0], tk, tv, qwA, qwB, la, lo);
+#endif
       __syncwarp();
       if (lane == 0 && it + FK_NS < nslots) {   // every lane has read the slot: refill it
         fence_proxy_async();
@@ -891,6 +932,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
 
   // ---- merge 8 warps x 2 streams (+ the appended token) -> partial (natural log)
   __syncthreads();   // pool tiles consumed: the pool area becomes merge scratch
+  FK_TR(12);
   const float ln2 = 0.6931471805599453f;
 #pragma unroll
   for (int mt = 0; mt < 8; ++mt) {
@@ -907,39 +949,44 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     mg.l[warp][2 * t + 1] = lsum1;
   }
   __syncthreads();
+  // per head: max, weights of the 16 streams (+ the appended token), normaliser
+  float *mw = reinterpret_cast<float *>(&sm.ring[0][0][0]);   // [4][17] weights, [4] M, [4] L
+  if (threadIdx.x < 4) {
+    const int hh = threadIdx.x;
+    float M = sm.xm[hh];
+#pragma unroll
+    for (int src = 0; src < 2 * FK_WARPS; ++src) M = fmaxf(M, mg.m[src >> 1][hh + 4 * (src & 1)]);
+    float L = 0.f;
+#pragma unroll
+    for (int src = 0; src < 2 * FK_WARPS; ++src) {
+      const float mv = mg.m[src >> 1][hh + 4 * (src & 1)];
+      const float f = (mv == -INFINITY) ? 0.f : ex2(mv - M);
+      mw[hh * 17 + src] = f;
+      L += f * mg.l[src >> 1][hh + 4 * (src & 1)];
+    }
+    const float fx = (sm.xm[hh] == -INFINITY) ? 0.f : ex2(sm.xm[hh] - M);
+    mw[hh * 17 + 16] = fx;
+    L += fx;
+    mw[68 + hh] = M;
+    mw[72 + hh] = L;
+  }
+  __syncthreads();
   const int64_t rows = (int64_t)c.B * c.Hq;
   const int64_t row0 = ((int64_t)split * c.B + b) * c.Hq + h * 4;
   for (int i = threadIdx.x; i < 4 * 128; i += FK_THREADS) {
     const int hh = i >> 7, dim = i & 127;
-    float M = sm.xm[hh];
+    float O = mw[hh * 17 + 16] != 0.f ? mw[hh * 17 + 16] * sm.xo[hh][dim] : 0.f;   // xo unset unless prep
 #pragma unroll
-    for (int ww = 0; ww < FK_WARPS; ++ww) M = fmaxf(M, fmaxf(mg.m[ww][hh], mg.m[ww][hh + 4]));
-    float L = 0.f, O = 0.f;
-    if (M != -INFINITY) {
-      if (sm.xm[hh] != -INFINITY) {
-        const float f = ex2(sm.xm[hh] - M);
-        L = f;
-        O = f * sm.xo[hh][dim];
-      }
-#pragma unroll
-      for (int ww = 0; ww < FK_WARPS; ++ww) {
-#pragma unroll
-        for (int src = 0; src < 2; ++src) {
-          const float mv = mg.m[ww][hh + 4 * src];
-          if (mv == -INFINITY) continue;
-          const float f = ex2(mv - M);
-          L += f * mg.l[ww][hh + 4 * src];
-          O += f * mg.o[ww][hh + 4 * src][dim];
-        }
-      }
-    }
+    for (int src = 0; src < 2 * FK_WARPS; ++src)
+      O = fmaf(mw[hh * 17 + src], mg.o[src >> 1][hh + 4 * (src & 1)][dim], O);
     a.ws_o[(row0 + hh) * 128 + dim] = O;
     if (dim == 0) {
-      a.ws_m[row0 + hh] = M * ln2;
-      a.ws_l[row0 + hh] = L;
+      a.ws_m[row0 + hh] = mw[68 + hh] * ln2;
+      a.ws_l[row0 + hh] = mw[72 + hh];
     }
   }
 
+  FK_TR(13);
   // ---- tickets: the last CTA of (b, h) combines and commits; the last CTA
   // of sequence b publishes its new length
   __threadfence();
@@ -954,8 +1001,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     unsigned long long *o =
         a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
     o[0] = smid() | ((unsigned long long)sm.ticket << 32);
-    for (int i = 1; i <= 10; ++i) o[i] = tr[i];
+    for (int i = 2; i <= 10; ++i) o[i] = tr[i] - tr[1];
+    o[1] = g0;
     o[11] = 0;
+    o[12] = tr[12] - tr[1];
+    o[13] = tr[13] - tr[1];
+    o[14] = tr[14] - tr[1];
+    o[15] = 0;
+    sm.t0clk = tr[1];
   }
   if (threadIdx.x == 0 && sm.gticket == c.Hkv * S - 1) {
     // every CTA of sequence b has read seq_len: publish the appended token
@@ -965,32 +1018,34 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   if (sm.ticket != S - 1) return;
   __threadfence();
   if (warp < 4) {
-    // warp hh combines head hh: lane = 4 dims; one pass over the splits with
-    // a running max (all loads of a chunk of 8 splits in flight together)
+    // warp hh combines head hh: lane = 4 dims; the loads of up to 24 splits
+    // are in flight together, then a running max across passes
     const int hh = warp, d4 = 4 * lane;
     const int64_t row = (int64_t)b * c.Hq + h * 4 + hh;
     float M = -INFINITY, L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s0 = 0; s0 < S; s0 += 8) {
-      float ms[8], ls[8];
-      float4 v[8];
+    constexpr int CH = 24;
+    for (int s0 = 0; s0 < S; s0 += CH) {
+      float ms[CH], ls[CH];
+      float4 v[CH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < CH; ++u) {
         const int s2 = min(s0 + u, S - 1);
-        ms[u] = (s0 + u < S) ? __ldcg(a.ws_m + s2 * rows + row) : -INFINITY;
+        ms[u] = __ldcg(a.ws_m + s2 * rows + row);
         ls[u] = __ldcg(a.ws_l + s2 * rows + row);
         v[u] = __ldcg(reinterpret_cast<const float4 *>(a.ws_o + (s2 * rows + row) * 128 + d4));
       }
       float mc = M;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) mc = fmaxf(mc, ms[u]);
+      for (int u = 0; u < CH; ++u)
+        if (s0 + u < S) mc = fmaxf(mc, ms[u]);
       if (mc == -INFINITY) continue;
       const float al = (M == -INFINITY) ? 0.f : __expf(M - mc);
       L *= al;
       acc.x *= al; acc.y *= al; acc.z *= al; acc.w *= al;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float wv = (ms[u] == -INFINITY) ? 0.f : __expf(ms[u] - mc);
+      for (int u = 0; u < CH; ++u) {
+        const float wv = (s0 + u >= S || ms[u] == -INFINITY) ? 0.f : __expf(ms[u] - mc);
         L = fmaf(wv, ls[u], L);
         acc.x = fmaf(wv, v[u].x, acc.x);
         acc.y = fmaf(wv, v[u].y, acc.y);
@@ -1003,10 +1058,18 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     *reinterpret_cast<float4 *>(a.out + row * 128 + d4) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     if (lane == 0 && a.lse) a.lse[row] = M + logf(L);
+    if (a.trace && threadIdx.x == 0) {
+      unsigned long long *o =
+          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+      o[15] = clock64() - sm.t0clk;
+    }
   } else if (threadIdx.x == 128) {
     if (a.knew) commit_update(c, a, b, h, n);   // overlaps the combine
-    if (a.trace)
-      a.trace[FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) + 11] = gtimer();
+    if (a.trace) {
+      unsigned long long *o =
+          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+      o[11] = clock64() - sm.t0clk;
+    }
     a.cnt[bh] = 0;
   }
 }
@@ -1108,8 +1171,20 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
     cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
-  dim3 grid(a.splits, c.Hkv, c.B);
-  decode_fast_kernel<<<grid, FK_THREADS, smem, st>>>(c, a);
+  // programmatic dependent launch: the prologue's immutable prefetch overlaps
+  // the previous kernel's tail (griddepcontrol.wait orders the rest)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.splits, c.Hkv, c.B);
+  cfg.blockDim = dim3(FK_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, decode_fast_kernel, c, a);
+  if (e != cudaSuccess) return cuda_status(e, "decode_fast_kernel");
   ANTKV_LAUNCH_CHECK("decode_fast_kernel");
   return ANTKV_OK;
 }

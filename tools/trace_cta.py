@@ -20,8 +20,9 @@ import bench  # noqa: E402
 from paper_2506_19505_b200 import _lib  # noqa: E402
 
 WORDS = 16
-NAMES = {1: "start", 2: "barriers", 3: "loads issued", 4: "frames", 5: "pool wait",
-         6: "pool done", 7: "prepare done", 8: "loop start", 9: "loop end", 10: "partial"}
+NAMES = {1: "start", 2: "barriers", 3: "loads issued", 14: "angles done", 4: "frames", 5: "pool wait",
+         6: "pool done", 7: "prepare done", 8: "loop start", 9: "loop end (w0)",
+         12: "all warps done", 13: "partial written", 10: "ticket", 15: "combined", 11: "committed"}
 
 
 def main():
@@ -51,16 +52,18 @@ def main():
     a = a[:ncta]
     splits = ncta // (8 * cli.batch)
     sm = a[:, 0] & 0xffffffff
-    t0 = a[:, 1].min()
-    rel = (a - t0) / 1e3
+    # word 1: global timer at the CTA start (ns); the others: SM cycles since
+    # the CTA start (clock64); converted at the SM clock
+    mhz = float(os.environ.get("SM_MHZ", "1965"))
+    start = (a[:, 1] - a[:, 1].min()) / 1e3
+    rel = start[:, None] + a / (mhz)
+    rel[:, 1] = start
     print("CTAs", ncta, "distinct SMs", len(set(sm.tolist())), "splits per head", splits)
     for i, name in NAMES.items():
         ok = a[:, i] > 0
         if ok.any():
             col = rel[ok, i]
             print(f"{i:2d} {name:14s} min {col.min():6.1f}  med {np.median(col):6.1f}  max {col.max():6.1f} us")
-    last = a[:, 11] > 0
-    print("commit (last CTAs):", np.round(rel[last, 11], 1))
     order = np.argsort(-rel[:, 10])[:6]
     for i in order:
         print(f"  cta {i:3d} split {i % splits:2d} head {i // splits} sm {sm[i]:3d} " +
