@@ -586,7 +586,7 @@ def main():
     res, caches = run_ours(args)
     rank = int(os.environ.get("RANK", "0"))
     if rank == 0:
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and int(os.environ.get("WORLD_SIZE", "1")) == 1:
             items = cpu_sample_from_cache(caches[0], HKV)
             walls, cores = run_cpu(items, 2)
             t = float(np.mean(walls[1:])) if len(walls) > 1 else walls[0]
