@@ -536,6 +536,7 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
                                  const int32_t *anchors, int n_anchors, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
+  previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   ANTKV_REQUIRE(n >= 0 && n <= c->capacity, "prefill length exceeds capacity");
   ANTKV_REQUIRE(n_anchors + c->window_size + 1 <= c->pool_capacity, "pool capacity too small");
   cudaStream_t st = as_stream(stream);
@@ -564,6 +565,7 @@ extern "C" int antkv_cache_append(const antkv_cache_desc *c, const void *k, cons
                                   int dtype, const int64_t *position, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
+  previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   ANTKV_REQUIRE(c->Hkv <= 256, "at most 256 KV heads");
   cache_append_kernel<<<c->B, 256, 0, as_stream(stream)>>>(*c, k, v, dtype, position);
   ANTKV_LAUNCH_CHECK("cache_append_kernel");
@@ -573,6 +575,7 @@ extern "C" int antkv_cache_append(const antkv_cache_desc *c, const void *k, cons
 extern "C" int antkv_cache_evict(const antkv_cache_desc *c, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
+  previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   const size_t cbn = (size_t)c->m * c->d_sub;
   const int cb_in_smem = cbn * 2 * sizeof(float) <= 64 * 1024;
   const size_t smem = sizeof(float) * (2 * c->d + (cb_in_smem ? 2 * cbn : 0));
@@ -586,6 +589,7 @@ extern "C" int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *K
                                       void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
+  previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   if (n == 0) return ANTKV_OK;
   cudaStream_t st = as_stream(stream);
   dim3 g1(ceil_div((int64_t)n * c->d, 256), c->B * c->Hkv);
@@ -600,6 +604,7 @@ extern "C" int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *K
 extern "C" int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
+  previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   ANTKV_REQUIRE(c->d == 128 && c->d_sub == 8 && c->m <= 256 && c->codebook_f16 && c->fast_tables,
                 "fast path needs d=128, d_sub=8, m<=256");
   cudaStream_t st = as_stream(stream);

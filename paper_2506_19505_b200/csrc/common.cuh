@@ -32,6 +32,12 @@ int cuda_status(cudaError_t e, const char *where);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// The cache (identified by its codes buffer) touched by the last library
+// launch on `st`; records `key` as the new one.  The fused decode kernel reads
+// cache state before griddepcontrol.wait only when the previous launch on the
+// stream was for another cache.
+const void *previous_cache_on_stream(cudaStream_t st, const void *key);
+
 // ---------------------------------------------------------------- dtypes
 __device__ __forceinline__ float load_elem(const void *p, int64_t i, int dtype) {
   if (dtype == ANTKV_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);

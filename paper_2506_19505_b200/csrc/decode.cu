@@ -328,6 +328,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   float *wl = wm + (int64_t)used * rows;
   int *cnt = reinterpret_cast<int *>(reinterpret_cast<char *>(workspace) + workspace_bytes -
                                      256 - counter_bytes(*c));
+  if (!use_fast) previous_cache_on_stream(st, c->codes);   // (the fast launch records itself)
   if (use_fast)
     return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
                               splits, st);

@@ -196,6 +196,8 @@ struct StepArgs {
   int *cnt;                // [B*Hkv] CTA tickets, [B] sequence tickets (self-resetting),
                            // [B*Hkv][kPlanWords] cache-update plans
   int splits;              // CTAs per (b, head)
+  int early;               // the previous kernel in the stream wrote no state of this
+                           // cache: read cache state before griddepcontrol.wait
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
 };
 
@@ -701,7 +703,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     mbar_expect_tx(&sm.tbar, sizeof(FastTables));
     tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
   }
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // key-rotation constants and frame steps into registers (tables only)
   WarpState w;
   mbar_wait(&sm.tbar, 0);
@@ -719,17 +720,12 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       w.kc[s][4 * u + 3] = k.w;
     }
   }
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  // scalar loads (not used until phase 1) and the 4 query rows
-  const int64_t qp = a.qpos[b];
+  // Cache state is read before the wait only when the host knows the
+  // previous kernel in the stream did not write this cache (a.early).
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n = c.seq_len[b];
   const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
   const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&sm.qbar, qbytes);
-    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
-                 qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
-  }
   FK_TR(2);
 
   // ---- phase 1 (needs n / pool_high): work split, bulk copies of the code
@@ -782,6 +778,17 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   if (pt0 + warp < pt1) {
     kd0 = kinds[(pt0 + warp) * 16 + g];
     kd1 = kinds[(pt0 + warp) * 16 + g + 8];
+  }
+  // inputs produced by earlier kernels (q, positions, the appended rows) are
+  // read after the previous kernel completed; only then may the next kernel
+  // start (a dependency chain of depth one)
+  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int64_t qp = a.qpos[b];
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&sm.qbar, qbytes);
+    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
+                 qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
   }
   FK_TR(3);
 
@@ -1165,6 +1172,7 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   decode_fast_plan(c, splits, cs, ps);
   a.splits = cs + ps;
   a.trace = debug_trace_buffer();
+  a.early = previous_cache_on_stream(st, c.codes) != c.codes;
   const size_t smem = sizeof(FastSmem);
   static bool attr_set = false;
   if (!attr_set) {
@@ -1181,8 +1189,13 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  static int pdl = -1;   // ANTKV_NO_PDL=1 disables programmatic dependent launch (A/B timing)
+  if (pdl < 0) {
+    const char *e = getenv("ANTKV_NO_PDL");
+    pdl = !(e && e[0] == '1');
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaError_t e = cudaLaunchKernelEx(&cfg, decode_fast_kernel, c, a);
   if (e != cudaSuccess) return cuda_status(e, "decode_fast_kernel");
   ANTKV_LAUNCH_CHECK("decode_fast_kernel");

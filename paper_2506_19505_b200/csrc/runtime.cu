@@ -1,9 +1,24 @@
 // Error reporting and device checks for the C ABI.
 #include <stdarg.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 
 namespace antkv {
+
+const void *previous_cache_on_stream(cudaStream_t st, const void *key) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, const void *> last;
+  std::lock_guard<std::mutex> lock(mu);
+  const void *prev = nullptr;
+  auto it = last.find(st);
+  if (it != last.end()) prev = it->second;
+  last[st] = key;
+  return prev;
+}
+
 
 static thread_local char g_err[512] = "";
 
