@@ -2,10 +2,11 @@
 // Alg. 1 anchor-score column sums, and the reference FFI entry points that
 // share these kernels (antkv._ckernels.flash_aux / ans_blocked).
 //
-// v1 numerics: float32 CUDA-core tiles.  The anchor scores need S accurate to
-// ~1e-7 relative so that anchor sets match the float64 oracle wherever the
-// budget-boundary margin allows (SURVEY.md §7 hard part 3); float32 FMA tiles
-// meet that bar.
+// d = 128 runs on the tensor-core kernels of prefill_mma.cu (split-precision
+// logits); other head sizes use the float32 CUDA-core tiles below.  The
+// anchor scores need S accurate enough that anchor sets match the float64
+// oracle wherever the budget-boundary margin allows (SURVEY.md §7 hard
+// part 3).
 #include "common.cuh"
 
 namespace antkv {
@@ -275,6 +276,13 @@ ans_kernel(const float *__restrict__ Qs, const float *__restrict__ Kr,
   }
 }
 
+int launch_flash_mma(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads,
+                     int n_q, int n_k, int d, int dv, int causal, float *O, float *L, float *M,
+                     cudaStream_t st);
+int launch_ans_mma(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
+                   int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
+                   float *ans_k, float *ans_v, cudaStream_t st);
+
 static int launch_flash(const float *Qs, const float *Kr, const float *V, int heads,
                         int kv_heads, int n_q, int n_k, int d, int dv, int causal,
                         float *O, float *L, float *M, cudaStream_t st) {
@@ -285,6 +293,10 @@ static int launch_flash(const float *Qs, const float *Kr, const float *V, int he
   ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
   if (n_q == 0) return ANTKV_OK;
   ANTKV_REQUIRE(n_k >= 1, "empty key set");
+  {  // d = 128: tensor-core kernel (prefill_mma.cu)
+    const int rc = launch_flash_mma(Qs, Kr, V, heads, kv_heads, n_q, n_k, d, dv, causal, O, L, M, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+  }
   size_t smem = sizeof(float) * (64 * (d + 1) * 2 + 64 * (dv + 1) + 64 * 65);
   cudaFuncSetAttribute(flash_aux_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(n_q, FA_BQ), heads);
@@ -303,6 +315,11 @@ static int launch_ans(const float *Qs, const float *Kr, const float *M, const fl
                 "heads must be a multiple of kv_heads");
   ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
   if (n_k == 0) return ANTKV_OK;
+  {  // d = 128: tensor-core kernel (prefill_mma.cu)
+    const int rc = launch_ans_mma(Qs, Kr, M, L, qn, heads, kv_heads, sum_group, n_q, n_k, d, causal,
+                                  ans_k, ans_v, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+  }
   size_t smem = sizeof(float) * (64 * (d + 1) * 2 + 3 * 64 + 2 * 16 * 64);
   cudaFuncSetAttribute(ans_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid(ceil_div(n_k, FA_BK), heads / sum_group);
