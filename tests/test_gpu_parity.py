@@ -411,3 +411,90 @@ def test_fast_matches_generic_at_128k():
             ref = (A @ Vh[0, h].cpu().numpy().astype(np.float64))[0]
             assert rel(outs[False][hq], ref) < 1e-3
             assert rel(outs[True][hq], ref) < 2e-2
+
+
+# ------------------------------------------------------ tensor-core paths
+@pytest.mark.parametrize("dtype,m,code_bytes", [(torch.bfloat16, 256, 1), (torch.float16, 256, 1),
+                                                (torch.bfloat16, 200, 2)])
+def test_tensor_core_encoder_matches_oracle(dtype, m, code_bytes):
+    """encode_mma.cu (d = 128, d_sub = 8): codes vs the exhaustive float64
+    argmin of the oracle (margin rule), including a duplicated centroid
+    (ties -> lowest index) and rows far from the codebook scale."""
+    from paper_2506_19505_b200 import _lib
+    rng = np.random.default_rng(31)
+    n = 3000
+    X = rng.standard_normal((n, 128)).astype(np.float32)
+    X[:50] *= 40.0                      # large rows
+    X[50:100] *= 1e-3                   # tiny rows
+    C = rng.standard_normal((m, 8)).astype(np.float32)
+    C[7] = C[3]                         # duplicate: index 3 must win
+    Xt = torch.from_numpy(X).cuda().to(dtype)
+    Ct = torch.from_numpy(C).cuda()
+    codes = torch.empty((n, 16), dtype=torch.uint8 if code_bytes == 1 else torch.int16, device="cuda")
+    _lib.call("antkv_vq_encode", _lib.ptr(Xt), _lib.dtype_tag(Xt), n, 128, _lib.ptr(Ct), m, 8,
+              _lib.ptr(codes), code_bytes, _lib.stream())
+    got = codes.cpu().numpy().astype(np.int64)
+    Xd = Xt.float().cpu().numpy().astype(np.float64).reshape(-1, 8)
+    ref, _ = O.assign_nearest(Xd, C.astype(np.float64))
+    assert_codes_parity(Xd, C, got, ref)
+    assert not np.any(got == 7)
+
+
+@pytest.mark.parametrize("scale", [1.0, 300.0, 1e-3])
+def test_tensor_core_flash_aux_noncausal_and_scaled(scale):
+    """prefill_mma.cu through the _ckernels shim: non-causal, n_q != n_k,
+    and inputs far from unit scale (the power-of-two tile scaling)."""
+    from paper_2506_19505_b200 import kernels
+    rng = np.random.default_rng(5)
+    nq, nk = 150, 333
+    Qs = rng.standard_normal((nq, 128)) * scale / np.sqrt(128)
+    Kr = rng.standard_normal((nk, 128)) * (1.0 if scale > 1 else scale * 10)
+    V = rng.standard_normal((nk, 128))
+    Og, Lg, Mg = kernels.flash_aux(Qs, Kr, V, 64, 64, False)
+    S = Qs @ Kr.T
+    M = S.max(1)
+    P = np.exp(S - M[:, None])
+    L = P.sum(1)
+    Or = (P / L[:, None]) @ V
+    # float32 logits carry ~1e-7 * |S| absolute error, which exp() turns into
+    # relative errors of L and O: the tolerances scale with max |S| beyond 1
+    smax = max(1.0, np.abs(S).max())
+    assert np.abs(Mg - M).max() <= 1e-5 * smax
+    assert np.abs(Lg / L - 1).max() < 1e-5 * smax
+    assert rel(Og, Or) < 1e-4 * smax
+
+
+def test_pdl_early_reads_with_interleaved_caches():
+    """Two caches stepped alternately on one stream (the fused kernel then
+    reads cache state before griddepcontrol.wait) must give the same outputs
+    as each cache stepped alone."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d8m256")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.02, window_size=8)
+
+    def make(seed):
+        Q, K, V = qkv(seed, 8, 2, 700, 128, heavy=2)
+        ck, cv = codebooks(seed, 2, 256, 8)
+        c = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=8, batch=1)
+        dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+        c.prefill(dev(Q[None, :, :640]), dev(K[None, :, :640]), dev(V[None, :, :640]), np.arange(640))
+        steps = [(dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])) for t in range(640, 700)]
+        return c, steps
+
+    outs = {}
+    for mode in ("alone", "interleaved"):
+        ca, sa = make(41)
+        cb, sb = make(42)
+        oa, ob = [], []
+        if mode == "alone":
+            for i, (q, k, v) in enumerate(sa):
+                oa.append(ca.decode_step(q, k, v, 640 + i).clone())
+            for i, (q, k, v) in enumerate(sb):
+                ob.append(cb.decode_step(q, k, v, 640 + i).clone())
+        else:
+            for i in range(len(sa)):
+                oa.append(ca.decode_step(*sa[i], 640 + i).clone())
+                ob.append(cb.decode_step(*sb[i], 640 + i).clone())
+        outs[mode] = (torch.stack(oa).cpu().numpy(), torch.stack(ob).cpu().numpy())
+    for x, y in zip(outs["alone"], outs["interleaved"]):
+        assert np.array_equal(x, y)
