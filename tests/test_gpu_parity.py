@@ -498,3 +498,51 @@ def test_pdl_early_reads_with_interleaved_caches():
         outs[mode] = (torch.stack(oa).cpu().numpy(), torch.stack(ob).cpu().numpy())
     for x, y in zip(outs["alone"], outs["interleaved"]):
         assert np.array_equal(x, y)
+
+
+def test_llama_caller_matches_dense_reference_when_lossless():
+    """§8(f) rank 1 caller: with the window covering every token the cache is
+    lossless, so the model's prefill and decode logits must match a dense
+    float32 RoPE attention implementation of the same random weights."""
+    from paper_2506_19505_b200.llama import AnTKVLlama, LlamaConfig, _rms
+    cfg = LlamaConfig(layers=2, hidden=512, q_heads=4, kv_heads=1, head_dim=128, ffn=1024, vocab=1000,
+                      theta=10000.0, window=4096)
+    model = AnTKVLlama(cfg, batch=1, seed=3)
+    n, steps = 96, 6
+    toks = torch.randint(0, cfg.vocab, (1, n + steps), device="cuda",
+                         generator=torch.Generator(device="cuda").manual_seed(0))
+    got = [model.prefill(toks[:, :n])]
+    for i in range(steps - 1):
+        got.append(model.decode(toks[:, n + i]))
+
+    def rope(x, pos):                                    # x [h, t, d] fp32, interleaved pairs
+        d = x.shape[-1]
+        f = torch.tensor(cfg.theta, dtype=torch.float64) ** (-torch.arange(0, d, 2, dtype=torch.float64) / d)
+        ang = pos[:, None].double() * f[None]
+        c, s = torch.cos(ang).float().cuda(), torch.sin(ang).float().cuda()
+        x0, x1 = x[..., 0::2], x[..., 1::2]
+        out = torch.empty_like(x)
+        out[..., 0::2] = x0 * c - x1 * s
+        out[..., 1::2] = x0 * s + x1 * c
+        return out
+
+    def dense_logits(tokens):
+        t = tokens.shape[1]
+        x = model.embed[tokens]
+        pos = torch.arange(t)
+        for L in model.layers:
+            q, k, v = model._split(_rms(x, L["n1"]) @ L["wqkv"].t(), t)
+            q, k, v = q[0].float(), k[0].float(), v[0].float()
+            qr, kr = rope(q, pos), rope(k, pos)
+            kr = kr.repeat_interleave(cfg.q_heads // cfg.kv_heads, 0)
+            vv = v.repeat_interleave(cfg.q_heads // cfg.kv_heads, 0)
+            s = qr @ kr.transpose(1, 2) / np.sqrt(cfg.head_dim)
+            s = s.masked_fill(torch.triu(torch.ones(t, t, dtype=torch.bool, device="cuda"), 1), -float("inf"))
+            o = torch.softmax(s, -1) @ vv                        # [h, t, d]
+            x = x + o.transpose(0, 1).reshape(1, t, -1).to(torch.bfloat16) @ L["wo"].t()
+            x = model._mlp(L, x)
+        return (_rms(x[:, -1], model.norm) @ model.lm_head.t()).float()
+
+    for i, lg in enumerate(got):
+        ref = dense_logits(toks[:, :n + i])
+        assert rel(lg.cpu().numpy(), ref.cpu().numpy()) < 3e-2, i
