@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    p.add_argument("--no-prefill", action="store_true", help="skip the prefill timing")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     return p.parse_args()
 
@@ -219,6 +220,38 @@ def encode_throughput(torch, n=131072, reps=5):
     return {"value": n / (ms / 1e3), "unit": "tok/s", "ms_per_layer": ms, "tokens": n,
             "config": "d8m256, K+V, 8 KV heads, d=128, float32 distances",
             "tflops": flops / (ms / 1e3) / 1e12}
+
+
+def prefill_throughput(torch, n=32768):
+    """One layer's prefill (FA + aux, AnS, anchor selection, encode, layout)
+    at LLaMA-3-8B attention shapes, bf16 inputs."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d8m256")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=500000.0)
+    rng = np.random.default_rng(3)
+    cbk = rng.standard_normal((HKV, vq.m, vq.d_sub)).astype(np.float32)
+    cbv = rng.standard_normal((HKV, vq.m, vq.d_sub)).astype(np.float32)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    Q = torch.randn((1, HQ, n, D), device="cuda", generator=g).to(torch.bfloat16)
+    K = torch.randn((1, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
+    V = torch.randn((1, HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
+    pos = np.arange(n)
+    times = []
+    for _ in range(2):   # the first run warms up
+        cache = QuantizedKVCache(cfg, Codebook(vq, cbk), Codebook(vq, cbv), batch=1, q_heads=HQ)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cache.prefill(Q, K, V, pos)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = times[-1]
+    flops = 6 * HQ * D * n * n / 2      # FA (4 HQ d n^2 / 2) + AnS (2 HQ d n^2 / 2), causal
+    del Q, K, V, cache
+    return {"ctx": n, "ms_per_layer": ms, "tok_s": n / (ms / 1e3), "tflops_attention": flops / (ms / 1e3) / 1e12,
+            "config": "one layer, 32 Q / 8 KV heads, d=128, d8m256, 1% anchors; includes host-side "
+                      "checks and the anchor-count readback"}
 
 
 def run_ours(args):
@@ -394,6 +427,7 @@ def run_ours(args):
     e2e_ms = float(t.item())
 
     enc = encode_throughput(torch) if rank == 0 else None
+    pre = prefill_throughput(torch) if rank == 0 and not args.no_prefill else None
     peak, peak_kind = peaks()
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
     value = B * L / (ms / 1e3) * world          # weak scaling: 128K-context equivalents
@@ -439,6 +473,7 @@ def run_ours(args):
                                               else (3 if args.kernel == "fast" else 4)),
             "clocks": clk.summary(),
             "encode": enc,
+            "prefill": pre,
         }
     return result, caches
 
