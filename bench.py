@@ -128,7 +128,9 @@ def build_layers(args, rank, world, torch):
     from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
     from paper_2506_19505_b200.anchors import select_anchors_device
     vq = VqConfig.from_notation(args.notation)
-    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=500000.0)
+    # only the tail shard holds the full-precision window (and appends)
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32 if rank == world - 1 else 0,
+                      theta_base=500000.0)
     n = args.ctx
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
     rng = np.random.default_rng(1000 + rank)

@@ -122,6 +122,7 @@ class QuantizedKVCache:
         self._t = None          # device tensors
         self._contiguous = True
         self._desc = None
+        self._pool_min_anchors = 0
 
     # ------------------------------------------------------------ layout
     @property
@@ -133,8 +134,12 @@ class QuantizedKVCache:
         return self._desc.capacity if self._desc is not None else 0
 
     def _pool_capacity(self, cap):
-        # a multiple of 16: the fast decode kernel streams the pool in 16-slot tiles
-        return _round_up(self.config.budget_for(cap) + self.config.window_size + 2, 16)
+        # anchors (the budget of the whole sequence when this cache is a
+        # sequence shard starting at token_offset; at least the anchors it was
+        # built with) + window + the appended row; a multiple of 16: the fast
+        # decode kernel streams the pool in 16-slot tiles
+        anchors = max(self.config.budget_for(cap + self.token_offset), self._pool_min_anchors)
+        return _round_up(anchors + self.config.window_size + 2, 16)
 
     def _alloc(self, cap):
         """(Re)allocate device state for `cap` token slots, keeping contents."""
@@ -324,8 +329,7 @@ class QuantizedKVCache:
         if self.Hq is None:
             self.Hq = Hkv
         self.d = d
-        if anchors.shape[-1] + self.config.window_size + 1 > self._pool_capacity(max(n, 1)):
-            raise ValueError("anchor count exceeds the pool capacity")
+        self._pool_min_anchors = max(self._pool_min_anchors, int(anchors.shape[-1]))
         K = self._row_dtype(K)
         V = self._row_dtype(V.to(K.dtype))
         if self.row_dtype is None:

@@ -546,3 +546,54 @@ def test_llama_caller_matches_dense_reference_when_lossless():
     for i, lg in enumerate(got):
         ref = dense_logits(toks[:, :n + i])
         assert rel(lg.cpu().numpy(), ref.cpu().numpy()) < 3e-2, i
+
+
+def test_sequence_sharded_decode_matches_single_cache():
+    """Multi-GPU decode logic on one device: two shard caches (the head shard
+    without a window; the tail shard with the window, the appends, the
+    evictions and the global anchor count) merged with the LSE combine must
+    reproduce the single-cache decode outputs and anchor set."""
+    import ctypes
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200 import _lib as lib
+    from paper_2506_19505_b200.parallel import lse_merge
+    vq = VqConfig.from_notation("d8m256")
+    Hq, Hkv, n, steps, W = 4, 1, 900, 30, 8
+    Q, K, V = qkv(51, Hq, Hkv, n + steps, 128, heavy=2)
+    ck, cv = codebooks(51, Hkv, 256, 8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    cfg = lambda w: CacheConfig(vq=vq, anchor_fraction=0.02, window_size=w)
+    ref = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    ref.prefill(dev(Q[None, :, :n]), dev(K[None, :, :n]), dev(V[None, :, :n]), np.arange(n))
+    anchors = np.asarray(ref.anchor_indices_of(0, 0))
+    cut = 448
+    shards = []
+    for lo, hi, w in ((0, cut, 0), (cut, n, W)):
+        c = QuantizedKVCache(cfg(w), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq, token_offset=lo,
+                             capacity=hi - lo + steps + 64)
+        loc = np.array([j - lo for j in anchors if lo <= j < hi], dtype=np.int32)[None, None]
+        pos = torch.arange(lo, hi, device="cuda")[None]
+        c.build_from(dev(K[None, :, lo:hi]), dev(V[None, :, lo:hi]), pos, torch.from_numpy(loc).cuda())
+        shards.append(c)
+    head, tail = shards
+    tail.tensors["hstate"][:, :, 0] = len(anchors)   # promotions follow the global budget
+    for t in range(n, n + steps):
+        q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
+        want = ref.decode_step(q, k, v, t)
+        qpos = torch.tensor([t], device="cuda")
+        lib.check(lib.load().antkv_cache_append(ctypes.byref(tail.desc), lib.ptr(k), lib.ptr(v), lib.BF16,
+                                                lib.ptr(qpos), lib.stream()))
+        parts, lses = [], []
+        for c in shards:
+            o = torch.empty((1, Hq, 128), device="cuda")
+            l = torch.empty((1, Hq), device="cuda")
+            c.attend_device(q, qpos, o, l)
+            parts.append(o)
+            lses.append(l)
+        lib.check(lib.load().antkv_cache_evict(ctypes.byref(tail.desc), lib.stream()))
+        tail._n += 1
+        got = lse_merge(torch.stack(parts), torch.stack(lses))
+        assert rel(got.cpu().numpy(), want.cpu().numpy()) < 2e-2, t
+    merged = sorted([int(j) for j in head.anchor_indices_of(0, 0)] +
+                    [int(j) + cut for j in tail.anchor_indices_of(0, 0)])
+    assert merged == [int(j) for j in ref.anchor_indices_of(0, 0)]
