@@ -597,3 +597,10 @@ def test_sequence_sharded_decode_matches_single_cache():
     merged = sorted([int(j) for j in head.anchor_indices_of(0, 0)] +
                     [int(j) + cut for j in tail.anchor_indices_of(0, 0)])
     assert merged == [int(j) for j in ref.anchor_indices_of(0, 0)]
+
+
+def test_gqa_batch2_fast_d8m256():
+    """The fused kernel with two sequences (grid z = B) against the oracle."""
+    cache, outs, refs = _gqa(24, 2, 8, 2, 400, 128, "d8m256", 10, window=16, theta=5e5, fast=True)
+    for i in range(outs.shape[0]):
+        assert rel(outs[i], refs[i]) < 2e-2
