@@ -262,9 +262,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_SINGLE_DEVICE_CHECK=1: functional check of the N>1 path with every
+    # rank on device 0 and gloo collectives (no timing value)
+    single = os.environ.get("BENCH_SINGLE_DEVICE_CHECK") == "1"
+    if single:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if single:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_19505_b200 import _lib
     from paper_2506_19505_b200.parallel import gather_partials, lse_merge
     _lib.load()
@@ -287,16 +295,12 @@ def run_ours(args):
         if world == 1:
             cache.step_device(qs[s, l], ks[s, l], vs[s, l], qpos[s], out)
             return out
+        # sequence shards: the tail appends / attends / evicts in one fused
+        # launch, the other shards attend; (o, lse) all-gathered and merged
         if is_tail:
-            import ctypes
-            D_ = ctypes.byref(cache.desc)
-            lib = _lib.load(check_device=False)
-            _lib.check(lib.antkv_cache_append(D_, _lib.ptr(ks[s, l]), _lib.ptr(vs[s, l]), _lib.BF16,
-                                              _lib.ptr(qpos[s]), _lib.stream()))
-        cache.attend_device(qs[s, l], qpos[s], out, lse)
-        if is_tail:
-            _lib.check(_lib.load(check_device=False).antkv_cache_evict(ctypes.byref(cache.desc),
-                                                                        _lib.stream()))
+            cache.step_device(qs[s, l], ks[s, l], vs[s, l], qpos[s], out, lse)
+        else:
+            cache.attend_device(qs[s, l], qpos[s], out, lse)
         o_all, l_all = gather_partials(out, lse)
         return lse_merge(o_all, l_all, merged)
 
@@ -399,7 +403,10 @@ def run_ours(args):
             if world == 1:
                 caches[l].step_device(dq[l], dk[l], dv[l], p_dev, o_dev[l])
             else:
-                caches[l].attend_device(dq[l], p_dev, out, lse)
+                if is_tail:
+                    caches[l].step_device(dq[l], dk[l], dv[l], p_dev, out, lse)
+                else:
+                    caches[l].attend_device(dq[l], p_dev, out, lse)
                 o_all, l_all = gather_partials(out, lse)
                 o_dev[l].copy_(lse_merge(o_all, l_all, merged))
         outh.copy_(o_dev, non_blocking=True)
@@ -468,11 +475,16 @@ def run_ours(args):
             "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,
                     "d2h_bytes_per_step": outh.numel() * 4, "ms_per_step": e2e_ms,
-                    "path": "QuantizedKVCache.step_device per layer (antkv_decode_step) with "
-                            "pinned-host q/k/v H2D and output D2H inside the timed region"
+                    "path": ("QuantizedKVCache.step_device per layer (antkv_decode_step)" if world == 1
+                             else "per layer: fused step on the tail shard / attention on the others, "
+                                  "NCCL all-gather of (o, lse), antkv_lse_combine")
+                            + " with pinned-host q/k/v H2D and output D2H inside the timed region"
                             + (", CUDA-graph replay" if use_graph else "")},
+            # our kernels per layer-step on rank 0: the fused step (N=1) or attention +
+            # LSE combine (N>1, rank 0 is not the tail); generic path: append, attention,
+            # combine, evict
             "gpu_launches": args.steps * L * ((1 if args.kernel == "fast" else 4) if world == 1
-                                              else (3 if args.kernel == "fast" else 4)),
+                                              else (2 if args.kernel == "fast" else 3)),
             "clocks": clk.summary(),
             "encode": enc,
             "prefill": pre,

@@ -9,8 +9,6 @@ with the LSE combine kernel.  This is the only exchange on the decode path
 (SURVEY.md §5, §8e).
 """
 
-import ctypes
-
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -71,16 +69,14 @@ class ShardedDecoder:
         self.combine = combine or lse_merge
 
     def step(self, q, k, v, qpos, out_local, lse_local):
-        """q [B, Hq, d], k/v [B, Hkv, d] (only used on the tail), qpos [B]."""
+        """q [B, Hq, d], k/v [B, Hkv, d] (only used on the tail), qpos [B].
+        The tail shard appends, attends and evicts in one fused launch
+        (antkv_decode_step with the log-sum-exp output); the others attend."""
         c = self.cache
-        D = ctypes.byref(c.desc)
-        st = _lib.stream()
-        lib = _lib.load(check_device=False)
         if self.is_tail:
-            _lib.check(lib.antkv_cache_append(D, _lib.ptr(k), _lib.ptr(v), _lib.dtype_tag(k),
-                                              _lib.ptr(qpos), st))
-        c.attend_device(q, qpos, out_local, lse_local)
-        if self.is_tail:
-            _lib.check(lib.antkv_cache_evict(D, st))
+            c.step_device(q, k, v, qpos, out_local, lse_local)
+            c._n += 1
+        else:
+            c.attend_device(q, qpos, out_local, lse_local)
         o_all, l_all = gather_partials(out_local, lse_local, self.group)
         return self.combine(o_all, l_all)

@@ -553,9 +553,7 @@ def test_sequence_sharded_decode_matches_single_cache():
     without a window; the tail shard with the window, the appends, the
     evictions and the global anchor count) merged with the LSE combine must
     reproduce the single-cache decode outputs and anchor set."""
-    import ctypes
     from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
-    from paper_2506_19505_b200 import _lib as lib
     from paper_2506_19505_b200.parallel import lse_merge
     vq = VqConfig.from_notation("d8m256")
     Hq, Hkv, n, steps, W = 4, 1, 900, 30, 8
@@ -581,17 +579,17 @@ def test_sequence_sharded_decode_matches_single_cache():
         q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
         want = ref.decode_step(q, k, v, t)
         qpos = torch.tensor([t], device="cuda")
-        lib.check(lib.load().antkv_cache_append(ctypes.byref(tail.desc), lib.ptr(k), lib.ptr(v), lib.BF16,
-                                                lib.ptr(qpos), lib.stream()))
         parts, lses = [], []
         for c in shards:
             o = torch.empty((1, Hq, 128), device="cuda")
             l = torch.empty((1, Hq), device="cuda")
-            c.attend_device(q, qpos, o, l)
+            if c is tail:   # fused append + attention (with lse) + evict
+                c.step_device(q, k, v, qpos, o, l)
+                c._n += 1
+            else:
+                c.attend_device(q, qpos, o, l)
             parts.append(o)
             lses.append(l)
-        lib.check(lib.load().antkv_cache_evict(ctypes.byref(tail.desc), lib.stream()))
-        tail._n += 1
         got = lse_merge(torch.stack(parts), torch.stack(lses))
         assert rel(got.cpu().numpy(), want.cpu().numpy()) < 2e-2, t
     merged = sorted([int(j) for j in head.anchor_indices_of(0, 0)] +
