@@ -602,3 +602,23 @@ def test_gqa_batch2_fast_d8m256():
     cache, outs, refs = _gqa(24, 2, 8, 2, 400, 128, "d8m256", 10, window=16, theta=5e5, fast=True)
     for i in range(outs.shape[0]):
         assert rel(outs[i], refs[i]) < 2e-2
+
+
+def test_fast_kernel_one_split_multi_round_pool():
+    """splits = 1: every code tile and >8 pool tiles in one CTA per head
+    (several pool rounds, the refill path), against the generic kernel."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d8m256")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.1, window_size=32, theta_base=5e5)
+    Q, K, V = qkv(61, 8, 2, 2100, 128, heavy=4)
+    ck, cv = codebooks(61, 2, 256, 8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    outs = []
+    for fast in (True, False):
+        c = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=8, fast=fast, splits=1)
+        c.prefill(dev(Q[None, :, :2000]), dev(K[None, :, :2000]), dev(V[None, :, :2000]), np.arange(2000))
+        assert c.tensors["hstate"][0, 0, 4].item() > 8 * 16   # pool high-water: > 8 tiles
+        outs.append(np.stack([c.decode_step(dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t]), t)
+                              .cpu().numpy() for t in range(2000, 2012)]))
+    for i in range(outs[0].shape[0]):
+        assert rel(outs[0][i], outs[1][i]) < 2e-2
