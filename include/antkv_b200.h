@@ -19,6 +19,7 @@
  *   antkv_prefill_attention <- attention.flash_attention_aux (attention.py:146-169)
  *                             with RoPE (attention.py:89-106) fused, GQA-batched
  *   antkv_prefill_anchor_scores <- anchors.anchor_scores_blocked (anchors.py:66-87)
+ *   antkv_prefill_*_block  <- (new) the same two passes per sequence-shard block
  *   antkv_select_anchors   <- anchors.select_anchors  (anchors.py:96-132)
  *   antkv_cache_build      <- QuantizedKVCache.prefill layout step (cache.py:122-139)
  *   antkv_cache_append     <- QuantizedKVCache.decode_step append (cache.py:157-166)
@@ -134,6 +135,28 @@ ANTKV_API int antkv_prefill_anchor_scores(const void *Q, const void *K, int dtyp
                                 double theta_base, float *ans_k, float *ans_v,
                                 void *stream);
 
+/* Sequence-shard blocks of the two prefill passes (context parallelism,
+ * SURVEY.md §8e; parallel.py ShardedPrefill).  A query block Q [B][Hq][n_q][d]
+ * at q_positions [B][n_q] against a key block K/V [B][Hkv][n_k][d] at
+ * k_positions [B][n_k]; `causal` masks key index j > query index i within
+ * the block (diagonal blocks only: requires n_q == n_k).  The attention
+ * block returns the block-local (O, M, L) that parallel.merge_partial folds
+ * together, plus q_norms; the score block returns this block's share of
+ * ans_k/ans_v [B][Hkv][n_k] (summed over the query group, overwritten).
+ * antkv_prefill_attention / antkv_prefill_anchor_scores are the single-block
+ * case. */
+ANTKV_API int antkv_prefill_attention_block(const void *Q, const void *K, const void *V,
+                            int dtype, const int64_t *q_positions,
+                            const int64_t *k_positions, int B, int Hq, int Hkv,
+                            int n_q, int n_k, int d, double theta_base, int causal,
+                            float *O, float *M, float *L, float *q_norms, void *stream);
+ANTKV_API int antkv_prefill_anchor_scores_block(const void *Q, const void *K, int dtype,
+                            const int64_t *q_positions, const int64_t *k_positions,
+                            const float *M, const float *L, const float *q_norms,
+                            int B, int Hq, int Hkv, int n_q, int n_k, int d,
+                            double theta_base, int causal, float *ans_k, float *ans_v,
+                            void *stream);
+
 /* Top-budget selection per (b, kv head) under `policy`, ties to the lower
  * index, result sorted ascending: anchors int32 [B][Hkv][budget].
  * budget is clipped to [0, n] by the caller (anchors.py:104). */
@@ -195,7 +218,8 @@ ANTKV_API int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int sp
 
 /* Populate an EMPTY cache from prefill results (cache.py:122-139):
  * K/V [B][Hkv][n][d] (dtype), positions int64 [B][n], anchors int32
- * [B][Hkv][n_anchors] sorted.  Anchors keep full-precision rows, the last
+ * [B][Hkv][n_anchors] sorted, optionally ending in -1 padding (per-head
+ * counts may differ, e.g. on sequence shards).  Anchors keep full-precision rows, the last
  * window_size non-anchor tokens are windowed, the rest are encoded. */
 ANTKV_API int antkv_cache_build(const antkv_cache_desc *c, const void *K, const void *V,
                       int dtype, const int64_t *positions, int n,

@@ -56,6 +56,10 @@ _SIGS = {
     "antkv_rope_rotate": (_i, [_vp, _i, _vp, _i, _i, _i, _i, _d, _f, _vp, _vp, _vp]),
     "antkv_prefill_attention": (_i, [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp]),
     "antkv_prefill_anchor_scores": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp]),
+    "antkv_prefill_attention_block": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _i, _d, _i,
+                                           _vp, _vp, _vp, _vp, _vp]),
+    "antkv_prefill_anchor_scores_block": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,
+                                               _i, _d, _i, _vp, _vp, _vp]),
     "antkv_select_anchors": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "antkv_vq_encode": (_i, [_vp, _i, _i64, _i, _vp, _i, _i, _vp, _i, _vp]),
     "antkv_vq_decode": (_i, [_vp, _i, _i64, _i, _vp, _i, _i, _vp, _vp]),

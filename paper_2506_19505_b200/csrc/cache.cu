@@ -146,10 +146,20 @@ __device__ __forceinline__ int64_t bh_index(int b, int h, int H) { return (int64
 __global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ K,
                                    const void *__restrict__ V, int dtype,
                                    const int64_t *__restrict__ positions, int n,
-                                   const int32_t *__restrict__ anchors, int n_anchors) {
+                                   const int32_t *__restrict__ anchors, int anchor_stride) {
   const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
   const int64_t bh = bh_index(b, h, c.Hkv);
-  const int32_t *anc = anchors + bh * n_anchors;
+  const int32_t *anc = anchors + bh * anchor_stride;
+  // a list may end in -1 padding (sequence shards hold different anchor
+  // counts per head); the valid prefix is sorted ascending
+  __shared__ int s_na;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    while (k < anchor_stride && anc[k] >= 0) ++k;
+    s_na = k;
+  }
+  __syncthreads();
+  const int n_anchors = s_na;
   uint32_t *qm = c.qmask + bh * (c.capacity / 32);
   // quantized bit = not anchor and j < n - window
   const int wstart = n - c.window_size > 0 ? n - c.window_size : 0;

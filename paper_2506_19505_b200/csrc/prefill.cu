@@ -375,37 +375,87 @@ extern "C" int antkv_ans_blocked(const float *Qs, const float *Kr, const float *
 
 // Scratch for the rotated operands is allocated with cudaMallocAsync on the
 // caller's stream (stream-ordered, freed at the end of the call's work).
-extern "C" int antkv_prefill_attention(const void *Q, const void *K, const void *V,
-                                       int dtype, const int64_t *positions, int B, int Hq,
-                                       int Hkv, int n, int d, double theta_base, float *O,
-                                       float *M, float *L, float *q_norms, void *stream) {
+extern "C" int antkv_prefill_attention_block(const void *Q, const void *K, const void *V,
+                                             int dtype, const int64_t *q_positions,
+                                             const int64_t *k_positions, int B, int Hq, int Hkv,
+                                             int n_q, int n_k, int d, double theta_base,
+                                             int causal, float *O, float *M, float *L,
+                                             float *q_norms, void *stream) {
   ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
   ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
   ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
-  if ((int64_t)B * n == 0) return ANTKV_OK;
+  ANTKV_REQUIRE(B >= 0 && n_q >= 0 && n_k >= 0, "negative size");
+  ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
+  if ((int64_t)B * n_q == 0) return ANTKV_OK;
   cudaStream_t st = as_stream(stream);
   float *qs = nullptr, *kr = nullptr, *vf = nullptr;
-  size_t qbytes = sizeof(float) * (size_t)B * Hq * n * d;
-  size_t kbytes = sizeof(float) * (size_t)B * Hkv * n * d;
+  size_t qbytes = sizeof(float) * (size_t)B * Hq * n_q * d;
+  size_t kbytes = sizeof(float) * (size_t)B * Hkv * n_k * d;
   cudaError_t e = cudaMallocAsync(&qs, qbytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&kr, kbytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&vf, kbytes, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&kr, kbytes ? kbytes : 4, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&vf, kbytes ? kbytes : 4, st);
   if (e != cudaSuccess) return cuda_status(e, "prefill scratch");
-  int rc = rope_rotate(Q, dtype, positions, B, Hq, n, d, theta_base, 1.f / sqrtf((float)d), qs,
-                       q_norms, st);
-  if (rc == ANTKV_OK) rc = rope_rotate(K, dtype, positions, B, Hkv, n, d, theta_base, 1.f, kr,
-                                       nullptr, st);
-  if (rc == ANTKV_OK) rc = rope_rotate(V, dtype, nullptr, B, Hkv, n, d, theta_base, 1.f, vf,
+  int rc = rope_rotate(Q, dtype, q_positions, B, Hq, n_q, d, theta_base, 1.f / sqrtf((float)d),
+                       qs, q_norms, st);
+  if (rc == ANTKV_OK) rc = rope_rotate(K, dtype, k_positions, B, Hkv, n_k, d, theta_base, 1.f,
+                                       kr, nullptr, st);
+  if (rc == ANTKV_OK) rc = rope_rotate(V, dtype, nullptr, B, Hkv, n_k, d, theta_base, 1.f, vf,
                                        nullptr, st);
   for (int b = 0; b < B && rc == ANTKV_OK; ++b) {
-    rc = launch_flash(qs + (size_t)b * Hq * n * d, kr + (size_t)b * Hkv * n * d,
-                      vf + (size_t)b * Hkv * n * d, Hq, Hkv, n, n, d, d, 1,
-                      O + (size_t)b * Hq * n * d, L + (size_t)b * Hq * n,
-                      M + (size_t)b * Hq * n, st);
+    rc = launch_flash(qs + (size_t)b * Hq * n_q * d, kr + (size_t)b * Hkv * n_k * d,
+                      vf + (size_t)b * Hkv * n_k * d, Hq, Hkv, n_q, n_k, d, d, causal,
+                      O + (size_t)b * Hq * n_q * d, L + (size_t)b * Hq * n_q,
+                      M + (size_t)b * Hq * n_q, st);
   }
   cudaFreeAsync(qs, st);
   cudaFreeAsync(kr, st);
   cudaFreeAsync(vf, st);
+  return rc;
+}
+
+extern "C" int antkv_prefill_attention(const void *Q, const void *K, const void *V,
+                                       int dtype, const int64_t *positions, int B, int Hq,
+                                       int Hkv, int n, int d, double theta_base, float *O,
+                                       float *M, float *L, float *q_norms, void *stream) {
+  return antkv_prefill_attention_block(Q, K, V, dtype, positions, positions, B, Hq, Hkv, n, n,
+                                       d, theta_base, 1, O, M, L, q_norms, stream);
+}
+
+extern "C" int antkv_prefill_anchor_scores_block(const void *Q, const void *K, int dtype,
+                                                 const int64_t *q_positions,
+                                                 const int64_t *k_positions, const float *M,
+                                                 const float *L, const float *q_norms, int B,
+                                                 int Hq, int Hkv, int n_q, int n_k, int d,
+                                                 double theta_base, int causal, float *ans_k,
+                                                 float *ans_v, void *stream) {
+  ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
+  ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
+  ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  ANTKV_REQUIRE(B >= 0 && n_q >= 0 && n_k >= 0, "negative size");
+  ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
+  if ((int64_t)B * n_k == 0) return ANTKV_OK;
+  cudaStream_t st = as_stream(stream);
+  if (n_q == 0) {  // no queries: this block contributes nothing
+    cudaError_t e = cudaMemsetAsync(ans_k, 0, sizeof(float) * (size_t)B * Hkv * n_k, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ans_v, 0, sizeof(float) * (size_t)B * Hkv * n_k, st);
+    return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "anchor-score clear");
+  }
+  float *qs = nullptr, *kr = nullptr;
+  cudaError_t e = cudaMallocAsync(&qs, sizeof(float) * (size_t)B * Hq * n_q * d, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&kr, sizeof(float) * (size_t)B * Hkv * n_k * d, st);
+  if (e != cudaSuccess) return cuda_status(e, "anchor-score scratch");
+  int rc = rope_rotate(Q, dtype, q_positions, B, Hq, n_q, d, theta_base, 1.f / sqrtf((float)d),
+                       qs, nullptr, st);
+  if (rc == ANTKV_OK) rc = rope_rotate(K, dtype, k_positions, B, Hkv, n_k, d, theta_base, 1.f,
+                                       kr, nullptr, st);
+  for (int b = 0; b < B && rc == ANTKV_OK; ++b) {
+    rc = launch_ans(qs + (size_t)b * Hq * n_q * d, kr + (size_t)b * Hkv * n_k * d,
+                    M + (size_t)b * Hq * n_q, L + (size_t)b * Hq * n_q,
+                    q_norms + (size_t)b * Hq * n_q, Hq, Hkv, Hq / Hkv, n_q, n_k, d, causal,
+                    ans_k + (size_t)b * Hkv * n_k, ans_v + (size_t)b * Hkv * n_k, st);
+  }
+  cudaFreeAsync(qs, st);
+  cudaFreeAsync(kr, st);
   return rc;
 }
 
@@ -414,25 +464,6 @@ extern "C" int antkv_prefill_anchor_scores(const void *Q, const void *K, int dty
                                            const float *L, const float *q_norms, int B,
                                            int Hq, int Hkv, int n, int d, double theta_base,
                                            float *ans_k, float *ans_v, void *stream) {
-  ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
-  ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
-  if ((int64_t)B * n == 0) return ANTKV_OK;
-  cudaStream_t st = as_stream(stream);
-  float *qs = nullptr, *kr = nullptr;
-  cudaError_t e = cudaMallocAsync(&qs, sizeof(float) * (size_t)B * Hq * n * d, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&kr, sizeof(float) * (size_t)B * Hkv * n * d, st);
-  if (e != cudaSuccess) return cuda_status(e, "anchor-score scratch");
-  int rc = rope_rotate(Q, dtype, positions, B, Hq, n, d, theta_base, 1.f / sqrtf((float)d), qs,
-                       nullptr, st);
-  if (rc == ANTKV_OK) rc = rope_rotate(K, dtype, positions, B, Hkv, n, d, theta_base, 1.f, kr,
-                                       nullptr, st);
-  for (int b = 0; b < B && rc == ANTKV_OK; ++b) {
-    rc = launch_ans(qs + (size_t)b * Hq * n * d, kr + (size_t)b * Hkv * n * d,
-                    M + (size_t)b * Hq * n, L + (size_t)b * Hq * n, q_norms + (size_t)b * Hq * n,
-                    Hq, Hkv, Hq / Hkv, n, n, d, 1, ans_k + (size_t)b * Hkv * n,
-                    ans_v + (size_t)b * Hkv * n, st);
-  }
-  cudaFreeAsync(qs, st);
-  cudaFreeAsync(kr, st);
-  return rc;
+  return antkv_prefill_anchor_scores_block(Q, K, dtype, positions, positions, M, L, q_norms, B,
+                                           Hq, Hkv, n, n, d, theta_base, 1, ans_k, ans_v, stream);
 }

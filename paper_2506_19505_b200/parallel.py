@@ -7,6 +7,16 @@ a normalised partial output and its log-sum-exp, all-gathers the partials
 (NCCL over NVLink; ~Hq*(d+1)*4 bytes per rank per layer-step) and merges them
 with the LSE combine kernel.  This is the only exchange on the decode path
 (SURVEY.md §5, §8e).
+
+Prefill shards the same way (context parallelism, SURVEY.md §8e "prefill
+partitioning"): the FA pass rings the key/value blocks past every rank and
+folds the block partials (O, M, L) online; the AnS pass rings the query
+blocks (with their final M, L and ‖q‖) past every rank, each rank summing the
+column scores of its own keys; selection all-gathers each shard's candidate
+set (its local top-B by each score, with both scores and global indices)
+and every rank runs the same selection on the union, which contains every
+token the global by_k / by_v / by_sum selection can reach.  Ties keep the
+lower global index because the union is laid out in global order.
 """
 
 import numpy as np
@@ -15,7 +25,9 @@ import torch.distributed as dist
 
 from . import _lib
 
-__all__ = ["shard_ranges", "gather_partials", "lse_merge", "ShardedDecoder"]
+__all__ = ["shard_ranges", "gather_partials", "lse_merge", "ShardedDecoder", "RingTransport",
+           "CudaPrefillOps", "merge_partial", "sharded_attention", "sharded_anchor_scores",
+           "shard_candidates", "choose_anchors", "sharded_prefill"]
 
 
 def shard_ranges(n, world):
@@ -80,3 +92,245 @@ class ShardedDecoder:
             c.attend_device(q, qpos, out_local, lse_local)
         o_all, l_all = gather_partials(out_local, lse_local, self.group)
         return self.combine(o_all, l_all)
+
+
+# ------------------------------------------------------------------ prefill
+class RingTransport:
+    """Blocks travel rank r -> r+1 over the process group; while the caller
+    computes on the block it was handed, the next one is already in flight
+    (one batched isend/irecv per step).  NCCL moves device tensors directly;
+    other backends (gloo, CPU tests) stage through host memory."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self._device_ok = dist.get_backend(group) == "nccl"
+
+    def _peer(self, r):
+        return r if self.group is None else dist.get_global_rank(self.group, r)
+
+    def _exchange(self, send, recv):
+        dst = self._peer((self.rank + 1) % self.world)
+        src = self._peer((self.rank - 1) % self.world)
+        if self._device_ok:
+            stage_s, stage_r = [t.contiguous() for t in send], list(recv)
+        else:
+            stage_s = [t.detach().cpu().contiguous() for t in send]
+            stage_r = [torch.empty(t.shape, dtype=t.dtype) for t in recv]
+        ops = [dist.P2POp(dist.isend, t, dst, self.group) for t in stage_s]
+        ops += [dist.P2POp(dist.irecv, t, src, self.group) for t in stage_r]
+        return dist.batch_isend_irecv(ops), stage_r
+
+    def ring(self, local, like):
+        """Yield (origin, block) for origin = r, r-1, ..., r-P+1 (mod P).
+        `local` is this rank's block (a tuple of tensors), `like(origin)`
+        returns empty tensors shaped as that origin's block."""
+        cur = tuple(local)
+        for s in range(self.world):
+            pending = None
+            if s < self.world - 1:
+                nxt = like((self.rank - s - 1) % self.world)
+                pending = (nxt,) + self._exchange(cur, nxt)
+            yield (self.rank - s) % self.world, cur
+            if pending is not None:
+                nxt, works, staged = pending
+                for w in works:
+                    w.wait()
+                if not self._device_ok:
+                    for dst_t, src_t in zip(nxt, staged):
+                        dst_t.copy_(src_t)
+                cur = nxt
+
+    def all_gather(self, t):
+        """[*shape] -> [P, *shape]."""
+        t = t.contiguous()
+        src = t if self._device_ok else t.cpu()
+        out = torch.empty((self.world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype,
+                          device=src.device)
+        dist.all_gather_into_tensor(out, src, group=self.group)
+        return out.view((self.world,) + tuple(src.shape)).to(t.device)
+
+
+class CudaPrefillOps:
+    """Per-block prefill kernels (antkv_prefill_attention_block,
+    antkv_prefill_anchor_scores_block, antkv_select_anchors)."""
+
+    @staticmethod
+    def _tag(*ts):
+        tag = _lib.dtype_tag(ts[0])
+        if any(_lib.dtype_tag(t) != tag for t in ts[1:]):
+            raise ValueError("Q, K and V must share one dtype")
+        return tag
+
+    def attention_block(self, Q, K, V, qpos, kpos, causal, theta):
+        B, Hq, nq, d = Q.shape
+        Hkv, nk = K.shape[1], K.shape[2]
+        O = torch.empty((B, Hq, nq, d), dtype=torch.float32, device=Q.device)
+        M = torch.empty((B, Hq, nq), dtype=torch.float32, device=Q.device)
+        L = torch.empty_like(M)
+        qn = torch.empty_like(M)
+        _lib.call("antkv_prefill_attention_block", _lib.ptr(Q), _lib.ptr(K), _lib.ptr(V),
+                  self._tag(Q, K, V), _lib.ptr(qpos), _lib.ptr(kpos), B, Hq, Hkv, nq, nk, d,
+                  float(theta), int(bool(causal)), _lib.ptr(O), _lib.ptr(M), _lib.ptr(L),
+                  _lib.ptr(qn), _lib.stream())
+        return O, M, L, qn
+
+    def score_block(self, Q, K, qpos, kpos, M, L, qn, causal, theta):
+        B, Hq, nq, d = Q.shape
+        Hkv, nk = K.shape[1], K.shape[2]
+        ak = torch.empty((B, Hkv, nk), dtype=torch.float32, device=K.device)
+        av = torch.empty_like(ak)
+        _lib.call("antkv_prefill_anchor_scores_block", _lib.ptr(Q), _lib.ptr(K), self._tag(Q, K),
+                  _lib.ptr(qpos), _lib.ptr(kpos), _lib.ptr(M.contiguous()),
+                  _lib.ptr(L.contiguous()), _lib.ptr(qn.contiguous()), B, Hq, Hkv, nq, nk, d,
+                  float(theta), int(bool(causal)), _lib.ptr(ak), _lib.ptr(av), _lib.stream())
+        return ak, av
+
+    def select(self, sk, sv, budget, policy):
+        from .anchors import select_anchors_device
+        return select_anchors_device(sk.contiguous(), sv.contiguous(), int(budget), policy)
+
+
+def merge_partial(acc, part):
+    """Fold a block partial (O, M, L) into the running one: the softmax over
+    the union of the two key sets (normalised O, M = max scaled logit, L =
+    sum of exp(s - M))."""
+    if acc is None:
+        return part
+    O1, M1, L1 = acc
+    O2, M2, L2 = part
+    M = torch.maximum(M1, M2)
+    a1 = L1 * torch.exp(M1 - M)
+    a2 = L2 * torch.exp(M2 - M)
+    L = a1 + a2
+    O = (O1 * a1[..., None] + O2 * a2[..., None]) / L[..., None]
+    return O, M, L
+
+
+def sharded_attention(Q, K, V, pos, ring, rank, ops, theta):
+    """FA pass on rank `rank`: Q [B, Hq, n_r, d] against every key block
+    of ranks <= rank (causal on the diagonal).  `ring` yields (origin,
+    (K_o, V_o, pos_o)).  Returns (O, M, L, q_norms) of the local queries."""
+    acc, qn = None, None
+    for o, (Ko, Vo, po) in ring:
+        if o > rank:
+            continue
+        O, M, L, qn_b = ops.attention_block(Q, Ko, Vo, pos, po, o == rank, theta)
+        acc = merge_partial(acc, (O, M, L))
+        if o == rank:
+            qn = qn_b
+    return acc[0], acc[1], acc[2], qn
+
+
+def sharded_anchor_scores(K, pos, ring, rank, ops, theta):
+    """AnS pass on rank `rank`: the column scores of the local keys
+    [B, Hkv, n_r] summed over every query block of ranks >= rank.  `ring`
+    yields (origin, (Q_o, pos_o, M_o, L_o, qn_o))."""
+    ak = av = None
+    for o, (Qo, po, Mo, Lo, qno) in ring:
+        if o < rank:
+            continue
+        bk, bv = ops.score_block(Qo, K, po, pos, Mo, Lo, qno, o == rank, theta)
+        ak = bk if ak is None else ak + bk
+        av = bv if av is None else av + bv
+    return ak, av
+
+
+def shard_candidates(ak, av, budget, start, ops):
+    """One shard's selection candidates: the union of its local top-budget by
+    ans_k and by ans_v, in ascending index order, padded to 2*budget with
+    score -1 / index -1.  ak/av [R, n_r] -> (sk, sv float32, gidx int64)
+    [R, 2*budget].  (Scores are nonnegative, so padding never wins.)"""
+    R, n = ak.shape
+    c = min(int(budget), n)
+    width = 2 * int(budget)
+    sk = torch.full((R, width), -1.0, dtype=torch.float32, device=ak.device)
+    sv = torch.full_like(sk, -1.0)
+    gidx = torch.full((R, width), -1, dtype=torch.int64, device=ak.device)
+    if c == 0:
+        return sk, sv, gidx
+    ik = ops.select(ak, ak, c, "by_k").long()
+    iv = ops.select(av, av, c, "by_v").long()
+    cand, _ = torch.cat([ik, iv], 1).sort(1)
+    dup = torch.zeros_like(cand, dtype=torch.bool)
+    dup[:, 1:] = cand[:, 1:] == cand[:, :-1]
+    cand, _ = torch.where(dup, n, cand).sort(1)
+    valid = cand < n
+    safe = cand.clamp(max=n - 1)
+    w = cand.shape[1]
+    sk[:, :w] = torch.where(valid, ak.float().gather(1, safe), -1.0)
+    sv[:, :w] = torch.where(valid, av.float().gather(1, safe), -1.0)
+    gidx[:, :w] = torch.where(valid, cand + int(start), -1)
+    return sk, sv, gidx
+
+
+def choose_anchors(sk_all, sv_all, g_all, budget, policy, start, stop, ops):
+    """Global selection from every shard's candidates ([P, R, C] each, rank
+    order): the policy runs on the union laid out in global index order, so
+    ties resolve to the lower global index as in anchors.py:90-93.  Returns
+    (local int32 [R, A] sorted, -1 padded; global int64 [R, budget])."""
+    P, R, C = sk_all.shape
+    SK = sk_all.permute(1, 0, 2).reshape(R, P * C).contiguous()
+    SV = sv_all.permute(1, 0, 2).reshape(R, P * C).contiguous()
+    G = g_all.permute(1, 0, 2).reshape(R, P * C)
+    sel = ops.select(SK, SV, int(budget), policy).long()
+    glob = G.gather(1, sel)
+    mine = (glob >= start) & (glob < stop)
+    big = torch.iinfo(torch.int64).max
+    local, _ = torch.where(mine, glob - start, big).sort(1)
+    width = max(int(mine.sum(1).max()) if R else 0, 1)
+    local = local[:, :width]
+    local = torch.where(local == big, -1, local).to(torch.int32)
+    return local, glob
+
+
+def sharded_prefill(cache, Q, K, V, positions, start, n_total, transport, is_tail, ops=None):
+    """Context-parallel prefill of one rank's shard [start, start + n_r) of
+    every sequence: FA ring, AnS ring, global anchor selection, and the
+    shard's cache layout (cache.py:100-140 over the whole sequence).  The
+    cache must be empty and created with token_offset=start (window 0 on
+    non-tail ranks).  Returns the shard's full-precision output
+    O [B, Hq, n_r, d] float32."""
+    ops = ops or CudaPrefillOps()
+    B, Hq, n, d = Q.shape
+    Hkv = K.shape[1]
+    theta = float(cache.config.theta_base)
+    pos = positions.contiguous()
+    ranges = shard_ranges(n_total, transport.world)
+    if ranges[transport.rank] != (start, start + n):
+        raise ValueError("shard does not match shard_ranges(n_total, world)")
+    dev = Q.device
+
+    def like_kv(o):
+        m = ranges[o][1] - ranges[o][0]
+        return (torch.empty((B, Hkv, m, d), dtype=K.dtype, device=dev),
+                torch.empty((B, Hkv, m, d), dtype=V.dtype, device=dev),
+                torch.empty((B, m), dtype=torch.int64, device=dev))
+
+    O, M, L, qn = sharded_attention(Q, K, V, pos, transport.ring((K, V, pos), like_kv),
+                                    transport.rank, ops, theta)
+
+    def like_q(o):
+        m = ranges[o][1] - ranges[o][0]
+        return (torch.empty((B, Hq, m, d), dtype=Q.dtype, device=dev),
+                torch.empty((B, m), dtype=torch.int64, device=dev),
+                torch.empty((B, Hq, m), dtype=torch.float32, device=dev),
+                torch.empty((B, Hq, m), dtype=torch.float32, device=dev),
+                torch.empty((B, Hq, m), dtype=torch.float32, device=dev))
+
+    ak, av = sharded_anchor_scores(K, pos, transport.ring((Q, pos, M, L, qn), like_q),
+                                   transport.rank, ops, theta)
+    budget = int(cache.config.budget_for(n_total))
+    sk, sv, g = shard_candidates(ak.view(B * Hkv, n), av.view(B * Hkv, n), budget, start,
+                                ops)
+    local, _ = choose_anchors(transport.all_gather(sk), transport.all_gather(sv),
+                              transport.all_gather(g), budget, cache.config.policy, start,
+                              start + n, ops)
+    cache.Hq, cache.Hkv = Hq, Hkv
+    cache.build_from(K, V, pos, local.view(B, Hkv, -1))
+    if is_tail:
+        # promotions on the tail follow the global anchor count
+        cache.tensors["hstate"][:, :, _lib.HS_ANCHORS] = budget
+    cache.last_scores = (ak, av)
+    return O

@@ -622,3 +622,147 @@ def test_fast_kernel_one_split_multi_round_pool():
                               .cpu().numpy() for t in range(2000, 2012)]))
     for i in range(outs[0].shape[0]):
         assert rel(outs[0][i], outs[1][i]) < 2e-2
+
+
+class _LocalRing:
+    """Every rank's block, visited in the ring order rank r sees
+    (r, r-1, ...): drives the sharded prefill phases of P ranks in one
+    process, with the same per-block CUDA kernels as the NCCL path."""
+
+    def __init__(self, rank, blocks):
+        self.rank, self.blocks = rank, blocks
+
+    def __iter__(self):
+        P = len(self.blocks)
+        for s in range(P):
+            o = (self.rank - s) % P
+            yield o, self.blocks[o]
+
+
+def test_sequence_sharded_prefill_then_decode_matches_single_cache():
+    """Context-parallel prefill on 3 shards (FA ring, AnS ring, global
+    selection from the shards' candidates, per-shard layout) followed by
+    sharded decode reproduces the single-cache prefill output, anchor set and
+    decode outputs."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.parallel import (CudaPrefillOps, choose_anchors, lse_merge,
+                                                shard_candidates, shard_ranges,
+                                                sharded_anchor_scores, sharded_attention)
+    vq = VqConfig.from_notation("d8m256")
+    Hq, Hkv, n, steps, W, P = 8, 2, 1000, 24, 8, 3
+    Q, K, V = qkv(61, Hq, Hkv, n + steps, 128, heavy=3)
+    ck, cv = codebooks(61, Hkv, 256, 8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    cfg = lambda w: CacheConfig(vq=vq, anchor_fraction=0.02, window_size=w, theta_base=5e5)
+    ref = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    O_ref = ref.prefill(dev(Q[None, :, :n]), dev(K[None, :, :n]), dev(V[None, :, :n]), np.arange(n))
+    ops = CudaPrefillOps()
+    ranges = shard_ranges(n, P)
+    blk = [(dev(Q[None, :, s:e]), dev(K[None, :, s:e]), dev(V[None, :, s:e]),
+            torch.arange(s, e, device="cuda")[None]) for s, e in ranges]
+    fa = [sharded_attention(blk[r][0], blk[r][1], blk[r][2], blk[r][3],
+                            _LocalRing(r, [(b[1], b[2], b[3]) for b in blk]), r, ops, 5e5)
+          for r in range(P)]
+    O_sh = torch.cat([f[0] for f in fa], dim=2)
+    assert rel(O_sh.cpu().numpy(), O_ref.cpu().numpy()) < 1e-4
+    qblocks = [(blk[o][0], blk[o][3], fa[o][1], fa[o][2], fa[o][3]) for o in range(P)]
+    scores = [sharded_anchor_scores(blk[r][1], blk[r][3], _LocalRing(r, qblocks), r, ops, 5e5)
+              for r in range(P)]
+    ak_ref, av_ref = ref.last_scores
+    ak = torch.cat([s[0] for s in scores], dim=2)
+    av = torch.cat([s[1] for s in scores], dim=2)
+    assert rel(ak.cpu().numpy(), ak_ref.cpu().numpy()) < 1e-4
+    assert rel(av.cpu().numpy(), av_ref.cpu().numpy()) < 1e-4
+    budget = ref.config.budget_for(n)
+    cands = [shard_candidates(s[0].view(Hkv, -1), s[1].view(Hkv, -1), budget, ranges[r][0], ops)
+             for r, s in enumerate(scores)]
+    stack = [torch.stack([c[i] for c in cands]) for i in range(3)]
+    shards = []
+    for r, (s, e) in enumerate(ranges):
+        local, glob = choose_anchors(*stack, budget, "by_sum", s, e, ops)
+        for h in range(Hkv):
+            assert glob[h].tolist() == [int(j) for j in ref.anchor_indices_of(0, h)]
+        tail = r == P - 1
+        c = QuantizedKVCache(cfg(W if tail else 0), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq,
+                             token_offset=s, capacity=e - s + steps + 64)
+        c.Hq = Hq
+        c.build_from(blk[r][1], blk[r][2], blk[r][3], local.view(1, Hkv, -1))
+        if tail:
+            c.tensors["hstate"][:, :, 0] = budget
+        shards.append(c)
+    for t in range(n, n + steps):
+        q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
+        want = ref.decode_step(q, k, v, t)
+        qpos = torch.tensor([t], device="cuda")
+        parts, lses = [], []
+        for c in shards:
+            o = torch.empty((1, Hq, 128), device="cuda")
+            l = torch.empty((1, Hq), device="cuda")
+            if c is shards[-1]:
+                c.step_device(q, k, v, qpos, o, l)
+                c._n += 1
+            else:
+                c.attend_device(q, qpos, o, l)
+            parts.append(o)
+            lses.append(l)
+        got = lse_merge(torch.stack(parts), torch.stack(lses))
+        assert rel(got.cpu().numpy(), want.cpu().numpy()) < 2e-2, t
+    for h in range(Hkv):
+        merged = sorted(int(j) + s for c, (s, _) in zip(shards, ranges) for j in c.anchor_indices_of(0, h))
+        assert merged == [int(j) for j in ref.anchor_indices_of(0, h)]
+
+
+def _sharded_prefill_worker(rank, world, port, Q, K, V, ck, cv, W, ret):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.parallel import RingTransport, shard_ranges, sharded_prefill
+    vq = VqConfig.from_notation("d8m256")
+    n = Q.shape[1]
+    s, e = shard_ranges(n, world)[rank]
+    tail = rank == world - 1
+    cache = QuantizedKVCache(CacheConfig(vq=vq, anchor_fraction=0.02, window_size=W if tail else 0),
+                             Codebook(vq, ck), Codebook(vq, cv), q_heads=Q.shape[0], token_offset=s,
+                             capacity=e - s + 64)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    O_r = sharded_prefill(cache, dev(Q[None, :, s:e]), dev(K[None, :, s:e]), dev(V[None, :, s:e]),
+                          torch.arange(s, e, device="cuda")[None], s, n, RingTransport(), tail)
+    anchors = [[int(j) + s for j in cache.anchor_indices_of(0, h)] for h in range(K.shape[0])]
+    ret.put((rank, O_r.cpu().numpy(), anchors, cache.kinds_of(0, 0)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharded_prefill_driver_two_processes_gloo():
+    """parallel.sharded_prefill end to end in two processes (gloo ring,
+    host-staged, both on cuda:0): shard outputs, anchors and token kinds
+    equal the single-cache prefill."""
+    import os
+    import torch.multiprocessing as mp
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d8m256")
+    Hq, Hkv, n, W = 4, 1, 700, 8
+    Q, K, V = qkv(71, Hq, Hkv, n, 128, heavy=3)
+    ck, cv = codebooks(71, Hkv, 256, 8)
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = 29700 + (os.getpid() % 200)
+    procs = [ctx.Process(target=_sharded_prefill_worker, args=(r, 2, port, Q, K, V, ck, cv, W, ret))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([ret.get(timeout=300) for _ in range(2)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    ref = QuantizedKVCache(CacheConfig(vq=vq, anchor_fraction=0.02, window_size=W),
+                           Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    O_ref = ref.prefill(dev(Q[None]), dev(K[None]), dev(V[None]), np.arange(n)).cpu().numpy()
+    O_sh = np.concatenate([r[1] for r in res], axis=2)
+    assert rel(O_sh, O_ref) < 1e-4
+    assert sorted(res[0][2][0] + res[1][2][0]) == [int(j) for j in ref.anchor_indices_of(0, 0)]
+    assert list(res[0][3]) + list(res[1][3]) == list(ref.kinds_of(0, 0))

@@ -186,3 +186,135 @@ def test_package_never_imports_the_oracle():
         assert not re.search(r"^\s*(import|from)\s+\S*oracle", src, re.M), f
         assert "antkv_oracle" not in src, f
         assert "/root/reference" not in src, f
+
+
+class _OraclePrefillOps:
+    """Block ops restated with the oracle (fp64, per head), so the ring
+    schedule, the partial merge and the candidate selection of the sharded
+    prefill can run on CPU ranks over gloo."""
+
+    def __init__(self, block=16):
+        self.block = block
+
+    def attention_block(self, Q, K, V, qpos, kpos, causal, theta):
+        B, Hq, nq, d = Q.shape
+        g = Hq // K.shape[1]
+        O_, M_, L_, N_ = (np.zeros((B, Hq, nq, d)), np.zeros((B, Hq, nq)), np.zeros((B, Hq, nq)),
+                          np.zeros((B, Hq, nq)))
+        for b in range(B):
+            for h in range(Hq):
+                q = Q[b, h].double().numpy()
+                Qs = O.apply_rope(q, qpos[b].numpy(), theta) / np.sqrt(d)
+                Kr = O.apply_rope(K[b, h // g].double().numpy(), kpos[b].numpy(), theta)
+                O_[b, h], L_[b, h], M_[b, h] = O.flash_aux(Qs, Kr, V[b, h // g].double().numpy(),
+                                                           self.block, self.block, causal)
+                N_[b, h] = np.sqrt((q ** 2).sum(axis=1))
+        return tuple(torch.from_numpy(x) for x in (O_, M_, L_, N_))
+
+    def score_block(self, Q, K, qpos, kpos, M, L, qn, causal, theta):
+        B, Hq, nq, d = Q.shape
+        Hkv, nk = K.shape[1], K.shape[2]
+        g = Hq // Hkv
+        ak, av = np.zeros((B, Hkv, nk)), np.zeros((B, Hkv, nk))
+        for b in range(B):
+            for h in range(Hq):
+                Qs = O.apply_rope(Q[b, h].double().numpy(), qpos[b].numpy(), theta) / np.sqrt(d)
+                Kr = O.apply_rope(K[b, h // g].double().numpy(), kpos[b].numpy(), theta)
+                k_, v_ = O.ans_blocked(Qs, Kr, M[b, h].numpy(), L[b, h].numpy(), qn[b, h].numpy(),
+                                       self.block, self.block, causal)
+                ak[b, h // g] += k_
+                av[b, h // g] += v_
+        return torch.from_numpy(ak), torch.from_numpy(av)
+
+    def select(self, sk, sv, budget, policy):
+        rows = [O.select_anchors(sk[r].double().numpy(), sv[r].double().numpy(), budget, policy)
+                for r in range(sk.shape[0])]
+        return torch.from_numpy(np.stack(rows)).to(torch.int32)
+
+
+def _prefill_shard_worker(rank, world, port, Q, K, V, budget, policy, theta, ret):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_19505_b200.parallel import (RingTransport, choose_anchors, shard_candidates,
+                                                shard_ranges, sharded_anchor_scores,
+                                                sharded_attention)
+    ops = _OraclePrefillOps()
+    tr = RingTransport()
+    B, Hq, n, d = Q.shape
+    Hkv = K.shape[1]
+    ranges = shard_ranges(n, world)
+    s, e = ranges[rank]
+    pos = torch.arange(n, dtype=torch.int64)[None].repeat(B, 1)
+    Qr, Kr, Vr, pr = Q[:, :, s:e], K[:, :, s:e], V[:, :, s:e], pos[:, s:e].contiguous()
+
+    def like_kv(o):
+        m = ranges[o][1] - ranges[o][0]
+        return (torch.empty((B, Hkv, m, d), dtype=K.dtype), torch.empty((B, Hkv, m, d), dtype=V.dtype),
+                torch.empty((B, m), dtype=torch.int64))
+
+    def like_q(o):
+        m = ranges[o][1] - ranges[o][0]
+        return (torch.empty((B, Hq, m, d), dtype=Q.dtype), torch.empty((B, m), dtype=torch.int64),
+                *[torch.empty((B, Hq, m), dtype=torch.float64) for _ in range(3)])
+
+    Ob, Mb, Lb, qn = sharded_attention(Qr, Kr, Vr, pr, tr.ring((Kr, Vr, pr), like_kv), rank, ops,
+                                       theta)
+    ak, av = sharded_anchor_scores(Kr, pr, tr.ring((Qr, pr, Mb, Lb, qn), like_q), rank, ops, theta)
+    sk, sv, g = shard_candidates(ak.view(B * Hkv, -1), av.view(B * Hkv, -1), budget, s, ops)
+    local, glob = choose_anchors(tr.all_gather(sk), tr.all_gather(sv), tr.all_gather(g), budget,
+                                 policy, s, e, ops)
+    ret.put((rank, Ob.numpy(), Mb.numpy(), Lb.numpy(), ak.numpy(), av.numpy(), local.numpy(),
+             glob.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", ["by_sum", "by_k", "by_v"])
+def test_sequence_sharded_prefill_gloo_world3(policy):
+    """Context-parallel prefill over 3 gloo ranks (FA ring, AnS ring,
+    candidate all-gather + global selection) reproduces the unsharded
+    reference pipeline: O/M/L/AnS to fp64 rounding, anchors exactly."""
+    rng = np.random.default_rng(11)
+    B, Hq, Hkv, n, d, theta, budget = 1, 4, 2, 70, 8, 10000.0, 9
+    Q = torch.from_numpy(rng.standard_normal((B, Hq, n, d)))
+    K = torch.from_numpy(rng.standard_normal((B, Hkv, n, d)))
+    V = torch.from_numpy(rng.standard_normal((B, Hkv, n, d)))
+    K[0, :, [5, 33, 61]] *= 4.0          # heavy hitters on every shard
+    world = 3
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    port = 29500 + ((os.getpid() + 7 + len(policy)) % 1000)
+    procs = [ctx.Process(target=_prefill_shard_worker,
+                         args=(r, world, port, Q, K, V, budget, policy, theta, ret))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([ret.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    g = Hq // Hkv
+    pos = np.arange(n)
+    from paper_2506_19505_b200.parallel import shard_ranges
+    ranges = shard_ranges(n, world)
+    ans_k = np.zeros((Hkv, n))
+    ans_v = np.zeros((Hkv, n))
+    for h in range(Hq):
+        q, k, v = Q[0, h].numpy(), K[0, h // g].numpy(), V[0, h // g].numpy()
+        Or, Lr, Mr, qn = O.flash_attention_aux(q, k, v, 16, 16, pos, theta, causal=True)
+        ak, av = O.anchor_scores_blocked(q, k, Mr, Lr, qn, 16, 16, pos, theta, causal=True)
+        ans_k[h // g] += ak
+        ans_v[h // g] += av
+        for r, (s, e) in enumerate(ranges):
+            assert np.abs(res[r][1][0, h] - Or[s:e]).max() < 1e-10
+            assert np.abs(res[r][2][0, h] - Mr[s:e]).max() < 1e-10
+            assert np.abs(res[r][3][0, h] / Lr[s:e] - 1).max() < 1e-10
+    for h in range(Hkv):
+        want = O.select_anchors(ans_k[h], ans_v[h], budget, policy)
+        for r, (s, e) in enumerate(ranges):
+            assert np.abs(res[r][4][0, h] - ans_k[h, s:e]).max() < 1e-9
+            assert np.abs(res[r][5][0, h] - ans_v[h, s:e]).max() < 1e-9
+            assert res[r][7][h].tolist() == want.tolist()
+            loc = res[r][6][h]
+            assert [int(j) + s for j in loc if j >= 0] == [int(j) for j in want if s <= j < e]
