@@ -28,6 +28,8 @@
  *   antkv_cache_dequantize <- QuantizedKVCache.dequantize (cache.py:196-211)
  *   antkv_vq_encode        <- vq.encode_rows (vq.py:226-232)
  *   antkv_vq_decode        <- vq.decode_rows (vq.py:243-248)
+ *   antkv_kmeans_*_f64     <- vq.weighted_kmeans Lloyd step (vq.py:178-197) with
+ *                             kernels.assign_nearest (_ckernels.pyx:134-163)
  *   antkv_lse_combine      <- (new) split-KV / sequence-shard log-sum-exp merge
  */
 #ifndef ANTKV_B200_H
@@ -269,6 +271,19 @@ ANTKV_API int antkv_cache_dequantize(const antkv_cache_desc *c, int n, float *Kh
  * out [rows][d], lse_out [rows] (may be NULL). */
 ANTKV_API int antkv_lse_combine(const float *o, const float *lse, int P, int64_t rows,
                       int d, float *out, float *lse_out, void *stream);
+
+/* Codebook training (weighted k-means, vq.py:141-214), float64 with the
+ * reference's operation order (bit-identical results).
+ * assign: X [n][d], C [m][d] -> idx int64 [n], d2 float64 [n]; sequential
+ *   sum over t of (x_t - c_t)^2 without FMA, strict-< argmin (d <= 64).
+ * update: members of cluster c are perm[offsets[c] .. offsets[c+1]) in
+ *   ascending point order (a stable sort of idx); C_new[c] = sum w_j x_j /
+ *   sum w_j for clusters with positive weight, else C_old[c]; wsum [m]. */
+ANTKV_API int antkv_kmeans_assign_f64(const double *X, const double *C, int64_t n, int m,
+                                      int d, int64_t *idx, double *d2, void *stream);
+ANTKV_API int antkv_kmeans_update_f64(const int64_t *perm, const int64_t *offsets,
+                                      const double *X, const double *w, const double *C_old,
+                                      int m, int d, double *C_new, double *wsum, void *stream);
 
 /* Debug: per-CTA timeline of the last fast-decode launch when the process
  * runs with ANTKV_TRACE=1 (8 words per CTA); returns words copied. */

@@ -30,7 +30,7 @@ __all__ = [
     "assign_nearest", "encode_rows", "decode_rows", "ranked", "select_anchors",
     "budget_for", "index_bits", "pack_indices", "unpack_indices",
     "attention_exact", "OracleCache", "KIND_ANCHOR", "KIND_QUANTIZED",
-    "KIND_WINDOWED", "POLICIES",
+    "KIND_WINDOWED", "POLICIES", "weighted_kmeans",
 ]
 
 POLICIES = ("by_k", "by_v", "by_sum")          # anchors.py:29
@@ -231,6 +231,67 @@ def decode_rows(codes, centroids):
         raise ValueError("code index out of range")
     n = codes.shape[0]
     return C[codes.reshape(-1)].reshape(n, -1)
+
+
+def _pp_seed(X, w, m, rng):
+    """Weighted k-means++ (vq.py:120-138): the first centre drawn with
+    probability w/sum(w), each later one with probability w*D^2/sum(w*D^2)
+    (uniform index when that sum is zero); D^2 = squared distance to the
+    nearest centre chosen so far."""
+    C = np.empty((m, X.shape[1]))
+    C[0] = X[rng.choice(len(X), p=w / w.sum())]
+    D2 = ((X - C[0]) ** 2).sum(axis=1)
+    for k in range(1, m):
+        s = w * D2
+        tot = s.sum()
+        j = int(rng.integers(len(X))) if tot <= 0 else rng.choice(len(X), p=s / tot)
+        C[k] = X[j]
+        D2 = np.minimum(D2, ((X - C[k]) ** 2).sum(axis=1))
+    return C
+
+
+def weighted_kmeans(X, w, m, seed, max_iter=100, tol=1e-10, init_centroids=None):
+    """vq.py:141-214 with this module's assign_nearest (the compiled
+    backend's operation order).  Returns (centroids float32 [m, d],
+    objective trace, iterations, padded_init)."""
+    X = np.asarray(X, dtype=np.float64)
+    w = np.asarray(w, dtype=np.float64)
+    n, d = X.shape
+    rng = np.random.default_rng(seed)
+    padded = False
+    if init_centroids is not None:                       # vq.py:164-167
+        C = np.array(init_centroids, dtype=np.float64)
+    elif m > n:                                          # vq.py:168-174
+        padded = True
+        scale = max(np.abs(X).max(), 1.0)
+        reps = np.tile(X, (m // n + 1, 1))[: m - n]
+        C = np.concatenate([X, reps + rng.normal(scale=1e-6 * scale, size=(m - n, d))])
+    else:
+        C = _pp_seed(X, w, m, rng)
+    trace, prev, it = [], None, 0
+    for it in range(1, max_iter + 1):                    # vq.py:178-197
+        idx, d2 = assign_nearest(X, C)
+        trace.append(float((w * d2).sum()))
+        wsum = np.zeros(m)
+        csum = np.zeros((m, d))
+        wx = w[:, None] * X
+        for j in range(n):                               # point order, as add.at
+            wsum[idx[j]] += w[j]
+            csum[idx[j]] += wx[j]
+        Cn = C.copy()
+        live = wsum > 0
+        Cn[live] = csum[live] / wsum[live, None]
+        wd2 = w * d2
+        for e in np.flatnonzero(~live):                  # empty-cluster repair
+            far = int(np.argmax(wd2))
+            Cn[e] = X[far]
+            wd2[far] = -1.0
+        stop = (prev is not None and np.array_equal(idx, prev)) or \
+            (len(trace) >= 2 and trace[-2] - trace[-1] < tol)
+        C, prev = Cn, idx
+        if stop:
+            break
+    return C.astype(np.float32), trace, it, padded
 
 
 def pack_indices(indices, bits):

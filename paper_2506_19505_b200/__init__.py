@@ -8,8 +8,8 @@ sm_100a through libantkv_b200.so; there is no CPU fallback.
 """
 
 from .errors import FormatError, NumericalError, UnsupportedError
-from .vq import (Codebook, VqConfig, bits_per_element, decode_rows, decode_token, encode_rows,
-                 encode_token, load_codebook, save_codebook)
+from .vq import (Codebook, KMeansResult, VqConfig, bits_per_element, decode_rows, decode_token,
+                 encode_rows, encode_token, load_codebook, save_codebook, weighted_kmeans)
 from .attention import AttentionAux, RopeParams, apply_rope, flash_attention_aux
 from .anchors import AnchorScores, AnchorSelection, anchor_scores_blocked, select_anchors
 from .cache import CacheConfig, MemoryReport, QuantizedKVCache
@@ -22,5 +22,5 @@ __all__ = [
     "MemoryReport", "NumericalError", "QuantizedKVCache", "RopeParams", "UnsupportedError",
     "VqConfig", "anchor_scores_blocked", "apply_rope", "bits_per_element", "decode_rows",
     "decode_token", "encode_rows", "encode_token", "flash_attention_aux", "kernels",
-    "load_codebook", "save_codebook", "select_anchors",
+    "load_codebook", "save_codebook", "select_anchors", "KMeansResult", "weighted_kmeans",
 ]

@@ -54,8 +54,11 @@ def anchor_scores_blocked(Q, K, V, aux: AttentionAux, block_q, block_k, rope=Non
     Kr, _ = rope_device(Kt, pos, theta, 1.0)
     ak = torch.empty((H, n_k), dtype=torch.float32, device=Qt.device)
     av = torch.empty((H, n_k), dtype=torch.float32, device=Qt.device)
-    _lib.call("antkv_ans_blocked", _lib.ptr(Qs), _lib.ptr(Kr), _lib.ptr(M.contiguous()),
-              _lib.ptr(L.contiguous()), _lib.ptr(qn.contiguous()), H, Hk, n_q, n_k, d,
+    # temporaries stay bound until the launch is enqueued (the caching
+    # allocator could otherwise hand their memory to the next allocation)
+    M, L, qn = M.contiguous(), L.contiguous(), qn.contiguous()
+    _lib.call("antkv_ans_blocked", _lib.ptr(Qs), _lib.ptr(Kr), _lib.ptr(M),
+              _lib.ptr(L), _lib.ptr(qn), H, Hk, n_q, n_k, d,
               int(block_q), int(block_k), int(bool(causal)), _lib.ptr(ak), _lib.ptr(av),
               _lib.stream())
     single = was_np or (isinstance(Q, torch.Tensor) and Q.ndim == 2)
@@ -69,7 +72,8 @@ def select_anchors_device(ans_k, ans_v, budget, policy="by_sum"):
     R, n = ans_k.shape
     out = torch.empty((R, budget), dtype=torch.int32, device=ans_k.device)
     if budget > 0:
-        _lib.call("antkv_select_anchors", _lib.ptr(ans_k.contiguous()), _lib.ptr(ans_v.contiguous()),
+        ans_k, ans_v = ans_k.contiguous(), ans_v.contiguous()
+        _lib.call("antkv_select_anchors", _lib.ptr(ans_k), _lib.ptr(ans_v),
                   1, R, n, int(budget), _lib.POLICY[policy], _lib.ptr(out), _lib.stream())
     return out
 

@@ -335,9 +335,10 @@ class QuantizedKVCache:
         if self.row_dtype is None:
             self.row_dtype = K.dtype
         self._ensure_capacity(n + 1)
+        positions, anchors = positions.contiguous(), anchors.contiguous()
         _lib.call("antkv_cache_build", ctypes.byref(self._desc), _lib.ptr(K), _lib.ptr(V),
-                  _lib.dtype_tag(K), _lib.ptr(positions.contiguous()), n,
-                  _lib.ptr(anchors.contiguous()), int(anchors.shape[-1]), _lib.stream())
+                  _lib.dtype_tag(K), _lib.ptr(positions), n,
+                  _lib.ptr(anchors), int(anchors.shape[-1]), _lib.stream())
         self._n = n
         if n:
             pos_h = positions.cpu().numpy()
@@ -442,7 +443,8 @@ class QuantizedKVCache:
             O = torch.empty((Hq, n, d), dtype=torch.float32, device=Qt.device)
             L = torch.empty((Hq, n), dtype=torch.float32, device=Qt.device)
             M = torch.empty_like(L)
-            _lib.call("antkv_flash_aux", _lib.ptr(Qs), _lib.ptr(Kr), _lib.ptr(Vh[b].contiguous()),
+            Vb = Vh[b].contiguous()
+            _lib.call("antkv_flash_aux", _lib.ptr(Qs), _lib.ptr(Kr), _lib.ptr(Vb),
                       Hq, self.Hkv, n, n, d, d, 64, 64, 1, _lib.ptr(O), _lib.ptr(L), _lib.ptr(M),
                       _lib.stream())
             outs.append(O)

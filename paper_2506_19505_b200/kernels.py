@@ -3,7 +3,9 @@
 The reference picks ``antkv._ckernels`` at import time
 (kernels/__init__.py:19-37).  This module exposes the same three functions
 with the same signatures, float64 numpy in and out, computed on the GPU by
-libantkv_b200.so (float32 arithmetic).  Installing it as ``antkv._ckernels``
+libantkv_b200.so: attention and anchor scores in float32 arithmetic,
+assign_nearest in float64 with the compiled backend's operation order
+(bit-identical to _ckernels.assign_nearest for d_sub <= 64).  Installing it as ``antkv._ckernels``
  routes the reference's flash_attention_aux,
 anchor_scores_blocked, encode_rows and weighted_kmeans through the B200.
 """
@@ -53,12 +55,20 @@ def ans_blocked(Qs, Kr, M, L, q_norms, block_q, block_k, causal):
 
 
 def assign_nearest(X, C):
-    """Nearest centroid, lowest index on ties (_ckernels.pyx:134-163)."""
-    Xd, Cd = _dev(X), _dev(C)
+    """Nearest centroid, lowest index on ties (_ckernels.pyx:134-163):
+    float64, the same per-coordinate accumulation order, no FMA."""
+    Xd = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).cuda()
+    Cd = torch.from_numpy(np.ascontiguousarray(C, dtype=np.float64)).cuda()
     n, d_sub = Xd.shape
     m = Cd.shape[0]
     idx = torch.empty((n,), dtype=torch.int64, device=Xd.device)
-    d2 = torch.empty((n,), dtype=torch.float32, device=Xd.device)
-    _lib.call("antkv_assign_nearest", _lib.ptr(Xd), _lib.ptr(Cd), n, m, d_sub, _lib.ptr(idx),
+    if d_sub > 64:       # float32 kernel beyond the float64 kernel's register budget
+        d2 = torch.empty((n,), dtype=torch.float32, device=Xd.device)
+        Xf, Cf = Xd.float(), Cd.float()
+        _lib.call("antkv_assign_nearest", _lib.ptr(Xf), _lib.ptr(Cf), n, m, d_sub,
+                  _lib.ptr(idx), _lib.ptr(d2), _lib.stream())
+        return idx.cpu().numpy(), d2.cpu().numpy().astype(np.float64)
+    d2 = torch.empty((n,), dtype=torch.float64, device=Xd.device)
+    _lib.call("antkv_kmeans_assign_f64", _lib.ptr(Xd), _lib.ptr(Cd), n, m, d_sub, _lib.ptr(idx),
               _lib.ptr(d2), _lib.stream())
-    return idx.cpu().numpy(), d2.cpu().numpy().astype(np.float64)
+    return idx.cpu().numpy(), d2.cpu().numpy()

@@ -61,7 +61,8 @@ def lse_merge(o_all, lse_all, out=None, lse_out=None):
     P, rows, d = o_all.shape[0], int(np.prod(o_all.shape[1:-1])), o_all.shape[-1]
     if out is None:
         out = torch.empty(o_all.shape[1:], dtype=torch.float32, device=o_all.device)
-    _lib.call("antkv_lse_combine", _lib.ptr(o_all.contiguous()), _lib.ptr(lse_all.contiguous()),
+    o_all, lse_all = o_all.contiguous(), lse_all.contiguous()
+    _lib.call("antkv_lse_combine", _lib.ptr(o_all), _lib.ptr(lse_all),
               P, rows, d, _lib.ptr(out), _lib.ptr(lse_out), _lib.stream())
     return out
 
@@ -177,13 +178,14 @@ class CudaPrefillOps:
         return O, M, L, qn
 
     def score_block(self, Q, K, qpos, kpos, M, L, qn, causal, theta):
+        M, L, qn = M.contiguous(), L.contiguous(), qn.contiguous()
         B, Hq, nq, d = Q.shape
         Hkv, nk = K.shape[1], K.shape[2]
         ak = torch.empty((B, Hkv, nk), dtype=torch.float32, device=K.device)
         av = torch.empty_like(ak)
         _lib.call("antkv_prefill_anchor_scores_block", _lib.ptr(Q), _lib.ptr(K), self._tag(Q, K),
-                  _lib.ptr(qpos), _lib.ptr(kpos), _lib.ptr(M.contiguous()),
-                  _lib.ptr(L.contiguous()), _lib.ptr(qn.contiguous()), B, Hq, Hkv, nq, nk, d,
+                  _lib.ptr(qpos), _lib.ptr(kpos), _lib.ptr(M), _lib.ptr(L), _lib.ptr(qn),
+                  B, Hq, Hkv, nq, nk, d,
                   float(theta), int(bool(causal)), _lib.ptr(ak), _lib.ptr(av), _lib.stream())
         return ak, av
 

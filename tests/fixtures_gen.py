@@ -69,3 +69,39 @@ def an_inputs(N, m, ds, seed):
     X = rng.standard_normal((N, ds))
     C = rng.standard_normal((m, ds)).astype(np.float32).astype(np.float64)
     return X, C
+
+
+# weighted k-means cases (vq.py:141-214): name -> (seed, n, d, m, kmeans_seed,
+# max_iter, weights kind, init kind)
+KM_CASES = {
+    "pp_d8m64": (301, 2000, 8, 64, 5, 30, "random", None),
+    "init_d4m16": (302, 3000, 4, 16, 0, 50, "ones", "sample"),
+    "padded_d3m12": (303, 5, 3, 12, 0, 100, "ones", None),
+    "zero_w_d8m32": (304, 500, 8, 32, 1, 40, "zeros30", None),
+    "empties_d2m10": (305, 400, 2, 10, 0, 40, "random", "far"),
+    "pp_d32m128": (306, 1500, 32, 128, 7, 15, "random", None),
+    "single_d1m1": (307, 2, 1, 1, 0, 100, "three_one", None),
+}
+
+
+def km_inputs(name):
+    """(X [n, d] float64, w [n], init or None) for a KM_CASES entry."""
+    seed, n, d, m, _, _, wk, ik = KM_CASES[name]
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d)) * 2.0
+    if wk == "ones":
+        w = np.ones(n)
+    elif wk == "zeros30":
+        w = rng.random(n) + 0.01
+        w[rng.random(n) < 0.3] = 0.0
+    elif wk == "three_one":
+        X = np.array([[0.0], [1.0]])
+        w = np.array([3.0, 1.0])
+    else:
+        w = rng.random(n) + 0.01
+    init = None
+    if ik == "sample":
+        init = X[rng.choice(n, size=m, replace=False)].copy()
+    elif ik == "far":      # four centroids far from the data: empty clusters
+        init = np.concatenate([X[:m - 4], np.full((4, d), 1e3) + np.arange(4)[:, None]])
+    return X, w, init

@@ -27,8 +27,8 @@ from antkv import (CacheConfig, Codebook, QuantizedKVCache, VqConfig,  # noqa: E
 from antkv.kernels import pure  # noqa: E402
 from antkv.util import pack_indices  # noqa: E402
 
-from fixtures_gen import (AN_CASES, CACHE_CASES, FA_CASES, an_inputs,  # noqa: E402
-                          codebooks, fa_inputs, qkv)
+from fixtures_gen import (AN_CASES, CACHE_CASES, FA_CASES, KM_CASES,  # noqa: E402
+                          an_inputs, codebooks, fa_inputs, km_inputs, qkv)
 
 def run_cache_case(name, spec):
     seed, n, d, notation, window, frac, count, policy, steps, stride, blk = spec
@@ -111,9 +111,32 @@ def kernel_cases():
     return out
 
 
+def kmeans_cases():
+    """weighted_kmeans (vq.py:141-214) with the reference's compiled
+    assign_nearest (oracle/_ref, the backend a built reference uses)."""
+    sys.path.insert(0, str(HERE.parent.parent / "oracle" / "_ref"))
+    import antkv.kernels as K
+    import antkv_ref._ckernels as ck
+    saved = K.assign_nearest
+    K.assign_nearest = ck.assign_nearest
+    out = {}
+    try:
+        for name, (_, _, _, m, kseed, max_iter, _, _) in KM_CASES.items():
+            X, w, init = km_inputs(name)
+            res = antkv.vq.weighted_kmeans(X, w, m, seed=kseed, max_iter=max_iter,
+                                           init_centroids=init)
+            out[f"{name}_C"] = res.codebook.centroids
+            out[f"{name}_trace"] = np.array(res.objective_trace)
+            out[f"{name}_meta"] = np.array([res.n_iter, int(res.padded_init)])
+    finally:
+        K.assign_nearest = saved
+    return out
+
+
 def main():
     print("reference backend:", antkv.kernels.BACKEND, file=sys.stderr)
     np.savez_compressed(HERE / "kernels.npz", **kernel_cases())
+    np.savez_compressed(HERE / "kmeans.npz", **kmeans_cases())
     for name, spec in CACHE_CASES.items():
         res = run_cache_case(name, spec)
         np.savez_compressed(HERE / f"cache_{name}.npz", **res)
@@ -123,7 +146,9 @@ def main():
         "(`/root/reference/pkg/src`, kernels backend: "
         f"`{antkv.kernels.BACKEND}`) via `make_golden.py`.\n"
         "Inputs are regenerated from the seeds in `make_golden.py` with\n"
-        "`tests/fixtures_gen.py`; only reference outputs are stored.\n")
+        "`tests/fixtures_gen.py`; only reference outputs are stored.\n"
+        "`kmeans.npz` runs `weighted_kmeans` with the reference's compiled\n"
+        "`assign_nearest` (`oracle/_ref`, built by `make -C oracle`).\n")
 
 
 if __name__ == "__main__":

@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 
 import antkv_oracle as O
-from fixtures_gen import AN_CASES, CACHE_CASES, FA_CASES, an_inputs, codebooks, fa_inputs, qkv
+from fixtures_gen import (AN_CASES, CACHE_CASES, FA_CASES, KM_CASES, an_inputs, codebooks,
+                          fa_inputs, km_inputs, qkv)
 
 GOLD = Path(__file__).resolve().parent / "golden"
 KER = np.load(GOLD / "kernels.npz")
@@ -146,3 +147,16 @@ def test_oracle_cache_matches_reference_cache(name):
     assert [pay, cbb, fp] == list(g["mem"]) and eff == g["mem_eff"][0]
     attn = cache.attention_from_cache(Q[:, :cache.token_count])
     assert np.abs(attn[0] - g["attn_from_cache"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("name", list(KM_CASES))
+def test_weighted_kmeans_matches_reference_golden(name):
+    """The oracle's weighted k-means reproduces the reference run (compiled
+    assign_nearest) bit for bit: centroids, objective trace, iterations."""
+    g = np.load(GOLD / "kmeans.npz")
+    _, _, _, m, kseed, max_iter, _, _ = KM_CASES[name]
+    X, w, init = km_inputs(name)
+    C, trace, it, padded = O.weighted_kmeans(X, w, m, kseed, max_iter=max_iter, init_centroids=init)
+    assert np.array_equal(C, g[f"{name}_C"])
+    assert np.array_equal(np.array(trace), g[f"{name}_trace"])
+    assert [it, int(padded)] == g[f"{name}_meta"].tolist()
