@@ -276,14 +276,15 @@ ANTKV_API int antkv_lse_combine(const float *o, const float *lse, int P, int64_t
  * reference's operation order (bit-identical results).
  * assign: X [n][d], C [m][d] -> idx int64 [n], d2 float64 [n]; sequential
  *   sum over t of (x_t - c_t)^2 without FMA, strict-< argmin (d <= 64).
- * update: members of cluster c are perm[offsets[c] .. offsets[c+1]) in
- *   ascending point order (a stable sort of idx); C_new[c] = sum w_j x_j /
- *   sum w_j for clusters with positive weight, else C_old[c]; wsum [m]. */
+ * update (d <= 63): Xs [n][d] / ws [n] are X and w in member order (a
+ *   stable sort of idx: cluster c owns rows offsets[c] .. offsets[c+1], in
+ *   ascending point order); C_new[c] = sum w_j x_j / sum w_j for clusters
+ *   with positive weight, else C_old[c]; wsum [m]. */
 ANTKV_API int antkv_kmeans_assign_f64(const double *X, const double *C, int64_t n, int m,
                                       int d, int64_t *idx, double *d2, void *stream);
-ANTKV_API int antkv_kmeans_update_f64(const int64_t *perm, const int64_t *offsets,
-                                      const double *X, const double *w, const double *C_old,
-                                      int m, int d, double *C_new, double *wsum, void *stream);
+ANTKV_API int antkv_kmeans_update_f64(const int64_t *offsets, const double *Xs,
+                                      const double *ws, const double *C_old, int m, int d,
+                                      double *C_new, double *wsum, void *stream);
 
 /* Debug: per-CTA timeline of the last fast-decode launch when the process
  * runs with ANTKV_TRACE=1 (8 words per CTA); returns words copied. */

@@ -66,10 +66,12 @@ def main():
     off[1:] = torch.cumsum(torch.bincount(idx, minlength=a.m), 0)
     Cn = torch.empty_like(Cd)
     ws = torch.empty((a.m,), dtype=torch.float64, device=dev)
+    Xs = Xd.index_select(0, perm)
+    wsr = wd.index_select(0, perm)
     ev[2].record()
     for _ in range(5):
-        _lib.call("antkv_kmeans_update_f64", _lib.ptr(perm), _lib.ptr(off), _lib.ptr(Xd),
-                  _lib.ptr(wd), _lib.ptr(Cd), a.m, a.d, _lib.ptr(Cn), _lib.ptr(ws), st)
+        _lib.call("antkv_kmeans_update_f64", _lib.ptr(off), _lib.ptr(Xs), _lib.ptr(wsr),
+                  _lib.ptr(Cd), a.m, a.d, _lib.ptr(Cn), _lib.ptr(ws), st)
     ev[3].record()
     torch.cuda.synchronize()
     assign_ms = ev[0].elapsed_time(ev[1]) / 5
