@@ -30,6 +30,8 @@
  *   antkv_vq_decode        <- vq.decode_rows (vq.py:243-248)
  *   antkv_kmeans_*_f64     <- vq.weighted_kmeans Lloyd step (vq.py:178-197) with
  *                             kernels.assign_nearest (_ckernels.pyx:134-163)
+ *   antkv_eval_pair_l1     <- harness.per_token_errors / anchors.k_perturbation_bound
+ *                             pair sums (harness.py:111-134, anchors.py:152-186)
  *   antkv_lse_combine      <- (new) split-KV / sequence-shard log-sum-exp merge
  */
 #ifndef ANTKV_B200_H
@@ -285,6 +287,17 @@ ANTKV_API int antkv_kmeans_assign_f64(const double *X, const double *C, int64_t 
 ANTKV_API int antkv_kmeans_update_f64(const int64_t *offsets, const double *Xs,
                                       const double *ws, const double *C_old, int m, int d,
                                       double *C_new, double *wsum, void *stream);
+
+/* Evaluation harness (harness.py:109-235), float64:
+ *   out[j] = sum_i W_ij * sum_t |P_ij (X_jt - Y_it) - R_ij (Z_jt - Y_it)|
+ * Y [n_i][d], X/Z [n_j][d], W/P/R [n_i][n_j] (NULL: W = 1, P = 1, R = 0;
+ * Z NULL drops the R term); i_from_j0 = 1 skips rows i < 32*floor(j/32)
+ * (causal masks zero them).  Carries the K perturbation bound
+ * (anchors.py:152-186) and the per-token quantisation errors
+ * (harness.py:111-134) in O(n^2 d). */
+ANTKV_API int antkv_eval_pair_l1(const double *Y, const double *X, const double *Z,
+                                 const double *W, const double *P, const double *R, int n_i,
+                                 int n_j, int d, int i_from_j0, double *out, void *stream);
 
 /* Debug: per-CTA timeline of the last fast-decode launch when the process
  * runs with ANTKV_TRACE=1 (8 words per CTA); returns words copied. */

@@ -105,3 +105,16 @@ def km_inputs(name):
     elif ik == "far":      # four centroids far from the data: empty clusters
         init = np.concatenate([X[:m - 4], np.full((4, d), 1e3) + np.arange(4)[:, None]])
     return X, w, init
+
+
+# evaluation grid points (harness.eval_point): name -> (data seed, n, d,
+# structure, notation, codebook seed, anchor_fraction, window, policy,
+# controls, per-token mode, wiring, decode_steps)
+EVAL_CASES = {
+    "e1_heavy_d4m16_decode": (401, 96, 16, "heavy_hitter", "d4m16", 411, 0.05, 8, "by_sum", 2,
+                              "joint", "decode", 8),
+    "e2_clustered_d8m64_konly": (402, 128, 32, "clustered", "d8m64", 412, 0.02, 0, "by_sum", 1,
+                                 "k_only", "prefill", 0),
+    "e3_gauss_d2m16_vonly_byk": (403, 80, 16, "gaussian", "d2m16", 413, 0.1, 4, "by_k", 0,
+                                 "v_only", "prefill", 0),
+}

@@ -27,8 +27,8 @@ from antkv import (CacheConfig, Codebook, QuantizedKVCache, VqConfig,  # noqa: E
 from antkv.kernels import pure  # noqa: E402
 from antkv.util import pack_indices  # noqa: E402
 
-from fixtures_gen import (AN_CASES, CACHE_CASES, FA_CASES, KM_CASES,  # noqa: E402
-                          an_inputs, codebooks, fa_inputs, km_inputs, qkv)
+from fixtures_gen import (AN_CASES, CACHE_CASES, EVAL_CASES, FA_CASES,  # noqa: E402
+                          KM_CASES, an_inputs, codebooks, fa_inputs, km_inputs, qkv)
 
 def run_cache_case(name, spec):
     seed, n, d, notation, window, frac, count, policy, steps, stride, blk = spec
@@ -133,10 +133,47 @@ def kmeans_cases():
     return out
 
 
+def eval_cases():
+    """harness.eval_point on small grid points, compiled assign_nearest."""
+    import json
+    sys.path.insert(0, str(HERE.parent.parent / "oracle" / "_ref"))
+    import antkv.kernels as K
+    import antkv.harness as H
+    import antkv.vq as VQ
+    import antkv_ref._ckernels as ck
+    saved = (K.assign_nearest, VQ.kernels.assign_nearest)
+    K.assign_nearest = ck.assign_nearest
+    out = {}
+    try:
+        for name, spec in EVAL_CASES.items():
+            (dseed, n, d, structure, notation, cseed, frac, window, policy, controls, mode,
+             wiring, steps) = spec
+            cfg = VqConfig.from_notation(notation)
+            ck_, cv_ = codebooks(cseed, 1, cfg.m, cfg.d_sub)
+            data = H.generate_qkv(dseed, n, d, structure)
+            rec = H.eval_point(data, Codebook(config=cfg, centroids=ck_[0]),
+                               Codebook(config=cfg, centroids=cv_[0]), frac, window_size=window,
+                               policy=policy, seed=dseed, controls=controls, per_token_mode=mode,
+                               compute_per_token=True, wiring=wiring, decode_steps=steps)
+            rec.pop("runtime_ms")
+            errs = H.per_token_errors(data["Q"], data["K"], data["V"],
+                                      Codebook(config=cfg, centroids=ck_[0]),
+                                      Codebook(config=cfg, centroids=cv_[0]),
+                                      H.RopeParams(positions=data["positions"]), mode=mode)
+            rec["per_token_errors"] = [float(e) for e in errs]
+            rec["data_Q_sum"] = float(np.asarray(data["Q"], np.float64).sum())
+            out[name] = rec
+    finally:
+        K.assign_nearest = saved[0]
+    (HERE / "eval.json").write_text(json.dumps(out, indent=1))
+    return out
+
+
 def main():
     print("reference backend:", antkv.kernels.BACKEND, file=sys.stderr)
     np.savez_compressed(HERE / "kernels.npz", **kernel_cases())
     np.savez_compressed(HERE / "kmeans.npz", **kmeans_cases())
+    eval_cases()
     for name, spec in CACHE_CASES.items():
         res = run_cache_case(name, spec)
         np.savez_compressed(HERE / f"cache_{name}.npz", **res)

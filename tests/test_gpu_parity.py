@@ -820,3 +820,77 @@ def test_weighted_kmeans_reference_properties():
     res = weighted_kmeans(rng.standard_normal((3, 2)), np.ones(3), 8, seed=0)
     assert res.padded_init and res.codebook.centroids.shape == (8, 2)
     assert res.objective_trace[-1] < 1e-9
+
+
+def _eval_inputs(name):
+    from fixtures_gen import EVAL_CASES
+    from paper_2506_19505_b200 import Codebook, VqConfig
+    from paper_2506_19505_b200.harness import generate_qkv
+    spec = EVAL_CASES[name]
+    dseed, n, d, structure, notation, cseed = spec[:6]
+    cfg = VqConfig.from_notation(notation)
+    ck, cv = codebooks(cseed, 1, cfg.m, cfg.d_sub)
+    return spec, generate_qkv(dseed, n, d, structure), Codebook(cfg, ck[0]), Codebook(cfg, cv[0])
+
+
+@pytest.mark.parametrize("name", ["e1_heavy_d4m16_decode", "e2_clustered_d8m64_konly",
+                                  "e3_gauss_d2m16_vonly_byk"])
+def test_eval_point_matches_reference_golden(name):
+    """harness.eval_point on the GPU against the reference's record: every
+    float64 quantity to 1e-9 relative (the cache's codes and anchors are the
+    reference's, the dense maths is float64), the decode-wiring error (the
+    cache's float32 decode kernel) to 1e-4, per-token errors (the exact
+    single-column update vs n attention passes) to 1e-9."""
+    import json
+    from paper_2506_19505_b200.harness import eval_point, per_token_errors, _Rope
+    g = json.loads((GOLD / "eval.json").read_text())[name]
+    spec, data, cbk, cbv = _eval_inputs(name)
+    (_, n, d, _, _, _, frac, window, policy, controls, mode, wiring, steps) = spec
+    rec = eval_point(data, cbk, cbv, frac, window_size=window, policy=policy, seed=spec[0],
+                     controls=controls, per_token_mode=mode, compute_per_token=True,
+                     wiring=wiring, decode_steps=steps)
+    for key in ("attention_l1_error", "v_bound", "k_bound", "first_order_residual"):
+        assert abs(rec[key] - g[key]) <= 1e-9 * abs(g[key]), key
+    for key in ("vq", "bits_per_element", "n", "d", "policy", "wiring", "window_size"):
+        assert rec[key] == g[key], key
+    ra, ga = rec["ans_rank_agreement"], g["ans_rank_agreement"]
+    assert ra["topk"] == ga["topk"] and ra["topk_overlap"] == ga["topk_overlap"]
+    assert abs(ra["spearman"] - ga["spearman"]) < 1e-9
+    if controls:
+        assert np.allclose(rec["random_control"]["errors"], g["random_control"]["errors"],
+                           rtol=1e-9, atol=0)
+    if wiring == "decode":
+        assert abs(rec["decode_l1_error"] - g["decode_l1_error"]) <= 1e-4 * g["decode_l1_error"]
+    errs = per_token_errors(data["Q"], data["K"], data["V"], cbk, cbv,
+                            _Rope(data["positions"], d), mode=mode)
+    ref = np.array(g["per_token_errors"])
+    assert np.abs(errs - ref).max() <= 1e-9 * ref.max()
+
+
+def test_per_token_errors_at_scale_vs_direct_recomputation():
+    """At 4096 tokens (the reference would need 4096 attention passes) the
+    single-column update agrees with direct float64 recomputation for
+    sampled tokens, in every mode."""
+    import math
+    from paper_2506_19505_b200 import Codebook, VqConfig
+    from paper_2506_19505_b200.harness import (_Rope, _dev64, _quantize64, _scores,
+                                               generate_qkv, per_token_errors)
+    n, d = 4096, 64
+    data = generate_qkv(5, n, d, "heavy_hitter")
+    cfg = VqConfig.from_notation("d8m256")
+    ck, cv = codebooks(9, 1, 256, 8)
+    cbk, cbv = Codebook(cfg, ck[0]), Codebook(cfg, cv[0])
+    R = _Rope(data["positions"], d)
+    Q, K, V = _dev64(data["Q"]), _dev64(data["K"]), _dev64(data["V"])
+    base = _scores(R(Q), R(K), True) @ V
+    Kq, Vq = _quantize64(K, cbk), _quantize64(V, cbv)
+    for mode in ("joint", "k_only", "v_only"):
+        errs = per_token_errors(data["Q"], data["K"], data["V"], cbk, cbv, R, mode=mode)
+        for j in (0, 1, 777, 2048, n - 1):
+            K2, V2 = K.clone(), V.clone()
+            if mode != "v_only":
+                K2[j] = Kq[j]
+            if mode != "k_only":
+                V2[j] = Vq[j]
+            want = float(((_scores(R(Q), R(K2), True) @ V2) - base).abs().sum())
+            assert abs(errs[j] - want) <= 1e-7 * max(want, 1e-300) + 1e-12, (mode, j)

@@ -318,3 +318,17 @@ def test_sequence_sharded_prefill_gloo_world3(policy):
             assert res[r][7][h].tolist() == want.tolist()
             loc = res[r][6][h]
             assert [int(j) + s for j in loc if j >= 0] == [int(j) for j in want if s <= j < e]
+
+
+def test_generate_qkv_matches_reference_streams():
+    """The evaluation data generator draws the reference's streams
+    (harness.py:35-72): the golden records carry sum(Q) per case."""
+    import json
+    from fixtures_gen import EVAL_CASES
+    from paper_2506_19505_b200.harness import generate_qkv
+    g = json.loads((ROOT / "tests" / "golden" / "eval.json").read_text())
+    for name, spec in EVAL_CASES.items():
+        data = generate_qkv(spec[0], spec[1], spec[2], spec[3])
+        assert float(np.asarray(data["Q"], np.float64).sum()) == g[name]["data_Q_sum"]
+    hh = generate_qkv(1, 300, 8, "heavy_hitter")
+    assert hh["planted"] == [1, 3, 5]
