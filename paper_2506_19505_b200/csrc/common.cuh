@@ -38,6 +38,12 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // stream was for another cache.
 const void *previous_cache_on_stream(cudaStream_t st, const void *key);
 
+// Stream-ordered scratch (cudaMallocAsync from the device's default pool).
+// The first call per device raises the pool's release threshold so freed
+// scratch stays mapped for the next call instead of being returned to the
+// driver at every synchronisation (re-mapping GBs costs milliseconds).
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st);
+
 // ---------------------------------------------------------------- dtypes
 __device__ __forceinline__ float load_elem(const void *p, int64_t i, int dtype) {
   if (dtype == ANTKV_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(p)[i]);

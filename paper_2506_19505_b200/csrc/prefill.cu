@@ -391,9 +391,9 @@ extern "C" int antkv_prefill_attention_block(const void *Q, const void *K, const
   float *qs = nullptr, *kr = nullptr, *vf = nullptr;
   size_t qbytes = sizeof(float) * (size_t)B * Hq * n_q * d;
   size_t kbytes = sizeof(float) * (size_t)B * Hkv * n_k * d;
-  cudaError_t e = cudaMallocAsync(&qs, qbytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&kr, kbytes ? kbytes : 4, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&vf, kbytes ? kbytes : 4, st);
+  cudaError_t e = scratch_alloc((void **)&qs, qbytes, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&kr, kbytes ? kbytes : 4, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&vf, kbytes ? kbytes : 4, st);
   if (e != cudaSuccess) return cuda_status(e, "prefill scratch");
   int rc = rope_rotate(Q, dtype, q_positions, B, Hq, n_q, d, theta_base, 1.f / sqrtf((float)d),
                        qs, q_norms, st);
@@ -441,8 +441,8 @@ extern "C" int antkv_prefill_anchor_scores_block(const void *Q, const void *K, i
     return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "anchor-score clear");
   }
   float *qs = nullptr, *kr = nullptr;
-  cudaError_t e = cudaMallocAsync(&qs, sizeof(float) * (size_t)B * Hq * n_q * d, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&kr, sizeof(float) * (size_t)B * Hkv * n_k * d, st);
+  cudaError_t e = scratch_alloc((void **)&qs, sizeof(float) * (size_t)B * Hq * n_q * d, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&kr, sizeof(float) * (size_t)B * Hkv * n_k * d, st);
   if (e != cudaSuccess) return cuda_status(e, "anchor-score scratch");
   int rc = rope_rotate(Q, dtype, q_positions, B, Hq, n_q, d, theta_base, 1.f / sqrtf((float)d),
                        qs, nullptr, st);

@@ -543,9 +543,9 @@ int launch_flash_mma(const float *Qs, const float *Kr, const float *V, int heads
   uint8_t *kt = nullptr, *vt = nullptr;
   float *ksc = nullptr;
   const size_t tb = (size_t)kv_heads * nkt * PM_TILE;
-  cudaError_t e = cudaMallocAsync(&kt, tb, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&vt, tb, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&ksc, sizeof(float) * (size_t)kv_heads * nkt, st);
+  cudaError_t e = scratch_alloc((void **)&kt, tb, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&vt, tb, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nkt, st);
   if (e != cudaSuccess) return cuda_status(e, "prefill tile scratch");
   presplit_kernel<true><<<dim3(nkt, kv_heads), PM_THREADS, 0, st>>>(Kr, n_k, kt, ksc);
   presplit_kernel<false><<<dim3(nkt, kv_heads), PM_THREADS, 0, st>>>(V, n_k, vt, nullptr);
@@ -570,8 +570,8 @@ int launch_ans_mma(const float *Qs, const float *Kr, const float *M, const float
   const int nqt = ceil_div(n_q, PM_B);
   uint8_t *qt = nullptr;
   float *qsc = nullptr;
-  cudaError_t e = cudaMallocAsync(&qt, (size_t)heads * nqt * PM_TILE, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&qsc, sizeof(float) * (size_t)heads * nqt, st);
+  cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * nqt * PM_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * nqt, st);
   if (e != cudaSuccess) return cuda_status(e, "anchor-score tile scratch");
   presplit_kernel<true><<<dim3(nqt, heads), PM_THREADS, 0, st>>>(Qs, n_q, qt, qsc);
   dim3 grid(ceil_div(n_k, PM_B), heads / sum_group);

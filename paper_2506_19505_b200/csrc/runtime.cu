@@ -46,6 +46,28 @@ extern "C" int antkv_version(void) { return 1; }
 
 namespace antkv { int decode_fast_smem_base_ok(); }
 
+namespace antkv {
+cudaError_t scratch_alloc(void **p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 0 && dev < 64) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      done[dev] = true;
+    }
+  }
+  return cudaMallocAsync(p, bytes, st);
+}
+}  // namespace antkv
+
 extern "C" int antkv_device_check(int device) {
   cudaDeviceProp p;
   cudaError_t e = cudaGetDeviceProperties(&p, device);
