@@ -279,6 +279,9 @@ ans_kernel(const float *__restrict__ Qs, const float *__restrict__ Kr,
 int launch_flash_mma(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads,
                      int n_q, int n_k, int d, int dv, int causal, float *O, float *L, float *M,
                      cudaStream_t st);
+int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
+                  int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
+                  float *ans_k, float *ans_v, cudaStream_t st);
 int launch_ans_mma(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
                    int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
                    float *ans_k, float *ans_v, cudaStream_t st);
@@ -315,8 +318,11 @@ static int launch_ans(const float *Qs, const float *Kr, const float *M, const fl
                 "heads must be a multiple of kv_heads");
   ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
   if (n_k == 0) return ANTKV_OK;
-  {  // d = 128: tensor-core kernel (prefill_mma.cu)
-    const int rc = launch_ans_mma(Qs, Kr, M, L, qn, heads, kv_heads, sum_group, n_q, n_k, d, causal,
+  {  // d = 128: tcgen05 kernel (prefill_tc.cu), else mma.sync (prefill_mma.cu)
+    int rc = launch_ans_tc(Qs, Kr, M, L, qn, heads, kv_heads, sum_group, n_q, n_k, d, causal, ans_k,
+                           ans_v, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+    rc = launch_ans_mma(Qs, Kr, M, L, qn, heads, kv_heads, sum_group, n_q, n_k, d, causal,
                                   ans_k, ans_v, st);
     if (rc != ANTKV_EUNSUPPORTED) return rc;
   }

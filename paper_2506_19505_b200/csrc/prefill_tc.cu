@@ -1,0 +1,452 @@
+// Anchor-score column sums (Alg. 1 second pass, anchors.py:66-87,
+// _ckernels.pyx:91-131) on the 5th-generation tensor cores: tcgen05.mma with
+// operands in shared memory (bulk-copied, 128B-swizzled K-major tiles) and
+// the logit tile accumulated in tensor memory.
+//
+// Each CTA owns 128 keys of one KV head and walks the query tiles of the
+// heads in its group (causal: only tiles at or after its own).  The logit
+// tile is computed TRANSPOSED, S^T[128 keys x 128 queries] = K . Q^T, so the
+// epilogue thread that owns TMEM lane j owns key j and sums its column of A
+// over the queries in registers — no cross-thread reduction:
+//   A_ij = exp(S_ij - M_i) / L_i = 2^(S_ij log2e - (M_i log2e + log2 L_i)),
+//   ans_v_j += A_ij,  ans_k_j += A_ij (1 - A_ij) ||q_i||.
+// Numerics as the mma.sync kernels (prefill_mma.cu): S from two-part fp16
+// splits of power-of-two-scaled tiles (Kh.Qh + Kh.Ql + Kl.Qh, float32
+// accumulation), scale removed exactly.
+//
+// Warp roles (10 warps): warp 0 lane 0 issues the bulk copies (K tile once,
+// Q tiles through a 2-stage ring); warp 1 owns the TMEM allocation and its
+// lane 0 issues the 24 MMAs per query tile; warps 2-9 are the epilogue —
+// warps w and w + 4 share TMEM lanes 32 (w % 4) .. + 31 and split the 128
+// query columns.  TMEM: two 128-column logit buffers (the MMAs of tile t + 1
+// overlap the exponentials of tile t) and the K tile's fp16 parts (128
+// columns), which the epilogue warps copy there once so the MMAs read only
+// the Q tile from shared memory (at N = 128 both operands from shared memory
+// would saturate its bandwidth).
+#include "common.cuh"
+
+namespace antkv {
+
+constexpr int TC_ROWS = 128;                 // keys / queries per tile
+constexpr int TC_PART = TC_ROWS * 128 * 2;   // one fp16 part of a tile: 32 KB
+constexpr int TC_TILE = 2 * TC_PART;         // hi | lo
+constexpr int TC_WARPS = 10;
+constexpr int TC_THREADS = 32 * TC_WARPS;
+constexpr int TC_EPI = 8 * 32;               // epilogue threads
+constexpr uint32_t TC_AH = 256, TC_AL = 320; // TMEM columns of the K tile (A operand): hi, lo
+
+// Byte offset of element (row, k) in one 128B-swizzled K-major part: two
+// 64-column atoms of [128 rows][128 B], 16-byte chunks XOR-ed with row & 7.
+__host__ __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
+  return (k >> 6) * (TC_ROWS * 128) + row * 128 + ((((k & 63) >> 3) ^ (row & 7)) << 4) + (k & 7) * 2;
+}
+
+__device__ __forceinline__ uint32_t tc_smem(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tc_mbar_init(uint32_t bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void tc_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tc_bulk(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+// Shared-memory matrix descriptor: K-major, 128B swizzle, 8-row groups
+// 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+// 32 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tc_ex2(float x) {   // 2^x, x <= 0 here (-inf -> 0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 32 consecutive 32-bit columns of this thread's TMEM lane <- r[0..31]
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// Power of two that maps the magnitude mx into [2^13, 2^14) (1 for mx == 0).
+__device__ __forceinline__ float tc_pow2_scale(float mx) {
+  if (!(mx > 0.f)) return 1.f;
+  int e = (__float_as_int(mx) >> 23) & 0xff;
+  e = e < 14 ? 14 : (e > 266 ? 266 : e);
+  return __int_as_float((267 - e) << 23);
+}
+
+// X [heads][rows][128] float32 -> [heads][ceil(rows/128)][hi | lo] fp16 parts
+// of x * scale in the 128B-swizzled K-major layout, scale [heads][tiles].
+__global__ void __launch_bounds__(256)
+presplit_sw128_kernel(const float *__restrict__ X, int rows, uint8_t *__restrict__ tiles,
+                      float *__restrict__ scales) {
+  __shared__ float red[8];
+  const int h = blockIdx.y, tile = blockIdx.x, nt = gridDim.x;
+  const float *src = X + (int64_t)h * rows * 128;
+  uint8_t *dst = tiles + ((int64_t)h * nt + tile) * TC_TILE;
+  float mx = 0.f;
+  for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
+    const int r = tile * TC_ROWS + (e >> 5);
+    if (r < rows) {
+      const float4 v = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)r * 128) + (e & 31));
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  const float sc = tc_pow2_scale(mx);
+  if (threadIdx.x == 0) scales[(int64_t)h * nt + tile] = sc;
+  // one 16-byte chunk (8 elements) of one row per thread and step
+  for (int e = threadIdx.x; e < TC_ROWS * 16; e += 256) {
+    const int r = e >> 4, c = e & 15, gr = tile * TC_ROWS + r;
+    float x[8];
+    if (gr < rows) {
+      const float4 a = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)gr * 128 + 8 * c));
+      const float4 b = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)gr * 128 + 8 * c + 4));
+      x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = 0.f;
+    }
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float p = x[2 * i] * sc, q = x[2 * i + 1] * sc;
+      const __half ph = __float2half_rn(p), qh = __float2half_rn(q);
+      const __half pl = __float2half_rn(p - __half2float(ph)), ql = __float2half_rn(q - __half2float(qh));
+      __half2 hh = __halves2half2(ph, qh), ll = __halves2half2(pl, ql);
+      hi[i] = *reinterpret_cast<uint32_t *>(&hh);
+      lo[i] = *reinterpret_cast<uint32_t *>(&ll);
+    }
+    const uint32_t off = sw128_off(r, 8 * c);
+    *reinterpret_cast<uint4 *>(dst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4 *>(dst + TC_PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// Per query: c_i = M_i log2e + log2 L_i (+inf beyond n_q) and ||q_i||,
+// packed float2 [heads][nqt * 128].
+__global__ void ans_tc_stats_kernel(const float *__restrict__ M, const float *__restrict__ L,
+                                    const float *__restrict__ qn, int heads, int n_q, int padded,
+                                    float2 *__restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)heads * padded) return;
+  const int h = (int)(i / padded), q = (int)(i % padded);
+  float2 v = make_float2(INFINITY, 0.f);
+  if (q < n_q) {
+    const int64_t k = (int64_t)h * n_q + q;
+    v = make_float2(M[k] * 1.4426950408889634f + log2f(L[k]), qn[k]);
+  }
+  out[i] = v;
+}
+
+struct AnsTcSmem {
+  uint8_t k[TC_TILE];        // 1024-aligned (the struct is placed at a 1024 boundary)
+  uint8_t q[2][TC_TILE];
+  float2 stat[2][TC_ROWS];
+  float red[2][TC_ROWS];
+  unsigned long long kbar, aready, qfull[2], qempty[2], tfull[2], tempty[2];
+  uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, const uint8_t *__restrict__ Kt,
+              const float *__restrict__ Ksc, const float2 *__restrict__ stats, int group, int sum_group,
+              int n_q, int n_k, int causal, float *__restrict__ ans_k, float *__restrict__ ans_v) {
+  extern __shared__ uint8_t tc_raw[];
+  AnsTcSmem &sm = *reinterpret_cast<AnsTcSmem *>(tc_raw + ((1024 - (tc_smem(tc_raw) & 1023)) & 1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x, ho = blockIdx.y;                  // key tile, output head
+  const int nqt = (n_q + TC_ROWS - 1) / TC_ROWS, nkt = gridDim.x;
+  const int qt0 = causal ? kt : 0;
+  const int per_head = nqt - qt0 > 0 ? nqt - qt0 : 0;
+  const int items = sum_group * per_head;
+  const int hk = (ho * sum_group) / group;                     // KV head of this group
+  const int padded = nqt * TC_ROWS;
+
+  if (threadIdx.x == 0) {
+    tc_mbar_init(tc_smem(&sm.kbar), 1);
+    tc_mbar_init(tc_smem(&sm.aready), TC_EPI);
+    for (int s = 0; s < 2; ++s) {
+      tc_mbar_init(tc_smem(&sm.qfull[s]), 1);
+      tc_mbar_init(tc_smem(&sm.qempty[s]), 1);
+      tc_mbar_init(tc_smem(&sm.tfull[s]), 1);
+      tc_mbar_init(tc_smem(&sm.tempty[s]), TC_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc_smem(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+
+  // Producer and MMA warps run their loops warp-wide (aligned barriers stay
+  // convergent); lane 0 issues the copies / MMAs.
+  if (warp == 0) {                  // ---- bulk-copy producer
+    if (items > 0) {
+      if (lane == 0) {
+        tc_expect_tx(tc_smem(&sm.kbar), TC_TILE);
+        tc_bulk(tc_smem(sm.k), Kt + ((int64_t)hk * nkt + kt) * TC_TILE, TC_TILE, tc_smem(&sm.kbar));
+      }
+      for (int it = 0; it < items; ++it) {
+        const int s = it & 1;
+        if (it >= 2) tc_wait(tc_smem(&sm.qempty[s]), ((it >> 1) - 1) & 1);
+        const int h = ho * sum_group + it / per_head, qt = qt0 + it % per_head;
+        if (lane == 0) {
+          tc_expect_tx(tc_smem(&sm.qfull[s]), TC_TILE);
+          tc_bulk(tc_smem(sm.q[s]), Qt + ((int64_t)h * nqt + qt) * TC_TILE, TC_TILE, tc_smem(&sm.qfull[s]));
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {           // ---- MMA issuer
+    if (items > 0) {
+      // kind::f16, fp16 A/B, fp32 D, both K-major, N = 128 (bits 17-22), M = 128 (bits 24-28)
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_ROWS >> 3) << 17) | ((uint32_t)(TC_ROWS >> 4) << 24);
+      tc_wait(tc_smem(&sm.aready), 0);   // the K tile is in TMEM (columns 256..383)
+      for (int it = 0; it < items; ++it) {
+        const int s = it & 1;
+        tc_wait(tc_smem(&sm.qfull[s]), (it >> 1) & 1);
+        if (it >= 2) tc_wait(tc_smem(&sm.tempty[s]), ((it >> 1) - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t qa = tc_smem(sm.q[s]), d = tmem + s * TC_ROWS;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+            const uint32_t kh = tmem + TC_AH + 8 * kk, kl = tmem + TC_AL + 8 * kk;
+            const uint64_t qh = sw128_desc(qa + off), ql = sw128_desc(qa + TC_PART + off);
+            tc_mma_f16_ts(d, kh, qh, idesc, kk > 0);
+            tc_mma_f16_ts(d, kh, ql, idesc, 1);
+            tc_mma_f16_ts(d, kl, qh, idesc, 1);
+          }
+          tc_commit(tc_smem(&sm.qempty[s]));
+          tc_commit(tc_smem(&sm.tfull[s]));
+        }
+        __syncwarp();
+      }
+    }
+  } else {                          // ---- epilogue: 8 warps
+    const int et = threadIdx.x - 64;                  // 0 .. 255
+    const int quarter = warp & 3, half = (warp - 2) >> 2;   // TMEM lanes, column half
+    const int key_local = 32 * quarter + lane;
+    const int key = kt * TC_ROWS + key_local;
+    if (items > 0) {
+      // K tile -> TMEM as the MMA's A operand: lane = key row, column c = the
+      // fp16 pair (2c, 2c+1); warps of column half 0 write the hi part, 1 the lo
+      tc_wait(tc_smem(&sm.kbar), 0);
+      const uint8_t *part = sm.k + half * TC_PART;
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {   // 8 chunks of 8 elements = 64 dims
+          const uint4 v = *reinterpret_cast<const uint4 *>(part + sw128_off(key_local, 64 * cb + 8 * c));
+          r[4 * c] = v.x;
+          r[4 * c + 1] = v.y;
+          r[4 * c + 2] = v.z;
+          r[4 * c + 3] = v.w;
+        }
+        tc_st32(tmem + ((uint32_t)(32 * quarter) << 16) + (half ? TC_AL : TC_AH) + 32 * cb, r);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      tc_arrive(tc_smem(&sm.aready));
+    }
+    const float ksc_inv = __frcp_rn(__ldg(Ksc + (int64_t)hk * nkt + kt));   // powers of two: exact
+    float sv = 0.f, sk = 0.f;
+    // item it = (head gq of the group, query tile qt0 + qi); the next item's
+    // column statistics and scale are loaded one item ahead
+    int gq = 0, qi = 0;
+    float2 nst = make_float2(0.f, 0.f);
+    float nqsc = 1.f;
+    if (items > 0) {
+      const int h = ho * sum_group;
+      if (et < TC_ROWS) nst = __ldg(stats + (int64_t)h * padded + qt0 * TC_ROWS + et);
+      nqsc = __ldg(Qsc + (int64_t)h * nqt + qt0);
+    }
+    for (int it = 0; it < items; ++it) {
+      const int s = it & 1;
+      const int qt = qt0 + qi;
+      const float2 cst = nst;
+      const float u = 1.4426950408889634f * ksc_inv * __frcp_rn(nqsc);
+      if (++qi == per_head) {
+        qi = 0;
+        ++gq;
+      }
+      if (it + 1 < items) {
+        const int h1 = ho * sum_group + gq;
+        if (et < TC_ROWS) nst = __ldg(stats + (int64_t)h1 * padded + (qt0 + qi) * TC_ROWS + et);
+        nqsc = __ldg(Qsc + (int64_t)h1 * nqt + qt0 + qi);
+      }
+      if (et < TC_ROWS) sm.stat[s][et] = cst;
+      asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI) : "memory");
+      tc_wait(tc_smem(&sm.tfull[s]), (it >> 1) & 1);
+      tc_fence_after();
+      const bool diag = causal && qt == kt;
+      float tv = 0.f, tk = 0.f;   // this tile's share (two-level sums over long contexts)
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        const int c0 = 64 * half + 32 * cb;
+        float v[32];
+        tc_ld32(tmem + ((uint32_t)(32 * quarter) << 16) + s * TC_ROWS + c0, v);
+        const float4 *st4 = reinterpret_cast<const float4 *>(&sm.stat[s][c0]);
+        if (!diag) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float4 st = st4[i >> 1];   // (c, |q|) of columns c0 + i, c0 + i + 1
+            const float a0 = tc_ex2(fmaf(v[i], u, -st.x)), a1 = tc_ex2(fmaf(v[i + 1], u, -st.z));
+            tv += a0 + a1;
+            tk = fmaf(fmaf(-a0, a0, a0), st.y, tk);
+            tk = fmaf(fmaf(-a1, a1, a1), st.w, tk);
+          }
+        } else {                    // keys after the query are masked (causal)
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float2 st = sm.stat[s][c0 + i];
+            const float a = c0 + i < key_local ? 0.f : tc_ex2(fmaf(v[i], u, -st.x));
+            tv += a;
+            tk = fmaf(fmaf(-a, a, a), st.y, tk);
+          }
+        }
+      }
+      sv += tv;
+      sk += tk;
+      tc_fence_before();
+      tc_arrive(tc_smem(&sm.tempty[s]));
+    }
+    // combine the two column halves of each key
+    if (half == 1) {
+      sm.red[0][key_local] = sv;
+      sm.red[1][key_local] = sk;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI) : "memory");
+    if (half == 0 && key < n_k) {
+      ans_v[(int64_t)ho * n_k + key] = sv + sm.red[0][key_local];
+      ans_k[(int64_t)ho * n_k + key] = sk + sm.red[1][key_local];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
+                  int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
+                  float *ans_k, float *ans_v, cudaStream_t st) {
+  if (d != 128) return ANTKV_EUNSUPPORTED;
+  if (getenv("ANTKV_NO_TCGEN05")) return ANTKV_EUNSUPPORTED;
+  if (n_k == 0) return ANTKV_OK;
+  const int nqt = ceil_div(n_q, TC_ROWS), nkt = ceil_div(n_k, TC_ROWS);
+  uint8_t *qt = nullptr, *kt = nullptr;
+  float *qsc = nullptr, *ksc = nullptr;
+  float2 *stats = nullptr;
+  cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * (nqt ? nqt : 1) * TC_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&kt, (size_t)kv_heads * nkt * TC_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * (nqt ? nqt : 1), st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nkt, st);
+  if (e == cudaSuccess)
+    e = scratch_alloc((void **)&stats, sizeof(float2) * (size_t)heads * (nqt ? nqt : 1) * TC_ROWS, st);
+  if (e != cudaSuccess) return cuda_status(e, "anchor-score tile scratch");
+  if (nqt > 0) {
+    presplit_sw128_kernel<<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
+    const int64_t ns = (int64_t)heads * nqt * TC_ROWS;
+    ans_tc_stats_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(M, L, qn, heads, n_q, nqt * TC_ROWS,
+                                                                       stats);
+  }
+  presplit_sw128_kernel<<<dim3(nkt, kv_heads), 256, 0, st>>>(Kr, n_k, kt, ksc);
+  const int smem = (int)sizeof(AnsTcSmem) + 1024;
+  cudaFuncSetAttribute(ans_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  ans_tc_kernel<<<dim3(nkt, heads / sum_group), TC_THREADS, smem, st>>>(
+      qt, qsc, kt, ksc, stats, heads / kv_heads, sum_group, n_q, n_k, causal, ans_k, ans_v);
+  const cudaError_t le = cudaGetLastError();
+  cudaFreeAsync(qt, st);
+  cudaFreeAsync(kt, st);
+  cudaFreeAsync(qsc, st);
+  cudaFreeAsync(ksc, st);
+  cudaFreeAsync(stats, st);
+  if (le != cudaSuccess) return cuda_status(le, "ans_tc_kernel");
+  return ANTKV_OK;
+}
+
+}  // namespace antkv
