@@ -279,6 +279,9 @@ ans_kernel(const float *__restrict__ Qs, const float *__restrict__ Kr,
 int launch_flash_mma(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads,
                      int n_q, int n_k, int d, int dv, int causal, float *O, float *L, float *M,
                      cudaStream_t st);
+int launch_flash_tc(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads, int n_q,
+                    int n_k, int d, int dv, int causal, int v_bf16, float *O, float *L, float *M,
+                    cudaStream_t st);
 int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
                   int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
                   float *ans_k, float *ans_v, cudaStream_t st);
@@ -288,7 +291,7 @@ int launch_ans_mma(const float *Qs, const float *Kr, const float *M, const float
 
 static int launch_flash(const float *Qs, const float *Kr, const float *V, int heads,
                         int kv_heads, int n_q, int n_k, int d, int dv, int causal,
-                        float *O, float *L, float *M, cudaStream_t st) {
+                        float *O, float *L, float *M, cudaStream_t st, int v_bf16 = 0) {
   ANTKV_REQUIRE(d >= 1 && d <= FA_DMAX && dv >= 1 && dv <= FA_DMAX,
                 "head dimension must be in [1, %d]", FA_DMAX);
   ANTKV_REQUIRE(heads >= 1 && kv_heads >= 1 && heads % kv_heads == 0,
@@ -296,8 +299,10 @@ static int launch_flash(const float *Qs, const float *Kr, const float *V, int he
   ANTKV_REQUIRE(!causal || n_q == n_k, "causal attention requires matching Q/K token counts");
   if (n_q == 0) return ANTKV_OK;
   ANTKV_REQUIRE(n_k >= 1, "empty key set");
-  {  // d = 128: tensor-core kernel (prefill_mma.cu)
-    const int rc = launch_flash_mma(Qs, Kr, V, heads, kv_heads, n_q, n_k, d, dv, causal, O, L, M, st);
+  {  // d = 128: tcgen05 kernel (prefill_tc.cu), else mma.sync (prefill_mma.cu)
+    int rc = launch_flash_tc(Qs, Kr, V, heads, kv_heads, n_q, n_k, d, dv, causal, v_bf16, O, L, M, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+    rc = launch_flash_mma(Qs, Kr, V, heads, kv_heads, n_q, n_k, d, dv, causal, O, L, M, st);
     if (rc != ANTKV_EUNSUPPORTED) return rc;
   }
   size_t smem = sizeof(float) * (64 * (d + 1) * 2 + 64 * (dv + 1) + 64 * 65);
@@ -411,7 +416,7 @@ extern "C" int antkv_prefill_attention_block(const void *Q, const void *K, const
     rc = launch_flash(qs + (size_t)b * Hq * n_q * d, kr + (size_t)b * Hkv * n_k * d,
                       vf + (size_t)b * Hkv * n_k * d, Hq, Hkv, n_q, n_k, d, d, causal,
                       O + (size_t)b * Hq * n_q * d, L + (size_t)b * Hq * n_q,
-                      M + (size_t)b * Hq * n_q, st);
+                      M + (size_t)b * Hq * n_q, st, dtype == ANTKV_BF16);
   }
   cudaFreeAsync(qs, st);
   cudaFreeAsync(kr, st);

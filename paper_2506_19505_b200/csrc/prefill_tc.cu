@@ -35,10 +35,12 @@ constexpr int TC_THREADS = 32 * TC_WARPS;
 constexpr int TC_EPI = 8 * 32;               // epilogue threads
 constexpr uint32_t TC_AH = 256, TC_AL = 320; // TMEM columns of the K tile (A operand): hi, lo
 
-// Byte offset of element (row, k) in one 128B-swizzled K-major part: two
-// 64-column atoms of [128 rows][128 B], 16-byte chunks XOR-ed with row & 7.
+// Byte offset of element (row, k) in one 128B-swizzled K-major part of R
+// rows: 64-column atoms of [R rows][128 B], 16-byte chunks XOR-ed with
+// row & 7 (8-row groups 1024 B apart).
+template <int R = TC_ROWS>
 __host__ __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
-  return (k >> 6) * (TC_ROWS * 128) + row * 128 + ((((k & 63) >> 3) ^ (row & 7)) << 4) + (k & 7) * 2;
+  return (k >> 6) * (R * 128) + row * 128 + ((((k & 63) >> 3) ^ (row & 7)) << 4) + (k & 7) * 2;
 }
 
 __device__ __forceinline__ uint32_t tc_smem(const void *p) {
@@ -93,6 +95,20 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
+// 32 consecutive fp32 columns of this thread's TMEM lane (no wait: pair with
+// tc_ld_wait before using v)
+__device__ __forceinline__ void tc_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tc_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // 32 consecutive fp32 columns of this thread's TMEM lane
 __device__ __forceinline__ void tc_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -144,18 +160,20 @@ __device__ __forceinline__ float tc_pow2_scale(float mx) {
   return __int_as_float((267 - e) << 23);
 }
 
-// X [heads][rows][128] float32 -> [heads][ceil(rows/128)][hi | lo] fp16 parts
+// X [heads][rows][128] float32 -> [heads][ceil(rows/R)][hi | lo] fp16 parts
 // of x * scale in the 128B-swizzled K-major layout, scale [heads][tiles].
+template <int R>
 __global__ void __launch_bounds__(256)
 presplit_sw128_kernel(const float *__restrict__ X, int rows, uint8_t *__restrict__ tiles,
                       float *__restrict__ scales) {
+  constexpr int PART = R * 128 * 2;
   __shared__ float red[8];
   const int h = blockIdx.y, tile = blockIdx.x, nt = gridDim.x;
   const float *src = X + (int64_t)h * rows * 128;
-  uint8_t *dst = tiles + ((int64_t)h * nt + tile) * TC_TILE;
+  uint8_t *dst = tiles + ((int64_t)h * nt + tile) * (2 * PART);
   float mx = 0.f;
-  for (int e = threadIdx.x; e < TC_ROWS * 32; e += 256) {
-    const int r = tile * TC_ROWS + (e >> 5);
+  for (int e = threadIdx.x; e < R * 32; e += 256) {
+    const int r = tile * R + (e >> 5);
     if (r < rows) {
       const float4 v = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)r * 128) + (e & 31));
       mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
@@ -170,8 +188,8 @@ presplit_sw128_kernel(const float *__restrict__ X, int rows, uint8_t *__restrict
   const float sc = tc_pow2_scale(mx);
   if (threadIdx.x == 0) scales[(int64_t)h * nt + tile] = sc;
   // one 16-byte chunk (8 elements) of one row per thread and step
-  for (int e = threadIdx.x; e < TC_ROWS * 16; e += 256) {
-    const int r = e >> 4, c = e & 15, gr = tile * TC_ROWS + r;
+  for (int e = threadIdx.x; e < R * 16; e += 256) {
+    const int r = e >> 4, c = e & 15, gr = tile * R + r;
     float x[8];
     if (gr < rows) {
       const float4 a = __ldg(reinterpret_cast<const float4 *>(src + (int64_t)gr * 128 + 8 * c));
@@ -191,9 +209,9 @@ presplit_sw128_kernel(const float *__restrict__ X, int rows, uint8_t *__restrict
       hi[i] = *reinterpret_cast<uint32_t *>(&hh);
       lo[i] = *reinterpret_cast<uint32_t *>(&ll);
     }
-    const uint32_t off = sw128_off(r, 8 * c);
+    const uint32_t off = sw128_off<R>(r, 8 * c);
     *reinterpret_cast<uint4 *>(dst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4 *>(dst + TC_PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    *reinterpret_cast<uint4 *>(dst + PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
 
@@ -318,7 +336,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
         uint32_t r[32];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {   // 8 chunks of 8 elements = 64 dims
-          const uint4 v = *reinterpret_cast<const uint4 *>(part + sw128_off(key_local, 64 * cb + 8 * c));
+          const uint4 v = *reinterpret_cast<const uint4 *>(part + sw128_off<>(key_local, 64 * cb + 8 * c));
           r[4 * c] = v.x;
           r[4 * c + 1] = v.y;
           r[4 * c + 2] = v.z;
@@ -429,12 +447,12 @@ int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float 
     e = scratch_alloc((void **)&stats, sizeof(float2) * (size_t)heads * (nqt ? nqt : 1) * TC_ROWS, st);
   if (e != cudaSuccess) return cuda_status(e, "anchor-score tile scratch");
   if (nqt > 0) {
-    presplit_sw128_kernel<<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
+    presplit_sw128_kernel<TC_ROWS><<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
     const int64_t ns = (int64_t)heads * nqt * TC_ROWS;
     ans_tc_stats_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(M, L, qn, heads, n_q, nqt * TC_ROWS,
                                                                        stats);
   }
-  presplit_sw128_kernel<<<dim3(nkt, kv_heads), 256, 0, st>>>(Kr, n_k, kt, ksc);
+  presplit_sw128_kernel<TC_ROWS><<<dim3(nkt, kv_heads), 256, 0, st>>>(Kr, n_k, kt, ksc);
   const int smem = (int)sizeof(AnsTcSmem) + 1024;
   cudaFuncSetAttribute(ans_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   ans_tc_kernel<<<dim3(nkt, heads / sum_group), TC_THREADS, smem, st>>>(
@@ -446,6 +464,373 @@ int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float 
   cudaFreeAsync(ksc, st);
   cudaFreeAsync(stats, st);
   if (le != cudaSuccess) return cuda_status(le, "ans_tc_kernel");
+  return ANTKV_OK;
+}
+
+
+// ============================================================================
+// Flash attention with the (O, L, M) auxiliaries (attention.py:146-169,
+// _ckernels.pyx:10-88) on tcgen05, for bf16-exact V (the prefill path with
+// bf16 inputs).  CTA = (head, 128 queries): the query tile's fp16 parts live
+// in TMEM as the A operand of S = Q.K^T (M = 128 queries, N = 128 keys per
+// tile — below N = 128 a tcgen05.mma runs at half rate, measured); each
+// softmax thread owns one query row (its TMEM lane), keeps a lazily raised
+// reference max (rescale only when a tile's max exceeds it by 2^8, so P <=
+// 2^8 keeps exact bf16 parts) and the exact running max for M, and writes
+// P's bf16 parts back over its S columns as the A operand of O += P.V
+// (N = 128 dims, B = the V^T tile).  Products are the mma.sync kernel's
+// two-part splits (S: fp16 parts of power-of-two-scaled tiles, three
+// products; P.V: bf16 parts of P against exact bf16 V, two products),
+// float32 accumulation in TMEM.
+//
+// Warps: 0 bulk-copy producer (two rings of two stages: K hi | K lo, 64 KB,
+// freed as soon as S(t) completes; V^T, 32 KB, freed by P.V(t)), 1 TMEM owner + MMA issuer (S of tile t is issued before P.V of
+// tile t - 1 so the tensor core works while the softmax of t - 1 runs), 2-9
+// softmax: warps w and w + 4 own the same 32 rows (TMEM lanes) and split the
+// 128 key columns, exchanging half-row maxima through shared memory.  TMEM columns: S/P buffers 0 and 128, O 256..383,
+// Q parts 384..511.  Per 16-key step kk the P parts sit at columns 16 kk
+// (hi) and 16 kk + 8 (lo) of the buffer, so the 32 columns a softmax chunk
+// writes are exactly the S columns it has just read.
+constexpr int FT_KR = 128;                   // keys per tile
+constexpr int FT_KPART = FT_KR * 128 * 2;    // 32 KB (one fp16 part of a K tile)
+constexpr int FT_VTILE = 128 * FT_KR * 2;    // 32 KB (V^T bf16)
+constexpr int FT_NS = 2;                     // stages of each ring (K: 64 KB, V^T: 32 KB)
+constexpr int FT_THREADS = 10 * 32;
+constexpr uint32_t FT_O = 256, FT_QH = 384, FT_QL = 448;
+
+struct FlashTcSmem {
+  uint8_t k[FT_NS][2 * FT_KPART];   // K hi | K lo, released when S(t) completes
+  uint8_t v[FT_NS][FT_VTILE];       // V^T, released when P.V(t) completes
+  unsigned long long kfull[FT_NS], kempty[FT_NS], vfull[FT_NS], vempty[FT_NS];
+  unsigned long long sfull[2], pfull[2], pvdone[2], qready;
+  float xm[2][2][TC_ROWS];   // [buffer][column half][row]: half-row maxima
+  float lx[2][TC_ROWS];      // [column half][row]: half-row sums at the end
+  uint32_t tmem;
+};
+
+// V [heads][rows][128] float32 (bf16-exact) -> [heads][ceil(rows/128)] tiles
+// V^T[128 dims][128 keys] bf16, K-major, 128B-swizzled: the B operand of O +=
+// P.V.
+__global__ void __launch_bounds__(256)
+presplit_vt_kernel(const float *__restrict__ V, int rows, uint8_t *__restrict__ tiles) {
+  const int h = blockIdx.y, tile = blockIdx.x, nt = gridDim.x;
+  const float *src = V + (int64_t)h * rows * 128;
+  uint8_t *dst = tiles + ((int64_t)h * nt + tile) * FT_VTILE;
+  // thread -> (dim, chunk of 8 keys); consecutive threads take consecutive dims
+  for (int e = threadIdx.x; e < 128 * 16; e += 256) {
+    const int dim = e & 127, c = e >> 7;
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k0 = tile * FT_KR + 8 * c + 2 * i;
+      const float a = k0 < rows ? __ldg(src + (int64_t)k0 * 128 + dim) : 0.f;
+      const float b = k0 + 1 < rows ? __ldg(src + (int64_t)(k0 + 1) * 128 + dim) : 0.f;
+      const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
+      w[i] = *reinterpret_cast<const uint32_t *>(&v2);
+    }
+    *reinterpret_cast<uint4 *>(dst + sw128_off<128>(dim, 8 * c)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1)
+flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, const uint8_t *__restrict__ Kt,
+                const float *__restrict__ Ksc, const uint8_t *__restrict__ Vt, int group, int n_q, int n_k,
+                int causal, float *__restrict__ O, float *__restrict__ Lout, float *__restrict__ Mout) {
+  extern __shared__ uint8_t ft_raw[];
+  FlashTcSmem &sm = *reinterpret_cast<FlashTcSmem *>(ft_raw + ((1024 - (tc_smem(ft_raw) & 1023)) & 1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nqt = gridDim.x, h = blockIdx.y, hk = h / group;
+  const int qt = nqt - 1 - blockIdx.x;              // long causal rows first
+  const int q0 = qt * TC_ROWS;
+  const int nkt = (n_k + FT_KR - 1) / FT_KR;
+  const int last = causal ? min(q0 + TC_ROWS, n_q) - 1 : n_k - 1;
+  const int T = min(nkt, last / FT_KR + 1);         // key tiles this CTA visits
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FT_NS; ++s) {
+      tc_mbar_init(tc_smem(&sm.kfull[s]), 1);
+      tc_mbar_init(tc_smem(&sm.kempty[s]), 1);
+      tc_mbar_init(tc_smem(&sm.vfull[s]), 1);
+      tc_mbar_init(tc_smem(&sm.vempty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc_mbar_init(tc_smem(&sm.sfull[b]), 1);
+      tc_mbar_init(tc_smem(&sm.pfull[b]), 256);
+      tc_mbar_init(tc_smem(&sm.pvdone[b]), 1);
+    }
+    tc_mbar_init(tc_smem(&sm.qready), 256);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(tc_smem(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = sm.tmem;
+  const uint8_t *Kg = Kt + (int64_t)hk * nkt * (2 * FT_KPART);
+  const uint8_t *Vg = Vt + (int64_t)hk * nkt * FT_VTILE;
+
+  if (warp == 0) {                  // ---- producer: K and V^T rings, in tile order
+    for (int t = 0; t < T; ++t) {
+      const int st = t % FT_NS, ph = ((t / FT_NS) - 1) & 1;
+      if (t >= FT_NS) tc_wait(tc_smem(&sm.kempty[st]), ph);
+      if (lane == 0) {
+        const uint32_t bar = tc_smem(&sm.kfull[st]);
+        tc_expect_tx(bar, 2 * FT_KPART);
+        tc_bulk(tc_smem(sm.k[st]), Kg + (int64_t)t * (2 * FT_KPART), 2 * FT_KPART, bar);
+      }
+      __syncwarp();
+      if (t >= FT_NS) tc_wait(tc_smem(&sm.vempty[st]), ph);
+      if (lane == 0) {
+        const uint32_t bar = tc_smem(&sm.vfull[st]);
+        tc_expect_tx(bar, FT_VTILE);
+        tc_bulk(tc_smem(sm.v[st]), Vg + (int64_t)t * FT_VTILE, FT_VTILE, bar);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {           // ---- MMA issuer
+    const uint32_t idS = (1u << 4) | ((uint32_t)(FT_KR >> 3) << 17) | ((uint32_t)(TC_ROWS >> 4) << 24);
+    const uint32_t idPV = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                          ((uint32_t)(TC_ROWS >> 4) << 24);
+    tc_wait(tc_smem(&sm.qready), 0);
+    for (int t = 0; t <= T; ++t) {
+      if (t < T) {                  // S(t) = Q . K_t^T into buffer t & 1
+        const int b = t & 1, st = t % FT_NS;
+        tc_wait(tc_smem(&sm.kfull[st]), (t / FT_NS) & 1);
+        // buffer b still holds P(t-2), read by P.V(t-2): that MMA was issued
+        // before this one and tcgen05.mma executes in issue order, so no wait
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t kb = tc_smem(sm.k[st]), d = tmem + 128 * b;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * (FT_KR * 128) + (kk & 3) * 32;
+            const uint64_t kh = sw128_desc(kb + off), kl = sw128_desc(kb + FT_KPART + off);
+            tc_mma_f16_ts(d, tmem + FT_QH + 8 * kk, kh, idS, kk > 0);
+            tc_mma_f16_ts(d, tmem + FT_QH + 8 * kk, kl, idS, 1);
+            tc_mma_f16_ts(d, tmem + FT_QL + 8 * kk, kh, idS, 1);
+          }
+          tc_commit(tc_smem(&sm.kempty[st]));
+          tc_commit(tc_smem(&sm.sfull[b]));
+        }
+        __syncwarp();
+      }
+      if (t >= 1) {                 // O += P(t-1) . V_{t-1}
+        const int u = t - 1, b = u & 1, st = u % FT_NS;
+        tc_wait(tc_smem(&sm.vfull[st]), (u / FT_NS) & 1);
+        tc_wait(tc_smem(&sm.pfull[b]), (u >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t vb = tc_smem(sm.v[st]);
+#pragma unroll
+          for (int kk = 0; kk < FT_KR / 16; ++kk) {
+#ifdef FT_EXP_NOPV
+            break;
+#endif
+            const uint32_t ph = tmem + 128 * b + 16 * kk, pl = ph + 8;
+            const uint64_t vh = sw128_desc(vb + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
+            tc_mma_f16_ts(tmem + FT_O, ph, vh, idPV, (u > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_f16_ts(tmem + FT_O, pl, vh, idPV, 1);
+          }
+          tc_commit(tc_smem(&sm.vempty[st]));
+          tc_commit(tc_smem(&sm.pvdone[b]));
+        }
+        __syncwarp();
+      }
+    }
+  } else {                          // ---- softmax: warps w, w + 4 share rows, split columns
+    const int quarter = warp & 3, half = (warp - 2) >> 2, row = 32 * quarter + lane, qi = q0 + row;
+    const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+    const int bar_id = 1 + quarter;                 // named barrier of the warp pair
+    {   // Q tile parts -> TMEM (A operand of S): half 0 the hi part, half 1 the lo part
+      const uint8_t *qg = Qt + ((int64_t)h * nqt + qt) * TC_TILE + half * TC_PART;
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb) {
+        uint32_t r[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 v = __ldg(reinterpret_cast<const uint4 *>(qg + sw128_off<>(row, 64 * cb + 8 * c)));
+          r[4 * c] = v.x;
+          r[4 * c + 1] = v.y;
+          r[4 * c + 2] = v.z;
+          r[4 * c + 3] = v.w;
+        }
+        tc_st32(tmem + lane_base + (half ? FT_QL : FT_QH) + 32 * cb, r);
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      tc_arrive(tc_smem(&sm.qready));
+    }
+    const float qs_inv = __frcp_rn(__ldg(Qsc + (int64_t)h * nqt + qt));
+    float mref = -INFINITY, mex = -INFINITY, l = 0.f, lc = 0.f;
+    float ksc_next = T > 0 ? __ldg(Ksc + (int64_t)hk * nkt) : 1.f;
+    for (int t = 0; t < T; ++t) {
+      const int b = t & 1, k0 = t * FT_KR + 64 * half;   // first key of this half
+      const uint32_t sb = tmem + lane_base + 128 * b + 64 * half;
+      const float u = 1.4426950408889634f * qs_inv * __frcp_rn(ksc_next);   // log2 units, exact scales
+      if (t + 1 < T) ksc_next = __ldg(Ksc + (int64_t)hk * nkt + t + 1);
+      tc_wait(tc_smem(&sm.sfull[b]), (t >> 1) & 1);
+      tc_fence_after();
+#ifdef FT_EXP_NOSOFT
+      tc_fence_before();
+      tc_arrive(tc_smem(&sm.pfull[b]));
+      continue;
+#endif
+      const bool full = (!causal || t * FT_KR + FT_KR - 1 <= q0) && t * FT_KR + FT_KR <= n_k;
+      // pass 1: max of this half (raw accumulator; u > 0 commutes with max),
+      // combined with the partner warp's half through shared memory
+      float mt;
+      uint32_t c0[32], c1[32];   // this half's 64 logits, kept for pass 2
+      {
+        tc_ld32_nowait(sb, c0);
+        tc_ld32_nowait(sb + 32, c1);
+        tc_ld_wait();
+        float m8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m8[j] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          float x = __uint_as_float(i < 32 ? c0[i] : c1[i - 32]);
+          if (!full && (k0 + i >= n_k || (causal && k0 + i > qi))) x = -INFINITY;
+          m8[i & 7] = fmaxf(m8[i & 7], x);
+        }
+        const float pm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                               fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+        sm.xm[b][half][row] = pm;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        mt = fmaxf(pm, sm.xm[b][half ^ 1][row]) * u;
+      }
+      mex = fmaxf(mex, mt);
+      if (__any_sync(0xffffffffu, mt > mref + 8.f)) {   // same decision in both warps of the pair
+        const float mn = fmaxf(mref, mt);
+        const float al = mref == -INFINITY ? 0.f : tc_ex2(mref - mn);
+        l *= al;
+        lc *= al;
+        if (t > 0) {        // O holds P.V of earlier tiles: wait for the last one, rescale this half
+          tc_wait(tc_smem(&sm.pvdone[(t - 1) & 1]), ((t - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int cb = 0; cb < 2; ++cb) {
+            float ov[32];
+            tc_ld32(tmem + lane_base + FT_O + 64 * half + 32 * cb, ov);
+            uint32_t r[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(ov[i] * al);
+            tc_st32(tmem + lane_base + FT_O + 64 * half + 32 * cb, r);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        mref = mn;
+      }
+      const float msub = mref == -INFINITY ? 0.f : mref;
+      // pass 2: P in bf16 parts over the S columns read in pass 1, 32 keys at a time
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {   // key pair (2i, 2i+1) of this chunk
+          float x0 = __uint_as_float(c ? c1[2 * i] : c0[2 * i]);
+          float x1 = __uint_as_float(c ? c1[2 * i + 1] : c0[2 * i + 1]);
+          const int kk0 = k0 + 32 * c + 2 * i;
+          if (!full) {
+            if (kk0 >= n_k || (causal && kk0 > qi)) x0 = -INFINITY;
+            if (kk0 + 1 >= n_k || (causal && kk0 + 1 > qi)) x1 = -INFINITY;
+          }
+          const float p0 = tc_ex2(fmaf(x0, u, -msub)), p1 = tc_ex2(fmaf(x1, u, -msub));
+          ls4[i & 3] += p0 + p1;
+          const __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
+          const float2 hf = __bfloat1622float2(hh);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+          // 16-key step s = i / 8 of this chunk: hi words at 16 s + (i % 8), lo at + 8
+          w[16 * (i >> 3) + (i & 7)] = *reinterpret_cast<const uint32_t *>(&hh);
+          w[16 * (i >> 3) + 8 + (i & 7)] = *reinterpret_cast<const uint32_t *>(&lo);
+        }
+        tc_st32(sb + 32 * c, w);
+      }
+      const float ls = (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      {   // l += ls, compensated (long contexts add thousands of tile sums)
+        const float y = ls - lc, tt = l + y;
+        lc = (tt - l) - y;
+        l = tt;
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      tc_arrive(tc_smem(&sm.pfull[b]));
+    }
+    // the row's l = both halves' sums
+    sm.lx[half][row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    const float lrow = l + sm.lx[half ^ 1][row];
+    // O / l (this half's 64 columns), L relative to the exact max M (natural log)
+    if (T > 0) {
+      tc_wait(tc_smem(&sm.pvdone[(T - 1) & 1]), ((T - 1) >> 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
+    float *orow = O + ((int64_t)h * n_q + qi) * 128 + 64 * half;
+#pragma unroll
+    for (int cb = 0; cb < 2; ++cb) {
+      float v[32];
+      if (T > 0) {
+        tc_ld32(tmem + lane_base + FT_O + 64 * half + 32 * cb, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (qi < n_q) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4)
+          *reinterpret_cast<float4 *>(orow + 32 * cb + i) =
+              make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv, v[i + 3] * inv);
+      }
+    }
+    if (qi < n_q && half == 0) {
+      const bool any = mex > -INFINITY;
+      Mout[(int64_t)h * n_q + qi] = any ? mex * 0.6931471805599453f : -INFINITY;
+      Lout[(int64_t)h * n_q + qi] = any ? lrow * exp2f(mref - mex) : 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// v_bf16: every V element is exactly a bf16 (the prefill path's bf16 inputs);
+// otherwise the mma.sync kernel (which splits V) runs instead.
+int launch_flash_tc(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads, int n_q,
+                    int n_k, int d, int dv, int causal, int v_bf16, float *O, float *L, float *M,
+                    cudaStream_t st) {
+  if (d != 128 || dv != 128 || !v_bf16) return ANTKV_EUNSUPPORTED;
+  if (getenv("ANTKV_NO_TCGEN05")) return ANTKV_EUNSUPPORTED;
+  if (n_q == 0) return ANTKV_OK;
+  const int nqt = ceil_div(n_q, TC_ROWS), nkt = ceil_div(n_k, FT_KR);
+  uint8_t *qt = nullptr, *kt = nullptr, *vt = nullptr;
+  float *qsc = nullptr, *ksc = nullptr;
+  cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * nqt * TC_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&kt, (size_t)kv_heads * nkt * 2 * FT_KPART, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&vt, (size_t)kv_heads * nkt * FT_VTILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * nqt, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nkt, st);
+  if (e != cudaSuccess) return cuda_status(e, "attention tile scratch");
+  presplit_sw128_kernel<TC_ROWS><<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
+  presplit_sw128_kernel<FT_KR><<<dim3(nkt, kv_heads), 256, 0, st>>>(Kr, n_k, kt, ksc);
+  presplit_vt_kernel<<<dim3(nkt, kv_heads), 256, 0, st>>>(V, n_k, vt);
+  const int smem = (int)sizeof(FlashTcSmem) + 1024;
+  cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  flash_tc_kernel<<<dim3(nqt, heads), FT_THREADS, smem, st>>>(qt, qsc, kt, ksc, vt, heads / kv_heads, n_q, n_k,
+                                                              causal, O, L, M);
+  const cudaError_t le = cudaGetLastError();
+  cudaFreeAsync(qt, st);
+  cudaFreeAsync(kt, st);
+  cudaFreeAsync(vt, st);
+  cudaFreeAsync(qsc, st);
+  cudaFreeAsync(ksc, st);
+  if (le != cudaSuccess) return cuda_status(le, "flash_tc_kernel");
   return ANTKV_OK;
 }
 

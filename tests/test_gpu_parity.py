@@ -894,3 +894,44 @@ def test_per_token_errors_at_scale_vs_direct_recomputation():
                 V2[j] = Vq[j]
             want = float(((_scores(R(Q), R(K2), True) @ V2) - base).abs().sum())
             assert abs(errs[j] - want) <= 1e-7 * max(want, 1e-300) + 1e-12, (mode, j)
+
+
+@pytest.mark.parametrize("causal", [True, False])
+def test_tcgen05_prefill_kernels_vs_oracle(causal):
+    """The tcgen05 attention (bf16 inputs: V is bf16-exact) and anchor-score
+    kernels at d = 128 against the float64 oracle: causal full prefill
+    (n = 1000, GQA 4) and a non-causal shard block (300 queries x 700 keys),
+    at the reference's own tolerances (O 1e-4, M 1e-5, L 1e-5 relative; AnS
+    1e-4 relative)."""
+    from paper_2506_19505_b200 import _lib
+    from paper_2506_19505_b200.parallel import CudaPrefillOps
+    Hq, Hkv, d, theta = 8, 2, 128, 5e5
+    nq, nk = (1000, 1000) if causal else (300, 700)
+    Q, K, V = qkv(81, Hq, Hkv, max(nq, nk), d, heavy=3)
+    Q, K, V = Q[:, :nq], K[:, :nk], V[:, :nk]
+    qpos = np.arange(nk - nq, nk) if not causal else np.arange(nq)
+    kpos = np.arange(nk)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    ops = CudaPrefillOps()
+    Qd, Kd, Vd = dev(Q[None]), dev(K[None]), dev(V[None])
+    qp = torch.from_numpy(qpos).cuda()[None].contiguous()
+    kp = torch.from_numpy(kpos).cuda()[None].contiguous()
+    Og, Mg, Lg, qn = ops.attention_block(Qd, Kd, Vd, qp, kp, causal, theta)
+    ak, av = ops.score_block(Qd, Kd, qp, kp, Mg, Lg, qn, causal, theta)
+    g = Hq // Hkv
+    ref_k = np.zeros((Hkv, nk))
+    ref_v = np.zeros((Hkv, nk))
+    for h in range(Hq):
+        q = Q[h].astype(np.float64)
+        k, v = K[h // g].astype(np.float64), V[h // g].astype(np.float64)
+        Qs = O.apply_rope(q, qpos, theta) / np.sqrt(d)
+        Kr = O.apply_rope(k, kpos, theta)
+        Or, Lr, Mr = O.flash_aux(Qs, Kr, v, 64, 64, causal)
+        assert rel(Og[0, h].cpu().numpy(), Or) < 1e-4
+        assert np.abs(Mg[0, h].cpu().numpy() - Mr).max() < 1e-5 * max(1.0, np.abs(Mr).max())
+        assert np.abs(Lg[0, h].cpu().numpy() / Lr - 1).max() < 1e-5
+        kk, vv = O.ans_blocked(Qs, Kr, Mr, Lr, np.sqrt((q ** 2).sum(1)), 64, 64, causal)
+        ref_k[h // g] += kk
+        ref_v[h // g] += vv
+    assert rel(ak[0].cpu().numpy(), ref_k) < 1e-4
+    assert rel(av[0].cpu().numpy(), ref_v) < 1e-4
