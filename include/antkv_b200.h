@@ -19,6 +19,7 @@
  *   antkv_prefill_attention <- attention.flash_attention_aux (attention.py:146-169)
  *                             with RoPE (attention.py:89-106) fused, GQA-batched
  *   antkv_prefill_anchor_scores <- anchors.anchor_scores_blocked (anchors.py:66-87)
+ *   antkv_prefill_attention_scores <- both passes of cache.py:100-121 in one call
  *   antkv_prefill_*_block  <- (new) the same two passes per sequence-shard block
  *   antkv_select_anchors   <- anchors.select_anchors  (anchors.py:96-132)
  *   antkv_cache_build      <- QuantizedKVCache.prefill layout step (cache.py:122-139)
@@ -138,6 +139,16 @@ ANTKV_API int antkv_prefill_anchor_scores(const void *Q, const void *K, int dtyp
                                 int B, int Hq, int Hkv, int n, int d,
                                 double theta_base, float *ans_k, float *ans_v,
                                 void *stream);
+
+/* Both prefill passes in one call (what QuantizedKVCache.prefill needs):
+ * antkv_prefill_attention's outputs plus antkv_prefill_anchor_scores'
+ * ans_k/ans_v [B][Hkv][n].  For bf16 rows with d = 128 the two tcgen05
+ * kernels share one set of rotated, split Q/K tiles (RoPE fused into the
+ * split); other inputs run the two calls. */
+ANTKV_API int antkv_prefill_attention_scores(const void *Q, const void *K, const void *V, int dtype,
+                            const int64_t *positions, int B, int Hq, int Hkv, int n, int d,
+                            double theta_base, float *O, float *M, float *L, float *q_norms,
+                            float *ans_k, float *ans_v, void *stream);
 
 /* Sequence-shard blocks of the two prefill passes (context parallelism,
  * SURVEY.md §8e; parallel.py ShardedPrefill).  A query block Q [B][Hq][n_q][d]

@@ -59,6 +59,8 @@ _SIGS = {
     "antkv_kmeans_assign_f64": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]),
     "antkv_kmeans_update_f64": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "antkv_eval_pair_l1": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "antkv_prefill_attention_scores": (_i, [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp,
+                                            _vp, _vp, _vp, _vp]),
     "antkv_prefill_attention_block": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _i, _d, _i,
                                            _vp, _vp, _vp, _vp, _vp]),
     "antkv_prefill_anchor_scores_block": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,

@@ -300,14 +300,13 @@ class QuantizedKVCache:
         qn = torch.empty_like(M)
         th = float(self.config.theta_base)
         st = _lib.stream()
-        _lib.call("antkv_prefill_attention", _lib.ptr(Qc), _lib.ptr(Kc), _lib.ptr(Vc), dt,
-                  _lib.ptr(pos), B, Hq, Hkv, n, d, th, _lib.ptr(O), _lib.ptr(M), _lib.ptr(L),
-                  _lib.ptr(qn), st)
         ans_k = torch.empty((B, Hkv, n), dtype=torch.float32, device=dev)
         ans_v = torch.empty_like(ans_k)
-        _lib.call("antkv_prefill_anchor_scores", _lib.ptr(Qc), _lib.ptr(Kc), dt, _lib.ptr(pos),
-                  _lib.ptr(M), _lib.ptr(L), _lib.ptr(qn), B, Hq, Hkv, n, d, th,
-                  _lib.ptr(ans_k), _lib.ptr(ans_v), st)
+        # FA + aux and AnS (cache.py:100-121) in one call: bf16 d = 128 rows
+        # share one set of RoPE'd, split tiles between the two tcgen05 kernels
+        _lib.call("antkv_prefill_attention_scores", _lib.ptr(Qc), _lib.ptr(Kc), _lib.ptr(Vc), dt,
+                  _lib.ptr(pos), B, Hq, Hkv, n, d, th, _lib.ptr(O), _lib.ptr(M), _lib.ptr(L),
+                  _lib.ptr(qn), _lib.ptr(ans_k), _lib.ptr(ans_v), st)
         self.last_scores = (ans_k, ans_v)
         budget = self.config.budget_for(n)
         anchors = select_anchors_device(ans_k.view(B * Hkv, n), ans_v.view(B * Hkv, n), budget,

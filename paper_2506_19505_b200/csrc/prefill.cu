@@ -282,6 +282,9 @@ int launch_flash_mma(const float *Qs, const float *Kr, const float *V, int heads
 int launch_flash_tc(const float *Qs, const float *Kr, const float *V, int heads, int kv_heads, int n_q,
                     int n_k, int d, int dv, int causal, int v_bf16, float *O, float *L, float *M,
                     cudaStream_t st);
+int prefill_tc_fused(const void *Q, const void *K, const void *V, int dtype, const int64_t *positions, int B,
+                     int Hq, int Hkv, int n, int d, double theta, float *O, float *M, float *L, float *qn,
+                     float *ans_k, float *ans_v, cudaStream_t st);
 int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float *L, const float *qn,
                   int heads, int kv_heads, int sum_group, int n_q, int n_k, int d, int causal,
                   float *ans_k, float *ans_v, cudaStream_t st);
@@ -477,4 +480,21 @@ extern "C" int antkv_prefill_anchor_scores(const void *Q, const void *K, int dty
                                            float *ans_k, float *ans_v, void *stream) {
   return antkv_prefill_anchor_scores_block(Q, K, dtype, positions, positions, M, L, q_norms, B,
                                            Hq, Hkv, n, n, d, theta_base, 1, ans_k, ans_v, stream);
+}
+
+extern "C" int antkv_prefill_attention_scores(const void *Q, const void *K, const void *V, int dtype,
+                                              const int64_t *positions, int B, int Hq, int Hkv, int n,
+                                              int d, double theta_base, float *O, float *M, float *L,
+                                              float *q_norms, float *ans_k, float *ans_v, void *stream) {
+  ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
+  ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
+  ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
+  int rc = prefill_tc_fused(Q, K, V, dtype, positions, B, Hq, Hkv, n, d, theta_base, O, M, L, q_norms,
+                            ans_k, ans_v, as_stream(stream));
+  if (rc != ANTKV_EUNSUPPORTED) return rc;
+  rc = antkv_prefill_attention(Q, K, V, dtype, positions, B, Hq, Hkv, n, d, theta_base, O, M, L, q_norms,
+                               stream);
+  if (rc != ANTKV_OK) return rc;
+  return antkv_prefill_anchor_scores(Q, K, dtype, positions, M, L, q_norms, B, Hq, Hkv, n, d, theta_base,
+                                     ans_k, ans_v, stream);
 }

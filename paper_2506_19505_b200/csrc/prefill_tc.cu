@@ -231,12 +231,12 @@ __global__ void ans_tc_stats_kernel(const float *__restrict__ M, const float *__
   out[i] = v;
 }
 
+constexpr int TC_QS = 3;      // Q stages; stage 2 first carries the K tile (until it is in TMEM)
 struct AnsTcSmem {
-  uint8_t k[TC_TILE];        // 1024-aligned (the struct is placed at a 1024 boundary)
-  uint8_t q[2][TC_TILE];
+  uint8_t q[TC_QS][TC_TILE];  // 1024-aligned (the struct is placed at a 1024 boundary)
   float2 stat[2][TC_ROWS];
   float red[2][TC_ROWS];
-  unsigned long long kbar, aready, qfull[2], qempty[2], tfull[2], tempty[2];
+  unsigned long long kbar, aready, qfull[TC_QS], qempty[TC_QS], tfull[2], tempty[2];
   uint32_t tmem;
 };
 
@@ -258,9 +258,11 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
   if (threadIdx.x == 0) {
     tc_mbar_init(tc_smem(&sm.kbar), 1);
     tc_mbar_init(tc_smem(&sm.aready), TC_EPI);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < TC_QS; ++s) {
       tc_mbar_init(tc_smem(&sm.qfull[s]), 1);
       tc_mbar_init(tc_smem(&sm.qempty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       tc_mbar_init(tc_smem(&sm.tfull[s]), 1);
       tc_mbar_init(tc_smem(&sm.tempty[s]), TC_EPI);
     }
@@ -281,11 +283,12 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
     if (items > 0) {
       if (lane == 0) {
         tc_expect_tx(tc_smem(&sm.kbar), TC_TILE);
-        tc_bulk(tc_smem(sm.k), Kt + ((int64_t)hk * nkt + kt) * TC_TILE, TC_TILE, tc_smem(&sm.kbar));
+        tc_bulk(tc_smem(sm.q[TC_QS - 1]), Kt + ((int64_t)hk * nkt + kt) * TC_TILE, TC_TILE, tc_smem(&sm.kbar));
       }
       for (int it = 0; it < items; ++it) {
-        const int s = it & 1;
-        if (it >= 2) tc_wait(tc_smem(&sm.qempty[s]), ((it >> 1) - 1) & 1);
+        const int s = it % TC_QS;
+        if (it >= TC_QS) tc_wait(tc_smem(&sm.qempty[s]), ((it / TC_QS) - 1) & 1);
+        else if (s == TC_QS - 1) tc_wait(tc_smem(&sm.aready), 0);   // the K tile has left stage 2
         const int h = ho * sum_group + it / per_head, qt = qt0 + it % per_head;
         if (lane == 0) {
           tc_expect_tx(tc_smem(&sm.qfull[s]), TC_TILE);
@@ -300,12 +303,12 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_ROWS >> 3) << 17) | ((uint32_t)(TC_ROWS >> 4) << 24);
       tc_wait(tc_smem(&sm.aready), 0);   // the K tile is in TMEM (columns 256..383)
       for (int it = 0; it < items; ++it) {
-        const int s = it & 1;
-        tc_wait(tc_smem(&sm.qfull[s]), (it >> 1) & 1);
-        if (it >= 2) tc_wait(tc_smem(&sm.tempty[s]), ((it >> 1) - 1) & 1);
+        const int s = it % TC_QS, b = it & 1;
+        tc_wait(tc_smem(&sm.qfull[s]), (it / TC_QS) & 1);
+        if (it >= 2) tc_wait(tc_smem(&sm.tempty[b]), ((it >> 1) - 1) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t qa = tc_smem(sm.q[s]), d = tmem + s * TC_ROWS;
+          const uint32_t qa = tc_smem(sm.q[s]), d = tmem + b * TC_ROWS;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
@@ -316,7 +319,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
             tc_mma_f16_ts(d, kl, qh, idesc, 1);
           }
           tc_commit(tc_smem(&sm.qempty[s]));
-          tc_commit(tc_smem(&sm.tfull[s]));
+          tc_commit(tc_smem(&sm.tfull[b]));
         }
         __syncwarp();
       }
@@ -330,7 +333,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       // K tile -> TMEM as the MMA's A operand: lane = key row, column c = the
       // fp16 pair (2c, 2c+1); warps of column half 0 write the hi part, 1 the lo
       tc_wait(tc_smem(&sm.kbar), 0);
-      const uint8_t *part = sm.k + half * TC_PART;
+      const uint8_t *part = sm.q[TC_QS - 1] + half * TC_PART;
 #pragma unroll
       for (int cb = 0; cb < 2; ++cb) {
         uint32_t r[32];
@@ -511,10 +514,11 @@ struct FlashTcSmem {
 // V [heads][rows][128] float32 (bf16-exact) -> [heads][ceil(rows/128)] tiles
 // V^T[128 dims][128 keys] bf16, K-major, 128B-swizzled: the B operand of O +=
 // P.V.
+template <typename T>
 __global__ void __launch_bounds__(256)
-presplit_vt_kernel(const float *__restrict__ V, int rows, uint8_t *__restrict__ tiles) {
+presplit_vt_kernel(const T *__restrict__ V, int rows, uint8_t *__restrict__ tiles) {
   const int h = blockIdx.y, tile = blockIdx.x, nt = gridDim.x;
-  const float *src = V + (int64_t)h * rows * 128;
+  const T *src = V + (int64_t)h * rows * 128;
   uint8_t *dst = tiles + ((int64_t)h * nt + tile) * FT_VTILE;
   // thread -> (dim, chunk of 8 keys); consecutive threads take consecutive dims
   for (int e = threadIdx.x; e < 128 * 16; e += 256) {
@@ -523,8 +527,8 @@ presplit_vt_kernel(const float *__restrict__ V, int rows, uint8_t *__restrict__ 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int k0 = tile * FT_KR + 8 * c + 2 * i;
-      const float a = k0 < rows ? __ldg(src + (int64_t)k0 * 128 + dim) : 0.f;
-      const float b = k0 + 1 < rows ? __ldg(src + (int64_t)(k0 + 1) * 128 + dim) : 0.f;
+      const float a = k0 < rows ? (float)src[(int64_t)k0 * 128 + dim] : 0.f;
+      const float b = k0 + 1 < rows ? (float)src[(int64_t)(k0 + 1) * 128 + dim] : 0.f;
       const __nv_bfloat162 v2 = __floats2bfloat162_rn(a, b);
       w[i] = *reinterpret_cast<const uint32_t *>(&v2);
     }
@@ -819,7 +823,7 @@ int launch_flash_tc(const float *Qs, const float *Kr, const float *V, int heads,
   if (e != cudaSuccess) return cuda_status(e, "attention tile scratch");
   presplit_sw128_kernel<TC_ROWS><<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
   presplit_sw128_kernel<FT_KR><<<dim3(nkt, kv_heads), 256, 0, st>>>(Kr, n_k, kt, ksc);
-  presplit_vt_kernel<<<dim3(nkt, kv_heads), 256, 0, st>>>(V, n_k, vt);
+  presplit_vt_kernel<float><<<dim3(nkt, kv_heads), 256, 0, st>>>(V, n_k, vt);
   const int smem = (int)sizeof(FlashTcSmem) + 1024;
   cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   flash_tc_kernel<<<dim3(nqt, heads), FT_THREADS, smem, st>>>(qt, qsc, kt, ksc, vt, heads / kv_heads, n_q, n_k,
@@ -831,6 +835,131 @@ int launch_flash_tc(const float *Qs, const float *Kr, const float *V, int heads,
   cudaFreeAsync(qsc, st);
   cudaFreeAsync(ksc, st);
   if (le != cudaSuccess) return cuda_status(le, "flash_tc_kernel");
+  return ANTKV_OK;
+}
+
+
+// ============================================================================
+// Fused prefill front end for bf16 inputs: RoPE (float64-reduced angles, as
+// rope_rotate_kernel), the 1/sqrt(d) query scale and the fp16 hi/lo split of
+// power-of-two-scaled 128-row tiles in one pass from the bf16 rows, plus the
+// pre-RoPE query norms; V goes straight to its bf16 V^T tiles.  The attention
+// and anchor-score kernels then share the same Q and K tiles.
+__global__ void __launch_bounds__(256)
+presplit_rope_kernel(const __nv_bfloat16 *__restrict__ X, const int64_t *__restrict__ positions, int heads_per_b,
+                     int rows, double theta, float scale, uint8_t *__restrict__ tiles, float *__restrict__ scales,
+                     float *__restrict__ norms) {
+  constexpr int PER = TC_ROWS * 16 / 256;   // (row, 8-element chunk) items per thread
+  __shared__ double freq[64];
+  __shared__ float red[8];
+  const int h = blockIdx.y, tile = blockIdx.x, nt = gridDim.x;
+  const int b = h / heads_per_b;
+  const __nv_bfloat16 *src = X + (int64_t)h * rows * 128;
+  if (threadIdx.x < 64) freq[threadIdx.x] = rope_freq(theta, threadIdx.x, 128);
+  __syncthreads();
+  // item e = threadIdx.x + 256 j -> row e / 16, chunk e % 16 (16 lanes per row)
+  float y[PER][8];
+  float mx = 0.f;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int e = threadIdx.x + 256 * j, r = e >> 4, c = e & 15, gr = tile * TC_ROWS + r;
+    float nrm = 0.f;
+    if (gr < rows) {
+      const uint4 raw = *reinterpret_cast<const uint4 *>(src + (int64_t)gr * 128 + 8 * c);
+      const __nv_bfloat162 *p2 = reinterpret_cast<const __nv_bfloat162 *>(&raw);
+      const double pos = (double)positions[(int64_t)b * rows + gr];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(p2[k]);
+        nrm = fmaf(x.x, x.x, fmaf(x.y, x.y, nrm));
+        float cs, sn;
+        rope_cs(pos * freq[4 * c + k], cs, sn);
+        y[j][2 * k] = (x.x * cs - x.y * sn) * scale;
+        y[j][2 * k + 1] = (x.x * sn + x.y * cs) * scale;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[j][k] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mx = fmaxf(mx, fabsf(y[j][k]));
+    if (norms) {
+#pragma unroll
+      for (int o = 8; o >= 1; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+      if (c == 0 && gr < rows) norms[(int64_t)h * rows + gr] = sqrtf(nrm);
+    }
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  const float sc = tc_pow2_scale(mx);
+  if (threadIdx.x == 0) scales[(int64_t)h * nt + tile] = sc;
+  uint8_t *dst = tiles + ((int64_t)h * nt + tile) * TC_TILE;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int e = threadIdx.x + 256 * j, r = e >> 4, c = e & 15;
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float p = y[j][2 * k] * sc, q = y[j][2 * k + 1] * sc;
+      const __half ph = __float2half_rn(p), qh = __float2half_rn(q);
+      const __half pl = __float2half_rn(p - __half2float(ph)), ql = __float2half_rn(q - __half2float(qh));
+      __half2 hh = __halves2half2(ph, qh), ll = __halves2half2(pl, ql);
+      hi[k] = *reinterpret_cast<uint32_t *>(&hh);
+      lo[k] = *reinterpret_cast<uint32_t *>(&ll);
+    }
+    const uint32_t off = sw128_off<>(r, 8 * c);
+    *reinterpret_cast<uint4 *>(dst + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4 *>(dst + TC_PART + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// Causal prefill of bf16 rows, d = 128: (O, M, L, ||q||) and the GQA-summed
+// anchor scores from one set of tiles.  B is folded into the head index.
+int prefill_tc_fused(const void *Q, const void *K, const void *V, int dtype, const int64_t *positions, int B,
+                     int Hq, int Hkv, int n, int d, double theta, float *O, float *M, float *L, float *qn,
+                     float *ans_k, float *ans_v, cudaStream_t st) {
+  if (d != 128 || dtype != ANTKV_BF16) return ANTKV_EUNSUPPORTED;
+  if (getenv("ANTKV_NO_TCGEN05")) return ANTKV_EUNSUPPORTED;
+  if ((int64_t)B * n == 0) return ANTKV_OK;
+  const int heads = B * Hq, kv_heads = B * Hkv, nt = ceil_div(n, TC_ROWS), group = Hq / Hkv;
+  uint8_t *qt = nullptr, *kt = nullptr, *vt = nullptr;
+  float *qsc = nullptr, *ksc = nullptr;
+  float2 *stats = nullptr;
+  cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * nt * TC_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&kt, (size_t)kv_heads * nt * TC_TILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&vt, (size_t)kv_heads * nt * FT_VTILE, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * nt, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nt, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&stats, sizeof(float2) * (size_t)heads * nt * TC_ROWS, st);
+  if (e != cudaSuccess) return cuda_status(e, "prefill tile scratch");
+  const __nv_bfloat16 *Qb = reinterpret_cast<const __nv_bfloat16 *>(Q);
+  const __nv_bfloat16 *Kb = reinterpret_cast<const __nv_bfloat16 *>(K);
+  presplit_rope_kernel<<<dim3(nt, heads), 256, 0, st>>>(Qb, positions, Hq, n, theta, 1.f / sqrtf(128.f), qt,
+                                                        qsc, qn);
+  presplit_rope_kernel<<<dim3(nt, kv_heads), 256, 0, st>>>(Kb, positions, Hkv, n, theta, 1.f, kt, ksc, nullptr);
+  presplit_vt_kernel<__nv_bfloat16><<<dim3(nt, kv_heads), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16 *>(V), n, vt);
+  const int fsmem = (int)sizeof(FlashTcSmem) + 1024;
+  cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fsmem);
+  flash_tc_kernel<<<dim3(nt, heads), FT_THREADS, fsmem, st>>>(qt, qsc, kt, ksc, vt, group, n, n, 1, O, L, M);
+  const int64_t ns = (int64_t)heads * nt * TC_ROWS;
+  ans_tc_stats_kernel<<<(unsigned)((ns + 255) / 256), 256, 0, st>>>(M, L, qn, heads, n, nt * TC_ROWS, stats);
+  const int asmem = (int)sizeof(AnsTcSmem) + 1024;
+  cudaFuncSetAttribute(ans_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, asmem);
+  ans_tc_kernel<<<dim3(nt, kv_heads), TC_THREADS, asmem, st>>>(qt, qsc, kt, ksc, stats, group, group, n, n, 1,
+                                                               ans_k, ans_v);
+  const cudaError_t le = cudaGetLastError();
+  cudaFreeAsync(qt, st);
+  cudaFreeAsync(kt, st);
+  cudaFreeAsync(vt, st);
+  cudaFreeAsync(qsc, st);
+  cudaFreeAsync(ksc, st);
+  cudaFreeAsync(stats, st);
+  if (le != cudaSuccess) return cuda_status(le, "fused prefill kernels");
   return ANTKV_OK;
 }
 
