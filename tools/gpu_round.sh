@@ -10,11 +10,14 @@ python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_o
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 if [ "${NCU:-1}" = 1 ]; then
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
       --log-file gpurun_out/launches_$TAG.csv \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu launches rc=$?"
   ncu --set full --clock-control none --import-source on -k regex:decode_fast -s 64 -c 1 \
       -o gpurun_out/decode_fast_$TAG -f \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:'flash_tc|ans_tc' -c 2 \
+      -o gpurun_out/prefill_tc_$TAG -f \
+      python tools/flash_tc_once.py 32768 > gpurun_out/ncu_prefill_$TAG.log 2>&1; echo "ncu prefill rc=$?"
 fi
 tail -c 2500 gpurun_out/bench_$TAG.json; echo; cat gpurun_out/bench_ref_$TAG.json; tail -3 gpurun_out/pytest_gpu_$TAG.log
