@@ -576,6 +576,9 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
   const uint8_t *Vg = Vt + (int64_t)hk * nkt * FT_VTILE;
 
   if (warp == 0) {                  // ---- producer: K and V^T rings, in tile order
+#ifdef FT_EXP_NOLOAD
+    if (false)
+#endif
     for (int t = 0; t < T; ++t) {
       const int st = t % FT_NS, ph = ((t / FT_NS) - 1) & 1;
       if (t >= FT_NS) tc_wait(tc_smem(&sm.kempty[st]), ph);
@@ -601,7 +604,9 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
     for (int t = 0; t <= T; ++t) {
       if (t < T) {                  // S(t) = Q . K_t^T into buffer t & 1
         const int b = t & 1, st = t % FT_NS;
+#ifndef FT_EXP_NOLOAD
         tc_wait(tc_smem(&sm.kfull[st]), (t / FT_NS) & 1);
+#endif
         // buffer b still holds P(t-2), read by P.V(t-2): that MMA was issued
         // before this one and tcgen05.mma executes in issue order, so no wait
         tc_fence_after();
@@ -622,7 +627,9 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       }
       if (t >= 1) {                 // O += P(t-1) . V_{t-1}
         const int u = t - 1, b = u & 1, st = u % FT_NS;
+#ifndef FT_EXP_NOLOAD
         tc_wait(tc_smem(&sm.vfull[st]), (u / FT_NS) & 1);
+#endif
         tc_wait(tc_smem(&sm.pfull[b]), (u >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
