@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                   help="N > 1: shard partials over peer memory (default) or NCCL all-gather")
     p.add_argument("--no-prefill", action="store_true", help="skip the prefill timing")
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     return p.parse_args()
@@ -274,9 +276,23 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_19505_b200 import _lib
-    from paper_2506_19505_b200.parallel import gather_partials, lse_merge
+    from paper_2506_19505_b200.parallel import PeerExchange, gather_partials, lse_merge
     _lib.load()
     caches, cfg = build_layers(args, rank, world, torch)
+    # N > 1: partials travel over peer memory (the decode launch stores them
+    # into every rank's receive slots, antkv_lse_merge_wait merges); NCCL
+    # all-gather if the buffers cannot be mapped (--exchange nccl forces it)
+    exchange, exchange_kind = None, "none"
+    if world > 1:
+        exchange_kind = "nccl"
+        # (the one-device functional check keeps NCCL/gloo: ranks sharing a GPU
+        # must not spin on each other's flags)
+        if args.exchange == "p2p" and not single:
+            try:
+                exchange = PeerExchange(args.batch * HQ, D)
+                exchange_kind = "p2p"
+            except Exception as exc:  # noqa: BLE001 (reported in the JSON line)
+                print(f"peer exchange unavailable ({exc}); NCCL all-gather", file=sys.stderr)
     L, B = args.layers, args.batch
     n0 = caches[0].token_count
     is_tail = rank == world - 1
@@ -296,7 +312,13 @@ def run_ours(args):
             cache.step_device(qs[s, l], ks[s, l], vs[s, l], qpos[s], out)
             return out
         # sequence shards: the tail appends / attends / evicts in one fused
-        # launch, the other shards attend; (o, lse) all-gathered and merged
+        # launch, the other shards attend; (o, lse) exchanged and merged
+        if exchange is not None:
+            exchange.advance()
+            cache.step_publish(qs[s, l], ks[s, l] if is_tail else None, vs[s, l] if is_tail else None,
+                               qpos[s], out, lse, exchange)
+            exchange.merge(merged.view(-1, D))
+            return merged
         if is_tail:
             cache.step_device(qs[s, l], ks[s, l], vs[s, l], qpos[s], out, lse)
         else:
@@ -402,6 +424,11 @@ def run_ours(args):
         for l in range(L):
             if world == 1:
                 caches[l].step_device(dq[l], dk[l], dv[l], p_dev, o_dev[l])
+            elif exchange is not None:
+                exchange.advance()
+                caches[l].step_publish(dq[l], dk[l] if is_tail else None, dv[l] if is_tail else None,
+                                       p_dev, out, lse, exchange)
+                exchange.merge(o_dev[l].view(-1, D))
             else:
                 if is_tail:
                     caches[l].step_device(dq[l], dk[l], dv[l], p_dev, out, lse)
@@ -465,6 +492,7 @@ def run_ours(args):
                                     "decode-attention call) x GPUs (weak scaling)",
                 "model_tok_s": B / (ms / 1e3),
                 "launch": "CUDA graph per step" if use_graph else "eager",
+                "exchange": exchange_kind,
             },
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "kernel": "decode attention (split-KV + combine)",
@@ -477,7 +505,9 @@ def run_ours(args):
                     "d2h_bytes_per_step": outh.numel() * 4, "ms_per_step": e2e_ms,
                     "path": ("QuantizedKVCache.step_device per layer (antkv_decode_step)" if world == 1
                              else "per layer: fused step on the tail shard / attention on the others, "
-                                  "NCCL all-gather of (o, lse), antkv_lse_combine")
+                                  + ("partials stored into every rank's slots by the same launch over "
+                                     "peer memory, antkv_lse_merge_wait" if exchange is not None
+                                     else "NCCL all-gather of (o, lse), antkv_lse_combine"))
                             + " with pinned-host q/k/v H2D and output D2H inside the timed region"
                             + (", CUDA-graph replay" if use_graph else "")},
             # our kernels per layer-step on rank 0: the fused step (N=1) or attention +
@@ -489,6 +519,9 @@ def run_ours(args):
             "encode": enc,
             "prefill": pre,
         }
+    if exchange is not None:
+        barrier()
+        exchange.close()
     return result, caches
 
 

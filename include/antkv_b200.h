@@ -33,6 +33,8 @@
  *                             kernels.assign_nearest (_ckernels.pyx:134-163)
  *   antkv_eval_pair_l1     <- harness.per_token_errors / anchors.k_perturbation_bound
  *                             pair sums (harness.py:111-134, anchors.py:152-186)
+ *   antkv_decode_step_publish / antkv_lse_merge_wait / antkv_ipc_* / antkv_p2p_*
+ *                          <- (new) peer-memory exchange of sequence-shard partials
  *   antkv_lse_combine      <- (new) split-KV / sequence-shard log-sum-exp merge
  */
 #ifndef ANTKV_B200_H
@@ -309,6 +311,35 @@ ANTKV_API int antkv_kmeans_update_f64(const int64_t *offsets, const double *Xs,
 ANTKV_API int antkv_eval_pair_l1(const double *Y, const double *X, const double *Z,
                                  const double *W, const double *P, const double *R, int n_i,
                                  int n_j, int d, int i_from_j0, double *out, void *stream);
+
+/* Sequence-shard exchange over peer memory (replaces the NCCL all-gather of
+ * the shards' (o, lse) partials).  Every rank owns receive
+ * buffers (antkv_p2p_alloc: o [P][B*Hq][d] | lse [P][B*Hq] | flags [P]
+ * uint32, zeroed) and maps its peers' with antkv_ipc_get_handle (64-byte
+ * handle) / antkv_ipc_open_handle.
+ * antkv_decode_step_publish: antkv_decode_step (k == NULL: attention only)
+ *   whose combined partial is also stored, by the same launch on the fused
+ *   path, into slot `rank` of each of the n_dst receive buffers (dst_o /
+ *   dst_lse / dst_flags: DEVICE arrays of n_dst base pointers); then each
+ *   destination's flags[rank] is set to `seq` with a system-scope release.
+ *   lse must be non-NULL.
+ * antkv_lse_merge_wait: waits (system-scope acquire) until flags[p] reached
+ *   seq for every p < P, then merges the P partials (as antkv_lse_combine).
+ *   seq advances by one per step (compared modulo 2^32). */
+ANTKV_API int antkv_p2p_alloc(int64_t bytes, void **ptr);
+ANTKV_API int antkv_p2p_free(void *ptr);
+ANTKV_API int antkv_ipc_get_handle(const void *ptr, void *handle);
+ANTKV_API int antkv_ipc_open_handle(const void *handle, void **ptr);
+ANTKV_API int antkv_ipc_close_handle(void *ptr);
+ANTKV_API int antkv_decode_step_publish(const antkv_cache_desc *c, const void *q, const void *k,
+                                        const void *v, int dtype, const int64_t *qpos, float *out,
+                                        float *lse, void *workspace, int64_t workspace_bytes,
+                                        int splits, int fast, float *const *dst_o,
+                                        float *const *dst_lse, unsigned *const *dst_flags,
+                                        int n_dst, int rank, unsigned seq, void *stream);
+ANTKV_API int antkv_lse_merge_wait(const float *o, const float *lse, const unsigned *flags, int P,
+                                   unsigned seq, int64_t rows, int d, float *out, float *lse_out,
+                                   void *stream);
 
 /* Debug: per-CTA timeline of the last fast-decode launch when the process
  * runs with ANTKV_TRACE=1 (8 words per CTA); returns words copied. */

@@ -61,6 +61,14 @@ _SIGS = {
     "antkv_eval_pair_l1": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "antkv_prefill_attention_scores": (_i, [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp,
                                             _vp, _vp, _vp, _vp]),
+    "antkv_p2p_alloc": (_i, [_i64, _vp]),
+    "antkv_p2p_free": (_i, [_vp]),
+    "antkv_ipc_get_handle": (_i, [_vp, _vp]),
+    "antkv_ipc_open_handle": (_i, [_vp, _vp]),
+    "antkv_ipc_close_handle": (_i, [_vp]),
+    "antkv_decode_step_publish": (_i, [ctypes.POINTER(CacheDesc), _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i64, _i, _i, _vp, _vp,
+                                       _vp, _i, _i, ctypes.c_uint32, _vp]),
+    "antkv_lse_merge_wait": (_i, [_vp, _vp, _vp, _i, ctypes.c_uint32, _i64, _i, _vp, _vp, _vp]),
     "antkv_prefill_attention_block": (_i, [_vp, _vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _i, _i, _d, _i,
                                            _vp, _vp, _vp, _vp, _vp]),
     "antkv_prefill_anchor_scores_block": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i,

@@ -370,6 +370,19 @@ class QuantizedKVCache:
                                          _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws), ws.numel(),
                                          self.splits, int(self._use_fast(fast)), _lib.stream()))
 
+    def step_publish(self, q, k, v, qpos, out, lse, exchange, fast=None):
+        """step_device (k is None: attention only) whose partial (out, lse)
+        is also written into this rank's slot of every receive buffer of the
+        PeerExchange, then flagged (antkv_decode_step_publish)."""
+        ws = self._workspace()
+        lib = _lib.load(check_device=False)
+        seq = exchange.seq
+        _lib.check(lib.antkv_decode_step_publish(
+            ctypes.byref(self._desc), _lib.ptr(q), _lib.ptr(k), _lib.ptr(v), _lib.dtype_tag(q),
+            _lib.ptr(qpos), _lib.ptr(out), _lib.ptr(lse), _lib.ptr(ws), ws.numel(), self.splits,
+            int(self._use_fast(fast)), _lib.ptr(exchange.dst_o), _lib.ptr(exchange.dst_lse),
+            _lib.ptr(exchange.dst_flags), exchange.n_dst, exchange.rank, seq, _lib.stream()))
+
     def attend_device(self, q, qpos, out, lse=None, fast=None):
         """Attention only (no append/evict): used by sequence shards."""
         ws = self._workspace()

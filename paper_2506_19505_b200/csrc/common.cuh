@@ -38,6 +38,19 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // stream was for another cache.
 const void *previous_cache_on_stream(cudaStream_t st, const void *key);
 
+// Destinations of a sequence shard's partial (o, lse): n receive buffers
+// (device arrays of n base pointers, one per peer; this rank's slot is
+// `rank`: o [P][rows][d], lse [P][rows], flags [P]) and the release value.
+struct PublishArgs {
+  float *const *o;
+  float *const *lse;
+  unsigned *const *flag;
+  int n, rank;
+  int64_t rows;
+  int *cnt;        // device counter of finished heads / rows (self-resetting)
+  unsigned seq;
+};
+
 // Stream-ordered scratch (cudaMallocAsync from the device's default pool).
 // The first call per device raises the pool's release threshold so freed
 // scratch stays mapped for the next call instead of being returned to the

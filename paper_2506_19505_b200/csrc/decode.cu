@@ -18,7 +18,7 @@ __device__ __forceinline__ int load_code_unit(const antkv_cache_desc &c, int64_t
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
                        const void *vnew, int kvdtype, const int64_t *qpos, float *out, float *lse,
                        float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
-                       cudaStream_t st);
+                       cudaStream_t st, const PublishArgs *pub = nullptr);
 int decode_fast_supported(const antkv_cache_desc &c);
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits);
 
@@ -248,6 +248,60 @@ __global__ void lse_combine_kernel(const float *__restrict__ o, const float *__r
   if (lse_out && threadIdx.x == 0) lse_out[row] = M + logf(W);
 }
 
+// Generic-path publish: copy the rank's partial rows into each peer's slot,
+// then the last CTA releases the slot flags (system scope).
+__global__ void publish_partial_kernel(const float *__restrict__ out, const float *__restrict__ lse, int d,
+                                       PublishArgs pub) {
+  const int64_t row = blockIdx.x, prow = (int64_t)pub.rank * pub.rows + row;
+  for (int p = 0; p < pub.n; ++p) {
+    for (int t = threadIdx.x; t < d; t += blockDim.x) pub.o[p][prow * d + t] = out[row * d + t];
+    if (threadIdx.x == 0) pub.lse[p][prow] = lse[row];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(pub.cnt, 1) == (int)pub.rows - 1) {
+    *pub.cnt = 0;
+    __threadfence_system();
+    for (int p = 0; p < pub.n; ++p)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pub.flag[p] + pub.rank), "r"(pub.seq)
+                   : "memory");
+  }
+}
+
+// Waits until every slot's flag reached `seq` (system-scope acquire), then
+// merges the P partials like lse_combine_kernel.  Slots are read through L2
+// (__ldcg): peers write them over NVLink every step.
+__global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *__restrict__ lse,
+                                      const unsigned *__restrict__ flags, int P, unsigned seq,
+                                      int64_t rows, int d, float *__restrict__ out,
+                                      float *__restrict__ lse_out) {
+  if (threadIdx.x < P) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
+      if ((int)(v - seq) < 0) __nanosleep(64);
+    } while ((int)(v - seq) < 0);
+  }
+  __syncthreads();
+  const int64_t row = blockIdx.x;
+  float M = -INFINITY;
+  for (int p = 0; p < P; ++p) M = fmaxf(M, __ldcg(lse + p * rows + row));
+  float W = 0.f;
+  for (int p = 0; p < P; ++p) {
+    const float l = __ldcg(lse + p * rows + row);
+    if (l != -INFINITY) W += __expf(l - M);
+  }
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    float acc = 0.f;
+    for (int p = 0; p < P; ++p) {
+      const float l = __ldcg(lse + p * rows + row);
+      if (l != -INFINITY) acc = fmaf(__expf(l - M), __ldcg(o + (p * rows + row) * d + t), acc);
+    }
+    out[row * d + t] = acc / W;
+  }
+  if (lse_out && threadIdx.x == 0) lse_out[row] = M + logf(W);
+}
+
 static size_t generic_smem(const antkv_cache_desc &c, int gq, bool cb_smem) {
   size_t s = sizeof(double) * (c.d / 2) + sizeof(float) * (gq * c.d + gq * DG_T + 8 * gq) +
              sizeof(int) * (DG_T + DG_T * c.groups);
@@ -298,9 +352,10 @@ static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
 
 using namespace antkv;
 
-// tickets [B*Hkv] + [B] and the per-head cache-update plan [B*Hkv][4]
+// tickets [B*Hkv] + [B], the per-head cache-update plans [B*Hkv][kPlanWords]
+// and the publish counter [1]
 static int64_t counter_bytes(const antkv_cache_desc &c) {
-  return (int64_t)(c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv) * 4;
+  return (int64_t)(c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv + 1) * 4;
 }
 
 static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
@@ -319,7 +374,7 @@ extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int s
 static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, const void *knew,
                           const void *vnew, int kvdtype, const int64_t *qpos, float *out,
                           float *lse, void *workspace, int64_t workspace_bytes, int splits,
-                          bool use_fast, cudaStream_t st) {
+                          bool use_fast, cudaStream_t st, const PublishArgs *pub = nullptr) {
   const int used = planned_splits(*c, splits, use_fast);
   const int64_t rows = (int64_t)c->B * c->Hq;
   ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits), "decode workspace too small");
@@ -331,7 +386,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   if (!use_fast) previous_cache_on_stream(st, c->codes);   // (the fast launch records itself)
   if (use_fast)
     return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
-                              splits, st);
+                              splits, st, pub);
   const int gq = c->Hq / c->Hkv;
   int rc;
   switch (gq) {
@@ -397,5 +452,67 @@ extern "C" int antkv_lse_combine(const float *o, const float *lse, int P, int64_
   if (rows == 0) return ANTKV_OK;
   lse_combine_kernel<<<(unsigned)rows, 128, 0, as_stream(stream)>>>(o, lse, P, rows, d, out, lse_out);
   ANTKV_LAUNCH_CHECK("lse_combine_kernel");
+  return ANTKV_OK;
+}
+
+// ---------------------------------------------------------------- peer exchange
+// The counter for publish completion lives after the plans in the workspace.
+static int *publish_counter(const antkv_cache_desc &c, void *workspace, int64_t workspace_bytes) {
+  int *cnt = reinterpret_cast<int *>(reinterpret_cast<char *>(workspace) + workspace_bytes - 256 -
+                                     counter_bytes(c));
+  return cnt + c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv;
+}
+
+extern "C" int antkv_decode_step_publish(const antkv_cache_desc *c, const void *q, const void *k,
+                                         const void *v, int dtype, const int64_t *qpos, float *out,
+                                         float *lse, void *workspace, int64_t workspace_bytes,
+                                         int splits, int fast, float *const *dst_o,
+                                         float *const *dst_lse, unsigned *const *dst_flags, int n_dst,
+                                         int rank, unsigned seq, void *stream) {
+  int rc = check_decode_args(c, q, out);
+  if (rc) return rc;
+  ANTKV_REQUIRE(lse != nullptr, "publishing needs lse");
+  ANTKV_REQUIRE(n_dst >= 1 && dst_o != nullptr && dst_lse != nullptr && dst_flags != nullptr,
+                "publishing needs the destination pointer arrays");
+  ANTKV_REQUIRE(rank >= 0, "bad rank");
+  ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits), "decode workspace too small");
+  cudaStream_t st = as_stream(stream);
+  PublishArgs pub;
+  pub.o = dst_o;
+  pub.lse = dst_lse;
+  pub.flag = dst_flags;
+  pub.n = n_dst;
+  pub.rank = rank;
+  pub.rows = (int64_t)c->B * c->Hq;
+  pub.cnt = publish_counter(*c, workspace, workspace_bytes);
+  pub.seq = seq;
+  if (fast_ok(c, q, fast))   // one launch: attention (+ append / evict) + publish
+    return attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes,
+                          splits, true, st, &pub);
+  if (k) {
+    ANTKV_REQUIRE(v != nullptr, "null v");
+    rc = antkv_cache_append(c, k, v, dtype, qpos, stream);
+    if (rc) return rc;
+  }
+  rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
+                      workspace_bytes, splits, false, st);
+  if (rc) return rc;
+  if (k) {
+    rc = antkv_cache_evict(c, stream);
+    if (rc) return rc;
+  }
+  publish_partial_kernel<<<(unsigned)pub.rows, 128, 0, st>>>(out, lse, c->d, pub);
+  ANTKV_LAUNCH_CHECK("publish_partial_kernel");
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_lse_merge_wait(const float *o, const float *lse, const unsigned *flags, int P,
+                                    unsigned seq, int64_t rows, int d, float *out, float *lse_out,
+                                    void *stream) {
+  ANTKV_REQUIRE(P >= 1 && P <= 128 && d >= 1, "bad merge shape");
+  if (rows == 0) return ANTKV_OK;
+  lse_merge_wait_kernel<<<(unsigned)rows, 128, 0, as_stream(stream)>>>(o, lse, flags, P, seq, rows, d,
+                                                                       out, lse_out);
+  ANTKV_LAUNCH_CHECK("lse_merge_wait_kernel");
   return ANTKV_OK;
 }

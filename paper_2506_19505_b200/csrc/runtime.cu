@@ -1,5 +1,6 @@
 // Error reporting and device checks for the C ABI.
 #include <stdarg.h>
+#include <string.h>
 
 #include <mutex>
 #include <unordered_map>
@@ -84,4 +85,41 @@ extern "C" int antkv_device_check(int device) {
   }
   antkv::decode_fast_smem_base_ok();   // one-time probe, outside any stream capture
   return 1;
+}
+
+// ---------------------------------------------------------------- peer memory
+// Receive buffers for the sequence-shard exchange are plain cudaMalloc
+// allocations (an IPC handle maps a whole allocation), zero-filled.
+extern "C" int antkv_p2p_alloc(int64_t bytes, void **ptr) {
+  ANTKV_REQUIRE(bytes > 0 && ptr != nullptr, "bad p2p allocation");
+  cudaError_t e = cudaMalloc(ptr, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, (size_t)bytes);
+  return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "p2p buffer");
+}
+
+extern "C" int antkv_p2p_free(void *ptr) {
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "p2p buffer free");
+}
+
+extern "C" int antkv_ipc_get_handle(const void *ptr, void *handle) {
+  ANTKV_REQUIRE(ptr != nullptr && handle != nullptr, "null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(ptr));
+  if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+  memcpy(handle, &h, sizeof(h));
+  return ANTKV_OK;
+}
+
+extern "C" int antkv_ipc_open_handle(const void *handle, void **ptr) {
+  ANTKV_REQUIRE(ptr != nullptr && handle != nullptr, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "cudaIpcOpenMemHandle");
+}
+
+extern "C" int antkv_ipc_close_handle(void *ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? ANTKV_OK : cuda_status(e, "cudaIpcCloseMemHandle");
 }

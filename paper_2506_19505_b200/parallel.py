@@ -25,7 +25,8 @@ import torch.distributed as dist
 
 from . import _lib
 
-__all__ = ["shard_ranges", "gather_partials", "lse_merge", "ShardedDecoder", "RingTransport",
+__all__ = ["shard_ranges", "gather_partials", "lse_merge", "ShardedDecoder", "PeerExchange",
+           "RingTransport",
            "CudaPrefillOps", "merge_partial", "sharded_attention", "sharded_anchor_scores",
            "shard_candidates", "choose_anchors", "sharded_prefill"]
 
@@ -67,6 +68,84 @@ def lse_merge(o_all, lse_all, out=None, lse_out=None):
     return out
 
 
+class PeerExchange:
+    """Peer-memory exchange of the sequence-shard partials (the NCCL
+    all-gather replaced by NVLink stores from the decode kernel itself).
+
+    Every rank allocates receive buffers for all P slots (o [P][rows][d],
+    lse [P][rows], flags [P]); the CUDA IPC handles are all-gathered once and
+    each rank maps its peers' buffers.  A step: each rank's decode launch
+    stores its partial into its slot of every rank's buffers and releases the
+    slot flags with the step's sequence number (antkv_decode_step_publish);
+    each rank then merges locally once all flags reached it
+    (antkv_lse_merge_wait).  `local_slots` (no process group) emulates P
+    ranks inside one process on one buffer set, for tests."""
+
+    def __init__(self, rows, d, group=None, local_slots=None):
+        import ctypes
+        self.rows, self.d = int(rows), int(d)
+        if local_slots is not None:
+            self.P, self.rank, distributed = int(local_slots), 0, False
+        else:
+            self.P, self.rank, distributed = dist.get_world_size(group), dist.get_rank(group), True
+        P = self.P
+        self._sizes = (P * self.rows * self.d * 4, P * self.rows * 4, P * 4)
+        nbytes = sum(self._sizes)
+        lib = _lib.load()
+        base = ctypes.c_void_p()
+        _lib.check(lib.antkv_p2p_alloc(nbytes, ctypes.byref(base)))
+        self._own = base.value
+        self._mapped = []
+        bases = [self._own]
+        if distributed and P > 1:
+            h = (ctypes.c_ubyte * 64)()
+            _lib.check(lib.antkv_ipc_get_handle(ctypes.c_void_p(self._own), h))
+            handles = [None] * P
+            dist.all_gather_object(handles, bytes(h), group=group)
+            bases = []
+            for r in range(P):
+                if r == self.rank:
+                    bases.append(self._own)
+                    continue
+                ptr = ctypes.c_void_p()
+                hb = (ctypes.c_ubyte * 64).from_buffer_copy(handles[r])
+                _lib.check(lib.antkv_ipc_open_handle(hb, ctypes.byref(ptr)))
+                self._mapped.append(ptr.value)
+                bases.append(ptr.value)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        o_off, l_off = 0, self._sizes[0]
+        f_off = l_off + self._sizes[1]
+        self.dst_o = torch.tensor([b + o_off for b in bases], dtype=torch.int64, device=dev)
+        self.dst_lse = torch.tensor([b + l_off for b in bases], dtype=torch.int64, device=dev)
+        self.dst_flags = torch.tensor([b + f_off for b in bases], dtype=torch.int64, device=dev)
+        self.n_dst = len(bases)
+        self._recv = (self._own + o_off, self._own + l_off, self._own + f_off)
+        self.seq = 0
+
+    def advance(self):
+        """Start the next step (its flags carry the new sequence number)."""
+        self.seq = (self.seq + 1) & 0xFFFFFFFF
+        return self.seq
+
+    def merge(self, out, lse_out=None):
+        """Wait for every slot of this step, merge into out [rows, d] float32."""
+        o, l, f = self._recv
+        lib = _lib.load(check_device=False)
+        _lib.check(lib.antkv_lse_merge_wait(o, l, f, self.P, self.seq, self.rows, self.d, _lib.ptr(out),
+                                            _lib.ptr(lse_out), _lib.stream()))
+        return out
+
+    def close(self):
+        lib = _lib.load(check_device=False)
+        torch.cuda.synchronize()
+        for p in self._mapped:
+            lib.antkv_ipc_close_handle(p)
+        self._mapped = []
+        if self._own:
+            lib.antkv_p2p_free(self._own)
+            self._own = None
+
+
 class ShardedDecoder:
     """Decode driver for one rank's shard.
 
@@ -75,17 +154,29 @@ class ShardedDecoder:
     and evicts; every rank attends.  ``combine`` defaults to the GPU LSE merge;
     tests may pass another merge to exercise the collective on CPU/gloo."""
 
-    def __init__(self, cache, is_tail, group=None, combine=None):
+    def __init__(self, cache, is_tail, group=None, combine=None, exchange=None):
         self.cache = cache
         self.is_tail = is_tail
         self.group = group
         self.combine = combine or lse_merge
+        self.exchange = exchange
 
     def step(self, q, k, v, qpos, out_local, lse_local):
         """q [B, Hq, d], k/v [B, Hkv, d] (only used on the tail), qpos [B].
         The tail shard appends, attends and evicts in one fused launch
-        (antkv_decode_step with the log-sum-exp output); the others attend."""
+        (antkv_decode_step with the log-sum-exp output); the others attend.
+        With a PeerExchange the same launch publishes the partial to every
+        rank over peer memory and the merge waits on the slot flags; without
+        one the partials are all-gathered with NCCL."""
         c = self.cache
+        if self.exchange is not None:
+            ex = self.exchange
+            ex.advance()
+            c.step_publish(q, k if self.is_tail else None, v if self.is_tail else None, qpos,
+                           out_local, lse_local, ex)
+            if self.is_tail:
+                c._n += 1
+            return ex.merge(torch.empty_like(out_local).view(-1, out_local.shape[-1])).view_as(out_local)
         if self.is_tail:
             c.step_device(q, k, v, qpos, out_local, lse_local)
             c._n += 1

@@ -935,3 +935,60 @@ def test_tcgen05_prefill_kernels_vs_oracle(causal):
         ref_v[h // g] += vv
     assert rel(ak[0].cpu().numpy(), ref_k) < 1e-4
     assert rel(av[0].cpu().numpy(), ref_v) < 1e-4
+
+
+def test_peer_exchange_publish_and_merge_one_device():
+    """The peer-memory exchange of sequence-shard partials, two shards
+    emulated in one process on one receive buffer set: each shard's decode
+    launch publishes (o, lse) into its slot and releases its flag (fused
+    kernel for the tail shard's step, attention-only launch for the head
+    shard), the merge waits on both flags; outputs and anchors match the
+    single-cache decode, for both decode kernels."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.parallel import PeerExchange
+    vq = VqConfig.from_notation("d8m256")
+    Hq, Hkv, n, steps, W = 8, 2, 900, 12, 8
+    Q, K, V = qkv(91, Hq, Hkv, n + steps, 128, heavy=2)
+    ck, cv = codebooks(91, Hkv, 256, 8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    cfg = lambda w: CacheConfig(vq=vq, anchor_fraction=0.02, window_size=w)
+    for fast in (True, False):
+        ref = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+        ref.prefill(dev(Q[None, :, :n]), dev(K[None, :, :n]), dev(V[None, :, :n]), np.arange(n))
+        cut = 448
+        shards = []
+        for lo, hi, w in ((0, cut, 0), (cut, n, W)):
+            c = QuantizedKVCache(cfg(w), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq, token_offset=lo,
+                                 capacity=hi - lo + steps + 64, fast=fast)
+            loc = np.full((Hkv, 64), -1, dtype=np.int32)
+            for h in range(Hkv):
+                a = [j - lo for j in ref.anchor_indices_of(0, h) if lo <= j < hi]
+                loc[h, :len(a)] = a
+            c.Hq = Hq
+            c.build_from(dev(K[None, :, lo:hi]), dev(V[None, :, lo:hi]),
+                         torch.arange(lo, hi, device="cuda")[None], torch.from_numpy(loc).cuda()[None])
+            shards.append(c)
+        shards[1].tensors["hstate"][:, :, 0] = ref.config.budget_for(n)
+        ex = PeerExchange(Hq, 128, local_slots=2)
+        try:
+            for t in range(n, n + steps):
+                q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
+                want = ref.decode_step(q, k, v, t)
+                qpos = torch.tensor([t], device="cuda")
+                ex.advance()
+                for r, c in enumerate(shards):
+                    o = torch.empty((1, Hq, 128), device="cuda")
+                    l = torch.empty((1, Hq), device="cuda")
+                    ex.rank = r
+                    tail = r == 1
+                    c.step_publish(q, k if tail else None, v if tail else None, qpos, o, l, ex)
+                    if tail:
+                        c._n += 1
+                got = ex.merge(torch.empty((Hq, 128), device="cuda"))
+                assert rel(got.cpu().numpy(), want[0].cpu().numpy()) < 2e-2, (fast, t)
+        finally:
+            ex.close()
+        for h in range(Hkv):
+            merged = sorted([int(j) for j in shards[0].anchor_indices_of(0, h)] +
+                            [int(j) + cut for j in shards[1].anchor_indices_of(0, h)])
+            assert merged == [int(j) for j in ref.anchor_indices_of(0, h)]
