@@ -318,10 +318,10 @@ ANTKV_API int antkv_eval_pair_l1(const double *Y, const double *X, const double 
  * uint32, zeroed) and maps its peers' with antkv_ipc_get_handle (64-byte
  * handle) / antkv_ipc_open_handle.
  * antkv_decode_step_publish: antkv_decode_step (k == NULL: attention only)
- *   whose combined partial is also stored, by the same launch on the fused
- *   path, into slot `rank` of each of the n_dst receive buffers (dst_o /
- *   dst_lse / dst_flags: DEVICE arrays of n_dst base pointers); then each
- *   destination's flags[rank] is set to `seq` with a system-scope release.
+ *   whose combined partial is then stored into slot `rank` of each of the
+ *   n_dst receive buffers (dst_o / dst_lse / dst_flags: DEVICE arrays of
+ *   n_dst base pointers) by direct peer stores; then each destination's
+ *   flags[rank] is set to `seq` with a system-scope release.
  *   lse must be non-NULL.
  * antkv_lse_merge_wait: waits (system-scope acquire) until flags[p] reached
  *   seq for every p < P, then merges the P partials (as antkv_lse_combine).

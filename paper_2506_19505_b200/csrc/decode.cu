@@ -18,7 +18,7 @@ __device__ __forceinline__ int load_code_unit(const antkv_cache_desc &c, int64_t
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
                        const void *vnew, int kvdtype, const int64_t *qpos, float *out, float *lse,
                        float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
-                       cudaStream_t st, const PublishArgs *pub = nullptr);
+                       cudaStream_t st);
 int decode_fast_supported(const antkv_cache_desc &c);
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits);
 
@@ -353,9 +353,9 @@ static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
 using namespace antkv;
 
 // tickets [B*Hkv] + [B], the per-head cache-update plans [B*Hkv][kPlanWords]
-// and the publish counter [1]
+// and the publish counter [1] (padded to 4 words)
 static int64_t counter_bytes(const antkv_cache_desc &c) {
-  return (int64_t)(c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv + 1) * 4;
+  return (int64_t)(c.B * c.Hkv + c.B + kPlanWords * c.B * c.Hkv + 4) * 4;   // +4: keeps 16-byte alignment
 }
 
 static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
@@ -374,7 +374,7 @@ extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int s
 static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, const void *knew,
                           const void *vnew, int kvdtype, const int64_t *qpos, float *out,
                           float *lse, void *workspace, int64_t workspace_bytes, int splits,
-                          bool use_fast, cudaStream_t st, const PublishArgs *pub = nullptr) {
+                          bool use_fast, cudaStream_t st) {
   const int used = planned_splits(*c, splits, use_fast);
   const int64_t rows = (int64_t)c->B * c->Hq;
   ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits), "decode workspace too small");
@@ -386,7 +386,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   if (!use_fast) previous_cache_on_stream(st, c->codes);   // (the fast launch records itself)
   if (use_fast)
     return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
-                              splits, st, pub);
+                              splits, st);
   const int gq = c->Hq / c->Hkv;
   int rc;
   switch (gq) {
@@ -486,20 +486,26 @@ extern "C" int antkv_decode_step_publish(const antkv_cache_desc *c, const void *
   pub.rows = (int64_t)c->B * c->Hq;
   pub.cnt = publish_counter(*c, workspace, workspace_bytes);
   pub.seq = seq;
-  if (fast_ok(c, q, fast))   // one launch: attention (+ append / evict) + publish
-    return attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes,
-                          splits, true, st, &pub);
-  if (k) {
-    ANTKV_REQUIRE(v != nullptr, "null v");
-    rc = antkv_cache_append(c, k, v, dtype, qpos, stream);
+  // the step (one fused launch on the fast path), then the partial's rows go
+  // to every peer slot and the flags are released (a second, tiny launch: the
+  // fused decode kernel is kept exactly as timed)
+  if (fast_ok(c, q, fast)) {
+    rc = attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes, splits,
+                        true, st);
     if (rc) return rc;
-  }
-  rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
-                      workspace_bytes, splits, false, st);
-  if (rc) return rc;
-  if (k) {
-    rc = antkv_cache_evict(c, stream);
+  } else {
+    if (k) {
+      ANTKV_REQUIRE(v != nullptr, "null v");
+      rc = antkv_cache_append(c, k, v, dtype, qpos, stream);
+      if (rc) return rc;
+    }
+    rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
+                        workspace_bytes, splits, false, st);
     if (rc) return rc;
+    if (k) {
+      rc = antkv_cache_evict(c, stream);
+      if (rc) return rc;
+    }
   }
   publish_partial_kernel<<<(unsigned)pub.rows, 128, 0, st>>>(out, lse, c->d, pub);
   ANTKV_LAUNCH_CHECK("publish_partial_kernel");

@@ -199,10 +199,6 @@ struct StepArgs {
   int early;               // the previous kernel in the stream wrote no state of this
                            // cache: read cache state before griddepcontrol.wait
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
-  // sequence-shard exchange (antkv_decode_step_publish): the combined partial
-  // (o, lse) also goes to slot `rank` of a peer's receive buffers, then that
-  // slot's flag is released with value pub_seq; pub_cnt counts finished heads
-  PublishArgs pub;         // pub.n == 0: no exchange
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1066,14 +1062,9 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       M = mc;
     }
     const float inv = 1.f / L;
-    const float4 ov = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    *reinterpret_cast<float4 *>(a.out + row * 128 + d4) = ov;
+    *reinterpret_cast<float4 *>(a.out + row * 128 + d4) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
     if (lane == 0 && a.lse) a.lse[row] = M + logf(L);
-    for (int p = 0; p < a.pub.n; ++p) {   // the same values into each peer's slot (NVLink stores)
-      const int64_t prow = (int64_t)a.pub.rank * a.pub.rows + row;
-      *reinterpret_cast<float4 *>(a.pub.o[p] + prow * 128 + d4) = ov;
-      if (lane == 0) a.pub.lse[p][prow] = M + logf(L);
-    }
     if (a.trace && threadIdx.x == 0) {
       unsigned long long *o =
           a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
@@ -1087,18 +1078,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       o[11] = clock64() - sm.t0clk;
     }
     a.cnt[bh] = 0;
-  }
-  if (a.pub.n > 0) {
-    // every head's rows are out: the last head's CTA releases the flags
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(a.pub.cnt, 1) == c.B * c.Hkv - 1) {
-      *a.pub.cnt = 0;
-      __threadfence_system();
-      for (int p = 0; p < a.pub.n; ++p)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.pub.flag[p] + a.pub.rank), "r"(a.pub.seq)
-                     : "memory");
-    }
   }
 }
 
@@ -1175,13 +1154,8 @@ namespace antkv {
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,
                        const void *vnew, int kvdtype, const int64_t *qpos, float *out, float *lse,
                        float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
-                       cudaStream_t st, const PublishArgs *pub) {
+                       cudaStream_t st) {
   StepArgs a;
-  if (pub) {
-    a.pub = *pub;
-  } else {
-    memset(&a.pub, 0, sizeof(a.pub));
-  }
   a.q = q;
   a.knew = knew;
   a.vnew = vnew;
