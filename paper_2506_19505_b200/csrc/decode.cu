@@ -32,7 +32,8 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
   const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x, splits = gridDim.x;
   const int64_t bh = (int64_t)b * c.Hkv + h;
   double *sFreq = reinterpret_cast<double *>(smraw);                // [d/2]
-  float *sQ = reinterpret_cast<float *>(sFreq + d / 2);             // [GQ][d]
+  float2 *sRot = reinterpret_cast<float2 *>(sFreq + d / 2);         // [d/2][T]: R(t) of thread t
+  float *sQ = reinterpret_cast<float *>(sRot + (d / 2) * DG_T);     // [GQ][d] q in the chunk frame
   float *sS = sQ + GQ * d;                                          // [GQ][T]
   float *sRed = sS + GQ * DG_T;                                     // [GQ][4] + [GQ][4]
   int *sSrc = reinterpret_cast<int *>(sRed + 8 * GQ);               // [T] source tag
@@ -43,6 +44,14 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
   const float *cbV = CB_SMEM ? sCbV : c.codebook_v + (int64_t)h * c.m * dsub;
 
   for (int i = threadIdx.x; i < d / 2; i += DG_T) sFreq[i] = rope_freq(c.theta_base, i, d);
+  __syncthreads();
+  // residual rotations: thread t rotates a key t positions after the chunk
+  // frame by R(t) (position-independent, so computed once per CTA)
+  for (int p = 0; p < d / 2; ++p) {
+    float cs, sn;
+    rope_cs(static_cast<double>(threadIdx.x) * sFreq[p], cs, sn);
+    sRot[p * DG_T + threadIdx.x] = make_float2(cs, sn);
+  }
   if (CB_SMEM) {
     const float *gk = c.codebook_k + (int64_t)h * c.m * dsub;
     const float *gv = c.codebook_v + (int64_t)h * c.m * dsub;
@@ -52,18 +61,8 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
     }
   }
   __syncthreads();
-  // rotated, scaled queries of the group (attention.py:89-106 at p_q)
-  const double pq = static_cast<double>(qpos[b]);
   const float scale = rsqrtf(static_cast<float>(d));
-  for (int i = threadIdx.x; i < GQ * (d / 2); i += DG_T) {
-    const int hh = i / (d / 2), p = i % (d / 2);
-    const int64_t qb = ((int64_t)b * c.Hq + h * GQ + hh) * d;
-    float x0 = load_elem(q, qb + 2 * p, dtype), x1 = load_elem(q, qb + 2 * p + 1, dtype);
-    float cs, sn;
-    rope_cs(pq * sFreq[p], cs, sn);
-    sQ[hh * d + 2 * p] = (x0 * cs - x1 * sn) * scale;
-    sQ[hh * d + 2 * p + 1] = (x0 * sn + x1 * cs) * scale;
-  }
+  const int64_t pq = qpos[b];
   const int n = c.seq_len[b];
   const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
   const int total = n + pool_high;
@@ -82,6 +81,22 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
   }
   __syncthreads();
   for (int c0 = s0; c0 < s1; c0 += DG_T) {
+    // ---- chunk frame: positions are relative to pc (the first code slot's
+    // position); q is rotated by R(p_q - pc) and a key at pc + t by R(t)
+    // from the table, so only keys off that grid (anchors / window rows in
+    // the pool, non-contiguous caches) need their own angle
+    const int64_t pc = c0 < n ? c.positions[(int64_t)b * c.capacity + c0] : pq;
+    __syncthreads();   // the previous chunk's readers of sQ are done
+    for (int i = threadIdx.x; i < GQ * (d / 2); i += DG_T) {
+      const int hh = i / (d / 2), p = i % (d / 2);
+      const int64_t qb = ((int64_t)b * c.Hq + h * GQ + hh) * d;
+      const float x0 = load_elem(q, qb + 2 * p, dtype), x1 = load_elem(q, qb + 2 * p + 1, dtype);
+      float cs, sn;
+      rope_cs(static_cast<double>(pq - pc) * sFreq[p], cs, sn);
+      sQ[hh * d + 2 * p] = (x0 * cs - x1 * sn) * scale;
+      sQ[hh * d + 2 * p + 1] = (x0 * sn + x1 * cs) * scale;
+    }
+    __syncthreads();
     // ---- K side: one item per thread
     const int it = c0 + threadIdx.x;
     int src = -1;          // >= 0 code slot, <= -2 pool slot (-2 - s), -1 invalid
@@ -100,32 +115,52 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
 #pragma unroll
     for (int hh = 0; hh < GQ; ++hh) sc[hh] = 0.f;
     if (src != -1) {
-      const double pj = static_cast<double>(c.positions[(int64_t)b * c.capacity + tok]);
-      const bool r = src >= 0;
-      const int64_t prow = src >= 0 ? 0 : pool + (int64_t)(-2 - src) * 2 * d;
-      for (int p = 0; p < d / 2; ++p) {
-        float k0, k1;
-        if (r) {
-          const int e = 2 * p, g = e / dsub, o = e % dsub;
-          const int code = load_code_unit(c, hb + code_offset(src, 0, g, G));
-          k0 = cbK[code * dsub + o];
-          const int e1 = e + 1, g1 = e1 / dsub, o1 = e1 % dsub;
-          const int code1 = g1 == g ? code : load_code_unit(c, hb + code_offset(src, 0, g1, G));
-          k1 = cbK[code1 * dsub + o1];
-        } else {
-          k0 = load_elem(c.pool_rows, prow + 2 * p, c.row_dtype);
-          k1 = load_elem(c.pool_rows, prow + 2 * p + 1, c.row_dtype);
-        }
+      const int64_t rel = c.positions[(int64_t)b * c.capacity + tok] - pc;
+      const bool grid = rel == threadIdx.x;          // R(rel) is in the table
+      const double drel = static_cast<double>(rel);
+      auto pair = [&](int p, float k0, float k1) {
         float cs, sn;
-        rope_cs(pj * sFreq[p], cs, sn);
+        if (grid) {
+          const float2 r = sRot[p * DG_T + threadIdx.x];
+          cs = r.x;
+          sn = r.y;
+        } else {
+          rope_cs(drel * sFreq[p], cs, sn);
+        }
         const float r0 = k0 * cs - k1 * sn, r1 = k0 * sn + k1 * cs;
 #pragma unroll
         for (int hh = 0; hh < GQ; ++hh)
           sc[hh] = fmaf(sQ[hh * d + 2 * p], r0, fmaf(sQ[hh * d + 2 * p + 1], r1, sc[hh]));
-      }
-      if (r)
-        for (int g = 0; g < G; ++g)
+      };
+      if (src >= 0) {
+        // one code per group, its centroid read as pairs (d_sub is even for RoPE pairs
+        // that stay inside a group; odd d_sub falls back to element reads)
+        for (int g = 0; g < G; ++g) {
+          const int code = load_code_unit(c, hb + code_offset(src, 0, g, G));
+          const float *cen = cbK + (int64_t)code * dsub;
+          if ((dsub & 1) == 0) {
+            for (int o = 0; o < dsub; o += 2) {
+              const float2 kv = *reinterpret_cast<const float2 *>(cen + o);
+              pair((g * dsub + o) >> 1, kv.x, kv.y);
+            }
+          } else {
+            for (int o = 0; o < dsub; ++o) {
+              const int e = g * dsub + o;
+              if (e & 1) continue;
+              const int g1 = (e + 1) / dsub, o1 = (e + 1) % dsub;
+              const float k1 = g1 == g ? cen[o + 1]
+                                       : cbK[(int64_t)load_code_unit(c, hb + code_offset(src, 0, g1, G)) * dsub + o1];
+              pair(e >> 1, cen[o], k1);
+            }
+          }
           sVc[threadIdx.x * G + g] = load_code_unit(c, hb + code_offset(src, 1, g, G));
+        }
+      } else {
+        const int64_t prow = pool + (int64_t)(-2 - src) * 2 * d;
+        for (int p = 0; p < d / 2; ++p)
+          pair(p, load_elem(c.pool_rows, prow + 2 * p, c.row_dtype),
+               load_elem(c.pool_rows, prow + 2 * p + 1, c.row_dtype));
+      }
     }
     sSrc[threadIdx.x] = src;
 #pragma unroll
@@ -303,8 +338,8 @@ __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *
 }
 
 static size_t generic_smem(const antkv_cache_desc &c, int gq, bool cb_smem) {
-  size_t s = sizeof(double) * (c.d / 2) + sizeof(float) * (gq * c.d + gq * DG_T + 8 * gq) +
-             sizeof(int) * (DG_T + DG_T * c.groups);
+  size_t s = sizeof(double) * (c.d / 2) + sizeof(float2) * (c.d / 2) * DG_T +
+             sizeof(float) * (gq * c.d + gq * DG_T + 8 * gq) + sizeof(int) * (DG_T + DG_T * c.groups);
   if (cb_smem) s += sizeof(float) * 2 * c.m * c.d_sub;
   return s;
 }
