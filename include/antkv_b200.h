@@ -228,6 +228,9 @@ typedef struct antkv_cache_desc {
                           with the 16-byte chunks of slot r XOR-swizzled by
                           r & 7; pool_capacity is a multiple of 16          */
   void *fast_tables;   /* fast path: 16384-byte RoPE constant tables        */
+  uint16_t *codebook_f16g; /* staged tensor-core path (any d = 128 code shape
+                              but the d8m256 fast path): fp16 [Hkv][2 (K,V)]
+                              [m][d_sub], the float32 codebooks rounded      */
 } antkv_cache_desc;
 
 /* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */
@@ -253,8 +256,10 @@ ANTKV_API int antkv_cache_append(const antkv_cache_desc *c, const void *k, const
  * reconstruction, split-KV with an LSE merge.  Writes out float32
  * [B][Hq][d]; when lse != NULL also writes the log-sum-exp (natural log,
  * scaled logits) float32 [B][Hq] so sequence shards can be merged.
- * fast: 1 = use the sm_100a tensor-core kernel when the config allows
- * (d == 128, d_sub == 8, m <= 256), 0 = generic fp32 kernel. */
+ * fast: 1 = the best sm_100a tensor-core kernel the config allows (the fused
+ * d8m256 kernel for d == 128, d_sub == 8, m <= 256, 4 query heads per KV
+ * head; else the staged kernel for d == 128, d_sub 4..64, GQA 1/2/4/8),
+ * 2 = the staged kernel, 0 = generic fp32 kernel. */
 ANTKV_API int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
                            const int64_t *qpos, float *out, float *lse,
                            void *workspace, int64_t workspace_bytes, int splits,
@@ -348,6 +353,10 @@ ANTKV_API int antkv_debug_trace(unsigned long long *host, int max_words);
 /* Build the fast-path fp16 codebooks from codebook_k/v and the rotated
  * pool K rows for the rows currently held. */
 ANTKV_API int antkv_cache_prepare_fast(const antkv_cache_desc *c, void *stream);
+
+/* Build the staged tensor-core path's fp16 codebooks (codebook_f16g) and the
+ * RoPE tables from codebook_k/v (after the codebooks are set). */
+ANTKV_API int antkv_cache_prepare_tc(const antkv_cache_desc *c, void *stream);
 
 #ifdef __cplusplus
 }

@@ -43,6 +43,7 @@ class CacheDesc(ctypes.Structure):
         ("pool_kind", _vp), ("win_ring", _vp), ("free_stack", _vp), ("hstate", _vp),
         ("seq_len", _vp), ("positions", _vp), ("codebook_k", _vp), ("codebook_v", _vp),
         ("codebook_f16", _vp), ("pool_f16", _vp), ("fast_tables", _vp),
+        ("codebook_f16g", _vp),
     ]
 
 
@@ -85,6 +86,7 @@ _SIGS = {
     "antkv_cache_dequantize": (_i, [ctypes.POINTER(CacheDesc), _i, _vp, _vp, _vp]),
     "antkv_lse_combine": (_i, [_vp, _vp, _i, _i64, _i, _vp, _vp, _vp]),
     "antkv_cache_prepare_fast": (_i, [ctypes.POINTER(CacheDesc), _vp]),
+    "antkv_cache_prepare_tc": (_i, [ctypes.POINTER(CacheDesc), _vp]),
     "antkv_debug_trace": (_i, [_vp, _i]),
 }
 

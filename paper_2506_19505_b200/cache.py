@@ -111,7 +111,9 @@ class QuantizedKVCache:
         self.Hkv = kv_heads
         self.Hq = q_heads
         self.d = None
-        self.fast = bool(fast)
+        # 0: generic kernels; 1 (True): the best tensor-core kernel the shape
+        # allows (fused d8m256, else the staged kernel); "staged" / 2: staged
+        self.fast = 2 if fast in ("staged", 2) else int(bool(fast))
         self.row_dtype = None    # dtype of the full-precision pool rows = input dtype
         self.splits = int(splits)
         self._capacity_hint = capacity
@@ -166,9 +168,14 @@ class QuantizedKVCache:
             "cb_k": self.codebook_k.device_tensor(H),
             "cb_v": self.codebook_v.device_tensor(H),
         }
-        use_fast = self.fast and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
+        use_fast = bool(self.fast) and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
+        use_tc = (bool(self.fast) and d == 128 and cfg.d_sub in (4, 8, 16, 32, 64)
+                  and G * cb <= 32)
         if use_fast:
             t["cb_f16"] = torch.zeros((H, 256, 2, 64), dtype=torch.float16, device=dev)
+        if use_tc:
+            t["cb_f16g"] = torch.zeros((H, 2, cfg.m, cfg.d_sub), dtype=torch.float16, device=dev)
+        if use_fast or use_tc:
             t["fast_tables"] = _shared_fast_tables(dev, float(self.config.theta_base))
             t["pool_f16"] = torch.zeros((B, H, P, 2, d), dtype=torch.float16, device=dev)
         if old is not None:
@@ -193,13 +200,15 @@ class QuantizedKVCache:
                     merged = torch.cat([newslots, fs[b, h, :k]])
                     t["free_stack"][b, h, :merged.numel()] = merged
                     t["hstate"][b, h, _lib.HS_FREE_TOP] = merged.numel()
-            if use_fast and "pool_f16" in old:
+            if "pool_f16" in t and "pool_f16" in old:
                 t["pool_f16"][:, :, :oP] = old["pool_f16"]   # whole 16-slot tiles
         self._t = t
         self._desc = self._make_desc(cap, P, t)
         self._ws = None
         if use_fast:
             _lib.call("antkv_cache_prepare_fast", ctypes.byref(self._desc), _lib.stream())
+        if use_tc:
+            _lib.call("antkv_cache_prepare_tc", ctypes.byref(self._desc), _lib.stream())
 
     def _make_desc(self, cap, P, t):
         cfg = self.config.vq
@@ -219,7 +228,7 @@ class QuantizedKVCache:
                      ("free_stack", "free_stack"), ("hstate", "hstate"), ("seq_len", "seq_len"),
                      ("positions", "positions"), ("codebook_k", "cb_k"), ("codebook_v", "cb_v"),
                      ("codebook_f16", "cb_f16"), ("pool_f16", "pool_f16"),
-                     ("fast_tables", "fast_tables")):
+                     ("fast_tables", "fast_tables"), ("codebook_f16g", "cb_f16g")):
             setattr(D, f, t[k].data_ptr() if k in t else None)
         return D
 
@@ -355,7 +364,10 @@ class QuantizedKVCache:
         return self._ws
 
     def _use_fast(self, fast):
-        return (self.fast if fast is None else fast) and self._contiguous
+        """Kernel mode for the ABI's `fast` argument (0 generic, 1 best, 2
+        staged); the tensor-core kernels need contiguous positions."""
+        f = self.fast if fast is None else (2 if fast == "staged" else int(fast))
+        return f if self._contiguous else 0
 
     def step_device(self, q, k, v, qpos, out, lse=None, fast=None):
         """One decode step on device tensors, no host synchronisation:
@@ -691,5 +703,7 @@ class QuantizedKVCache:
         self._n = n
         self._last_pos = np.asarray([positions[-1]], dtype=np.int64) if n else None
         self._contiguous = bool(n == 0 or np.all(np.asarray(positions) == positions[0] + np.arange(n)))
-        if "pool_f16" in t:
+        if "cb_f16" in t:
             _lib.call("antkv_cache_prepare_fast", ctypes.byref(self._desc), _lib.stream())
+        if "cb_f16g" in t:
+            _lib.call("antkv_cache_prepare_tc", ctypes.byref(self._desc), _lib.stream())

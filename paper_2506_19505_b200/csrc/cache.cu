@@ -465,24 +465,7 @@ __global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__re
 // Block (Hkv*2) also writes the RoPE constant tables (FastTables).
 __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
   if (blockIdx.x == gridDim.x - 1) {
-    FastTables *tab = reinterpret_cast<FastTables *>(c.fast_tables);
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-      const double om = rope_freq(c.theta_base, i, 128);
-      tab->omega[i] = om;
-      tab->turns[i] = __double2ull_rn(om * 0.15915494309189535 * 18446744073709551616.0);
-      float cs, sn;
-      rope_cs(-32.0 * om, cs, sn);
-      float *st = reinterpret_cast<float *>(&tab->step[i >> 3][i & 3]) + 2 * ((i >> 2) & 1);
-      st[0] = cs;
-      st[1] = sn;
-      for (int r = 0; r < 16; ++r) {
-        rope_cs((double)r * om, cs, sn);
-        __half2 a = __floats2half2_rn(cs, sn), b = __floats2half2_rn(-sn, cs);
-        uint4 &k = tab->kc[i >> 3][(i >> 2) & 1][i & 3][r & 7];
-        (r < 8 ? k.x : k.z) = *reinterpret_cast<uint32_t *>(&a);
-        (r < 8 ? k.y : k.w) = *reinterpret_cast<uint32_t *>(&b);
-      }
-    }
+    fill_fast_tables(reinterpret_cast<FastTables *>(c.fast_tables), c.theta_base);
     return;
   }
   const int h = blockIdx.x / 2, kv = blockIdx.x % 2;

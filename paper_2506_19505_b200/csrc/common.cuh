@@ -149,6 +149,27 @@ struct FastTables {
   uint64_t turns[64];      // omega_i / (2 pi) in units of 2^-64 turns
 };
 
+// Fills the RoPE constant tables for d = 128 (one block; any blockDim).
+__device__ __forceinline__ void fill_fast_tables(FastTables *tab, double theta) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    const double om = rope_freq(theta, i, 128);
+    tab->omega[i] = om;
+    tab->turns[i] = __double2ull_rn(om * 0.15915494309189535 * 18446744073709551616.0);
+    float cs, sn;
+    rope_cs(-32.0 * om, cs, sn);
+    float *st = reinterpret_cast<float *>(&tab->step[i >> 3][i & 3]) + 2 * ((i >> 2) & 1);
+    st[0] = cs;
+    st[1] = sn;
+    for (int r = 0; r < 16; ++r) {
+      rope_cs((double)r * om, cs, sn);
+      __half2 a = __floats2half2_rn(cs, sn), b = __floats2half2_rn(-sn, cs);
+      uint4 &k = tab->kc[i >> 3][(i >> 2) & 1][i & 3][r & 7];
+      (r < 8 ? k.x : k.z) = *reinterpret_cast<uint32_t *>(&a);
+      (r < 8 ? k.y : k.w) = *reinterpret_cast<uint32_t *>(&b);
+    }
+  }
+}
+
 // cos/sin of delta * omega for an integer position difference, reduced
 // exactly in integer arithmetic: delta * turns mod 2^64 is the fractional
 // number of turns (error ~ |delta| * 2^-53 relative turns, < 1e-9 rad).

@@ -20,6 +20,14 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
                        float *ws_o, float *ws_m, float *ws_l, int *cnt, int splits,
                        cudaStream_t st);
 int decode_fast_supported(const antkv_cache_desc &c);
+int decode_tc_supported(const antkv_cache_desc &c);
+int decode_tc_plan(const antkv_cache_desc &c, int requested);
+int decode_tc_launch(const antkv_cache_desc &c, const void *q, int qdtype, const int64_t *qpos, float *ws_o,
+                     float *ws_m, float *ws_l, int splits, cudaStream_t st);
+
+// Decode kernel choice: the fused d8m256 kernel, the staged tensor-core
+// kernel (decode_tc.cu, any other d = 128 code shape) or the generic one.
+enum DecodeMode { kGeneric = 0, kFast = 1, kStaged = 2 };
 void decode_fast_plan(const antkv_cache_desc &c, int requested, int &code_splits, int &pool_splits);
 
 template <int GQ, bool CB_SMEM>
@@ -374,12 +382,13 @@ static int auto_splits(const antkv_cache_desc &c) {
 }
 
 // Number of partials a call produces (generic: splits; fast: code + pool CTAs).
-static int planned_splits(const antkv_cache_desc &c, int splits, bool fast) {
-  if (fast) {
+static int planned_splits(const antkv_cache_desc &c, int splits, int mode) {
+  if (mode == kFast) {
     int cs, ps;
     decode_fast_plan(c, splits, cs, ps);
     return cs + ps;
   }
+  if (mode == kStaged) return decode_tc_plan(c, splits);
   return splits > 0 ? splits : auto_splits(c);
 }
 
@@ -401,16 +410,17 @@ static int64_t partial_bytes(const antkv_cache_desc &c, int used) {
 // [B*Hkv + B] int32 at the end.  Zero it once before the first call.
 extern "C" int64_t antkv_decode_workspace_bytes(const antkv_cache_desc *c, int splits) {
   if (!c) return -1;
-  int s = planned_splits(*c, splits, false);
-  if (decode_fast_supported(*c)) s = max(s, planned_splits(*c, splits, true));
+  int s = planned_splits(*c, splits, kGeneric);
+  if (decode_fast_supported(*c)) s = max(s, planned_splits(*c, splits, kFast));
+  if (decode_tc_supported(*c)) s = max(s, planned_splits(*c, splits, kStaged));
   return partial_bytes(*c, s) + counter_bytes(*c) + 256;
 }
 
 static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, const void *knew,
                           const void *vnew, int kvdtype, const int64_t *qpos, float *out,
                           float *lse, void *workspace, int64_t workspace_bytes, int splits,
-                          bool use_fast, cudaStream_t st) {
-  const int used = planned_splits(*c, splits, use_fast);
+                          int mode, cudaStream_t st) {
+  const int used = planned_splits(*c, splits, mode);
   const int64_t rows = (int64_t)c->B * c->Hq;
   ANTKV_REQUIRE(workspace_bytes >= antkv_decode_workspace_bytes(c, splits), "decode workspace too small");
   float *wo = reinterpret_cast<float *>(workspace);
@@ -418,12 +428,19 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   float *wl = wm + (int64_t)used * rows;
   int *cnt = reinterpret_cast<int *>(reinterpret_cast<char *>(workspace) + workspace_bytes -
                                      256 - counter_bytes(*c));
-  if (!use_fast) previous_cache_on_stream(st, c->codes);   // (the fast launch records itself)
-  if (use_fast)
+  if (mode != kFast) previous_cache_on_stream(st, c->codes);   // (the fast launch records itself)
+  if (mode == kFast)
     return decode_fast_launch(*c, q, dtype, knew, vnew, kvdtype, qpos, out, lse, wo, wm, wl, cnt,
                               splits, st);
   const int gq = c->Hq / c->Hkv;
   int rc;
+  if (mode == kStaged) {
+    rc = decode_tc_launch(*c, q, dtype, qpos, wo, wm, wl, used, st);
+    if (rc) return rc;
+    decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
+    ANTKV_LAUNCH_CHECK("decode_combine_kernel");
+    return ANTKV_OK;
+  }
   switch (gq) {
     case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
     case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
@@ -449,7 +466,14 @@ static int check_decode_args(const antkv_cache_desc *c, const void *q, float *ou
 // The fused kernel bulk-copies the 4 query rows of a head: q must be 16-byte
 // aligned (any contiguous tensor is); otherwise the generic kernels run.
 static bool fast_ok(const antkv_cache_desc *c, const void *q, int fast) {
-  return fast && decode_fast_supported(*c) && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+  return fast == 1 && decode_fast_supported(*c) && (reinterpret_cast<uintptr_t>(q) & 15) == 0;
+}
+
+// fast: 0 generic, 1 best available (fused d8m256, else staged), 2 staged.
+static int decode_mode(const antkv_cache_desc *c, const void *q, int fast) {
+  if (fast_ok(c, q, fast)) return kFast;
+  if (fast >= 1 && decode_tc_supported(*c)) return kStaged;
+  return kGeneric;
 }
 
 extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, int dtype,
@@ -459,7 +483,7 @@ extern "C" int antkv_decode_attention(const antkv_cache_desc *c, const void *q, 
   int rc = check_decode_args(c, q, out);
   if (rc) return rc;
   return attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
-                        workspace_bytes, splits, fast_ok(c, q, fast), as_stream(stream));
+                        workspace_bytes, splits, decode_mode(c, q, fast), as_stream(stream));
 }
 
 extern "C" int antkv_decode_step(const antkv_cache_desc *c, const void *q, const void *k,
@@ -470,13 +494,14 @@ extern "C" int antkv_decode_step(const antkv_cache_desc *c, const void *q, const
   if (rc) return rc;
   ANTKV_REQUIRE(k != nullptr && v != nullptr, "null k/v");
   cudaStream_t st = as_stream(stream);
-  if (fast_ok(c, q, fast))   // one fused launch
+  const int mode = decode_mode(c, q, fast);
+  if (mode == kFast)   // one fused launch
     return attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes,
-                          splits, true, st);
+                          splits, kFast, st);
   rc = antkv_cache_append(c, k, v, dtype, qpos, stream);
   if (rc) return rc;
   rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
-                      workspace_bytes, splits, false, st);
+                      workspace_bytes, splits, mode, st);
   if (rc) return rc;
   return antkv_cache_evict(c, stream);
 }
@@ -524,9 +549,10 @@ extern "C" int antkv_decode_step_publish(const antkv_cache_desc *c, const void *
   // the step (one fused launch on the fast path), then the partial's rows go
   // to every peer slot and the flags are released (a second, tiny launch: the
   // fused decode kernel is kept exactly as timed)
-  if (fast_ok(c, q, fast)) {
+  const int mode = decode_mode(c, q, fast);
+  if (mode == kFast) {
     rc = attention_impl(c, q, dtype, k, v, dtype, qpos, out, lse, workspace, workspace_bytes, splits,
-                        true, st);
+                        kFast, st);
     if (rc) return rc;
   } else {
     if (k) {
@@ -535,7 +561,7 @@ extern "C" int antkv_decode_step_publish(const antkv_cache_desc *c, const void *
       if (rc) return rc;
     }
     rc = attention_impl(c, q, dtype, nullptr, nullptr, dtype, qpos, out, lse, workspace,
-                        workspace_bytes, splits, false, st);
+                        workspace_bytes, splits, mode, st);
     if (rc) return rc;
     if (k) {
       rc = antkv_cache_evict(c, stream);

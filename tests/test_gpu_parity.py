@@ -374,6 +374,64 @@ def test_lse_combine_kernel():
     assert np.abs(got - ref).max() < 1e-5
 
 
+@pytest.mark.parametrize("notation,B,Hq,Hkv,fast", [
+    ("d32m4096", 1, 4, 1, True),      # config #3 code shape (0.375 bit), GQA 4
+    ("d4m256", 2, 4, 4, True),        # config #4 code shape (2 bit), MHA
+    ("d16m256", 1, 8, 4, True),       # GQA 2
+    ("d8m256", 1, 16, 2, "staged"),   # the staged kernel on the fused kernel's shape, GQA 8
+    ("d16m4096", 1, 8, 2, True),      # 2-byte indices, GQA 4
+    ("d64m256", 1, 2, 1, True),       # 2 groups per row
+])
+def test_staged_kernel_vs_oracle(notation, B, Hq, Hkv, fast):
+    """decode_tc.cu (staged tensor-core kernel, fp16 operands): every d = 128
+    code shape the fused d8m256 kernel does not take, against the float64
+    oracle (2e-2, the bf16 tolerance of SURVEY §8c)."""
+    cache, outs, refs = _gqa(40 + Hq, B, Hq, Hkv, 300, 128, notation, 20, window=16, frac=0.02,
+                             theta=5e5, fast=fast)
+    assert cache.desc.codebook_f16g
+    for i in range(outs.shape[0]):
+        assert rel(outs[i], refs[i]) < 2e-2, (i, rel(outs[i], refs[i]))
+
+
+@pytest.mark.parametrize("notation,Hq,Hkv", [("d32m4096", 32, 8), ("d4m256", 8, 8)])
+def test_staged_matches_generic_at_128k(notation, Hq, Hkv):
+    """Full-size property for configs #3 / #4: the staged tensor-core kernel
+    and the generic float32 kernel agree on a 131072-token cache, and both
+    match a float64 attention over the dequantised cache."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.anchors import select_anchors_device
+    n, d = 131072, 128
+    vq = VqConfig.from_notation(notation)
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=5e5)
+    ck, cv = codebooks(33, Hkv, vq.m, vq.d_sub)
+    g = torch.Generator(device="cuda").manual_seed(33)
+    K = torch.randn((1, Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    V = torch.randn((1, Hkv, n, d), device="cuda", generator=g).to(torch.bfloat16)
+    scores = torch.rand((Hkv, n), device="cuda", generator=g)
+    anchors = select_anchors_device(scores, scores.flip(-1), cfg.budget_for(n)).view(1, Hkv, -1)
+    pos = torch.arange(n, device="cuda", dtype=torch.int64)[None]
+    cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    cache.build_from(K, V, pos, anchors)
+    q = torch.randn((1, Hq, d), device="cuda", generator=g).to(torch.bfloat16)
+    qp = torch.tensor([n - 1 + 7], device="cuda", dtype=torch.int64)
+    outs = {}
+    for fast in (1, 0):
+        out = torch.empty((1, Hq, d), device="cuda", dtype=torch.float32)
+        cache.attend_device(q, qp, out, fast=fast)
+        outs[fast] = out.cpu().numpy()[0]
+    assert rel(outs[1], outs[0]) < 2e-2
+    Kh, Vh = cache.dequantize()
+    gq = Hq // Hkv
+    for h in (0, Hkv - 1):
+        Kr = O.apply_rope(Kh[0, h].cpu().numpy(), np.arange(n), 5e5)
+        for hq in (gq * h, gq * h + gq - 1):
+            qr = O.apply_rope(q[0, hq].float().cpu().numpy()[None], np.array([n - 1 + 7]), 5e5)
+            A = O.softmax_rows((qr @ Kr.T) / np.sqrt(d))
+            ref = (A @ Vh[0, h].cpu().numpy().astype(np.float64))[0]
+            assert rel(outs[0][hq], ref) < 1e-3
+            assert rel(outs[1][hq], ref) < 2e-2
+
+
 def test_fast_matches_generic_at_128k():
     """Full-size property: the tensor-core and generic kernels agree on a
     131072-token d8m256 cache (32 Q / 8 KV heads), and the result equals a
