@@ -179,6 +179,27 @@ def measured_traffic(args):
     return None
 
 
+def smem_roofline(args, launch_ms, sm_mhz):
+    """The bound the fused kernel actually runs against: shared-memory
+    wavefronts (one 128-byte wavefront per SM per clock) of its codebook
+    gathers, from the committed ncu count per launch (decode_fast_traffic.json)
+    over the live launch time.  None off that workload."""
+    f = ROOT / "profiles" / "decode_fast_traffic.json"
+    try:
+        t = json.loads(f.read_text())
+    except (OSError, ValueError):
+        return None
+    if (t.get("ctx"), t.get("notation"), t.get("batch")) != (args.ctx, args.notation, args.batch) \
+            or args.kernel != "fast" or "smem_wavefronts_per_launch" not in t:
+        return None
+    w = t["smem_wavefronts_per_launch"]
+    per_clk = w / (launch_ms * 1e-3 * sm_mhz * 1e6 * 148)
+    return {"bound": "smem", "unit": "wavefronts/clk/SM", "achieved": per_clk, "peak": 1.0,
+            "frac": per_clk, "wavefronts_per_launch": w, "sm_mhz": sm_mhz,
+            "note": "whole launch incl. prologue/combine; ~4 wavefronts (512 B of fp16 centroids) "
+                    "per token-head are the floor of any exact fp16 reconstruction"}
+
+
 def algorithmic_bytes(cache, torch):
     """Bytes one decode-attention call must move (SURVEY.md §8d formula):
     H_kv*[n_q*(code bytes/token) + n_fp*2*d*2] + 2*H_q*d*2 + codebooks."""
@@ -399,6 +420,7 @@ def run_ours(args):
     a1.record()
     torch.cuda.synchronize()
     attn_ms = a0.elapsed_time(a1) / (reps * L)
+    clk_mhz = clk.summary().get("sm_mhz") or clk.max_mhz or 1965.0
     alg_bytes = algorithmic_bytes(caches[0], torch)
 
     # e2e through the public step API with pinned host buffers: every step
@@ -499,7 +521,8 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "traffic": measured_traffic(args), "algorithmic_bytes_per_launch": alg_bytes,
-                         "launch_ms": attn_ms},
+                         "launch_ms": attn_ms,
+                         "secondary": smem_roofline(args, attn_ms, clk_mhz)},
             "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,
                     "d2h_bytes_per_step": outh.numel() * 4, "ms_per_step": e2e_ms,
