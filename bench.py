@@ -179,6 +179,18 @@ def measured_traffic(args):
     return None
 
 
+def launches_per_layer_step(cache, args, world):
+    """Our kernel launches per layer-step on rank 0: the fused d8m256 step is
+    one launch (N=1) or attention + merge (N>1); the staged / generic paths
+    run append, attention, split combine and the two eviction launches
+    (attention + combine + merge on a non-tail shard)."""
+    vq = cache.config.vq
+    fused = (args.kernel == "fast" and vq.d_sub == 8 and vq.m <= 256 and HQ == 4 * HKV)
+    if world == 1:
+        return 1 if fused else 5
+    return 2 if fused else 3
+
+
 def smem_roofline(args, launch_ms, sm_mhz):
     """The bound the fused kernel actually runs against: shared-memory
     wavefronts (one 128-byte wavefront per SM per clock) of its codebook
@@ -506,7 +518,7 @@ def run_ours(args):
             "data": "synthetic (seeded randn bf16 K/V, random N(0,1) codebooks)",
             "config": {
                 "workload": f"decode attention, {args.ctx // 1024}K ctx per GPU x {world} GPU(s), "
-                            f"{args.notation} (1-bit), 1% anchors, window 32, {HQ} Q / {HKV} KV heads, "
+                            f"{args.notation} ({caches[0].config.vq.index_bits / caches[0].config.vq.d_sub:.3g}-bit), 1% anchors, window 32, {HQ} Q / {HKV} KV heads, "
                             f"d={D}, batch {B}, {L} layers per step",
                 "ctx_per_gpu": args.ctx, "layers_per_step": L, "batch": B, "kernel": args.kernel,
                 "l2": f"no flush: per-step working set {alg_bytes * L / 1e9:.2f} GB > 126 MB L2",
@@ -536,8 +548,7 @@ def run_ours(args):
             # our kernels per layer-step on rank 0: the fused step (N=1) or attention +
             # LSE combine (N>1, rank 0 is not the tail); generic path: append, attention,
             # combine, evict
-            "gpu_launches": args.steps * L * ((1 if args.kernel == "fast" else 4) if world == 1
-                                              else (2 if args.kernel == "fast" else 3)),
+            "gpu_launches": args.steps * L * launches_per_layer_step(caches[0], args, world),
             "clocks": clk.summary(),
             "encode": enc,
             "prefill": pre,
@@ -582,7 +593,11 @@ def cpu_sample_from_cache(cache, n_heads):
     t = cache.tensors
     n = cache.token_count
     G = D // cache.config.vq.d_sub
-    codes = t["codes"][0, :n_heads, :n].cpu().numpy().reshape(n_heads, n, 2, G)
+    cb = 1 if cache.config.vq.index_bits <= 8 else 2
+    cap = t["codes"].shape[2]
+    # tiled layout [tile][kv][16 slots][G] code units (common.cuh code_offset)
+    units = t["codes"][0, :n_heads].cpu().numpy().reshape(n_heads, -1).view(np.uint8 if cb == 1 else np.uint16)
+    codes = units.reshape(n_heads, cap // 16, 2, 16, G).transpose(0, 1, 3, 2, 4).reshape(n_heads, cap, 2, G)[:, :n]
     qm = t["qmask"][0, :n_heads].cpu().numpy().view(np.uint32)
     items = []
     rng = np.random.default_rng(5)

@@ -231,6 +231,9 @@ typedef struct antkv_cache_desc {
   uint16_t *codebook_f16g; /* staged tensor-core path (any d = 128 code shape
                               but the d8m256 fast path): fp16 [Hkv][2 (K,V)]
                               [m][d_sub], the float32 codebooks rounded      */
+  unsigned long long *evict_scratch; /* [B][Hkv][2*groups] minima of the
+                              eviction encoder, (float distance bits << 32) |
+                              centroid index; all ones between calls        */
 } antkv_cache_desc;
 
 /* Bytes of scratch needed by antkv_decode_attention for `splits` (0 = auto). */

@@ -43,7 +43,7 @@ class CacheDesc(ctypes.Structure):
         ("pool_kind", _vp), ("win_ring", _vp), ("free_stack", _vp), ("hstate", _vp),
         ("seq_len", _vp), ("positions", _vp), ("codebook_k", _vp), ("codebook_v", _vp),
         ("codebook_f16", _vp), ("pool_f16", _vp), ("fast_tables", _vp),
-        ("codebook_f16g", _vp),
+        ("codebook_f16g", _vp), ("evict_scratch", _vp),
     ]
 
 

@@ -165,6 +165,7 @@ class QuantizedKVCache:
             "hstate": torch.zeros((B, H, _lib.HSTATE_WORDS), dtype=torch.int32, device=dev),
             "seq_len": torch.zeros((B,), dtype=torch.int32, device=dev),
             "positions": torch.zeros((B, cap), dtype=torch.int64, device=dev),
+            "evict_scratch": torch.full((B, H, 2 * G), -1, dtype=torch.int64, device=dev),
             "cb_k": self.codebook_k.device_tensor(H),
             "cb_v": self.codebook_v.device_tensor(H),
         }
@@ -228,7 +229,7 @@ class QuantizedKVCache:
                      ("free_stack", "free_stack"), ("hstate", "hstate"), ("seq_len", "seq_len"),
                      ("positions", "positions"), ("codebook_k", "cb_k"), ("codebook_v", "cb_v"),
                      ("codebook_f16", "cb_f16"), ("pool_f16", "pool_f16"),
-                     ("fast_tables", "fast_tables"), ("codebook_f16g", "cb_f16g")):
+                     ("fast_tables", "fast_tables"), ("codebook_f16g", "cb_f16g"), ("evict_scratch", "evict_scratch")):
             setattr(D, f, t[k].data_ptr() if k in t else None)
         return D
 

@@ -310,7 +310,10 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
       const float x0 = load_elem(c.pool_rows, src + 2 * p, c.row_dtype);
       const float x1 = load_elem(c.pool_rows, src + 2 * p + 1, c.row_dtype);
       float cs, sn;
-      rope_cs(pos * rope_freq(c.theta_base, p, c.d), cs, sn);
+      const double om = (c.fast_tables && c.d == 128)
+                            ? reinterpret_cast<const FastTables *>(c.fast_tables)->omega[p]
+                            : rope_freq(c.theta_base, p, c.d);
+      rope_cs(pos * om, cs, sn);
       __half *dst = reinterpret_cast<__half *>(c.pool_f16) + bh * c.pool_capacity * 2 * c.d;
       dst[pool_f16_offset(slot, 0, 2 * p)] = __float2half_rn(x0 * cs - x1 * sn);
       dst[pool_f16_offset(slot, 0, 2 * p + 1)] = __float2half_rn(x0 * sn + x1 * cs);
@@ -327,96 +330,141 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
   }
 }
 
-// Evict (cache.py:180-193).  One CTA (256 threads) per (b, head).  Encoding
-// stages the row and (when they fit) both codebooks in shared memory, then
-// splits each (K/V, group) over a team of threads that scans a slice of the
-// codebook, reducing (distance, index) with the lowest index on ties.
+// Evict (cache.py:180-193) in two launches so the encode of a long-codebook
+// row spreads over many SMs: the oldest windowed row beyond window_size is
+// promoted to an anchor while the budget allows, otherwise encoded.
+// evict_plan() is the decision both launches derive from the unchanged state.
+struct EvictPlan {
+  int action;   // 0 none, 1 promote, 2 encode
+  int slot;     // pool slot of the oldest windowed row
+  int j;        // its token
+};
+
+__device__ __forceinline__ EvictPlan evict_plan(const antkv_cache_desc &c, int64_t bh, int b) {
+  const int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  EvictPlan p{0, -1, -1};
+  if (hs[ANTKV_HS_WIN_COUNT] > c.window_size) {
+    p.slot = c.win_ring[bh * (c.window_size + 1) + hs[ANTKV_HS_WIN_HEAD]];
+    const int n = c.seq_len[b];
+    const int budget = budget_for((int64_t)n + c.token_offset, c.anchor_count, c.anchor_fraction);
+    p.action = hs[ANTKV_HS_ANCHORS] < budget ? 1 : 2;
+    p.j = c.pool_tok[bh * c.pool_capacity + p.slot];
+  }
+  return p;
+}
+
+// Launch 1: CTA (b*Hkv + h, unit, slice) scans 512 centroids of sub-vector
+// `unit` = (kv, group) of the evicted row when the plan says so, and folds
+// its minimum into evict_scratch with a 64-bit atomicMin of (distance bits
+// << 32 | index): distances are >= 0, so the packed order is the distance
+// order with the lower index on ties — the strict-< scan of
+// _ckernels.pyx:150-162.  For d_sub = 2^k >= 4 a centroid is read by
+// LPC = min(32, d_sub / 4) adjacent lanes (one float4 each per pass, so a
+// warp load covers contiguous centroids); float32 distances.
+constexpr int kEvictSlice = 512;
+
 __global__ void __launch_bounds__(256)
-cache_evict_kernel(antkv_cache_desc c, int cb_in_smem) {
-  extern __shared__ float ev_sm[];
+cache_evict_encode_kernel(antkv_cache_desc c) {
+  __shared__ float sx[256];
+  __shared__ unsigned long long s_key[8];
   const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
   const int64_t bh = bh_index(b, h, c.Hkv);
-  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
-  __shared__ int s_slot, s_encode;
-  if (threadIdx.x == 0) {
-    s_slot = -1;
-    s_encode = 0;
-    if (hs[ANTKV_HS_WIN_COUNT] > c.window_size) {
-      int32_t *ring = c.win_ring + bh * (c.window_size + 1);
-      int slot = ring[hs[ANTKV_HS_WIN_HEAD]];
-      hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % (c.window_size + 1);
-      hs[ANTKV_HS_WIN_COUNT] -= 1;
-      const int n = c.seq_len[b];
-      const int budget = budget_for((int64_t)n + c.token_offset, c.anchor_count, c.anchor_fraction);
-      if (hs[ANTKV_HS_ANCHORS] < budget) {
-        c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_ANCHOR;
-        hs[ANTKV_HS_ANCHORS] += 1;
-      } else {
-        s_slot = slot;
-        s_encode = 1;
-      }
-    }
-  }
+  const EvictPlan p = evict_plan(c, bh, b);
+  if (p.action != 2) return;
+  const int unit = blockIdx.y, kv = unit / c.groups, g = unit % c.groups;
+  const int ds = c.d_sub;
+  const int m0 = blockIdx.z * kEvictSlice, m1 = min(c.m, m0 + kEvictSlice);
+  const int64_t row = (bh * c.pool_capacity + p.slot) * 2 * c.d + kv * c.d + g * ds;
+  for (int i = threadIdx.x; i < ds; i += blockDim.x) sx[i] = load_elem(c.pool_rows, row + i, c.row_dtype);
   __syncthreads();
-  if (!s_encode) return;
-  const int slot = s_slot;
-  const int j = c.pool_tok[bh * c.pool_capacity + slot];
-  const int64_t row = (bh * c.pool_capacity + slot) * 2 * c.d;
-  const int cbn = c.m * c.d_sub;
-  float *sx = ev_sm;                       // [2][d]
-  float *scb = ev_sm + 2 * c.d;            // [2][m][d_sub] when cb_in_smem
-  for (int i = threadIdx.x; i < 2 * c.d; i += blockDim.x) sx[i] = load_elem(c.pool_rows, row + i, c.row_dtype);
-  if (cb_in_smem) {
-    const float *gk = c.codebook_k + (int64_t)h * cbn, *gv = c.codebook_v + (int64_t)h * cbn;
-    for (int i = threadIdx.x; i < cbn; i += blockDim.x) {
-      scb[i] = gk[i];
-      scb[cbn + i] = gv[i];
-    }
-  }
-  __syncthreads();
-  const int units = 2 * c.groups;             // (kv, group) pairs
-  const int team = max(1, 256 / units);       // threads per unit (>= 1)
-  const int u = threadIdx.x / team, lane = threadIdx.x % team;
+  const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * ds;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float best = INFINITY;
   int best_i = 0x7fffffff;
-  if (u < units) {
-    const int kv = u / c.groups, g = u % c.groups;
-    const float *cb = cb_in_smem ? scb + kv * cbn
-                                 : (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * cbn;
-    const float *x = sx + kv * c.d + g * c.d_sub;
-    for (int ci = lane; ci < c.m; ci += team) {
+  if (ds >= 4 && (ds & (ds - 1)) == 0) {   // power of two: lanes per centroid divide the warp
+    const int lpc = min(32, ds >> 2);
+    const int cpw = 32 / lpc;                    // centroids per warp pass
+    const int sub = lane % lpc, ci0 = lane / lpc;
+    const int nq = ds >> 2;                      // float4s per centroid
+    constexpr int U = 4;                         // passes with their loads in flight together
+    for (int base = m0 + warp * cpw; base < m1; base += 8 * cpw * U) {
+      float part[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) part[u] = 0.f;
+      for (int q = sub; q < nq; q += lpc) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int ci = base + u * 8 * cpw + ci0;
+          v[u] = ci < m1 ? __ldg(reinterpret_cast<const float4 *>(cb + (int64_t)ci * ds) + q)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        const float x0 = sx[4 * q], x1 = sx[4 * q + 1], x2 = sx[4 * q + 2], x3 = sx[4 * q + 3];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float df = x0 - v[u].x; part[u] = fmaf(df, df, part[u]);
+          df = x1 - v[u].y; part[u] = fmaf(df, df, part[u]);
+          df = x2 - v[u].z; part[u] = fmaf(df, df, part[u]);
+          df = x3 - v[u].w; part[u] = fmaf(df, df, part[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        for (int off = lpc >> 1; off > 0; off >>= 1) part[u] += __shfl_down_sync(0xffffffffu, part[u], off, lpc);
+        const int ci = base + u * 8 * cpw + ci0;
+        if (sub == 0 && ci < m1 && part[u] < best) { best = part[u]; best_i = ci; }
+      }
+    }
+  } else {
+    for (int ci = m0 + threadIdx.x; ci < m1; ci += blockDim.x) {
       float s = 0.f;
-      for (int t = 0; t < c.d_sub; ++t) {
-        const float df = x[t] - cb[(int64_t)ci * c.d_sub + t];
+      for (int t = 0; t < ds; ++t) {
+        const float df = sx[t] - cb[(int64_t)ci * ds + t];
         s = fmaf(df, df, s);
       }
       if (s < best) { best = s; best_i = ci; }
     }
   }
-  // team reduction through shared memory (teams may span warps)
-  __shared__ float s_best[256];
-  __shared__ int s_idx[256];
-  s_best[threadIdx.x] = best;
-  s_idx[threadIdx.x] = best_i;
-  __syncthreads();
-  if (u < units && lane == 0) {
-    for (int l = 1; l < team; ++l) {
-      float o = s_best[threadIdx.x + l];
-      int oi = s_idx[threadIdx.x + l];
-      if (o < best || (o == best && oi < best_i)) { best = o; best_i = oi; }
-    }
-    const int kv = u / c.groups, g = u % c.groups;
-    const int64_t off = bh * c.capacity * 2 * c.groups + code_offset(j, kv, g, c.groups);
-    if (c.code_bytes == 1) c.codes[off] = static_cast<uint8_t>(best_i);
-    else reinterpret_cast<uint16_t *>(c.codes)[off] = static_cast<uint16_t>(best_i);
+  unsigned long long key = best_i == 0x7fffffff
+      ? ~0ull : ((unsigned long long)__float_as_uint(best) << 32) | (unsigned)best_i;
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_down_sync(0xffffffffu, key, off);
+    key = o < key ? o : key;
   }
+  if (lane == 0) s_key[warp] = key;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicOr(&c.qmask[bh * (c.capacity / 32) + j / 32], 1u << (j % 32));
-    c.pool_kind[bh * c.pool_capacity + slot] = ANTKV_KIND_FREE;
-    c.pool_tok[bh * c.pool_capacity + slot] = -1;
-    c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = slot;
+    for (int w = 1; w < 8; ++w) key = s_key[w] < key ? s_key[w] : key;
+    atomicMin(c.evict_scratch + bh * 2 * c.groups + unit, key);
+  }
+}
+
+// Launch 2: one thread per (b, head) applies the plan to the state words.
+__global__ void cache_evict_commit_kernel(antkv_cache_desc c) {
+  const int64_t bh = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (bh >= (int64_t)c.B * c.Hkv) return;
+  const int b = static_cast<int>(bh / c.Hkv);
+  const EvictPlan p = evict_plan(c, bh, b);
+  if (p.action == 0) return;
+  int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
+  hs[ANTKV_HS_WIN_HEAD] = (hs[ANTKV_HS_WIN_HEAD] + 1) % (c.window_size + 1);
+  hs[ANTKV_HS_WIN_COUNT] -= 1;
+  if (p.action == 1) {
+    c.pool_kind[bh * c.pool_capacity + p.slot] = ANTKV_KIND_ANCHOR;
+    hs[ANTKV_HS_ANCHORS] += 1;
+  } else {
+    unsigned long long *sk = c.evict_scratch + bh * 2 * c.groups;
+    for (int u = 0; u < 2 * c.groups; ++u) {   // the encoder's minima -> codes; reset the slots
+      const int idx = static_cast<int>(sk[u] & 0xffffffffu);
+      sk[u] = ~0ull;
+      const int64_t off = bh * c.capacity * 2 * c.groups + code_offset(p.j, u / c.groups, u % c.groups, c.groups);
+      if (c.code_bytes == 1) c.codes[off] = static_cast<uint8_t>(idx);
+      else reinterpret_cast<uint16_t *>(c.codes)[off] = static_cast<uint16_t>(idx);
+    }
+    atomicOr(&c.qmask[bh * (c.capacity / 32) + p.j / 32], 1u << (p.j % 32));
+    c.pool_kind[bh * c.pool_capacity + p.slot] = ANTKV_KIND_FREE;
+    c.pool_tok[bh * c.pool_capacity + p.slot] = -1;
+    c.free_stack[bh * c.pool_capacity + hs[ANTKV_HS_FREE_TOP]] = p.slot;
     hs[ANTKV_HS_FREE_TOP] += 1;
   }
 }
@@ -569,12 +617,15 @@ extern "C" int antkv_cache_evict(const antkv_cache_desc *c, void *stream) {
   int rc = check_desc(c);
   if (rc) return rc;
   previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
-  const size_t cbn = (size_t)c->m * c->d_sub;
-  const int cb_in_smem = cbn * 2 * sizeof(float) <= 64 * 1024;
-  const size_t smem = sizeof(float) * (2 * c->d + (cb_in_smem ? 2 * cbn : 0));
-  cudaFuncSetAttribute(cache_evict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cache_evict_kernel<<<c->B * c->Hkv, 256, smem, as_stream(stream)>>>(*c, cb_in_smem);
-  ANTKV_LAUNCH_CHECK("cache_evict_kernel");
+  ANTKV_REQUIRE(c->d_sub <= 256, "d_sub > 256 unsupported by the eviction encoder");
+  cudaStream_t st = as_stream(stream);
+  ANTKV_REQUIRE(c->evict_scratch != nullptr, "evict_scratch not allocated");
+  cache_evict_encode_kernel<<<dim3(c->B * c->Hkv, 2 * c->groups, (c->m + kEvictSlice - 1) / kEvictSlice), 256, 0,
+                              st>>>(*c);
+  ANTKV_LAUNCH_CHECK("cache_evict_encode_kernel");
+  const int nbh = c->B * c->Hkv;
+  cache_evict_commit_kernel<<<(nbh + 127) / 128, 128, 0, st>>>(*c);
+  ANTKV_LAUNCH_CHECK("cache_evict_commit_kernel");
   return ANTKV_OK;
 }
 

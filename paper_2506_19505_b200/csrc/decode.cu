@@ -245,27 +245,47 @@ decode_generic_kernel(antkv_cache_desc c, const void *__restrict__ q, int dtype,
 }
 
 // Split-KV combine: unnormalised partial o_s with (m_s, l_s) per split.
+// One CTA per output row: warp 0 turns the (m, l) of every split into
+// weights in shared memory, then each thread sums its dims over the splits
+// with all loads of a batch of 8 splits in flight.
 __global__ void decode_combine_kernel(const float *__restrict__ ws_o, const float *__restrict__ ws_m,
                                       const float *__restrict__ ws_l, int splits, int64_t rows,
                                       int d, float *__restrict__ out, float *__restrict__ lse) {
+  extern __shared__ float cw[];   // [splits] weights, then M, L
   const int64_t row = blockIdx.x;
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s) M = fmaxf(M, ws_m[s * rows + row]);
-  float L = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float ms = ws_m[s * rows + row];
-    if (ms != -INFINITY) L += __expf(ms - M) * ws_l[s * rows + row];
+  if (threadIdx.x < 32) {
+    float M = -INFINITY;
+    for (int s = threadIdx.x; s < splits; s += 32) M = fmaxf(M, ws_m[s * rows + row]);
+    M = warp_max(M);
+    float L = 0.f;
+    for (int s = threadIdx.x; s < splits; s += 32) {
+      const float ms = ws_m[s * rows + row];
+      const float wv = ms == -INFINITY ? 0.f : __expf(ms - M);
+      cw[s] = wv;
+      L += wv * ws_l[s * rows + row];
+    }
+    L = warp_sum(L);
+    if (threadIdx.x == 0) {
+      cw[splits] = M;
+      cw[splits + 1] = L;
+    }
   }
-  const float inv = 1.f / L;
+  __syncthreads();
+  const float inv = 1.f / cw[splits + 1];
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
     float acc = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float ms = ws_m[s * rows + row];
-      if (ms != -INFINITY) acc = fmaf(__expf(ms - M), ws_o[(s * rows + row) * d + t], acc);
+    int s = 0;
+    for (; s + 8 <= splits; s += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ws_o[((s + u) * rows + row) * d + t];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fmaf(cw[s + u], v[u], acc);
     }
+    for (; s < splits; ++s) acc = fmaf(cw[s], ws_o[(s * rows + row) * d + t], acc);
     out[row * d + t] = acc * inv;
   }
-  if (lse && threadIdx.x == 0) lse[row] = M + logf(L);
+  if (lse && threadIdx.x == 0) lse[row] = cw[splits] + logf(cw[splits + 1]);
 }
 
 // Merge of P normalised shard results with their LSE (sequence sharding).
@@ -437,7 +457,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
   if (mode == kStaged) {
     rc = decode_tc_launch(*c, q, dtype, qpos, wo, wm, wl, used, st);
     if (rc) return rc;
-    decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
+    decode_combine_kernel<<<(unsigned)rows, 128, (used + 2) * sizeof(float), st>>>(wo, wm, wl, used, rows, c->d, out, lse);
     ANTKV_LAUNCH_CHECK("decode_combine_kernel");
     return ANTKV_OK;
   }
@@ -451,7 +471,7 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
       return ANTKV_EUNSUPPORTED;
   }
   if (rc) return rc;
-  decode_combine_kernel<<<(unsigned)rows, 128, 0, st>>>(wo, wm, wl, used, rows, c->d, out, lse);
+  decode_combine_kernel<<<(unsigned)rows, 128, (used + 2) * sizeof(float), st>>>(wo, wm, wl, used, rows, c->d, out, lse);
   ANTKV_LAUNCH_CHECK("decode_combine_kernel");
   return ANTKV_OK;
 }
