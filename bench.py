@@ -182,13 +182,14 @@ def measured_traffic(args):
 def launches_per_layer_step(cache, args, world):
     """Our kernel launches per layer-step on rank 0: the fused d8m256 step is
     one launch (N=1) or attention + merge (N>1); the staged / generic paths
-    run append, attention, split combine and the two eviction launches
-    (attention + combine + merge on a non-tail shard)."""
+    run append, attention (+ split merge in the staged kernel, a separate
+    combine launch in the generic one) and the two eviction launches."""
     vq = cache.config.vq
     fused = (args.kernel == "fast" and vq.d_sub == 8 and vq.m <= 256 and HQ == 4 * HKV)
+    staged = args.kernel == "fast" and not fused
     if world == 1:
-        return 1 if fused else 5
-    return 2 if fused else 3
+        return 1 if fused else (4 if staged else 5)
+    return 2 if fused else (2 if staged else 3)
 
 
 def smem_roofline(args, launch_ms, sm_mhz):

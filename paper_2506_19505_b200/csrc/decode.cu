@@ -23,7 +23,7 @@ int decode_fast_supported(const antkv_cache_desc &c);
 int decode_tc_supported(const antkv_cache_desc &c);
 int decode_tc_plan(const antkv_cache_desc &c, int requested);
 int decode_tc_launch(const antkv_cache_desc &c, const void *q, int qdtype, const int64_t *qpos, float *ws_o,
-                     float *ws_m, float *ws_l, int splits, cudaStream_t st);
+                     float *ws_m, float *ws_l, float *out, float *lse, int *cnt, int splits, cudaStream_t st);
 
 // Decode kernel choice: the fused d8m256 kernel, the staged tensor-core
 // kernel (decode_tc.cu, any other d = 128 code shape) or the generic one.
@@ -454,13 +454,8 @@ static int attention_impl(const antkv_cache_desc *c, const void *q, int dtype, c
                               splits, st);
   const int gq = c->Hq / c->Hkv;
   int rc;
-  if (mode == kStaged) {
-    rc = decode_tc_launch(*c, q, dtype, qpos, wo, wm, wl, used, st);
-    if (rc) return rc;
-    decode_combine_kernel<<<(unsigned)rows, 128, (used + 2) * sizeof(float), st>>>(wo, wm, wl, used, rows, c->d, out, lse);
-    ANTKV_LAUNCH_CHECK("decode_combine_kernel");
-    return ANTKV_OK;
-  }
+  if (mode == kStaged)   // one launch: partials + the last CTA's merge
+    return decode_tc_launch(*c, q, dtype, qpos, wo, wm, wl, out, lse, cnt, used, st);
   switch (gq) {
     case 1: rc = launch_generic<1>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;
     case 2: rc = launch_generic<2>(*c, q, dtype, qpos, wo, wm, wl, used, st); break;

@@ -29,7 +29,8 @@
 // R(-16 F omega) per stage (packed fp32), seeded from integer-reduced angles.
 // Pool tiles (anchors + window, K rotated at its own position, fp16 in
 // pool_f16) are bulk-copied and attended in the absolute frame.  Each CTA
-// writes an (o, m, l) partial; decode_combine_kernel merges the splits.
+// writes an (o, m, l) partial; the last CTA of each (sequence, head) (atomic
+// ticket) merges the splits.
 #include "common.cuh"
 
 namespace antkv {
@@ -52,6 +53,7 @@ struct __align__(128) TcSmem {
   unsigned long long cfull[TW][TNCS];
   unsigned long long pfull[TW];
   float mw[8][TW * 8 + 1];            // merge weights per head and source (+ M, L)
+  int ticket;
 };
 
 struct TcArgs {
@@ -59,6 +61,8 @@ struct TcArgs {
   int qdtype;
   const int64_t *qpos;    // [B]
   float *ws_o, *ws_m, *ws_l;
+  float *out, *lse;       // [B][Hq][128], [B][Hq] (lse may be NULL)
+  int *cnt;               // [B*Hkv] self-resetting CTA tickets
   int splits;
   int gq;                 // query heads per KV head (1, 2, 4, 8)
 };
@@ -518,6 +522,55 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
       O = fmaf(sm.mw[x][e], mo[((e / F) * 8 + x + GQ * (e % F)) * 128 + dim], O);
     a.ws_o[(((int64_t)split * c.B + b) * c.Hq + (int64_t)h * GQ + x) * 128 + dim] = O;
   }
+
+  // ---- the last CTA of (b, h) (atomic ticket) merges the splits' partials
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
+  __syncthreads();
+  if (sm.ticket != S - 1) return;
+  __threadfence();
+  if (warp < GQ) {   // warp x: query head h GQ + x, lane: 4 dims; loads of 16 splits in flight
+    const int64_t rows = (int64_t)c.B * c.Hq;
+    const int64_t row = (int64_t)b * c.Hq + (int64_t)h * GQ + warp;
+    const int d4 = 4 * lane;
+    float M = -INFINITY, L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int CH = 16;
+    for (int s0 = 0; s0 < S; s0 += CH) {
+      float ms[CH], ls[CH];
+      float4 v[CH];
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int s2 = min(s0 + u, S - 1);
+        ms[u] = __ldcg(a.ws_m + s2 * rows + row);
+        ls[u] = __ldcg(a.ws_l + s2 * rows + row);
+        v[u] = __ldcg(reinterpret_cast<const float4 *>(a.ws_o + (s2 * rows + row) * 128 + d4));
+      }
+      float mc = M;
+#pragma unroll
+      for (int u = 0; u < CH; ++u)
+        if (s0 + u < S) mc = fmaxf(mc, ms[u]);
+      if (mc == -INFINITY) continue;
+      const float al = (M == -INFINITY) ? 0.f : __expf(M - mc);
+      L *= al;
+      acc.x *= al; acc.y *= al; acc.z *= al; acc.w *= al;
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const float wv = (s0 + u >= S || ms[u] == -INFINITY) ? 0.f : __expf(ms[u] - mc);
+        L = fmaf(wv, ls[u], L);
+        acc.x = fmaf(wv, v[u].x, acc.x);
+        acc.y = fmaf(wv, v[u].y, acc.y);
+        acc.z = fmaf(wv, v[u].z, acc.z);
+        acc.w = fmaf(wv, v[u].w, acc.w);
+      }
+      M = mc;
+    }
+    const float inv = 1.f / L;
+    *reinterpret_cast<float4 *>(a.out + row * 128 + d4) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    if (lane == 0 && a.lse) a.lse[row] = M + logf(L);
+  }
+  if (threadIdx.x == 0) a.cnt[bh] = 0;
 }
 
 template <int DSUB, int CB>
@@ -564,8 +617,11 @@ int decode_tc_plan(const antkv_cache_desc &c, int requested) {
 }
 
 int decode_tc_launch(const antkv_cache_desc &c, const void *q, int qdtype, const int64_t *qpos, float *ws_o,
-                     float *ws_m, float *ws_l, int splits, cudaStream_t st) {
+                     float *ws_m, float *ws_l, float *out, float *lse, int *cnt, int splits, cudaStream_t st) {
   TcArgs a;
+  a.out = out;
+  a.lse = lse;
+  a.cnt = cnt;
   a.q = q;
   a.qdtype = qdtype;
   a.qpos = qpos;

@@ -612,17 +612,19 @@ def test_llama_caller_matches_dense_reference_when_lossless():
         assert rel(lg.cpu().numpy(), ref.cpu().numpy()) < 3e-2, i
 
 
-def test_sequence_sharded_decode_matches_single_cache():
+@pytest.mark.parametrize("notation", ["d8m256", "d32m4096"])
+def test_sequence_sharded_decode_matches_single_cache(notation):
     """Multi-GPU decode logic on one device: two shard caches (the head shard
     without a window; the tail shard with the window, the appends, the
     evictions and the global anchor count) merged with the LSE combine must
-    reproduce the single-cache decode outputs and anchor set."""
+    reproduce the single-cache decode outputs and anchor set (d8m256: fused
+    kernel; d32m4096, config #3's code: staged kernel + eviction launches)."""
     from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
     from paper_2506_19505_b200.parallel import lse_merge
-    vq = VqConfig.from_notation("d8m256")
+    vq = VqConfig.from_notation(notation)
     Hq, Hkv, n, steps, W = 4, 1, 900, 30, 8
     Q, K, V = qkv(51, Hq, Hkv, n + steps, 128, heavy=2)
-    ck, cv = codebooks(51, Hkv, 256, 8)
+    ck, cv = codebooks(51, Hkv, vq.m, vq.d_sub)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
     cfg = lambda w: CacheConfig(vq=vq, anchor_fraction=0.02, window_size=w)
     ref = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
