@@ -231,20 +231,20 @@ def algorithmic_bytes(cache, torch):
     return total
 
 
-def encode_throughput(torch, n=131072, reps=5):
+def encode_throughput(torch, n=131072, reps=5, vq_m=256, d_sub=8):
     """tokens/s through K+V encoding of all 8 KV heads of one layer."""
     from paper_2506_19505_b200 import _lib
-    vq_m, d_sub = 256, 8
     g = torch.Generator(device="cuda").manual_seed(7)
     X = torch.randn((2 * HKV, n, D), device="cuda", generator=g).to(torch.bfloat16)
     C = torch.randn((2 * HKV, vq_m, d_sub), device="cuda", generator=g)
-    codes = torch.empty((2 * HKV, n, D // d_sub), dtype=torch.uint8, device="cuda")
+    cbytes = 1 if vq_m <= 256 else 2
+    codes = torch.empty((2 * HKV, n, D // d_sub * cbytes), dtype=torch.uint8, device="cuda")
     st = _lib.stream()
 
     def run():
         for i in range(2 * HKV):
             _lib.call("antkv_vq_encode", _lib.ptr(X[i]), _lib.BF16, n, D, _lib.ptr(C[i]), vq_m,
-                      d_sub, _lib.ptr(codes[i]), 1, st)
+                      d_sub, _lib.ptr(codes[i]), cbytes, st)
     run()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -256,7 +256,7 @@ def encode_throughput(torch, n=131072, reps=5):
     ms = e0.elapsed_time(e1) / reps
     flops = n * 2 * HKV * (D // d_sub) * vq_m * d_sub * 2
     return {"value": n / (ms / 1e3), "unit": "tok/s", "ms_per_layer": ms, "tokens": n,
-            "config": "d8m256, K+V, 8 KV heads, d=128, float32 distances",
+            "config": f"d{d_sub}m{vq_m}, K+V, 8 KV heads, d=128, float32 distances",
             "tflops": flops / (ms / 1e3) / 1e12}
 
 

@@ -93,6 +93,11 @@ int launch_encode_mma(const void *X, int dtype, int64_t rows, int d, int64_t x_s
                       int64_t code_tile_stride, int64_t code_row_stride, const float *d2,
                       cudaStream_t st);
 
+int launch_encode_tc(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride, int nsets,
+                     const float *codebooks, int cb_mod, int m, int d_sub, void *codes, int code_bytes,
+                     int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
+                     const float *d2, cudaStream_t st);
+
 int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride,
                   int nsets, const float *codebooks, int cb_mod, int m, int d_sub,
                   void *codes, int code_bytes, int64_t code_set_stride,
@@ -102,6 +107,13 @@ int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_s
     const int rc = launch_encode_mma(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m,
                                      d_sub, codes, code_bytes, code_set_stride, code_tile_stride,
                                      code_row_stride, d2, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+  }
+  // d_sub 16 / 32 / 64, any m, 16-bit inputs: tensor-core encoder (encode_tc.cu)
+  {
+    const int rc = launch_encode_tc(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m, d_sub,
+                                    codes, code_bytes, code_set_stride, code_tile_stride, code_row_stride,
+                                    d2, st);
     if (rc != ANTKV_EUNSUPPORTED) return rc;
   }
   ANTKV_REQUIRE(d_sub >= 1 && d_sub <= 64, "d_sub must be in [1, 64] on the GPU path");

@@ -504,6 +504,35 @@ def test_tensor_core_encoder_matches_oracle(dtype, m, code_bytes):
     assert not np.any(got == 7)
 
 
+@pytest.mark.parametrize("dtype,d_sub,m,code_bytes", [(torch.bfloat16, 32, 4096, 2), (torch.float16, 32, 4096, 2),
+                                                      (torch.bfloat16, 16, 256, 1), (torch.bfloat16, 64, 300, 2),
+                                                      (torch.bfloat16, 16, 4096, 2)])
+def test_tensor_core_encoder_long_codebooks(dtype, d_sub, m, code_bytes):
+    """encode_tc.cu (d_sub 16 / 32 / 64, any m; config #3's d32m4096): codes
+    vs the exhaustive float64 argmin of the oracle (margin rule), with a
+    duplicated centroid (ties -> lowest index), large and tiny rows and a
+    ragged row count."""
+    from paper_2506_19505_b200 import _lib
+    rng = np.random.default_rng(37)
+    n = 1999
+    X = rng.standard_normal((n, 128)).astype(np.float32)
+    X[:40] *= 40.0
+    X[40:80] *= 1e-3
+    C = rng.standard_normal((m, d_sub)).astype(np.float32)
+    C[m - 1] = C[5]                     # duplicate: index 5 must win
+    Xt = torch.from_numpy(X).cuda().to(dtype)
+    Ct = torch.from_numpy(C).cuda()
+    G = 128 // d_sub
+    codes = torch.empty((n, G), dtype=torch.uint8 if code_bytes == 1 else torch.int16, device="cuda")
+    _lib.call("antkv_vq_encode", _lib.ptr(Xt), _lib.dtype_tag(Xt), n, 128, _lib.ptr(Ct), m, d_sub,
+              _lib.ptr(codes), code_bytes, _lib.stream())
+    got = codes.cpu().numpy().astype(np.int64) & 0xffff
+    Xd = Xt.float().cpu().numpy().astype(np.float64).reshape(-1, d_sub)
+    ref, _ = O.assign_nearest(Xd, C.astype(np.float64))
+    assert_codes_parity(Xd, C, got.reshape(-1), ref)
+    assert not np.any(got == m - 1)
+
+
 @pytest.mark.parametrize("scale", [1.0, 300.0, 1e-3])
 def test_tensor_core_flash_aux_noncausal_and_scaled(scale):
     """prefill_mma.cu through the _ckernels shim: non-causal, n_q != n_k,
