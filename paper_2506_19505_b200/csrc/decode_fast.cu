@@ -198,6 +198,8 @@ struct StepArgs {
   int splits;              // CTAs per (b, head)
   int early;               // the previous kernel in the stream wrote no state of this
                            // cache: read cache state before griddepcontrol.wait
+  int early_q;             // ... and none of q / qpos: the query rows, its position and
+                           // the frame angles come before the wait too
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
 };
 
@@ -702,7 +704,20 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
                  FK_CB_BYTES, &sm.cbbar);
     mbar_expect_tx(&sm.tbar, sizeof(FastTables));
     tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
+    if (a.early_q) {
+      mbar_expect_tx(&sm.qbar, qbytes);
+      tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
+                   qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
+    }
   }
+  // Cache state is read before the wait only when the host knows the
+  // previous kernel in the stream did not write this cache (a.early); the
+  // loads and the table copy are in flight together.
+  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n = c.seq_len[b];
+  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
+  const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
+  int64_t qp = a.early_q ? a.qpos[b] : 0;
   // key-rotation constants and frame steps into registers (tables only)
   WarpState w;
   mbar_wait(&sm.tbar, 0);
@@ -720,12 +735,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       w.kc[s][4 * u + 3] = k.w;
     }
   }
-  // Cache state is read before the wait only when the host knows the
-  // previous kernel in the stream did not write this cache (a.early).
-  if (!a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int n = c.seq_len[b];
-  const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
-  const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
   FK_TR(2);
 
   // ---- phase 1 (needs n / pool_high): work split, bulk copies of the code
@@ -779,25 +788,10 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     kd0 = kinds[(pt0 + warp) * 16 + g];
     kd1 = kinds[(pt0 + warp) * 16 + g + 8];
   }
-  // inputs produced by earlier kernels (q, positions, the appended rows) are
-  // read after the previous kernel completed; only then may the next kernel
-  // start (a dependency chain of depth one)
-  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int64_t qp = a.qpos[b];
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&sm.qbar, qbytes);
-    tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
-                 qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
-  }
-  FK_TR(3);
-
-  // ---- phase 2: (cos, sin) of every query frame of the CTA, cooperatively
-  // from float64-reduced angles (frame 2w + e: warp w's even / odd tile
-  // frame; frame 16: the absolute frame p_q of the pool rows)
-  mbar_wait(&sm.qbar, 0);
-  const double pq = static_cast<double>(qp);
-  {
+  // (cos, sin) of every query frame of the CTA, cooperatively from
+  // integer-reduced angles (frame 2w + e: warp w's even / odd tile frame;
+  // frame 16: the absolute frame p_q of the pool rows)
+  auto frame_angles = [&]() {
     for (int e = threadIdx.x; e < (2 * FK_WARPS + 1) * 64; e += FK_THREADS) {
       const int f = e >> 6, p = e & 63;
       const int64_t delta = f < 2 * FK_WARPS
@@ -807,6 +801,30 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       turns_cs(delta, sm.tab.turns[p], cs, sn);
       sm.ang[f][lane_pair_pos(p)] = make_float2(cs, sn);
     }
+  };
+  if (a.early_q) frame_angles();
+  FK_TR(5);
+  // inputs produced by earlier kernels (q, positions, the appended rows) are
+  // read after the previous kernel completed unless the host vouched for
+  // them (early / early_q); only then may the next kernel start (a
+  // dependency chain of depth one)
+  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (!a.early_q) {
+    qp = a.qpos[b];
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&sm.qbar, qbytes);
+      tma_bulk_g2s(sm.qraw, reinterpret_cast<const uint8_t *>(a.q) + ((int64_t)b * c.Hq + h * 4) * (qbytes / 4),
+                   qbytes, &sm.qbar);   // rows h*4 .. h*4+3 of sequence b
+    }
+  }
+  FK_TR(3);
+
+  // ---- phase 2: query rows, frames (the angles overlap the query copy)
+  if (!a.early_q) frame_angles();
+  mbar_wait(&sm.qbar, 0);
+  const double pq = static_cast<double>(qp);
+  {
     const float sc = rsqrtf(128.f) * 1.4426950408889634f;   // 1/sqrt(d) * log2(e)
     for (int e = threadIdx.x; e < 256; e += FK_THREADS)
       sm.qf[e >> 6][lane_pair_pos(e & 63)] =
@@ -880,7 +898,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
         kd1 = kinds[tile * 16 + g + 8];
       }
       const uint32_t mrow = (kd0 != ANTKV_KIND_FREE ? 1u : 0u) | (kd1 != ANTKV_KIND_FREE ? 2u : 0u);
-      if (r == 0) FK_TR(5);
       mbar_wait(&sm.pfull[warp], r & 1);
       pool_tile(w, smem_u32(&sm.pool[warp][0]), bqa, mrow, lo);
       __syncwarp();
@@ -1172,7 +1189,17 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   decode_fast_plan(c, splits, cs, ps);
   a.splits = cs + ps;
   a.trace = debug_trace_buffer();
+  if (a.trace) {   // two halves, alternating per launch: the previous launch stays readable
+    static unsigned launch_no = 0;
+    a.trace += (size_t)(launch_no++ & 1) * FK_TRACE_WORDS * 32768;
+  }
   a.early = previous_cache_on_stream(st, c.codes) != c.codes;
+  // q / qpos before the wait too, unless the previous fused launch on this
+  // stream (the only kernel that can still be running then) wrote them
+  a.early_q = a.early && !overlaps_previous_fast_outputs(st, q, (int64_t)c.B * c.Hq * 128 * dtype_size(qdtype)) &&
+              !overlaps_previous_fast_outputs(st, qpos, (int64_t)c.B * sizeof(int64_t));
+  record_fast_outputs(st, out, (int64_t)c.B * c.Hq * 128 * sizeof(float), lse,
+                      lse ? (int64_t)c.B * c.Hq * sizeof(float) : 0);
   const size_t smem = sizeof(FastSmem);
   static bool attr_set = false;
   if (!attr_set) {

@@ -21,6 +21,41 @@ const void *previous_cache_on_stream(cudaStream_t st, const void *key) {
 }
 
 
+namespace {
+struct FastOutputs {
+  const char *out = nullptr, *lse = nullptr;
+  int64_t out_bytes = 0, lse_bytes = 0;
+};
+std::mutex g_fo_mu;
+std::unordered_map<cudaStream_t, FastOutputs> g_fo;
+bool overlap(const char *a, int64_t na, const char *b, int64_t nb) {
+  return a && b && na > 0 && nb > 0 && a < b + nb && b < a + na;
+}
+}  // namespace
+
+// The fused decode kernel lets its successor on the stream start early
+// (programmatic dependent launch): these record what the last fused launch
+// on a stream writes besides its own cache, so the next one knows whether
+// its q / qpos may be read before griddepcontrol.wait.
+void record_fast_outputs(cudaStream_t st, const void *out, int64_t out_bytes, const void *lse,
+                         int64_t lse_bytes) {
+  std::lock_guard<std::mutex> lock(g_fo_mu);
+  FastOutputs &f = g_fo[st];
+  f.out = static_cast<const char *>(out);
+  f.out_bytes = out_bytes;
+  f.lse = static_cast<const char *>(lse);
+  f.lse_bytes = lse_bytes;
+}
+
+bool overlaps_previous_fast_outputs(cudaStream_t st, const void *p, int64_t bytes) {
+  std::lock_guard<std::mutex> lock(g_fo_mu);
+  auto it = g_fo.find(st);
+  if (it == g_fo.end()) return false;
+  const char *c = static_cast<const char *>(p);
+  return overlap(c, bytes, it->second.out, it->second.out_bytes) ||
+         overlap(c, bytes, it->second.lse, it->second.lse_bytes);
+}
+
 static thread_local char g_err[512] = "";
 
 void set_error(const char *fmt, ...) {
