@@ -594,10 +594,11 @@ def cpu_sample_from_cache(cache, n_heads):
     t = cache.tensors
     n = cache.token_count
     G = D // cache.config.vq.d_sub
-    cb = 1 if cache.config.vq.index_bits <= 8 else 2
+    from paper_2506_19505_b200.cache import unpack_units
     cap = t["codes"].shape[2]
     # tiled layout [tile][kv][16 slots][G] code units (common.cuh code_offset)
-    units = t["codes"][0, :n_heads].cpu().numpy().reshape(n_heads, -1).view(np.uint8 if cb == 1 else np.uint16)
+    raw = t["codes"][0, :n_heads].cpu().numpy().reshape(n_heads, -1)
+    units = np.stack([unpack_units(raw[h], cache.desc.code_bytes) for h in range(n_heads)])
     codes = units.reshape(n_heads, cap // 16, 2, 16, G).transpose(0, 1, 3, 2, 4).reshape(n_heads, cap, 2, G)[:, :n]
     qm = t["qmask"][0, :n_heads].cpu().numpy().view(np.uint32)
     items = []

@@ -196,7 +196,9 @@ ANTKV_API int antkv_vq_decode(const void *codes, int code_bytes, int64_t rows, i
  * memory owned by the caller; sizes follow the bracketed shapes. */
 typedef struct antkv_cache_desc {
   int B, Hq, Hkv, d, d_sub, m, groups, index_bits;
-  int code_bytes;      /* 1 when index_bits <= 8, else 2                   */
+  int code_bytes;      /* 1 when index_bits <= 8; 3 = 12-bit indices packed
+                          two per 3 bytes (index_bits <= 12, groups a power
+                          of two <= 32); else 2                             */
   int capacity;        /* token slots per sequence                         */
   int pool_capacity;   /* full-precision row slots per (b, kv head)        */
   int window_size;
@@ -207,7 +209,9 @@ typedef struct antkv_cache_desc {
   double anchor_fraction;
   double theta_base;
   int64_t token_offset;/* global index of slot 0 (sequence sharding)       */
-  uint8_t *codes;      /* [B][Hkv][capacity][2][groups*code_bytes]         */
+  uint8_t *codes;      /* [B][Hkv][capacity/16 tiles][K 16 x groups | V 16 x
+                          groups] code units (code_bytes wide, or 12-bit
+                          packed: a slot's K+V codes take 3*groups bytes)   */
   uint32_t *qmask;     /* [B][Hkv][capacity/32] bit = slot holds codes     */
   void *pool_rows;     /* [B][Hkv][pool_capacity][2][d] (K row, V row)    */
   int32_t *pool_tok;   /* [B][Hkv][pool_capacity] token slot, -1 free      */

@@ -91,6 +91,51 @@ def _round_up(x, m):
     return (x + m - 1) // m * m
 
 
+def _code_kind(vq, groups):
+    """Code unit of the device layout (antkv_cache_desc::code_bytes): 1 byte
+    for m <= 256, 3 = 12-bit indices packed two per three bytes (m <= 4096,
+    a power-of-two number of groups <= 32: config #3's 0.375-bit d32m4096
+    really takes 0.375 bit per element), else 2 bytes."""
+    if vq.index_bits <= 8:
+        return 1
+    if vq.index_bits <= 12 and 2 <= groups <= 32 and groups & (groups - 1) == 0:
+        return 3
+    return 2
+
+
+def _slot_code_bytes(kind, groups):
+    return 3 * groups if kind == 3 else 2 * groups * kind
+
+
+def unpack_units(raw, kind):
+    """uint8 code stream -> code units (uint16) for a device code kind."""
+    raw = np.asarray(raw, dtype=np.uint8).reshape(-1)
+    if kind == 1:
+        return raw.astype(np.uint16)
+    if kind == 2:
+        return raw.view(np.uint16)
+    t = raw.reshape(-1, 3).astype(np.uint16)
+    out = np.empty((t.shape[0], 2), dtype=np.uint16)
+    out[:, 0] = t[:, 0] | ((t[:, 1] & 0xF) << 8)
+    out[:, 1] = (t[:, 1] >> 4) | (t[:, 2] << 4)
+    return out.reshape(-1)
+
+
+def pack_units(units, kind):
+    """code units -> uint8 code stream for a device code kind."""
+    u = np.asarray(units).reshape(-1)
+    if kind == 1:
+        return u.astype(np.uint8)
+    if kind == 2:
+        return u.astype(np.uint16).view(np.uint8)
+    u = u.astype(np.uint16).reshape(-1, 2)
+    out = np.empty((u.shape[0], 3), dtype=np.uint8)
+    out[:, 0] = u[:, 0] & 0xFF
+    out[:, 1] = ((u[:, 0] >> 8) & 0xF) | ((u[:, 1] & 0xF) << 4)
+    out[:, 2] = u[:, 1] >> 4
+    return out.reshape(-1)
+
+
 class QuantizedKVCache:
     """Anchor rows + sub-vector codes + a full-precision recent window, on
     the GPU (cache.py:68-98)."""
@@ -149,12 +194,12 @@ class QuantizedKVCache:
         dev = torch.device("cuda", torch.cuda.current_device())
         B, H, d = self.B, self.Hkv, self.d
         G = d // cfg.d_sub
-        cb = 1 if cfg.index_bits <= 8 else 2
+        kind = _code_kind(cfg, G)
         P = self._pool_capacity(cap)
         W = self.config.window_size
         old = self._t
         t = {
-            "codes": torch.zeros((B, H, cap, 2 * G * cb), dtype=torch.uint8, device=dev),
+            "codes": torch.zeros((B, H, cap, _slot_code_bytes(kind, G)), dtype=torch.uint8, device=dev),
             "qmask": torch.zeros((B, H, cap // 32), dtype=torch.int32, device=dev),
             "pool_rows": torch.zeros((B, H, P, 2, d), dtype=self.row_dtype or torch.bfloat16,
                                      device=dev),
@@ -171,7 +216,7 @@ class QuantizedKVCache:
         }
         use_fast = bool(self.fast) and d == 128 and cfg.d_sub == 8 and cfg.m <= 256
         use_tc = (bool(self.fast) and d == 128 and cfg.d_sub in (4, 8, 16, 32, 64)
-                  and G * cb <= 32)
+                  and _slot_code_bytes(kind, G) // 2 <= 32)
         if use_fast:
             t["cb_f16"] = torch.zeros((H, 256, 2, 64), dtype=torch.float16, device=dev)
         if use_tc:
@@ -216,7 +261,7 @@ class QuantizedKVCache:
         D = _lib.CacheDesc()
         D.B, D.Hq, D.Hkv, D.d = self.B, self.Hq, self.Hkv, self.d
         D.d_sub, D.m, D.groups, D.index_bits = cfg.d_sub, cfg.m, self.d // cfg.d_sub, cfg.index_bits
-        D.code_bytes = 1 if cfg.index_bits <= 8 else 2
+        D.code_bytes = _code_kind(cfg, self.d // cfg.d_sub)
         D.capacity, D.pool_capacity, D.window_size = cap, P, self.config.window_size
         D.policy = _lib.POLICY[self.config.policy]
         D.anchor_count = -1 if self.config.anchor_count is None else int(self.config.anchor_count)
@@ -518,10 +563,9 @@ class QuantizedKVCache:
         """(k_codes, v_codes) dicts {token: int64[groups]} for quantized tokens."""
         st = self._host_state()
         G = self.d // self.config.vq.d_sub
-        cb = 1 if self.config.vq.index_bits <= 8 else 2
         cap = st["codes"].shape[2]
         raw = st["codes"][b, h].numpy().reshape(-1)
-        units = raw.view(np.uint8 if cb == 1 else np.uint16)
+        units = unpack_units(raw, _code_kind(self.config.vq, G))
         # tiled layout [tile][kv][16 slots][G] (common.cuh code_offset)
         arr = units.reshape(cap // 16, 2, 16, G).transpose(0, 2, 1, 3).reshape(cap, 2, G)
         arr = arr[:self._n].astype(np.int64)
@@ -667,12 +711,12 @@ class QuantizedKVCache:
         self._ensure_capacity(n + 1)
         t = self._t
         G = d // self.config.vq.d_sub
-        cbw = 1 if self.config.vq.index_bits <= 8 else 2
+        kind = _code_kind(self.config.vq, G)
         cap = t["codes"].shape[2]
-        rec = np.zeros((cap, 2, G), dtype=np.uint8 if cbw == 1 else np.uint16)
+        rec = np.zeros((cap, 2, G), dtype=np.uint16)
         rec[:n, 0], rec[:n, 1] = kcodes, vcodes
-        tiled = rec.reshape(cap // 16, 16, 2, G).transpose(0, 2, 1, 3).reshape(cap, -1)
-        t["codes"][0, 0] = torch.from_numpy(np.ascontiguousarray(tiled).view(np.uint8)).cuda()
+        tiled = rec.reshape(cap // 16, 16, 2, G).transpose(0, 2, 1, 3).reshape(-1)
+        t["codes"][0, 0] = torch.from_numpy(pack_units(tiled, kind).reshape(cap, -1)).cuda()
         qbits = np.zeros(t["qmask"].shape[-1] * 32, dtype=np.uint8)
         P = t["pool_tok"].shape[-1]
         ptok = np.full(P, -1, np.int32)

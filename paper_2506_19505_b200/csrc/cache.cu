@@ -80,6 +80,18 @@ vq_encode_kernel(const void *__restrict__ X, int dtype, int64_t rows, int d,
     if (live)
       for (int c = 0; c < cn; ++c) nearest_update<MAXD>(x, sC + c * d_sub, d_sub, c0 + c, best, best_i);
   }
+  if (code_bytes == 3) {
+    // 12-bit packed rows: lane g == 0 of each row gathers the row's codes
+    // (a row's items are consecutive lanes; groups divide 32)
+    uint32_t row_codes[32];
+    const int lane = threadIdx.x & 31;
+    for (int k = 0; k < groups; ++k) row_codes[k] = __shfl_sync(0xffffffffu, (uint32_t)best_i, lane - g + k);
+    if (live && g == 0)
+      code_put_row(static_cast<uint8_t *>(codes), set * code_set_stride + (r >> 4) * code_tile_stride +
+                   (r & 15) * code_row_stride, groups, row_codes, 3);
+    if (live && d2out) d2out[set * rows * groups + item] = best;
+    return;
+  }
   if (live) {
     store_code(codes, set * code_set_stride + (r >> 4) * code_tile_stride + (r & 15) * code_row_stride + g,
                code_bytes, best_i);
@@ -466,12 +478,14 @@ __global__ void cache_evict_commit_kernel(antkv_cache_desc c) {
     hs[ANTKV_HS_ANCHORS] += 1;
   } else {
     unsigned long long *sk = c.evict_scratch + bh * 2 * c.groups;
-    for (int u = 0; u < 2 * c.groups; ++u) {   // the encoder's minima -> codes; reset the slots
-      const int idx = static_cast<int>(sk[u] & 0xffffffffu);
-      sk[u] = ~0ull;
-      const int64_t off = bh * c.capacity * 2 * c.groups + code_offset(p.j, u / c.groups, u % c.groups, c.groups);
-      if (c.code_bytes == 1) c.codes[off] = static_cast<uint8_t>(idx);
-      else reinterpret_cast<uint16_t *>(c.codes)[off] = static_cast<uint16_t>(idx);
+    uint32_t row[128];
+    for (int kv = 0; kv < 2; ++kv) {   // the encoder's minima -> the code rows; reset the slots
+      for (int g = 0; g < c.groups; ++g) {
+        row[g] = static_cast<uint32_t>(sk[kv * c.groups + g] & 0xffffffffu);
+        sk[kv * c.groups + g] = ~0ull;
+      }
+      code_put_row(c.codes, bh * c.capacity * 2 * c.groups + code_offset(p.j, kv, 0, c.groups), c.groups, row,
+                   c.code_bytes);
     }
     atomicOr(&c.qmask[bh * (c.capacity / 32) + p.j / 32], 1u << (p.j % 32));
     c.pool_kind[bh * c.pool_capacity + p.slot] = ANTKV_KIND_FREE;
@@ -495,10 +509,7 @@ __global__ void cache_dequant_codes_kernel(antkv_cache_desc c, int n, float *__r
     const int g = t / c.d_sub, e = t % c.d_sub;
     const int64_t hb = bh * c.capacity * 2 * c.groups;
     const int64_t ok = hb + code_offset(j, 0, g, c.groups), ov = hb + code_offset(j, 1, g, c.groups);
-    int ck, cv;
-    if (c.code_bytes == 1) { ck = c.codes[ok]; cv = c.codes[ov]; }
-    else { ck = reinterpret_cast<const uint16_t *>(c.codes)[ok];
-           cv = reinterpret_cast<const uint16_t *>(c.codes)[ov]; }
+    const int ck = code_get(c.codes, ok, c.code_bytes), cv = code_get(c.codes, ov, c.code_bytes);
     kv = c.codebook_k[((int64_t)h * c.m + ck) * c.d_sub + e];
     vv = c.codebook_v[((int64_t)h * c.m + cv) * c.d_sub + e];
   }
@@ -547,7 +558,10 @@ static int check_desc(const antkv_cache_desc *c) {
   ANTKV_REQUIRE(c->d >= 2 && c->d % 2 == 0 && c->d <= 256, "head dimension must be even and <= 256");
   ANTKV_REQUIRE(c->d_sub >= 1 && c->d % c->d_sub == 0, "d=%d not divisible by d_sub=%d", c->d, c->d_sub);
   ANTKV_REQUIRE(c->groups == c->d / c->d_sub, "groups mismatch");
-  ANTKV_REQUIRE(c->code_bytes == (c->index_bits <= 8 ? 1 : 2), "code_bytes mismatch");
+  ANTKV_REQUIRE(c->code_bytes == (c->index_bits <= 8 ? 1 : 2) ||
+                    (c->code_bytes == 3 && c->index_bits <= 12 && c->groups >= 2 && c->groups <= 32 &&
+                     (c->groups & (c->groups - 1)) == 0),
+                "code_bytes mismatch");
   ANTKV_REQUIRE(c->index_bits <= 16, "index_bits > 16 unsupported");
   ANTKV_REQUIRE(c->row_dtype == ANTKV_BF16 || c->row_dtype == ANTKV_F16 || c->row_dtype == ANTKV_F32,
                 "bad row dtype");
@@ -602,7 +616,7 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
                      nullptr, st);
   if (rc) return rc;
   rc = launch_encode(V, dtype, n, c->d, (int64_t)n * c->d, nsets, c->codebook_v, c->Hkv, c->m,
-                     c->d_sub, c->codes + 16 * G * c->code_bytes, c->code_bytes,
+                     c->d_sub, c->codes + code_stream_bytes(16 * G, c->code_bytes), c->code_bytes,
                      (int64_t)c->capacity * 2 * G, 32 * G, G, nullptr, st);
   if (rc) return rc;
   cache_build_kernel<<<nsets, 256, 0, st>>>(*c, K, V, dtype, positions, n, anchors, n_anchors);

@@ -127,6 +127,37 @@ __host__ __device__ __forceinline__ int64_t code_offset(int64_t slot, int kv, in
   return (slot >> 4) * (32 * (int64_t)G) + kv * (16 * G) + (slot & 15) * G + g;
 }
 
+// Cache code units (antkv_cache_desc::code_bytes): 1 byte, 2 bytes, or 3 =
+// 12-bit indices packed two per three bytes (unit u at bits [12u, 12u + 12)
+// of the byte stream, little-endian).  Rows hold an even number of groups
+// when packed, so every row starts on a byte and is written whole.
+__host__ __device__ __forceinline__ int64_t code_stream_bytes(int64_t units, int cb) {
+  return cb == 3 ? units * 3 / 2 : units * cb;
+}
+__device__ __forceinline__ uint32_t code_get(const uint8_t *base, int64_t unit, int cb) {
+  if (cb == 1) return base[unit];
+  if (cb == 2) return reinterpret_cast<const uint16_t *>(base)[unit];
+  const int64_t bit = 12 * unit;
+  const uint8_t *p = base + (bit >> 3);
+  const uint32_t v = p[0] | ((uint32_t)p[1] << 8);
+  return (v >> (bit & 7)) & 0xfffu;
+}
+// The G codes of one row: units unit0 .. unit0 + G - 1 (unit0 a multiple of G).
+__device__ __forceinline__ void code_put_row(uint8_t *base, int64_t unit0, int G, const uint32_t *v, int cb) {
+  if (cb == 1) {
+    for (int g = 0; g < G; ++g) base[unit0 + g] = static_cast<uint8_t>(v[g]);
+  } else if (cb == 2) {
+    for (int g = 0; g < G; ++g) reinterpret_cast<uint16_t *>(base)[unit0 + g] = static_cast<uint16_t>(v[g]);
+  } else {
+    uint8_t *p = base + (12 * unit0 >> 3);
+    for (int g = 0; g + 1 < G; g += 2, p += 3) {
+      p[0] = static_cast<uint8_t>(v[g]);
+      p[1] = static_cast<uint8_t>(((v[g] >> 8) & 0xfu) | ((v[g + 1] & 0xfu) << 4));
+      p[2] = static_cast<uint8_t>(v[g + 1] >> 4);
+    }
+  }
+}
+
 // Fast-path pool tile layout (antkv_cache_desc::pool_f16), in halves from the
 // (sequence, head) base: 16-slot tiles of [K rotated | V][16 slots][128], the
 // 16-byte chunk c of slot r stored at chunk c ^ (r & 7) so the eight row

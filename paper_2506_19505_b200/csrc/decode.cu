@@ -12,7 +12,7 @@ namespace antkv {
 constexpr int DG_T = 128;  // items per chunk == threads per CTA
 
 __device__ __forceinline__ int load_code_unit(const antkv_cache_desc &c, int64_t off) {
-  return c.code_bytes == 1 ? c.codes[off] : reinterpret_cast<const uint16_t *>(c.codes)[off];
+  return static_cast<int>(code_get(c.codes, off, c.code_bytes));
 }
 
 int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, const void *knew,

@@ -238,9 +238,10 @@ __device__ __forceinline__ uint32_t code_unit(const uint32_t (&cw)[NW], int g) {
 template <int DSUB, int CB>
 __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, TcArgs a) {
   constexpr int G = 128 / DSUB;
-  constexpr int RCB = G * CB;                 // code bytes of one token row (one side)
-  constexpr int NW = RCB >= 4 ? RCB / 4 : 1;  // 32-bit words of them
-  constexpr int TILEB = 32 * G * CB;          // code bytes of one 16-slot tile (K + V)
+  // CB = 3: 12-bit indices packed two per three bytes (common.cuh code_get)
+  constexpr int RCB = CB == 3 ? G * 3 / 2 : G * CB;   // code bytes of one token row (one side)
+  constexpr int NW = RCB >= 4 ? RCB / 4 : 1;          // 32-bit words of them
+  constexpr int TILEB = 32 * RCB;                     // code bytes of one 16-slot tile (K + V)
   constexpr int TPS = TCS / TILEB;            // tiles per code ring slot
   static_assert(TPS >= 1, "code tile larger than a ring slot");
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   const int wt0 = T0 + warp * Tw;
   const int nt = max(0, min(Tw, ntiles - wt0));
   const int nslots = (nt + TPS - 1) / TPS;
-  const uint8_t *codes = c.codes + bh * (int64_t)c.capacity * 2 * G * CB;
+  const uint8_t *codes = c.codes + bh * (int64_t)c.capacity / 16 * TILEB;   // per-head code stream
   auto issue_code = [&](int k) {   // ring slot k % TNCS <- tiles wt0 + k TPS ..
     const int cnt = min(TPS, nt - k * TPS);
     unsigned long long *bar = &sm.cfull[warp][k % TNCS];
@@ -371,14 +372,14 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int kvv = i >> 3, rr = (2 * i + rsel) & 15;
-          const uint8_t *u = cpt + kvv * 16 * RCB + rr * RCB + gq * CB;
-          const uint32_t code = min(CB == 1 ? (uint32_t)*u : (uint32_t)*reinterpret_cast<const uint16_t *>(u), mmax);
+          const uint32_t code = min(code_get(cpt, (int64_t)(kvv * 16 + rr) * G + gq, CB), mmax);
           cpa16(sb + kvv * 4096 + rr * 256 + ((jc ^ (rr & 7)) << 4), cb0 + kvv * side + (int64_t)code * (DSUB * 2));
         }
       } else {
       const uint8_t *cp = &sm.code[warp][slot][(j % TPS) * TILEB + kv * 16 * RCB + r * RCB];
       uint32_t cw[NW];
-      if (RCB >= 16) {
+      if (CB == 3) {
+      } else if (RCB >= 16) {
 #pragma unroll
         for (int i = 0; i < NW; i += 4) {
           const uint4 v = *reinterpret_cast<const uint4 *>(cp + 4 * i);
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
       const uint32_t dst = su32(&sm.stage[warp][j % TNST][0]) + kv * 4096 + r * 256;
 #pragma unroll
       for (int gg = 0; gg < G; ++gg) {
-        const uint32_t code = min(code_unit<CB, NW>(cw, gg), mmax);
+        const uint32_t code = min(CB == 3 ? code_get(cp, gg, 3) : code_unit<CB, NW>(cw, gg), mmax);
         const uint8_t *src = cbase + (int64_t)code * (DSUB * 2);
         if (DSUB >= 8) {
 #pragma unroll
@@ -605,7 +606,7 @@ int decode_tc_supported(const antkv_cache_desc &c) {
   const int gq = c.Hq / c.Hkv;
   if (gq != 1 && gq != 2 && gq != 4 && gq != 8) return 0;
   if (c.d_sub != 4 && c.d_sub != 8 && c.d_sub != 16 && c.d_sub != 32 && c.d_sub != 64) return 0;
-  if ((128 / c.d_sub) * c.code_bytes > 32) return 0;
+  if (code_stream_bytes(128 / c.d_sub, c.code_bytes) > 32) return 0;
   return c.codebook_f16g != nullptr && c.pool_f16 != nullptr && c.fast_tables != nullptr &&
          c.capacity % 32 == 0 && c.pool_capacity % 16 == 0 && c.m >= 1 && c.m <= 65536;
 }
@@ -641,6 +642,10 @@ int decode_tc_launch(const antkv_cache_desc &c, const void *q, int qdtype, const
     case 32 * 4 + 2: return launch_tc<32, 2>(c, a, st);
     case 64 * 4 + 1: return launch_tc<64, 1>(c, a, st);
     case 64 * 4 + 2: return launch_tc<64, 2>(c, a, st);
+    case 8 * 4 + 3: return launch_tc<8, 3>(c, a, st);
+    case 16 * 4 + 3: return launch_tc<16, 3>(c, a, st);
+    case 32 * 4 + 3: return launch_tc<32, 3>(c, a, st);
+    case 64 * 4 + 3: return launch_tc<64, 3>(c, a, st);
     default:
       set_error("staged tensor-core decode: d_sub=%d code_bytes=%d unsupported", c.d_sub, c.code_bytes);
       return ANTKV_EUNSUPPORTED;

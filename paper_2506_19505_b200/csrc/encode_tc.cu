@@ -202,6 +202,7 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
     }
   }
   // reduce over the 4 lanes of a row: smaller distance, then lower index
+  __shared__ uint32_t spk[ET_WARPS][ET_RT * 16];   // 12-bit packing: the warp's codes by sub-vector
 #pragma unroll
   for (int rt = 0; rt < ET_RT; ++rt) {
 #pragma unroll
@@ -215,12 +216,24 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
         if (ob < b || (ob == b && oi < bi)) { b = ob; bi = oi; }
       }
       const int64_t sv = sv0 + rt * 16 + g + 8 * h;
+      if (code_bytes == 3) {
+        if (t == 0) spk[warp][rt * 16 + g + 8 * h] = static_cast<uint32_t>(bi);
+        continue;
+      }
       if (t == 0 && sv < nsub) {
         const int64_t r = sv / G;
         const int gg = static_cast<int>(sv - r * G);
         store_code_u(codes, set * code_set_stride + (r >> 4) * code_tile_stride + (r & 15) * code_row_stride + gg,
                      code_bytes, bi);
       }
+    }
+  }
+  if (code_bytes == 3) {   // whole rows (G | 64, so the warp's 64 sub-vectors are 64 / G rows)
+    __syncwarp();
+    if (lane < ET_RT * 16 / G && sv0 + lane * G < nsub) {
+      const int64_t r = (sv0 + lane * G) / G;
+      code_put_row(static_cast<uint8_t *>(codes), set * code_set_stride + (r >> 4) * code_tile_stride +
+                   (r & 15) * code_row_stride, G, &spk[warp][lane * G], 3);
     }
   }
 }
