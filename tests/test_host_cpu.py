@@ -332,3 +332,20 @@ def test_generate_qkv_matches_reference_streams():
         assert float(np.asarray(data["Q"], np.float64).sum()) == g[name]["data_Q_sum"]
     hh = generate_qkv(1, 300, 8, "heavy_hitter")
     assert hh["planted"] == [1, 3, 5]
+
+
+def test_packed_code_units_roundtrip(rng):
+    """12-bit packed cache codes (code_bytes = 3): the host pack/unpack pair is
+    exact and follows the device layout (unit u at bits [12u, 12u + 12),
+    little-endian: common.cuh code_get / code_put_row)."""
+    from paper_2506_19505_b200.cache import pack_units, unpack_units
+    u = rng.integers(0, 4096, size=4 * 1000).astype(np.uint16)
+    raw = pack_units(u, 3)
+    assert raw.size == u.size * 3 // 2
+    assert np.array_equal(unpack_units(raw, 3), u)
+    bits = np.unpackbits(raw, bitorder="little")
+    for k in (0, 1, 2, 3, 777, 3999):
+        assert int(sum(int(bits[12 * k + i]) << i for i in range(12))) == int(u[k])
+    for kind, dt in ((1, np.uint8), (2, np.uint16)):
+        v = rng.integers(0, 256 if kind == 1 else 65536, size=64).astype(dt)
+        assert np.array_equal(unpack_units(pack_units(v, kind), kind), v)
