@@ -53,6 +53,7 @@ struct __align__(128) TcSmem {
   unsigned long long cfull[TW][TNCS];
   unsigned long long pfull[TW];
   float mw[8][TW * 8 + 1];            // merge weights per head and source (+ M, L)
+  uint16_t cunp[TW][32 * 8];          // a tile's 12-bit packed codes, unpacked (rows x groups <= 8)
   int ticket;
 };
 
@@ -366,13 +367,27 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
         const int jc = lane & 15, rsel = lane >> 4, gq = jc / CPC, within = jc % CPC;
         const uint8_t *cpt = &sm.code[warp][slot][(j % TPS) * TILEB];
         const uint32_t sb = su32(&sm.stage[warp][j % TNST][0]);
+        if (CB == 3) {   // lane = row (K rows 0-15, V rows 16-31): unpack it once for the 16 loads below
+          static_assert(CB != 3 || DSUB < 16 || G <= 8, "unpack scratch holds 8 groups per row");
+          __syncwarp();
+#pragma unroll
+          for (int gg = 0; gg < G; gg += 2) {
+            const uint8_t *p3 = cpt + lane * RCB + 3 * (gg >> 1);
+            const uint32_t b0 = p3[0], b1 = p3[1], b2 = p3[2];
+            sm.cunp[warp][lane * G + gg] = static_cast<uint16_t>(b0 | ((b1 & 0xfu) << 8));
+            sm.cunp[warp][lane * G + gg + 1] = static_cast<uint16_t>((b1 >> 4) | (b2 << 4));
+          }
+          __syncwarp();
+        }
         const uint8_t *cb0 = reinterpret_cast<const uint8_t *>(c.codebook_f16g) +
                              (int64_t)h * 2 * c.m * DSUB * 2 + within * 16;
         const int64_t side = (int64_t)c.m * DSUB * 2;
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int kvv = i >> 3, rr = (2 * i + rsel) & 15;
-          const uint32_t code = min(code_get(cpt, (int64_t)(kvv * 16 + rr) * G + gq, CB), mmax);
+          const uint32_t code =
+              min(CB == 3 ? (uint32_t)sm.cunp[warp][(kvv * 16 + rr) * G + gq] : code_get(cpt, (int64_t)(kvv * 16 + rr) * G + gq, CB),
+                  mmax);
           cpa16(sb + kvv * 4096 + rr * 256 + ((jc ^ (rr & 7)) << 4), cb0 + kvv * side + (int64_t)code * (DSUB * 2));
         }
       } else {
