@@ -179,6 +179,31 @@ def measured_traffic(args):
     return None
 
 
+def verify_exchange(exchange, cache, rank, world, torch):
+    """One attention-only step of layer 0 merged both ways (peer-memory
+    stores + antkv_lse_merge_wait vs NCCL all-gather + LSE combine): every
+    rank must agree before the timed run uses the peer path."""
+    import torch.distributed as dist
+    from paper_2506_19505_b200.parallel import gather_partials, lse_merge
+    B = cache.B
+    g = torch.Generator(device="cuda").manual_seed(91)
+    q = torch.randn((B, HQ, D), device="cuda", generator=g).to(torch.bfloat16)
+    qpos = torch.full((B,), cache.token_count * world, dtype=torch.int64, device="cuda")
+    out = torch.empty((B, HQ, D), dtype=torch.float32, device="cuda")
+    lse = torch.empty((B, HQ), dtype=torch.float32, device="cuda")
+    p2p = torch.empty((B * HQ, D), dtype=torch.float32, device="cuda")
+    exchange.advance()
+    cache.step_publish(q, None, None, qpos, out, lse, exchange)
+    exchange.merge(p2p)
+    cache.attend_device(q, qpos, out, lse)
+    o_all, l_all = gather_partials(out, lse)
+    ref = lse_merge(o_all, l_all, torch.empty((B, HQ, D), dtype=torch.float32, device="cuda"))
+    ok = torch.tensor([float(torch.isfinite(p2p).all() and
+                             (p2p.view_as(ref) - ref).abs().max() <= 1e-5 * ref.abs().max())], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    return bool(ok.item() > 0)
+
+
 def launches_per_layer_step(cache, args, world):
     """Our kernel launches per layer-step on rank 0: the fused d8m256 step is
     one launch (N=1) or attention + merge (N>1); the staged / generic paths
@@ -327,6 +352,10 @@ def run_ours(args):
                 exchange_kind = "p2p"
             except Exception as exc:  # noqa: BLE001 (reported in the JSON line)
                 print(f"peer exchange unavailable ({exc}); NCCL all-gather", file=sys.stderr)
+            if exchange is not None and not verify_exchange(exchange, caches[0], rank, world, torch):
+                print("peer exchange disagrees with the NCCL all-gather merge; using NCCL", file=sys.stderr)
+                exchange.close()
+                exchange, exchange_kind = None, "nccl"
     L, B = args.layers, args.batch
     n0 = caches[0].token_count
     is_tail = rank == world - 1

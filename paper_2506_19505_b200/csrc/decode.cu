@@ -338,14 +338,34 @@ __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *
                                       const unsigned *__restrict__ flags, int P, unsigned seq,
                                       int64_t rows, int d, float *__restrict__ out,
                                       float *__restrict__ lse_out) {
+  // bounded wait: a peer that never publishes (a dead rank, a mapping that
+  // does not reach this GPU) turns into NaN outputs after ~10 s, not a hang
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) timed_out = 0;
+  __syncthreads();
   if (threadIdx.x < P) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     unsigned v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
-      if ((int)(v - seq) < 0) __nanosleep(64);
+      if ((int)(v - seq) < 0) {
+        __nanosleep(64);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10000000000ull) {
+          timed_out = 1;
+          break;
+        }
+      }
     } while ((int)(v - seq) < 0);
   }
   __syncthreads();
+  if (timed_out) {
+    const int64_t row = blockIdx.x;
+    for (int t = threadIdx.x; t < d; t += blockDim.x) out[row * d + t] = __int_as_float(0x7fc00000);
+    if (lse_out && threadIdx.x == 0) lse_out[row] = __int_as_float(0x7fc00000);
+    return;
+  }
   const int64_t row = blockIdx.x;
   float M = -INFINITY;
   for (int p = 0; p < P; ++p) M = fmaxf(M, __ldcg(lse + p * rows + row));

@@ -13,8 +13,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--ctx", type=int, default=32768)
 ap.add_argument("--layers", type=int, default=32)
 ap.add_argument("--steps", type=int, default=64)
+ap.add_argument("--notation", default="d8m256")
 args = ap.parse_args()
-cfg = LlamaConfig(layers=args.layers)
+cfg = LlamaConfig(layers=args.layers, notation=args.notation)
 model = AnTKVLlama(cfg, batch=1, capacity=args.ctx + args.steps + 256)
 g = torch.Generator(device="cuda").manual_seed(0)
 toks = torch.randint(0, cfg.vocab, (1, args.ctx), device="cuda", generator=g)
