@@ -47,7 +47,7 @@ constexpr int TCS = 1024;             // code ring slot bytes
 constexpr int TNCS = 3;               // code ring slots per warp
 
 struct __align__(128) TcSmem {
-  uint8_t stage[TW][TNST][TSTAGE];
+  uint8_t stage[TNST][TW][TSTAGE];   // slot-major: slot 1 of all warps is one 64 KB block
   uint8_t code[TW][TNCS][TCS];
   float2 step[64];                    // (cos, sin) of -16 F omega_p, lane-pair order
   unsigned long long cfull[TW][TNCS];
@@ -245,6 +245,14 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   constexpr int TILEB = 32 * RCB;                     // code bytes of one 16-slot tile (K + V)
   constexpr int TPS = TCS / TILEB;            // tiles per code ring slot
   static_assert(TPS >= 1, "code tile larger than a ring slot");
+  // d_sub = 4 with byte codes (m <= 256): an 8-byte centroid costs a whole
+  // L1 wavefront when gathered from global memory, so the codebook is
+  // replicated 16x in shared memory (stage slot 1: [side][code][copy][8 B],
+  // copy = lane & 15 puts every lane of a half-warp on its own bank pair) and
+  // each tile is rebuilt synchronously into stage slot 0 (LDS.64 pairs ->
+  // STS.128); pool tiles then go through slot 0 before the loop
+  constexpr bool SCB = DSUB == 4 && CB == 1;
+  static_assert(!SCB || 2 * 256 * 16 * 8 <= TW * TSTAGE, "replicated codebook exceeds stage slot 1");
   extern __shared__ __align__(128) unsigned char smraw[];
   TcSmem &sm = *reinterpret_cast<TcSmem *>(smraw);
   const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
@@ -346,6 +354,14 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) w.o[i][e] = 0.f;
+  if (SCB) {
+    uint2 *cbs = reinterpret_cast<uint2 *>(&sm.stage[1][0][0]);
+    const uint2 *src = reinterpret_cast<const uint2 *>(c.codebook_f16g) + (int64_t)h * 2 * c.m;
+    for (int e = threadIdx.x; e < 2 * 256 * 16; e += TT) {
+      const int side = e >> 12, code = (e >> 4) & 255;
+      cbs[e] = code < c.m ? src[side * c.m + code] : make_uint2(0u, 0u);
+    }
+  }
   __syncthreads();   // frames read: the stage area becomes the tile rings
   if (lane == 0) fence_async();
 
@@ -359,14 +375,30 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
     if (j < nt) {
       const int ks = j / TPS, slot = ks % TNCS;
       mb_wait(&sm.cfull[warp][slot], (ks / TNCS) & 1);
-      if (DSUB >= 16) {
+      if (SCB) {
+        const int jc = lane & 15, rsel = lane >> 4;
+        const uint8_t *cpt = &sm.code[warp][slot][(j % TPS) * TILEB];
+        const uint32_t sb = su32(&sm.stage[0][warp][0]);
+        const uint32_t cbs = su32(&sm.stage[1][0][0]) + jc * 8;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int kvv = i >> 3, rr = (2 * i + rsel) & 15;
+          const uint32_t u = *reinterpret_cast<const uint16_t *>(cpt + kvv * 16 * RCB + rr * RCB + 2 * jc);
+          const uint32_t c0 = min(u & 0xffu, mmax), c1 = min(u >> 8, mmax);
+          uint32_t x0, x1, x2, x3;
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(cbs + ((kvv * 256 + c0) << 7)));
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(x2), "=r"(x3) : "r"(cbs + ((kvv * 256 + c1) << 7)));
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(sb + kvv * 4096 + rr * 256 + ((jc ^ (rr & 7)) << 4)),
+                       "r"(x0), "r"(x1), "r"(x2), "r"(x3) : "memory");
+        }
+      } else if (DSUB >= 16) {
         // two token rows per instruction, lanes of one centroid adjacent: the
         // 32 chunks of an instruction touch 2 G cache lines (L1 / L2 gathers
         // cost one wavefront per line, not per lane)
         constexpr int CPC = DSUB / 8;   // 16-byte chunks per centroid
         const int jc = lane & 15, rsel = lane >> 4, gq = jc / CPC, within = jc % CPC;
         const uint8_t *cpt = &sm.code[warp][slot][(j % TPS) * TILEB];
-        const uint32_t sb = su32(&sm.stage[warp][j % TNST][0]);
+        const uint32_t sb = su32(&sm.stage[j % TNST][warp][0]);
         if (CB == 3) {   // lane = row (K rows 0-15, V rows 16-31): unpack it once for the 16 loads below
           static_assert(CB != 3 || DSUB < 16 || G <= 8, "unpack scratch holds 8 groups per row");
           __syncwarp();
@@ -408,7 +440,7 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
       } else {
         cw[0] = *reinterpret_cast<const uint16_t *>(cp);
       }
-      const uint32_t dst = su32(&sm.stage[warp][j % TNST][0]) + kv * 4096 + r * 256;
+      const uint32_t dst = su32(&sm.stage[j % TNST][warp][0]) + kv * 4096 + r * 256;
 #pragma unroll
       for (int gg = 0; gg < G; ++gg) {
         const uint32_t code = min(CB == 3 ? code_get(cp, gg, 3) : code_unit<CB, NW>(cw, gg), mmax);
@@ -439,8 +471,15 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   };
   static_assert(TNST == 3, "the qmask words below rotate through three registers");
   uint32_t q0 = 0, q1 = 0, q2 = 0;
-  gather(0, q0);
-  gather(1, q1);
+  if (SCB) {
+    for (int k = 0; k < 2 && k < nt; ++k) {
+      const int gt = wt0 + k;
+      (k ? q1 : q0) = (__ldg(qmg + (gt >> 1)) >> (16 * (gt & 1))) & 0xffffu;
+    }
+  } else {
+    gather(0, q0);
+    gather(1, q1);
+  }
 
   // ---- pool tiles (anchors + window) through the warp's third ring slot
   {
@@ -450,7 +489,7 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
     const uint8_t *pool_g = reinterpret_cast<const uint8_t *>(c.pool_f16) + bh * (int64_t)c.pool_capacity * 512;
     const int8_t *kinds = c.pool_kind + bh * c.pool_capacity;
     const int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
-    uint8_t *pbuf = &sm.stage[warp][TNST - 1][0];
+    uint8_t *pbuf = &sm.stage[SCB ? 0 : TNST - 1][warp][0];
     int rnd = 0;
     for (int tile = pt0 + warp; tile < pt1; tile += TW, ++rnd) {
       if (lane == 0) {
@@ -470,12 +509,23 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   // ---- code tiles
   const int ph0 = (2 * t) / GQ, ph1 = (2 * t + 1) / GQ;
   for (int i = 0; i < nt; ++i) {
-    gather(i + 2, q2);
-    cpa_wait<TNST - 1>();
-    __syncwarp();
     const int ph = i % F;
     const uint32_t rows = ((q0 >> g) & 1u) | (((q0 >> (g + 8)) & 1u) << 1);
-    tile_attend<true>(w, su32(&sm.stage[warp][i % TNST][0]), w.bq, rows, ph0 == ph, ph1 == ph);
+    if (SCB) {   // synchronous rebuild into slot 0 (q words prefetched two tiles ahead)
+      if (i + 2 < nt) {
+        const int gt = wt0 + i + 2;
+        q2 = (__ldg(qmg + (gt >> 1)) >> (16 * (gt & 1))) & 0xffffu;
+      }
+      uint32_t unused;
+      gather(i, unused);
+      __syncwarp();
+      tile_attend<true>(w, su32(&sm.stage[0][warp][0]), w.bq, rows, ph0 == ph, ph1 == ph);
+    } else {
+      gather(i + 2, q2);
+      cpa_wait<TNST - 1>();
+      __syncwarp();
+      tile_attend<true>(w, su32(&sm.stage[i % TNST][warp][0]), w.bq, rows, ph0 == ph, ph1 == ph);
+    }
     if (ph == F - 1) {   // next stage: frames advance by R(-16 F omega)
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
