@@ -27,7 +27,9 @@ namespace antkv {
 namespace {
 
 constexpr int ET_WARPS = 8;
-constexpr int ET_RT = 4;                 // 16-row tiles per warp
+// 16-row tiles per warp: every B fragment feeds RT MMAs (8 measured best for
+// d_sub = 32, 4 for 16 and 64)
+__host__ __device__ constexpr int et_rt(int ds) { return ds == 32 ? 8 : 4; }
 constexpr int ET_CN = 128;               // centroids per shared-memory chunk
 
 template <bool BF16>
@@ -72,7 +74,7 @@ __device__ __forceinline__ void store_code_u(void *codes, int64_t off, int code_
   else reinterpret_cast<int64_t *>(codes)[off] = v;
 }
 
-// grid = (ceil(rows * G / (ET_WARPS * ET_RT * 16)), nsets); set s reads
+// grid = (ceil(rows * G / (ET_WARPS * RT * 16)), nsets); set s reads
 // X + s * x_set_stride, codebook (s % cb_mod) and writes the code of
 // (row r, group g) at s * code_set_stride + (r / 16) * code_tile_stride +
 // (r % 16) * code_row_stride + g (launch_encode's layout).
@@ -83,6 +85,7 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
                     int code_bytes, int64_t code_set_stride, int64_t code_tile_stride,
                     int64_t code_row_stride) {
   constexpr int KS = DS / 16;                      // k16 steps per sub-vector
+  constexpr int RT = et_rt(DS);                    // 16-row tiles per warp
   constexpr int UNITS = 3 * DS / 8;                // 16-byte units of a split centroid
   constexpr int PU = UNITS | 1;                    // padded to an odd count
   constexpr int PITCH = PU * 16;
@@ -94,12 +97,12 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
   const int set = blockIdx.y;
   const float *cb = codebooks + (int64_t)(set % cb_mod) * m * DS;
   const int64_t nsub = rows * G;
-  const int64_t sv0 = ((int64_t)blockIdx.x * ET_WARPS + warp) * (ET_RT * 16);
+  const int64_t sv0 = ((int64_t)blockIdx.x * ET_WARPS + warp) * (RT * 16);
   const uint16_t *xs = X + set * x_set_stride;
   // A = -2 x for the warp's 4 row tiles (rows beyond the end are zero)
-  uint32_t a[ET_RT][KS][4];
+  uint32_t a[RT][KS][4];
 #pragma unroll
-  for (int rt = 0; rt < ET_RT; ++rt) {
+  for (int rt = 0; rt < RT; ++rt) {
     const int64_t ra = sv0 + rt * 16 + g, rb = ra + 8;
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
@@ -127,24 +130,39 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
       }
     }
   }
-  float best[ET_RT][2];
-  int bidx[ET_RT][2];
+  float best[RT][2];
+  int bidx[RT][2];
 #pragma unroll
-  for (int rt = 0; rt < ET_RT; ++rt) {
+  for (int rt = 0; rt < RT; ++rt) {
     best[rt][0] = best[rt][1] = INFINITY;
     bidx[rt][0] = bidx[rt][1] = 0;
   }
   // ldmatrix lanes 0-7: centroids 8j + (lane & 7), chunk 2ks; lanes 8-15: chunk 2ks + 1
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(sb)) + (lane & 7) * PITCH +
                          ((lane >> 3) & 1) * 16;
+  // the chunk's fp32 centroids, one float4 (centroid cc, quad q) per
+  // element e = tid + 256 k; the next chunk's are loaded during this one's MMAs
+  constexpr int QPC = DS / 4;                              // quads per centroid
+  constexpr int PFN = CN * QPC / (ET_WARPS * 32);          // float4 per thread
+  static_assert(PFN * ET_WARPS * 32 == CN * QPC, "chunk split");
+  float4 pf[PFN];
+  auto load_chunk = [&](int base) {
+#pragma unroll
+    for (int k = 0; k < PFN; ++k) {
+      const int e = threadIdx.x + k * ET_WARPS * 32, cc = e / QPC, q = e % QPC;
+      pf[k] = base + cc < m ? __ldg(reinterpret_cast<const float4 *>(cb + (int64_t)(base + cc) * DS) + q)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  load_chunk(0);
   for (int c0 = 0; c0 < m; c0 += CN) {
     __syncthreads();   // the previous chunk is consumed
-    // split the chunk: thread -> (centroid, 4-dim quad)
-    for (int e = threadIdx.x; e < CN * (DS / 4); e += ET_WARPS * 32) {
-      const int cc = e / (DS / 4), q = e % (DS / 4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (c0 + cc < m) v = *reinterpret_cast<const float4 *>(cb + (int64_t)(c0 + cc) * DS + 4 * q);
-      const float x[4] = {v.x, v.y, v.z, v.w};
+    // split into hi / mid / lo parts; |c|^2 from the same values (QPC adjacent
+    // lanes hold one centroid: partial sums reduced across them)
+#pragma unroll
+    for (int k = 0; k < PFN; ++k) {
+      const int e = threadIdx.x + k * ET_WARPS * 32, cc = e / QPC, q = e % QPC;
+      const float x[4] = {pf[k].x, pf[k].y, pf[k].z, pf[k].w};
       uint32_t hi[2], mid[2], lo[2];
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
@@ -159,23 +177,22 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
       *reinterpret_cast<uint2 *>(row) = make_uint2(hi[0], hi[1]);
       *reinterpret_cast<uint2 *>(row + DS * 2) = make_uint2(mid[0], mid[1]);
       *reinterpret_cast<uint2 *>(row + DS * 4) = make_uint2(lo[0], lo[1]);
-    }
-    for (int cc = threadIdx.x; cc < CN; cc += ET_WARPS * 32) {
-      float s = INFINITY;
-      if (c0 + cc < m) {
-        const float *cr = cb + (int64_t)(c0 + cc) * DS;
-        s = 0.f;
-        for (int k = 0; k < DS; ++k) s = fmaf(cr[k], cr[k], s);
-      }
-      snorm[cc] = s;
+      float nrm = x[0] * x[0];
+      nrm = fmaf(x[1], x[1], nrm);
+      nrm = fmaf(x[2], x[2], nrm);
+      nrm = fmaf(x[3], x[3], nrm);
+#pragma unroll
+      for (int o = 1; o < QPC; o <<= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+      if (q == 0) snorm[cc] = c0 + cc < m ? nrm : INFINITY;
     }
     __syncthreads();
+    if (c0 + CN < m) load_chunk(c0 + CN);   // in flight during the MMAs below
     const int cn = min(CN, m - c0);
     for (int j = 0; j < (cn + 7) / 8; ++j) {
-      float acc[ET_RT][4];
+      float acc[RT][4];
       const float2 nn = *reinterpret_cast<const float2 *>(&snorm[8 * j + 2 * t]);
 #pragma unroll
-      for (int rt = 0; rt < ET_RT; ++rt) {
+      for (int rt = 0; rt < RT; ++rt) {
         acc[rt][0] = nn.x;
         acc[rt][1] = nn.y;
         acc[rt][2] = nn.x;
@@ -188,12 +205,12 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
           uint32_t b0, b1;
           ldsm2(sbase + j * 8 * PITCH + p * DS * 2 + ks * 32, b0, b1);
 #pragma unroll
-          for (int rt = 0; rt < ET_RT; ++rt) mma16<BF16>(acc[rt], a[rt][ks], b0, b1);
+          for (int rt = 0; rt < RT; ++rt) mma16<BF16>(acc[rt], a[rt][ks], b0, b1);
         }
       }
       const int col = c0 + 8 * j + 2 * t;
 #pragma unroll
-      for (int rt = 0; rt < ET_RT; ++rt) {   // columns in index order: strict < keeps the lowest
+      for (int rt = 0; rt < RT; ++rt) {   // columns in index order: strict < keeps the lowest
         if (acc[rt][0] < best[rt][0]) { best[rt][0] = acc[rt][0]; bidx[rt][0] = col; }
         if (acc[rt][1] < best[rt][0]) { best[rt][0] = acc[rt][1]; bidx[rt][0] = col + 1; }
         if (acc[rt][2] < best[rt][1]) { best[rt][1] = acc[rt][2]; bidx[rt][1] = col; }
@@ -202,9 +219,9 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
     }
   }
   // reduce over the 4 lanes of a row: smaller distance, then lower index
-  __shared__ uint32_t spk[ET_WARPS][ET_RT * 16];   // 12-bit packing: the warp's codes by sub-vector
+  __shared__ uint32_t spk[ET_WARPS][RT * 16];   // 12-bit packing: the warp's codes by sub-vector
 #pragma unroll
-  for (int rt = 0; rt < ET_RT; ++rt) {
+  for (int rt = 0; rt < RT; ++rt) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float b = best[rt][h];
@@ -230,7 +247,7 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
   }
   if (code_bytes == 3) {   // whole rows (G | 64, so the warp's 64 sub-vectors are 64 / G rows)
     __syncwarp();
-    if (lane < ET_RT * 16 / G && sv0 + lane * G < nsub) {
+    if (lane < RT * 16 / G && sv0 + lane * G < nsub) {
       const int64_t r = (sv0 + lane * G) / G;
       code_put_row(static_cast<uint8_t *>(codes), set * code_set_stride + (r >> 4) * code_tile_stride +
                    (r & 15) * code_row_stride, G, &spk[warp][lane * G], 3);
@@ -258,7 +275,7 @@ int launch_encode_tc(const void *X, int dtype, int64_t rows, int d, int64_t x_se
     return ANTKV_EUNSUPPORTED;
   if (rows == 0 || nsets == 0) return ANTKV_OK;
   const int G = d / d_sub;
-  const int64_t per_cta = ET_WARPS * ET_RT * 16;
+  const int64_t per_cta = ET_WARPS * et_rt(d_sub) * 16;
   dim3 grid(ceil_div(rows * G, per_cta), nsets);
   const uint16_t *Xh = reinterpret_cast<const uint16_t *>(X);
 #define ET_LAUNCH(BF, DSV)                                                                           \
