@@ -527,6 +527,8 @@ def run_ours(args):
     e2e_ms = float(t.item())
 
     enc = encode_throughput(torch) if rank == 0 else None
+    # config #3's 0.375-bit code (m = 4096): the tensor-core encoder of encode_tc.cu
+    enc3 = encode_throughput(torch, n=32768, vq_m=4096, d_sub=32) if rank == 0 else None
     pre = prefill_throughput(torch) if rank == 0 and not args.no_prefill else None
     peak, peak_kind = peaks()
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
@@ -581,6 +583,7 @@ def run_ours(args):
             "gpu_launches": args.steps * L * launches_per_layer_step(caches[0], args, world),
             "clocks": clk.summary(),
             "encode": enc,
+            "encode_d32m4096": enc3,
             "prefill": pre,
         }
     if exchange is not None:
