@@ -593,6 +593,9 @@ def run_ours(args):
 
 
 # ------------------------------------------------------------- reference
+_CPU_ITEMS = []   # the heads' host arrays, inherited by the forked workers (not pickled per task)
+
+
 def _cpu_head_worker(args_tuple):
     """Tokens [lo, hi) of one KV head of one layer-step with the reference's
     decode math (cache.py:168-178 via the oracle restatement): dequantize
@@ -601,7 +604,8 @@ def _cpu_head_worker(args_tuple):
     caller's LSE merge would combine (a head's range is split only to use
     every host core)."""
     import antkv_oracle as O
-    (kcodes, vcodes, qbits, rows_k, rows_v, fp_tok, ck, cv, q, qpos, theta), lo, hi = args_tuple
+    idx, lo, hi = args_tuple
+    kcodes, vcodes, qbits, rows_k, rows_v, fp_tok, ck, cv, q, qpos, theta = _CPU_ITEMS[idx]
     t0 = time.perf_counter()
     n = hi - lo
     Khat = np.empty((n, D), dtype=np.float32)
@@ -660,10 +664,11 @@ def run_cpu(items, repeats):
     ncpu = os.cpu_count() or 1
     per_head = max(1, -(-ncpu // len(items)))
     work = []
-    for it in items:
+    _CPU_ITEMS[:] = items
+    for idx, it in enumerate(items):
         n = len(it[2])
         cuts = np.linspace(0, n, per_head + 1).astype(int)
-        work += [(it, int(cuts[i]), int(cuts[i + 1])) for i in range(per_head)]
+        work += [(idx, int(cuts[i]), int(cuts[i + 1])) for i in range(per_head)]
     cores = min(len(work), ncpu)
     sys.path.insert(0, str(ROOT / "oracle"))
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
