@@ -363,6 +363,40 @@ def test_snapshot_roundtrip_and_reference_format(tmp_path):
         QuantizedKVCache.load(out)
 
 
+def test_packed_codes_snapshot_and_decode(tmp_path):
+    """Config #3's code (d32m4096, 12-bit indices packed two per 3 bytes on
+    the device): the device bytes really are 0.375 bit per element of codes,
+    codes_of() unpacks what the encoders packed (they equal a host argmin
+    under the margin rule), and a snapshot round trip restores the same
+    packed bytes and the same attention."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d32m4096")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.02, window_size=8)
+    n, d = 200, 128
+    Q, K, V = qkv(61, 1, 1, n + 6, d, heavy=2)
+    ck, cv = codebooks(61, 1, vq.m, vq.d_sub)
+    cache = QuantizedKVCache(cfg, Codebook(vq, ck[0]), Codebook(vq, cv[0]))
+    cache.prefill(Q[0, :n].astype(np.float64), K[0, :n].astype(np.float64), V[0, :n].astype(np.float64),
+                  np.arange(n))
+    for t in range(n, n + 6):   # evictions encode through the eviction kernels
+        cache.decode_step(Q[0, t].astype(np.float64), K[0, t].astype(np.float64), V[0, t].astype(np.float64), t)
+    assert cache.desc.code_bytes == 3
+    assert cache.tensors["codes"].shape[-1] == 3 * (d // vq.d_sub)   # 1.5 bytes per 12-bit index, K + V
+    kc, vc = cache.codes_of()
+    Kb = torch.from_numpy(K[0]).to(torch.bfloat16).float().numpy()
+    for j in list(kc)[:40]:
+        sub = Kb[j].astype(np.float64).reshape(-1, vq.d_sub)
+        ref, _ = O.assign_nearest(sub, ck[0].astype(np.float64))
+        assert_codes_parity(sub, ck[0], kc[j], ref)
+    out = cache.save(tmp_path / "snap")
+    loaded = QuantizedKVCache.load(out)
+    assert loaded.desc.code_bytes == 3
+    lc, lv = loaded.codes_of()
+    assert all(np.array_equal(lc[j], kc[j]) and np.array_equal(lv[j], vc[j]) for j in kc)
+    Qp = np.random.default_rng(1).standard_normal((cache.token_count, d))
+    assert rel(loaded.attention_from_cache(Qp), cache.attention_from_cache(Qp)) < 1e-6
+
+
 def test_lse_combine_kernel():
     from paper_2506_19505_b200.parallel import lse_merge
     rng = np.random.default_rng(5)
@@ -381,6 +415,7 @@ def test_lse_combine_kernel():
     ("d8m256", 1, 16, 2, "staged"),   # the staged kernel on the fused kernel's shape, GQA 8
     ("d16m4096", 1, 8, 2, True),      # 2-byte indices, GQA 4
     ("d64m256", 1, 2, 1, True),       # 2 groups per row
+    ("d32m3000", 1, 8, 1, True),      # 12-bit packed codes, m not a power of two, GQA 8
 ])
 def test_staged_kernel_vs_oracle(notation, B, Hq, Hkv, fast):
     """decode_tc.cu (staged tensor-core kernel, fp16 operands): every d = 128
