@@ -323,16 +323,20 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
     store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(v, bh * c.d + t, dtype));
   }
   if (c.pool_f16) {
-    __syncthreads();
+    // from the inputs rounded to the pool's dtype (the values just stored):
+    // no second round trip through pool_rows
+    auto rnd = [&](float x) {
+      return c.row_dtype == ANTKV_BF16 ? __bfloat162float(__float2bfloat16_rn(x))
+             : c.row_dtype == ANTKV_F16 ? __half2float(__float2half_rn(x)) : x;
+    };
     const double pos = static_cast<double>(position[b]);
     for (int i = threadIdx.x; i < c.Hkv * (c.d / 2); i += blockDim.x) {
       const int h = i / (c.d / 2), p = i % (c.d / 2);
       const int slot = s_slot[h];
       if (slot < 0) continue;
       const int64_t bh = bh_index(b, h, c.Hkv);
-      const int64_t src = (bh * c.pool_capacity + slot) * 2 * c.d;
-      const float x0 = load_elem(c.pool_rows, src + 2 * p, c.row_dtype);
-      const float x1 = load_elem(c.pool_rows, src + 2 * p + 1, c.row_dtype);
+      const float x0 = rnd(load_elem(k, bh * c.d + 2 * p, dtype));
+      const float x1 = rnd(load_elem(k, bh * c.d + 2 * p + 1, dtype));
       float cs, sn;
       const double om = (c.fast_tables && c.d == 128)
                             ? reinterpret_cast<const FastTables *>(c.fast_tables)->omega[p]
@@ -341,10 +345,8 @@ __global__ void cache_append_kernel(antkv_cache_desc c, const void *__restrict__
       __half *dst = reinterpret_cast<__half *>(c.pool_f16) + bh * c.pool_capacity * 2 * c.d;
       dst[pool_f16_offset(slot, 0, 2 * p)] = __float2half_rn(x0 * cs - x1 * sn);
       dst[pool_f16_offset(slot, 0, 2 * p + 1)] = __float2half_rn(x0 * sn + x1 * cs);
-      dst[pool_f16_offset(slot, 1, 2 * p)] =
-          __float2half_rn(load_elem(c.pool_rows, src + c.d + 2 * p, c.row_dtype));
-      dst[pool_f16_offset(slot, 1, 2 * p + 1)] =
-          __float2half_rn(load_elem(c.pool_rows, src + c.d + 2 * p + 1, c.row_dtype));
+      dst[pool_f16_offset(slot, 1, 2 * p)] = __float2half_rn(rnd(load_elem(v, bh * c.d + 2 * p, dtype)));
+      dst[pool_f16_offset(slot, 1, 2 * p + 1)] = __float2half_rn(rnd(load_elem(v, bh * c.d + 2 * p + 1, dtype)));
     }
   }
   // the slot's code bits stay clear (qmask initialised to zero above n)
