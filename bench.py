@@ -626,7 +626,7 @@ def _cpu_head_worker(args_tuple):
         mx = s.max()
         p = np.exp(s - mx)
         parts.append((mx, p.sum(), p @ Vhat.astype(np.float64)))
-    return time.perf_counter() - t0
+    return time.perf_counter() - t0, parts
 
 
 def cpu_sample_from_cache(cache, n_heads):

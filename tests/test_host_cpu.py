@@ -349,3 +349,22 @@ def test_packed_code_units_roundtrip(rng):
     for kind, dt in ((1, np.uint8), (2, np.uint16)):
         v = rng.integers(0, 256 if kind == 1 else 65536, size=64).astype(dt)
         assert np.array_equal(unpack_units(pack_units(v, kind), kind), v)
+
+
+def test_bench_cpu_arm_token_slices_merge_exactly():
+    """The CPU reference arm splits each KV head's tokens over the host
+    cores; the softmax partials of the slices merge (LSE) into the same
+    attention output as one pass over the whole range."""
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import bench
+    items = bench._host_items(1024)[:1]
+    bench._CPU_ITEMS[:] = items
+    _, whole = bench._cpu_head_worker((0, 0, 1024))
+    _, a = bench._cpu_head_worker((0, 0, 400))
+    _, b = bench._cpu_head_worker((0, 400, 1024))
+    for (m0, l0, o0), (m1, l1, o1), (mw, lw, ow) in zip(a, b, whole):
+        m = max(m0, m1)
+        l = l0 * np.exp(m0 - m) + l1 * np.exp(m1 - m)
+        o = (o0 * np.exp(m0 - m) + o1 * np.exp(m1 - m)) / l
+        assert np.allclose(o, ow / lw, rtol=1e-12, atol=1e-14)
