@@ -50,6 +50,8 @@ def parse():
     p.add_argument("--splits", type=int, default=0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graph", action="store_true", help="eager launches instead of CUDA graphs")
+    p.add_argument("--shared-stream", action="store_true",
+                   help="do not declare the captured decode chains exclusive (all reads after the PDL wait)")
     p.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                    help="N > 1: shard partials over peer memory (default) or NCCL all-gather")
     p.add_argument("--no-prefill", action="store_true", help="skip the prefill timing")
@@ -395,6 +397,13 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     use_graph = world == 1 and not args.no_graph
+
+    def chain_ctx():
+        # the captured chains hold only this library's kernels (plus memcpy
+        # nodes): the stream is declared exclusive so the fused decode launch
+        # may read its inputs before griddepcontrol.wait (antkv_stream_exclusive)
+        import contextlib
+        return contextlib.nullcontext() if args.shared_stream else _lib.exclusive_stream()
     if use_graph:
         # CUDA graphs: one step = the 32 per-layer decode kernels, replayed so
         # host launch overhead is outside the measurement
@@ -410,7 +419,7 @@ def run_ours(args):
         body()                       # eager warm-up (lazy init), advances the caches by 1
         torch.cuda.synchronize()
         step_graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(step_graph):
+        with torch.cuda.graph(step_graph), chain_ctx():
             body()
         run_step = step_graph.replay
         advanced = 1
@@ -448,7 +457,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     if use_graph:
         att_graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(att_graph):
+        with torch.cuda.graph(att_graph), chain_ctx():
             for l in range(L):
                 caches[l].attend_device(qs[0, l], qlast, out)
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -507,7 +516,7 @@ def run_ours(args):
         e2e_body()
         torch.cuda.synchronize()
         e2e_graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(e2e_graph):
+        with torch.cuda.graph(e2e_graph), chain_ctx():
             e2e_body()
         for c in caches:
             c._n += 1

@@ -84,6 +84,16 @@ ANTKV_API int antkv_version(void);
 /* 1 when the running device is sm_100 (B200) and the library kernels load. */
 ANTKV_API int antkv_device_check(int device);
 
+/* Declares that, on `stream`, only this library's kernels run between its
+ * decode launches (a decode-only layer chain, a CUDA graph of decode steps).
+ * Only then may the fused decode kernel, launched with programmatic
+ * dependent launch, read the cache state, q and the position before
+ * griddepcontrol.wait (its predecessor is then known to be one of ours and
+ * to leave them untouched).  Default off: a foreign kernel writing q (a
+ * GEMM, RoPE, a torch copy) may be the predecessor, so everything is read
+ * after the wait.  New (no reference counterpart). */
+ANTKV_API int antkv_stream_exclusive(void *stream, int exclusive);
+
 /* ------------------------------------------------------------------------
  * Reference FFI (antkv._ckernels).  Batched over `heads` query heads; query
  * head h reads K/V head h / (heads / kv_heads).  Inputs are float32, row
@@ -333,11 +343,17 @@ ANTKV_API int antkv_eval_pair_l1(const double *Y, const double *X, const double 
  *   whose combined partial is then stored into slot `rank` of each of the
  *   n_dst receive buffers (dst_o / dst_lse / dst_flags: DEVICE arrays of
  *   n_dst base pointers) by direct peer stores; then each destination's
- *   flags[rank] is set to `seq` with a system-scope release.
- *   lse must be non-NULL.
- * antkv_lse_merge_wait: waits (system-scope acquire) until flags[p] reached
- *   seq for every p < P, then merges the P partials (as antkv_lse_combine).
- *   seq advances by one per step (compared modulo 2^32). */
+ *   flag of that slot is set to `seq` with a system-scope release.  A receive
+ *   buffer has two halves selected by seq & 1 (o [2][P][rows][d],
+ *   lse [2][P][rows], flags [2][P], P = n_dst): consecutive steps never share
+ *   a half, so a rank one step ahead cannot overwrite a slot a slower peer
+ *   still merges (it cannot get two steps ahead: its step s + 2 publish is
+ *   stream-ordered after its merge of s + 1, which needs every peer's s + 1
+ *   publish, issued after that peer's merge of s).  lse must be non-NULL.
+ * antkv_lse_merge_wait: waits (system-scope acquire) until flags[seq & 1][p]
+ *   equals seq for every p < P, then merges the P partials of that half
+ *   (as antkv_lse_combine).  seq advances by one per step and is never 0
+ *   (0 is the flags' initial value). */
 ANTKV_API int antkv_p2p_alloc(int64_t bytes, void **ptr);
 ANTKV_API int antkv_p2p_free(void *ptr);
 ANTKV_API int antkv_ipc_get_handle(const void *ptr, void *handle);

@@ -387,6 +387,23 @@ class _HeadState:
         self.k_codes = {}
         self.v_codes = {}
         self.anchor_indices = np.empty(0, dtype=np.int64)
+        # dense dequantised rows (what dequantize() reassembles every call,
+        # cache.py:196-211), kept up to date as tokens change kind
+        self.Khat = np.zeros((0, 0), dtype=np.float32)
+        self.Vhat = np.zeros((0, 0), dtype=np.float32)
+
+    def set_row(self, j, k, v):
+        if j >= self.Khat.shape[0]:
+            grow = max(j + 1, 2 * self.Khat.shape[0], 64)
+            d = len(k)
+            K2 = np.zeros((grow, d), dtype=np.float32)
+            V2 = np.zeros((grow, d), dtype=np.float32)
+            if self.Khat.size:
+                K2[:self.Khat.shape[0]] = self.Khat
+                V2[:self.Vhat.shape[0]] = self.Vhat
+            self.Khat, self.Vhat = K2, V2
+        self.Khat[j] = k
+        self.Vhat[j] = v
 
 
 class OracleCache:
@@ -423,67 +440,77 @@ class OracleCache:
         return budget_for(n, self.anchor_fraction, self.anchor_count)
 
     # cache.py:100-140
-    def prefill(self, Q, K, V, positions):
-        Q = np.asarray(Q, dtype=np.float64)
+    def prefill(self, Q, K, V, positions, anchors=None):
+        """``anchors`` (test hook, not in the reference): per-KV-head index
+        arrays that replace the selection -- the FA + AnS passes are then
+        skipped and None is returned.  Used to replay the reference's layout,
+        decode and eviction from another implementation's anchor set when
+        the two sets legitimately differ at the float32 margin."""
         K = np.asarray(K, dtype=np.float64)
         V = np.asarray(V, dtype=np.float64)
-        h_q, n, d = Q.shape
-        group = h_q // self.h_kv
+        h_kv, n, d = K.shape
         self.d = d
         positions = np.asarray(positions, dtype=np.int64)
-        O = np.empty((h_q, n, d))
-        ans_k = np.zeros((self.h_kv, n))
-        ans_v = np.zeros((self.h_kv, n))
-        for hq in range(h_q):
-            hk = hq // group
-            O[hq], L, M, qn = flash_attention_aux(
-                Q[hq], K[hk], V[hk], self.block_q, self.block_k,
-                positions=positions, theta_base=self.theta_base, causal=True)
-            sk, sv = anchor_scores_blocked(
-                Q[hq], K[hk], M, L, qn, self.block_q, self.block_k,
-                positions=positions, theta_base=self.theta_base, causal=True)
-            ans_k[hk] += sk
-            ans_v[hk] += sv
-        self.last_scores = (ans_k, ans_v)
-        budget = self.budget_for(n)
+        O = None
+        if anchors is None:
+            Q = np.asarray(Q, dtype=np.float64)
+            h_q = Q.shape[0]
+            group = h_q // self.h_kv
+            O = np.empty((h_q, n, d))
+            ans_k = np.zeros((self.h_kv, n))
+            ans_v = np.zeros((self.h_kv, n))
+            for hq in range(h_q):
+                hk = hq // group
+                O[hq], L, M, qn = flash_attention_aux(
+                    Q[hq], K[hk], V[hk], self.block_q, self.block_k,
+                    positions=positions, theta_base=self.theta_base, causal=True)
+                sk, sv = anchor_scores_blocked(
+                    Q[hq], K[hk], M, L, qn, self.block_q, self.block_k,
+                    positions=positions, theta_base=self.theta_base, causal=True)
+                ans_k[hk] += sk
+                ans_v[hk] += sv
+            self.last_scores = (ans_k, ans_v)
+            budget = self.budget_for(n)
         K32 = K.astype(np.float32)
         V32 = V.astype(np.float32)
         self.positions = [int(p) for p in positions]
         for hk in range(self.h_kv):
             st = self.heads[hk]
-            st.anchor_indices = select_anchors(ans_k[hk], ans_v[hk], budget, self.policy)
+            if anchors is None:
+                st.anchor_indices = select_anchors(ans_k[hk], ans_v[hk], budget, self.policy)
+            else:
+                st.anchor_indices = np.sort(np.asarray(anchors[hk], dtype=np.int64))
             anchor_set = set(int(j) for j in st.anchor_indices)
             kc = encode_rows(K[hk], self.cb_k[hk])
             vc = encode_rows(V[hk], self.cb_v[hk])
+            Kd = decode_rows(kc, self.cb_k[hk])
+            Vd = decode_rows(vc, self.cb_v[hk])
             for j in range(n):
                 if j in anchor_set:
                     st.kinds.append(KIND_ANCHOR)
                     st.k_rows[j] = K32[hk, j].copy()
                     st.v_rows[j] = V32[hk, j].copy()
+                    st.set_row(j, K32[hk, j], V32[hk, j])
                 elif j >= n - self.window_size:
                     st.kinds.append(KIND_WINDOWED)
                     st.k_rows[j] = K32[hk, j].copy()
                     st.v_rows[j] = V32[hk, j].copy()
+                    st.set_row(j, K32[hk, j], V32[hk, j])
                 else:
                     st.kinds.append(KIND_QUANTIZED)
                     st.k_codes[j] = kc[j]
                     st.v_codes[j] = vc[j]
+                    st.set_row(j, Kd[j], Vd[j])
         return O
 
     def dequantize(self, hk):
-        """cache.py:196-211 for KV head hk."""
+        """cache.py:196-211 for KV head hk: anchors and window exact, the
+        rest decoded from their codes (decode_rows).  The rows are kept
+        assembled as tokens change kind (_HeadState.set_row) instead of
+        being re-gathered token by token on every call."""
         st = self.heads[hk]
         n = self.token_count
-        Khat = np.empty((n, self.d), dtype=np.float32)
-        Vhat = np.empty((n, self.d), dtype=np.float32)
-        for j, kind in enumerate(st.kinds):
-            if kind == KIND_QUANTIZED:
-                Khat[j] = decode_rows(st.k_codes[j][None, :], self.cb_k[hk])[0]
-                Vhat[j] = decode_rows(st.v_codes[j][None, :], self.cb_v[hk])[0]
-            else:
-                Khat[j] = st.k_rows[j]
-                Vhat[j] = st.v_rows[j]
-        return Khat, Vhat
+        return st.Khat[:n].copy(), st.Vhat[:n].copy()
 
     # cache.py:149-194
     def decode_step(self, q, k, v, position):
@@ -501,6 +528,7 @@ class OracleCache:
             st.kinds.append(KIND_WINDOWED)
             st.k_rows[j] = np.asarray(k[hk], dtype=np.float32).copy()
             st.v_rows[j] = np.asarray(v[hk], dtype=np.float32).copy()
+            st.set_row(j, st.k_rows[j], st.v_rows[j])
         out = np.empty((h_q, self.d))
         pos = np.asarray(self.positions, dtype=np.int64)
         for hk in range(self.h_kv):
@@ -529,6 +557,8 @@ class OracleCache:
                 st.v_codes[evicted] = encode_rows(
                     st.v_rows.pop(evicted).astype(np.float64)[None, :], self.cb_v[hk])[0]
                 st.kinds[evicted] = KIND_QUANTIZED
+                st.set_row(evicted, decode_rows(st.k_codes[evicted][None, :], self.cb_k[hk])[0],
+                           decode_rows(st.v_codes[evicted][None, :], self.cb_v[hk])[0])
 
     def attention_from_cache(self, Q):
         """cache.py:213-223 per Q head (materialised causal softmax)."""

@@ -50,6 +50,7 @@ class CacheDesc(ctypes.Structure):
 _SIGS = {
     "antkv_last_error": (ctypes.c_char_p, []),
     "antkv_version": (_i, []),
+    "antkv_stream_exclusive": (_i, [_vp, _i]),
     "antkv_device_check": (_i, [_i]),
     "antkv_flash_aux": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "antkv_ans_blocked": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
@@ -147,6 +148,22 @@ def call(name, *args):
 
 def stream():
     return _vp(torch.cuda.current_stream().cuda_stream)
+
+
+class exclusive_stream:
+    """Context manager: declare the current stream exclusive to this
+    library's launches (antkv_stream_exclusive) -- e.g. while capturing a
+    graph of decode steps -- so the fused decode kernel may read its inputs
+    before griddepcontrol.wait.  Only for chains with no foreign kernels."""
+
+    def __enter__(self):
+        self._s = stream()
+        check(load().antkv_stream_exclusive(self._s, 1))
+        return self
+
+    def __exit__(self, *exc):
+        check(load(check_device=False).antkv_stream_exclusive(self._s, 0))
+        return False
 
 
 def ptr(t):

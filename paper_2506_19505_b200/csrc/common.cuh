@@ -39,6 +39,7 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 const void *previous_cache_on_stream(cudaStream_t st, const void *key);
 void record_fast_outputs(cudaStream_t st, const void *out, int64_t out_bytes, const void *lse, int64_t lse_bytes);
 bool overlaps_previous_fast_outputs(cudaStream_t st, const void *p, int64_t bytes);
+bool stream_exclusive(cudaStream_t st);
 
 // Destinations of a sequence shard's partial (o, lse): n receive buffers
 // (device arrays of n base pointers, one per peer; this rank's slot is

@@ -311,14 +311,20 @@ __global__ void lse_combine_kernel(const float *__restrict__ o, const float *__r
   if (lse_out && threadIdx.x == 0) lse_out[row] = M + logf(W);
 }
 
-// Generic-path publish: copy the rank's partial rows into each peer's slot,
-// then the last CTA releases the slot flags (system scope).
+// Generic-path publish: copy the rank's partial rows into each peer's slot of
+// the step's buffer half (parity seq & 1), then the last CTA releases the slot
+// flags (system scope).  Two halves make reuse race-free by construction: a
+// rank publishes step s + 2 only after its merge of s + 1, which waited for
+// every peer's publish of s + 1, which each peer issued after its own merge of
+// s (stream order) -- so nobody still reads the half that s + 2 overwrites.
 __global__ void publish_partial_kernel(const float *__restrict__ out, const float *__restrict__ lse, int d,
                                        PublishArgs pub) {
   const int64_t row = blockIdx.x, prow = (int64_t)pub.rank * pub.rows + row;
+  const int64_t half = pub.seq & 1u;
   for (int p = 0; p < pub.n; ++p) {
-    for (int t = threadIdx.x; t < d; t += blockDim.x) pub.o[p][prow * d + t] = out[row * d + t];
-    if (threadIdx.x == 0) pub.lse[p][prow] = lse[row];
+    float *o = pub.o[p] + half * pub.n * pub.rows * d;
+    for (int t = threadIdx.x; t < d; t += blockDim.x) o[prow * d + t] = out[row * d + t];
+    if (threadIdx.x == 0) pub.lse[p][half * pub.n * pub.rows + prow] = lse[row];
   }
   __threadfence_system();
   __syncthreads();
@@ -326,13 +332,15 @@ __global__ void publish_partial_kernel(const float *__restrict__ out, const floa
     *pub.cnt = 0;
     __threadfence_system();
     for (int p = 0; p < pub.n; ++p)
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pub.flag[p] + pub.rank), "r"(pub.seq)
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pub.flag[p] + half * pub.n + pub.rank),
+                   "r"(pub.seq)
                    : "memory");
   }
 }
 
-// Waits until every slot's flag reached `seq` (system-scope acquire), then
-// merges the P partials like lse_combine_kernel.  Slots are read through L2
+// Waits until every slot's flag of the step's half (parity seq & 1) equals
+// `seq` exactly (system-scope acquire), then merges the P partials like
+// lse_combine_kernel.  Slots are read through L2
 // (__ldcg): peers write them over NVLink every step.
 __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *__restrict__ lse,
                                       const unsigned *__restrict__ flags, int P, unsigned seq,
@@ -340,6 +348,10 @@ __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *
                                       float *__restrict__ lse_out) {
   // bounded wait: a peer that never publishes (a dead rank, a mapping that
   // does not reach this GPU) turns into NaN outputs after ~10 s, not a hang
+  const int64_t half = seq & 1u;
+  o += half * P * rows * d;
+  lse += half * P * rows;
+  flags += half * P;
   __shared__ int timed_out;
   if (threadIdx.x == 0) timed_out = 0;
   __syncthreads();
@@ -349,7 +361,7 @@ __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *
     unsigned v;
     do {
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + threadIdx.x) : "memory");
-      if ((int)(v - seq) < 0) {
+      if (v != seq) {
         __nanosleep(64);
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         if (t - t0 > 10000000000ull) {
@@ -357,7 +369,7 @@ __global__ void lse_merge_wait_kernel(const float *__restrict__ o, const float *
           break;
         }
       }
-    } while ((int)(v - seq) < 0);
+    } while (v != seq);
   }
   __syncthreads();
   if (timed_out) {

@@ -1193,18 +1193,23 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
     static unsigned launch_no = 0;
     a.trace += (size_t)(launch_no++ & 1) * FK_TRACE_WORDS * 32768;
   }
-  a.early = previous_cache_on_stream(st, c.codes) != c.codes;
-  // q / qpos before the wait too, unless the previous fused launch on this
-  // stream (the only kernel that can still be running then) wrote them
+  // reads before griddepcontrol.wait only on a stream the caller declared
+  // exclusive to this library (antkv_stream_exclusive): then the previous
+  // kernel is one of ours, and the state of another cache ...
+  a.early = previous_cache_on_stream(st, c.codes) != c.codes && stream_exclusive(st);
+  // ... and q / qpos, unless the previous fused launch on this stream (the
+  // only kernel that can still be running then) wrote them
   a.early_q = a.early && !overlaps_previous_fast_outputs(st, q, (int64_t)c.B * c.Hq * 128 * dtype_size(qdtype)) &&
               !overlaps_previous_fast_outputs(st, qpos, (int64_t)c.B * sizeof(int64_t));
   record_fast_outputs(st, out, (int64_t)c.B * c.Hq * 128 * sizeof(float), lse,
                       lse ? (int64_t)c.B * c.Hq * sizeof(float) : 0);
   const size_t smem = sizeof(FastSmem);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[64] = {};   // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaFuncSetAttribute(decode_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   // programmatic dependent launch: the prologue's immutable prefetch overlaps
   // the previous kernel's tail (griddepcontrol.wait orders the rest)

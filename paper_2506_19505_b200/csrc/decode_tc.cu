@@ -650,10 +650,12 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
 template <int DSUB, int CB>
 int launch_tc(const antkv_cache_desc &c, const TcArgs &a, cudaStream_t st) {
   const size_t smem = sizeof(TcSmem);
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};   // the attribute is per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
     cudaFuncSetAttribute(decode_tc_kernel<DSUB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   decode_tc_kernel<DSUB, CB><<<dim3(a.splits, c.Hkv, c.B), TT, smem, st>>>(c, a);
   ANTKV_LAUNCH_CHECK("decode_tc_kernel");

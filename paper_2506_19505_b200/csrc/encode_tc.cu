@@ -245,12 +245,12 @@ vq_encode_tc_kernel(const uint16_t *__restrict__ X, int64_t rows, int G, int64_t
       }
     }
   }
-  if (code_bytes == 3) {   // whole rows (G | 64, so the warp's 64 sub-vectors are 64 / G rows)
-    __syncwarp();
-    if (lane < RT * 16 / G && sv0 + lane * G < nsub) {
-      const int64_t r = (sv0 + lane * G) / G;
+  if (code_bytes == 3) {   // whole rows (G | RT * 16, so the warp's sub-vectors are RT * 16 / G rows,
+    __syncwarp();          // up to 64 for d_sub = 32 with G = 2: lanes loop over them)
+    for (int rr = lane; rr < RT * 16 / G && sv0 + rr * G < nsub; rr += 32) {
+      const int64_t r = (sv0 + rr * G) / G;
       code_put_row(static_cast<uint8_t *>(codes), set * code_set_stride + (r >> 4) * code_tile_stride +
-                   (r & 15) * code_row_stride, G, &spk[warp][lane * G], 3);
+                   (r & 15) * code_row_stride, G, &spk[warp][rr * G], 3);
     }
   }
 }

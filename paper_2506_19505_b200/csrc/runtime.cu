@@ -21,6 +21,22 @@ const void *previous_cache_on_stream(cudaStream_t st, const void *key) {
 }
 
 
+// Streams whose caller declared that only this library's launches run on
+// them (antkv_stream_exclusive): only there may a fused decode launch read
+// its inputs before griddepcontrol.wait.  A foreign kernel (a torch copy, a
+// cuBLAS GEMM writing q) can be the PDL primary of our launch, and the host
+// cannot see it, so the default is to read everything after the wait.
+namespace {
+std::mutex g_ex_mu;
+std::unordered_map<cudaStream_t, int> g_exclusive;
+}  // namespace
+
+bool stream_exclusive(cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_ex_mu);
+  auto it = g_exclusive.find(st);
+  return it != g_exclusive.end() && it->second;
+}
+
 namespace {
 struct FastOutputs {
   const char *out = nullptr, *lse = nullptr;
@@ -79,6 +95,12 @@ using namespace antkv;
 extern "C" const char *antkv_last_error(void) { return g_err; }
 
 extern "C" int antkv_version(void) { return 1; }
+
+extern "C" int antkv_stream_exclusive(void *stream, int exclusive) {
+  std::lock_guard<std::mutex> lock(g_ex_mu);
+  g_exclusive[static_cast<cudaStream_t>(stream)] = exclusive ? 1 : 0;
+  return ANTKV_OK;
+}
 
 namespace antkv { int decode_fast_smem_base_ok(); }
 

@@ -72,8 +72,10 @@ class PeerExchange:
     """Peer-memory exchange of the sequence-shard partials (the NCCL
     all-gather replaced by NVLink stores from the decode kernel itself).
 
-    Every rank allocates receive buffers for all P slots (o [P][rows][d],
-    lse [P][rows], flags [P]); the CUDA IPC handles are all-gathered once and
+    Every rank allocates receive buffers for all P slots in two halves used
+    by alternate steps (o [2][P][rows][d], lse [2][P][rows], flags [2][P]:
+    a rank one step ahead never overwrites a slot a slower peer still
+    merges); the CUDA IPC handles are all-gathered once and
     each rank maps its peers' buffers.  A step: each rank's decode launch
     stores its partial into its slot of every rank's buffers and releases the
     slot flags with the step's sequence number (antkv_decode_step_publish);
@@ -89,14 +91,14 @@ class PeerExchange:
         else:
             self.P, self.rank, distributed = dist.get_world_size(group), dist.get_rank(group), True
         P = self.P
-        self._sizes = (P * self.rows * self.d * 4, P * self.rows * 4, P * 4)
+        self._sizes = (2 * P * self.rows * self.d * 4, 2 * P * self.rows * 4, 2 * P * 4)
         nbytes = sum(self._sizes)
         lib = _lib.load()
         base = ctypes.c_void_p()
         _lib.check(lib.antkv_p2p_alloc(nbytes, ctypes.byref(base)))
         self._own = base.value
         self._mapped = []
-        bases = [self._own]
+        bases = [self._own] * P   # local emulation: every "peer" is this buffer (n_dst == P)
         if distributed and P > 1:
             h = (ctypes.c_ubyte * 64)()
             _lib.check(lib.antkv_ipc_get_handle(ctypes.c_void_p(self._own), h))
@@ -124,7 +126,7 @@ class PeerExchange:
 
     def advance(self):
         """Start the next step (its flags carry the new sequence number)."""
-        self.seq = (self.seq + 1) & 0xFFFFFFFF
+        self.seq = (self.seq + 1) & 0xFFFFFFFF or 1   # 0 is the flags' initial value
         return self.seq
 
     def merge(self, out, lse_out=None):

@@ -1094,20 +1094,33 @@ def test_peer_exchange_publish_and_merge_one_device():
             shards.append(c)
         shards[1].tensors["hstate"][:, :, 0] = ref.config.budget_for(n)
         ex = PeerExchange(Hq, 128, local_slots=2)
+        o = torch.empty((1, Hq, 128), device="cuda")
+        l = torch.empty((1, Hq), device="cuda")
+
+        def publish(r, t, seq):
+            # shard r's partial of step t under sequence number seq
+            q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
+            ex.rank, ex.seq = r, seq
+            tail = r == 1
+            shards[r].step_publish(q, k if tail else None, v if tail else None,
+                                   torch.tensor([t], device="cuda"), o, l, ex)
+            if tail:
+                shards[r]._n += 1
+
         try:
-            for t in range(n, n + steps):
+            # the head shard (attention only) runs ONE STEP AHEAD: it publishes
+            # step t + 1 before the merge of step t reads the slots -- with one
+            # receive half it would overwrite its step-t slot and the merge
+            # (flag >= seq) would mix two steps; the two halves keep them apart
+            seq0 = ex.advance()
+            publish(0, n, seq0)
+            for i, t in enumerate(range(n, n + steps)):
                 q, k, v = dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t])
                 want = ref.decode_step(q, k, v, t)
-                qpos = torch.tensor([t], device="cuda")
-                ex.advance()
-                for r, c in enumerate(shards):
-                    o = torch.empty((1, Hq, 128), device="cuda")
-                    l = torch.empty((1, Hq), device="cuda")
-                    ex.rank = r
-                    tail = r == 1
-                    c.step_publish(q, k if tail else None, v if tail else None, qpos, o, l, ex)
-                    if tail:
-                        c._n += 1
+                publish(1, t, seq0 + i)
+                if t + 1 < n + steps:
+                    publish(0, t + 1, seq0 + i + 1)
+                ex.seq = seq0 + i
                 got = ex.merge(torch.empty((Hq, 128), device="cuda"))
                 assert rel(got.cpu().numpy(), want[0].cpu().numpy()) < 2e-2, (fast, t)
         finally:
