@@ -440,12 +440,15 @@ class OracleCache:
         return budget_for(n, self.anchor_fraction, self.anchor_count)
 
     # cache.py:100-140
-    def prefill(self, Q, K, V, positions, anchors=None):
+    def prefill(self, Q, K, V, positions, anchors=None, codes=None):
         """``anchors`` (test hook, not in the reference): per-KV-head index
         arrays that replace the selection -- the FA + AnS passes are then
         skipped and None is returned.  Used to replay the reference's layout,
         decode and eviction from another implementation's anchor set when
-        the two sets legitimately differ at the float32 margin."""
+        the two sets legitimately differ at the float32 margin.  ``codes``
+        (test hook): per-KV-head (k_codes, v_codes) int arrays [n, groups]
+        used instead of encoding the rows (for long contexts whose codes
+        are checked separately, on a sample, by the margin rule)."""
         K = np.asarray(K, dtype=np.float64)
         V = np.asarray(V, dtype=np.float64)
         h_kv, n, d = K.shape
@@ -481,8 +484,11 @@ class OracleCache:
             else:
                 st.anchor_indices = np.sort(np.asarray(anchors[hk], dtype=np.int64))
             anchor_set = set(int(j) for j in st.anchor_indices)
-            kc = encode_rows(K[hk], self.cb_k[hk])
-            vc = encode_rows(V[hk], self.cb_v[hk])
+            if codes is None:
+                kc = encode_rows(K[hk], self.cb_k[hk])
+                vc = encode_rows(V[hk], self.cb_v[hk])
+            else:
+                kc, vc = (np.asarray(x, dtype=np.int64) for x in codes[hk])
             Kd = decode_rows(kc, self.cb_k[hk])
             Vd = decode_rows(vc, self.cb_v[hk])
             for j in range(n):

@@ -523,56 +523,65 @@ class QuantizedKVCache:
             return O[0, 0].cpu().numpy().astype(np.float64) if was_np else O[0, 0]
         return O
 
-    def _host_state(self):
-        t = {k: v.cpu() for k, v in self._t.items() if k not in ("cb_k", "cb_v", "cb_f16", "pool_f16",
-                                                                  "fast_tables")}
-        return t
+    def _host(self, key, b, h):
+        """One (sequence, head) slice of a state tensor, on the host."""
+        return self._t[key][b, h].cpu().numpy()
+
+    def kinds_array(self, b=0, h=0):
+        """Per-token kinds of (sequence b, KV head h) as int8 (KIND_ANCHOR /
+        KIND_QUANTIZED / KIND_WINDOWED): one copy of the qmask and pool
+        bookkeeping of that head, no per-token Python loop."""
+        n = self._n
+        kinds = np.full(n, _lib.KIND_QUANTIZED, dtype=np.int8)
+        qm = self._host("qmask", b, h).view(np.uint32)
+        bits = np.unpackbits(qm.view(np.uint8), bitorder="little")[:n].astype(bool)
+        tok = self._host("pool_tok", b, h).astype(np.int64)
+        kd = self._host("pool_kind", b, h).astype(np.int64)
+        live = (tok >= 0) & (tok < n) & (kd != _lib.KIND_FREE)
+        kinds[tok[live]] = np.where(kd[live] == _lib.KIND_ANCHOR, _lib.KIND_ANCHOR,
+                                    _lib.KIND_WINDOWED).astype(np.int8)
+        orphan = (kinds == _lib.KIND_QUANTIZED) & ~bits
+        if orphan.any():
+            raise RuntimeError(f"token {int(np.flatnonzero(orphan)[0])} has neither codes nor a "
+                               "full-precision row")
+        return kinds
 
     def kinds_of(self, b=0, h=0):
         """Per-token kind strings for (sequence b, KV head h)."""
-        st = self._host_state()
-        n = self._n
-        kinds = [KIND_QUANTIZED] * n
-        qm = st["qmask"][b, h].numpy().view(np.uint32)
-        bits = np.unpackbits(qm.view(np.uint8), bitorder="little")[:n]
-        for s in range(st["pool_tok"].shape[2]):
-            j = int(st["pool_tok"][b, h, s])
-            kd = int(st["pool_kind"][b, h, s])
-            if 0 <= j < n and kd != _lib.KIND_FREE:
-                kinds[j] = KIND_ANCHOR if kd == _lib.KIND_ANCHOR else KIND_WINDOWED
-        for j in range(n):
-            if kinds[j] == KIND_QUANTIZED and not bits[j]:
-                raise RuntimeError(f"token {j} has neither codes nor a full-precision row")
-        return kinds
+        names = {_lib.KIND_ANCHOR: KIND_ANCHOR, _lib.KIND_QUANTIZED: KIND_QUANTIZED,
+                 _lib.KIND_WINDOWED: KIND_WINDOWED}
+        return [names[int(k)] for k in self.kinds_array(b, h)]
 
     @property
     def kinds(self):
         return self.kinds_of(0, 0)
 
     def anchor_indices_of(self, b=0, h=0):
-        st = self._host_state()
-        tok = st["pool_tok"][b, h].numpy()
-        kind = st["pool_kind"][b, h].numpy()
+        tok = self._host("pool_tok", b, h)
+        kind = self._host("pool_kind", b, h)
         return np.sort(tok[(kind == _lib.KIND_ANCHOR) & (tok >= 0)].astype(np.int64))
 
     @property
     def anchor_indices(self):
         return self.anchor_indices_of(0, 0)
 
-    def codes_of(self, b=0, h=0):
-        """(k_codes, v_codes) dicts {token: int64[groups]} for quantized tokens."""
-        st = self._host_state()
+    def codes_array(self, b=0, h=0):
+        """int64 [n, 2, groups] code indices (K, V) of every slot of
+        (sequence b, KV head h); rows of non-quantized tokens hold stale
+        values (see kinds_array)."""
         G = self.d // self.config.vq.d_sub
-        cap = st["codes"].shape[2]
-        raw = st["codes"][b, h].numpy().reshape(-1)
+        raw = self._host("codes", b, h).reshape(-1)
+        cap = self._t["codes"].shape[2]
         units = unpack_units(raw, _code_kind(self.config.vq, G))
         # tiled layout [tile][kv][16 slots][G] (common.cuh code_offset)
         arr = units.reshape(cap // 16, 2, 16, G).transpose(0, 2, 1, 3).reshape(cap, 2, G)
-        arr = arr[:self._n].astype(np.int64)
-        kinds = self.kinds_of(b, h)
-        kc = {j: arr[j, 0] for j in range(self._n) if kinds[j] == KIND_QUANTIZED}
-        vc = {j: arr[j, 1] for j in range(self._n) if kinds[j] == KIND_QUANTIZED}
-        return kc, vc
+        return arr[:self._n].astype(np.int64)
+
+    def codes_of(self, b=0, h=0):
+        """(k_codes, v_codes) dicts {token: int64[groups]} for quantized tokens."""
+        arr = self.codes_array(b, h)
+        q = np.flatnonzero(self.kinds_array(b, h) == _lib.KIND_QUANTIZED)
+        return {int(j): arr[j, 0] for j in q}, {int(j): arr[j, 1] for j in q}
 
     @property
     def positions(self):
@@ -583,10 +592,10 @@ class QuantizedKVCache:
         bits, as the reference stores them; on the GPU they are bf16)."""
         if self._n == 0:
             raise ValueError("cache is empty")
-        kinds = self.kinds_of(b, h)
+        nq = int((self.kinds_array(b, h) == _lib.KIND_QUANTIZED).sum())
         bits = self.config.vq.index_bits
         groups = self.d // self.config.vq.d_sub
-        payload = sum(2 * groups * bits if k == KIND_QUANTIZED else 2 * self.d * 32 for k in kinds)
+        payload = nq * 2 * groups * bits + (self._n - nq) * 2 * self.d * 32
         denom = 2 * self._n * self.d
         return MemoryReport(payload_bits=payload,
                             codebook_bits=2 * self.config.vq.m * self.config.vq.d_sub * 32,
@@ -613,12 +622,11 @@ class QuantizedKVCache:
 
     def _save_one(self, out_dir, b, h):
         out_dir.mkdir(parents=True, exist_ok=True)
-        st = self._host_state()
         bits = self.config.vq.index_bits
         kinds = self.kinds_of(b, h)
         kc, vc = self.codes_of(b, h)
-        tok = st["pool_tok"][b, h].numpy()
-        rows_bf = st["pool_rows"][b, h].float().numpy()
+        tok = self._host("pool_tok", b, h)
+        rows_bf = self._t["pool_rows"][b, h].float().cpu().numpy()
         slot_of = {int(tok[s]): s for s in range(len(tok)) if tok[s] >= 0}
         rows = bytearray()
         codes = bytearray()
@@ -638,7 +646,7 @@ class QuantizedKVCache:
                        "block_k": c.block_k},
             "n": self._n,
             "d": self.d,
-            "positions": [int(p) for p in st["positions"][b, :self._n]],
+            "positions": [int(p) for p in self._t["positions"][b, :self._n].cpu()],
             "kinds": kinds,
             "anchor_indices": [int(j) for j in self.anchor_indices_of(b, h)],
         }

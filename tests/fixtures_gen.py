@@ -118,3 +118,10 @@ EVAL_CASES = {
     "e3_gauss_d2m16_vonly_byk": (403, 80, 16, "gaussian", "d2m16", 413, 0.1, 4, "by_k", 0,
                                  "v_only", "prefill", 0),
 }
+
+
+# BASELINE config #1 at its real shape (tests/golden/make_config1_golden.py):
+# one LLaMA-3-8B layer, 32 Q / 8 KV heads, d = 128, 2048-token prefill + 128
+# decode steps, d8m256, 1 % anchors by_sum, window 32, LLaMA-3 RoPE base.
+CONFIG1 = dict(seed=101, Hq=32, Hkv=8, n=2048, steps=128, d=128, heavy=3, frac=0.01, window=32,
+               policy="by_sum", theta=5e5, o_stride=64)
