@@ -287,7 +287,7 @@ def encode_throughput(torch, n=131072, reps=5, vq_m=256, d_sub=8):
             "tflops": flops / (ms / 1e3) / 1e12}
 
 
-def prefill_throughput(torch, n=32768):
+def prefill_throughput(torch, n=131072):
     """One layer's prefill (FA + aux, AnS, anchor selection, encode, layout)
     at LLaMA-3-8B attention shapes, bf16 inputs."""
     from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
@@ -541,7 +541,9 @@ def run_ours(args):
     pre = prefill_throughput(torch) if rank == 0 and not args.no_prefill else None
     peak, peak_kind = peaks()
     achieved = alg_bytes / (attn_ms / 1e3) / 1e9
-    value = B * L / (ms / 1e3) * world          # weak scaling: 128K-context equivalents
+    # one token per sequence per layer-step, whatever the number of sequence
+    # shards: N GPUs serve an N-times longer context at (ideally) the same rate
+    value = B * L / (ms / 1e3)
     result = None
     if rank == 0:
         result = {
@@ -564,7 +566,9 @@ def run_ours(args):
                 "ctx_per_gpu": args.ctx, "layers_per_step": L, "batch": B, "kernel": args.kernel,
                 "l2": f"no flush: per-step working set {alg_bytes * L / 1e9:.2f} GB > 126 MB L2",
                 "tok_s_definition": "batch * layers / step time (BASELINE.md: batch / one layer's "
-                                    "decode-attention call) x GPUs (weak scaling)",
+                                    "decode-attention call); at N > 1 the context is N x ctx_per_gpu "
+                                    "(sequence shards) and the rate is NOT multiplied by N",
+                "context_tokens": args.ctx * world,
                 "model_tok_s": B / (ms / 1e3),
                 "launch": "CUDA graph per step" if use_graph else "eager",
                 "exchange": exchange_kind,
@@ -573,10 +577,11 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": "decode attention (split-KV + combine)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
+                         "aggregate_gbs": achieved * world, "aggregate_peak": peak * world,
                          "traffic": measured_traffic(args), "algorithmic_bytes_per_launch": alg_bytes,
                          "launch_ms": attn_ms,
                          "secondary": smem_roofline(args, attn_ms, clk_mhz)},
-            "e2e": {"value": B * L / (e2e_ms / 1e3) * world, "unit": "tok/s",
+            "e2e": {"value": B * L / (e2e_ms / 1e3), "unit": "tok/s",
                     "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * 2,
                     "d2h_bytes_per_step": outh.numel() * 4, "ms_per_step": e2e_ms,
                     "path": ("QuantizedKVCache.step_device per layer (antkv_decode_step)" if world == 1
@@ -602,159 +607,238 @@ def run_ours(args):
 
 
 # ------------------------------------------------------------- reference
-_CPU_ITEMS = []   # the heads' host arrays, inherited by the forked workers (not pickled per task)
+# The reference arm runs the reference package's OWN decode step,
+# QuantizedKVCache.decode_step (cache.py:149-194: append, dequantize, RoPE of
+# every cached key, softmax, A.V, window eviction with promotion or encode),
+# with its compiled _ckernels, staged by oracle/Makefile into
+# oracle/_ref/pkg/antkv (git-ignored; built from /root/reference in the build
+# container, travels to the GPU box).  Nothing of this repo's package or
+# native library is imported on this path.  The reference is single-head, so
+# the 32 query heads of a layer are 32 independent single-head caches (the
+# GQA group's KV rows replicated per query head, "MHA-expanded"); a layer-step
+# is 32 head decode steps.  One worker process per host core (one BLAS
+# thread each) owns one head cache; a timed step is one round of those
+# workers' decode steps -- a bounded sample of min(cores, 32)/32 of a
+# layer-step at the full context.  Without the staged package (no
+# /root/reference at build time) the oracle restatement stands in ("port").
 
-
-def _cpu_head_worker(args_tuple):
-    """Tokens [lo, hi) of one KV head of one layer-step with the reference's
-    decode math (cache.py:168-178 via the oracle restatement): dequantize
-    every token with a per-token centroid lookup, RoPE the keys in float64,
-    the group's query logits, softmax partials (max, sum, A.V) that the
-    caller's LSE merge would combine (a head's range is split only to use
-    every host core)."""
-    import antkv_oracle as O
-    idx, lo, hi = args_tuple
-    kcodes, vcodes, qbits, rows_k, rows_v, fp_tok, ck, cv, q, qpos, theta = _CPU_ITEMS[idx]
-    t0 = time.perf_counter()
-    n = hi - lo
-    Khat = np.empty((n, D), dtype=np.float32)
-    Vhat = np.empty((n, D), dtype=np.float32)
-    for j in range(lo, hi):      # dequantize() loop, cache.py:204-210
-        if qbits[j]:
-            Khat[j - lo] = O.decode_rows(kcodes[j][None], ck)[0]
-            Vhat[j - lo] = O.decode_rows(vcodes[j][None], cv)[0]
-    sel = (fp_tok >= lo) & (fp_tok < hi)
-    Khat[fp_tok[sel] - lo] = rows_k[sel]
-    Vhat[fp_tok[sel] - lo] = rows_v[sel]
-    pos = np.arange(lo, hi, dtype=np.int64)
-    Kr = O.apply_rope(Khat.astype(np.float64), pos, theta)
-    parts = []
-    for hq in range(q.shape[0]):
-        qr = O.apply_rope(q[hq][None], np.array([qpos]), theta)
-        s = ((qr @ Kr.T) / np.sqrt(D))[0]
-        mx = s.max()
-        p = np.exp(s - mx)
-        parts.append((mx, p.sum(), p @ Vhat.astype(np.float64)))
-    return time.perf_counter() - t0, parts
-
-
-def cpu_sample_from_cache(cache, n_heads):
-    """Host copies of (b=0) heads of a GPU cache for the CPU reference arm."""
-    import torch
-    t = cache.tensors
-    n = cache.token_count
-    G = D // cache.config.vq.d_sub
-    from paper_2506_19505_b200.cache import unpack_units
-    cap = t["codes"].shape[2]
-    # tiled layout [tile][kv][16 slots][G] code units (common.cuh code_offset)
-    raw = t["codes"][0, :n_heads].cpu().numpy().reshape(n_heads, -1)
-    units = np.stack([unpack_units(raw[h], cache.desc.code_bytes) for h in range(n_heads)])
-    codes = units.reshape(n_heads, cap // 16, 2, 16, G).transpose(0, 1, 3, 2, 4).reshape(n_heads, cap, 2, G)[:, :n]
-    qm = t["qmask"][0, :n_heads].cpu().numpy().view(np.uint32)
-    items = []
-    rng = np.random.default_rng(5)
-    for h in range(n_heads):
-        bits = np.unpackbits(qm[h].view(np.uint8), bitorder="little")[:n].astype(bool)
-        kind = t["pool_kind"][0, h].cpu().numpy()
-        tok = t["pool_tok"][0, h].cpu().numpy()
-        live = (kind >= 0) & (tok >= 0) & (tok < n)
-        rows = t["pool_rows"][0, h].float().cpu().numpy()
-        items.append((codes[h, :, 0].astype(np.int64), codes[h, :, 1].astype(np.int64), bits,
-                      rows[live, 0], rows[live, 1], tok[live],
-                      t["cb_k"][h].cpu().numpy(), t["cb_v"][h].cpu().numpy(),
-                      rng.standard_normal((HQ // HKV, D)), n, cache.config.theta_base))
-    return items
-
-
-def run_cpu(items, repeats):
-    """Time `repeats` layer-steps over every host core: each KV head's token
-    range is cut into as many slices as needed to give every core one."""
-    import multiprocessing as mp
-    ncpu = os.cpu_count() or 1
-    per_head = max(1, -(-ncpu // len(items)))
-    work = []
-    _CPU_ITEMS[:] = items
-    for idx, it in enumerate(items):
-        n = len(it[2])
-        cuts = np.linspace(0, n, per_head + 1).astype(int)
-        work += [(idx, int(cuts[i]), int(cuts[i + 1])) for i in range(per_head)]
-    cores = min(len(work), ncpu)
+def _reference_module():
+    pkg = ROOT / "oracle" / "_ref" / "pkg"
+    if (pkg / "antkv" / "cache.py").exists():
+        sys.path.insert(0, str(pkg))
+        import antkv
+        return antkv, "reference"
     sys.path.insert(0, str(ROOT / "oracle"))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    walls = []
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        for _ in range(repeats):
-            t0 = time.perf_counter()
-            pool.map(_cpu_head_worker, work)
-            walls.append(time.perf_counter() - t0)
-    return walls, cores
+    import antkv_oracle
+    return antkv_oracle, "port"
+
+
+def round_bf16(x):
+    """Round to the nearest bfloat16 (even on ties), returned as float32."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).reshape(np.shape(x))
+
+
+def _ref_head_state(n, m, d_sub, head, window=32, frac=0.01):
+    """Synthetic single-head cache contents at n tokens (seeded per head):
+    1 % anchors outside the window, the last `window` other tokens windowed,
+    the rest random code indices; bf16-exact float32 rows; N(0,1) codebooks."""
+    rng = np.random.default_rng(5000 + head)
+    G = D // d_sub
+    anchors = np.sort(rng.choice(n - window, size=math.ceil(frac * n), replace=False))
+    is_fp = np.zeros(n, dtype=bool)
+    is_fp[anchors] = True
+    win = np.flatnonzero(~is_fp)[-window:]
+    is_fp[win] = True
+    fp = np.flatnonzero(is_fp)
+    rows_k = round_bf16(rng.standard_normal((len(fp), D)))
+    rows_v = round_bf16(rng.standard_normal((len(fp), D)))
+    codes = rng.integers(0, m, size=(n, 2, G))
+    ck = rng.standard_normal((m, d_sub)).astype(np.float32)
+    cv = rng.standard_normal((m, d_sub)).astype(np.float32)
+    return anchors, win, fp, rows_k, rows_v, codes, ck, cv
+
+
+def _ref_build_cache(mod, kind, n, notation, head, theta):
+    """One single-head reference cache holding the synthetic state, installed
+    field by field as the reference's own load() does (cache.py:286-342)."""
+    vq = mod.VqConfig.from_notation(notation) if kind == "reference" else None
+    m = vq.m if vq else int(notation.split("m")[1])
+    d_sub = vq.d_sub if vq else int(notation[1:].split("m")[0])
+    anchors, win, fp, rows_k, rows_v, codes, ck, cv = _ref_head_state(n, m, d_sub, head)
+    if kind == "port":
+        c = mod.OracleCache([ck], [cv], anchor_fraction=0.01, window_size=32, theta_base=theta)
+        K = np.zeros((1, n, D))
+        V = np.zeros((1, n, D))
+        K[0, fp], V[0, fp] = rows_k, rows_v
+        c.prefill(None, K, V, np.arange(n), anchors=[anchors], codes=[(codes[:, 0], codes[:, 1])])
+        return c
+    cfg = mod.CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=theta)
+    c = mod.QuantizedKVCache(cfg, mod.Codebook(config=vq, centroids=ck), mod.Codebook(config=vq, centroids=cv))
+    c.d = D
+    c.positions = list(range(n))
+    kinds = [mod.cache.KIND_QUANTIZED] * n
+    for j in anchors:
+        kinds[j] = mod.cache.KIND_ANCHOR
+    for j in win:
+        kinds[j] = mod.cache.KIND_WINDOWED
+    c.kinds = kinds
+    fp_set = set(int(j) for j in fp)
+    c.k_rows = {int(j): rows_k[i] for i, j in enumerate(fp)}
+    c.v_rows = {int(j): rows_v[i] for i, j in enumerate(fp)}
+    c.k_codes = {j: codes[j, 0] for j in range(n) if j not in fp_set}
+    c.v_codes = {j: codes[j, 1] for j in range(n) if j not in fp_set}
+    c.anchor_indices = anchors.astype(np.int64)
+    return c
+
+
+def _ref_worker(conn, head, n, notation, theta):
+    from threadpoolctl import threadpool_limits
+    threadpool_limits(1)
+    mod, kind = _reference_module()
+    t0 = time.perf_counter()
+    cache = _ref_build_cache(mod, kind, n, notation, head, theta)
+    conn.send(time.perf_counter() - t0)
+    rng = np.random.default_rng(9000 + head)
+    while True:
+        s = conn.recv()
+        if s is None:
+            break
+        q, k, v = rng.standard_normal((3, D))
+        t0 = time.perf_counter()
+        if kind == "port":
+            cache.decode_step(q[None], k[None], v[None], n + s)
+        else:
+            cache.decode_step(q, k, v, n + s)
+        conn.send(time.perf_counter() - t0)
+    conn.close()
+
+
+class RefPool:
+    """One process per host core (at most HQ), each owning one single-head
+    reference cache at the workload's context; step(s) runs one decode step
+    on every worker and returns the round's wall time."""
+
+    def __init__(self, n, notation, theta=500000.0, workers=None):
+        import multiprocessing as mp
+        self.kind = _reference_module()[1]
+        self.P = max(1, min(HQ, workers or os.cpu_count() or 1))
+        ctx = mp.get_context("fork")
+        self.conns, self.procs = [], []
+        for h in range(self.P):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_ref_worker, args=(b, h, n, notation, theta), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+        self.build_s = max(c.recv() for c in self.conns)
+
+    def step(self, s):
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(s)
+        head_s = [c.recv() for c in self.conns]
+        return time.perf_counter() - t0, head_s
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=30)
+
+
+def ref_config1_timing(theta=500000.0):
+    """BASELINE config #1 on the reference itself, one core: a 2048-token
+    single-head prefill (cache.py:100-140) and 128 decode steps
+    (cache.py:149-194), d8m256, 1 % anchors, window 32.  Returns ms per head."""
+    mod, kind = _reference_module()
+    if kind != "reference":
+        return None
+    from threadpoolctl import threadpool_limits
+    rng = np.random.default_rng(101)
+    n, steps = 2048, 128
+    Q, K, V = (round_bf16(rng.standard_normal((n + steps, D))).astype(np.float64) for _ in range(3))
+    vq = mod.VqConfig.from_notation("d8m256")
+    cb = [mod.Codebook(config=vq, centroids=rng.standard_normal((256, 8)).astype(np.float32)) for _ in range(2)]
+    cache = mod.QuantizedKVCache(mod.CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=theta),
+                                 cb[0], cb[1])
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        cache.prefill(Q[:n], K[:n], V[:n], np.arange(n))
+        t1 = time.perf_counter()
+        for t in range(n, n + steps):
+            cache.decode_step(Q[t], K[t], V[t], t)
+        t2 = time.perf_counter()
+    dec = (t2 - t1) / steps
+    return {"prefill_ms_per_head": (t1 - t0) * 1e3, "decode_step_ms_per_head": dec * 1e3,
+            "layer_step_s_one_core": dec * HQ, "cores": 1,
+            "what": "reference QuantizedKVCache (its compiled _ckernels), one head, 2048-token prefill + "
+                    "128 decode steps; a layer-step is 32 such head steps"}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port) on the host."""
+    """--impl reference: the reference package's own decode step on the host
+    cores, on the same workload config as the GPU arm (rank 0 only)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
-    import torch
-    sys.path.insert(0, str(ROOT / "oracle"))
-    # the CPU arm needs the same cache contents; build one layer on the GPU
-    # (if present) to get identical codes, otherwise synthesise on the host
-    a = argparse.Namespace(**vars(args))
-    a.layers = 1
-    if torch.cuda.is_available():
-        from paper_2506_19505_b200 import _lib
-        _lib.load()
-        caches, _ = build_layers(a, 0, 1, torch)
-        items = cpu_sample_from_cache(caches[0], HKV)
-    else:
-        items = _host_items(args.ctx)
-    steps = max(1, min(args.steps, 3))
-    warm = 1 if args.warmup > 0 else 0
-    walls, cores = run_cpu(items, warm + steps)
-    walls = walls[warm:]
+    c1 = ref_config1_timing()
+    pool = RefPool(args.ctx, args.notation)
+    try:
+        for s in range(args.warmup):
+            pool.step(s)
+        walls, heads = [], []
+        for s in range(args.warmup, args.warmup + args.steps):
+            w, h = pool.step(s)
+            walls.append(w)
+            heads += h
+    finally:
+        pool.close()
     t = float(np.mean(walls))
-    value = args.batch / t
+    value = args.batch * (pool.P / HQ) / t      # layer-steps per second
+    sample = (f"each step: {pool.P} single-head reference caches at {args.ctx} tokens, one decode step "
+              f"each, in parallel ({pool.P} of the {HQ} head steps of a layer-step; {t:.2f} s wall, "
+              f"{np.mean(heads):.2f} s per head step)")
     return {
         "impl": "reference",
         "metric": METRIC,
         "value": value,
         "unit": "tok/s",
         "n_gpus": world,
-        "steps": steps,
-        "warmup": warm,
+        "steps": args.steps,
+        "warmup": args.warmup,
         "ms_per_step": t * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (same cache contents as the GPU arm)",
-        "config": {"workload": f"decode attention, {args.ctx // 1024}K ctx, {args.notation}, "
-                               f"1% anchors, window 32, {HQ} Q / {HKV} KV heads, d={D}, batch "
-                               f"{args.batch}; one step = one layer's decode-attention call",
-                   "ctx_per_gpu": args.ctx},
-        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": "port",
-                         "sample": f"{steps} layer-step(s) at {args.ctx} tokens, "
-                                   f"{HKV} KV heads split over all host cores"},
+        "data": "synthetic (seeded random codes, 1% anchors, bf16-exact rows, N(0,1) codebooks)",
+        "config": {"workload": f"decode step, {args.ctx // 1024}K ctx, {args.notation}, 1% anchors, window 32, "
+                               f"{HQ} Q / {HKV} KV heads (MHA-expanded: the reference is single-head), d={D}, "
+                               f"batch {args.batch}; value = layer-steps/s (= batch x layers / s)",
+                   "ctx_per_gpu": args.ctx, "path": f"{pool.kind}: QuantizedKVCache.decode_step "
+                                                    "(cache.py:149-194) incl. append and evict/encode",
+                   "head_cache_build_s": pool.build_s},
+        "cpu_baseline": {"value": value, "unit": "tok/s", "cores": pool.P, "kind": pool.kind,
+                         "sample": sample},
+        "config1_reference": c1,
         "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "native_so_loaded": repo_libraries_mapped(),
     }
 
 
-def _host_items(n):
-    rng = np.random.default_rng(0)
-    items = []
-    for h in range(HKV):
-        bits = np.ones(n, dtype=bool)
-        fp = np.sort(rng.choice(n, size=math.ceil(0.01 * n) + 32, replace=False))
-        bits[fp] = False
-        items.append((rng.integers(256, size=(n, 16)), rng.integers(256, size=(n, 16)), bits,
-                      rng.standard_normal((len(fp), D)).astype(np.float32),
-                      rng.standard_normal((len(fp), D)).astype(np.float32), fp,
-                      rng.standard_normal((256, 8)).astype(np.float32),
-                      rng.standard_normal((256, 8)).astype(np.float32),
-                      rng.standard_normal((HQ // HKV, D)), n, 500000.0))
-    return items
+def repo_libraries_mapped():
+    """Shared objects of this repository's product package mapped into this
+    process (the reference arm must map none)."""
+    try:
+        maps = Path("/proc/self/maps").read_text()
+    except OSError:
+        return None
+    pkg = str(ROOT / "paper_2506_19505_b200")
+    return sorted({ln.split()[-1] for ln in maps.splitlines() if ln.split() and ln.split()[-1].startswith(pkg)
+                   and ".so" in ln.split()[-1]})
 
 
 def main():
@@ -768,14 +852,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if rank == 0:
         if not args.no_cpu_baseline and int(os.environ.get("WORLD_SIZE", "1")) == 1:
-            items = cpu_sample_from_cache(caches[0], HKV)
-            walls, cores = run_cpu(items, 2)
-            t = float(np.mean(walls[1:])) if len(walls) > 1 else walls[0]
-            res["cpu_baseline"] = {"value": args.batch / t, "unit": "tok/s", "cores": cores,
-                                   "kind": "port",
-                                   "sample": f"1 layer-step at {args.ctx} tokens ({HKV} KV heads, "
-                                             f"reference decode math, each head's tokens split "
-                                             f"over the host cores), {t:.2f} s wall"}
+            pool = RefPool(args.ctx, args.notation)
+            try:
+                t, heads = pool.step(0)
+            finally:
+                pool.close()
+            res["cpu_baseline"] = {"value": args.batch * (pool.P / HQ) / t, "unit": "tok/s", "cores": pool.P,
+                                   "kind": pool.kind,
+                                   "sample": f"one round of {pool.P} single-head reference decode steps "
+                                             f"(QuantizedKVCache.decode_step at {args.ctx} tokens, one per "
+                                             f"core) = {pool.P}/{HQ} of a layer-step, {t:.2f} s wall"}
         print(json.dumps(res), flush=True)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         import torch.distributed as dist

@@ -8,6 +8,7 @@ import re
 import subprocess
 import sys
 import tempfile
+import json
 from pathlib import Path
 
 import numpy as np
@@ -351,20 +352,45 @@ def test_packed_code_units_roundtrip(rng):
         assert np.array_equal(unpack_units(pack_units(v, kind), kind), v)
 
 
-def test_bench_cpu_arm_token_slices_merge_exactly():
-    """The CPU reference arm splits each KV head's tokens over the host
-    cores; the softmax partials of the slices merge (LSE) into the same
-    attention output as one pass over the whole range."""
+def test_bench_reference_arm_installs_a_faithful_reference_cache():
+    """bench.py's reference arm installs its synthetic state into the
+    reference's own QuantizedKVCache (oracle/_ref/pkg, staged from
+    /root/reference by oracle/Makefile); its decode steps -- append,
+    dequantize, attention, eviction -- equal the oracle restatement holding
+    the same state (the port fallback) to 1e-12."""
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "oracle"))
     import bench
-    items = bench._host_items(1024)[:1]
-    bench._CPU_ITEMS[:] = items
-    _, whole = bench._cpu_head_worker((0, 0, 1024))
-    _, a = bench._cpu_head_worker((0, 0, 400))
-    _, b = bench._cpu_head_worker((0, 400, 1024))
-    for (m0, l0, o0), (m1, l1, o1), (mw, lw, ow) in zip(a, b, whole):
-        m = max(m0, m1)
-        l = l0 * np.exp(m0 - m) + l1 * np.exp(m1 - m)
-        o = (o0 * np.exp(m0 - m) + o1 * np.exp(m1 - m)) / l
-        assert np.allclose(o, ow / lw, rtol=1e-12, atol=1e-14)
+    mod, kind = bench._reference_module()
+    if kind != "reference":
+        pytest.skip("oracle/_ref/pkg not built (no /root/reference)")
+    import antkv_oracle
+    n = 300
+    ref = bench._ref_build_cache(mod, "reference", n, "d8m256", 3, 5e5)
+    port = bench._ref_build_cache(antkv_oracle, "port", n, "d8m256", 3, 5e5)
+    rng = np.random.default_rng(0)
+    for s in range(40):                       # past the window: promotions and encodes
+        q, k, v = rng.standard_normal((3, bench.D))
+        a = ref.decode_step(q, k, v, n + s)
+        b = port.decode_step(q[None], k[None], v[None], n + s)[0]
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+    assert list(ref.anchor_indices) == list(port.heads[0].anchor_indices)
+    assert ref.kinds == port.heads[0].kinds
+
+
+def test_bench_reference_arm_runs_without_the_native_library():
+    """`bench.py --impl reference` (tiny context) prints one JSON line with
+    the same steps / warm-up as requested, kind "reference", and never maps
+    this repo's libantkv_b200.so."""
+    import subprocess
+    if not (ROOT / "oracle" / "_ref" / "pkg" / "antkv" / "cache.py").exists():
+        pytest.skip("oracle/_ref/pkg not built (no /root/reference)")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--ctx", "2048",
+                          "--steps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600,
+                         env={**os.environ, "CUDA_VISIBLE_DEVICES": ""})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["steps"] == 2 and line["warmup"] == 1
+    assert line["cpu_baseline"]["kind"] == "reference"
+    assert line["native_so_loaded"] == []
+    assert line["value"] > 0
