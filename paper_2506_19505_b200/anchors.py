@@ -13,7 +13,7 @@ from . import _lib
 from ._tensors import as_cuda, back
 from .attention import AttentionAux, _check, rope_device
 
-__all__ = ["AnchorScores", "AnchorSelection", "POLICIES", "anchor_scores_blocked",
+__all__ = ["AnchorScores", "AnchorSelection", "POLICIES", "anchor_scores", "anchor_scores_blocked",
            "select_anchors", "select_anchors_device"]
 
 POLICIES = ("by_k", "by_v", "by_sum")
@@ -30,6 +30,20 @@ class AnchorSelection:
     indices: np.ndarray
     budget: int
     policy: str
+
+
+def anchor_scores(A, q_norms):
+    """Direct double-sum scores from a materialised attention matrix
+    (anchors.py:53-63): ans_v = sum_i A_ij, ans_k = sum_i A_ij (1 - A_ij) |q_i|.
+    The oracle of anchor_scores_blocked; float64 on the device."""
+    from .attention import _dev64, _out
+    At, was_np = _dev64(A, "A")
+    qn = torch.as_tensor(np.asarray(q_norms, dtype=np.float64) if not isinstance(q_norms, torch.Tensor)
+                         else q_norms).to(device=At.device, dtype=torch.float64)
+    if qn.shape != (At.shape[0],):
+        raise ValueError("q_norms length must match the query count")
+    return AnchorScores(ans_k=_out((At * (1.0 - At) * qn[:, None]).sum(dim=0), was_np),
+                        ans_v=_out(At.sum(dim=0), was_np))
 
 
 def anchor_scores_blocked(Q, K, V, aux: AttentionAux, block_q, block_k, rope=None,

@@ -15,7 +15,8 @@ from . import _lib
 from ._tensors import as_cuda, back
 from .errors import NumericalError
 
-__all__ = ["RopeParams", "AttentionAux", "apply_rope", "flash_attention_aux", "rope_device"]
+__all__ = ["RopeParams", "AttentionAux", "apply_rope", "flash_attention_aux", "rope_device",
+           "softmax_rows", "attention_scores", "attention_exact"]
 
 
 @dataclass(frozen=True)
@@ -135,3 +136,95 @@ def flash_attention_aux(Q, K, V, block_q, block_k, rope=None, causal=False):
     sq = (lambda x: x[0]) if single else (lambda x: x)
     return AttentionAux(O=back(sq(O), was_np), L=back(sq(L), was_np), M=back(sq(M), was_np),
                         q_norms=back(sq(qn), was_np), block_q=block_q, block_k=block_k)
+
+
+# ---------------------------------------------------------------- exact oracles
+# The reference's unblocked float64 attention (attention.py:70-79, 121-143),
+# the correctness oracle of every blocked and quantized path.  Computed on the
+# device in float64 (torch CUDA tensors; there is no CPU path); numpy in,
+# numpy out as in the reference, CUDA tensors in, tensors out.
+
+def _dev64(X, name, d_even=False):
+    """attention.py:59-67 (_check_matrix) on the device: float64, 2-d,
+    finite, even head dimension for RoPE."""
+    was_np = not isinstance(X, torch.Tensor)
+    if was_np:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(X, dtype=np.float64)))
+    else:
+        t = X.detach()
+    _lib.load()
+    t = t.to(device="cuda", dtype=torch.float64)
+    if t.ndim != 2:
+        raise ValueError(f"{name} must be 2-d, got shape {tuple(t.shape)}")
+    if not bool(torch.isfinite(t).all()):
+        raise NumericalError(f"non-finite values in {name}")
+    if d_even and t.shape[1] % 2 != 0:
+        raise ValueError(f"{name} head dimension must be even for RoPE")
+    return t, was_np
+
+
+def _out(t, was_np):
+    return t.cpu().numpy() if was_np else t
+
+
+def _softmax64(M, causal):
+    if causal:
+        n_q, n_k = M.shape
+        mask = torch.arange(n_k, device=M.device)[None, :] > torch.arange(n_q, device=M.device)[:, None]
+        M = M.masked_fill(mask, float("-inf"))
+    P = torch.exp(M - M.max(dim=1, keepdim=True).values)
+    return P / P.sum(dim=1, keepdim=True)
+
+
+def softmax_rows(M, causal=False):
+    """Row softmax with per-row max subtraction; causal masks j > i
+    (attention.py:70-79)."""
+    t, was_np = _dev64(M, "logits")
+    return _out(_softmax64(t, causal), was_np)
+
+
+def _rope64(X, params: RopeParams):
+    """attention.py:82-106 in float64 on the device (angles pos * freq formed
+    in float64, as _rope_trig does)."""
+    n, d = X.shape
+    if len(params.positions) < n:
+        raise ValueError("positions shorter than token count")
+    freqs = params.theta_base ** (-2.0 * np.arange(d // 2) / d)
+    ang = torch.from_numpy(params.positions[:n, None].astype(np.float64) * freqs[None, :]).to(X.device)
+    c, s = torch.cos(ang), torch.sin(ang)
+    x0, x1 = X[:, 0::2], X[:, 1::2]
+    out = torch.empty_like(X)
+    out[:, 0::2] = x0 * c - x1 * s
+    out[:, 1::2] = x0 * s + x1 * c
+    return out
+
+
+def _scores64(Q, K, rope, causal):
+    if Q.shape[1] != K.shape[1]:
+        raise ValueError("Q and K head dimensions differ")
+    if causal and Q.shape[0] != K.shape[0]:
+        raise ValueError("causal attention requires matching Q/K token counts")
+    if rope is not None:
+        if Q.shape[1] % 2:
+            raise ValueError("Q head dimension must be even for RoPE")
+        Q, K = _rope64(Q, rope), _rope64(K, rope)
+    return _softmax64((Q @ K.T) / np.sqrt(Q.shape[1]), causal)
+
+
+def attention_scores(Q, K, rope=None, causal=False):
+    """Softmax(Q~ K~^T / sqrt(d)), optionally RoPE-rotated and causal
+    (attention.py:121-131)."""
+    Qt, was_np = _dev64(Q, "Q")
+    Kt, _ = _dev64(K, "K")
+    return _out(_scores64(Qt, Kt, rope, causal), was_np)
+
+
+def attention_exact(Q, K, V, rope=None, causal=False):
+    """Attn(Q, K, V) = Softmax(Q~ K~^T / sqrt(d)) V, unblocked
+    (attention.py:134-143)."""
+    Vt, _ = _dev64(V, "V")
+    Kt, _ = _dev64(K, "K")
+    if Vt.shape[0] != Kt.shape[0]:
+        raise ValueError("K and V token counts differ")
+    Qt, was_np = _dev64(Q, "Q")
+    return _out(_scores64(Qt, Kt, rope, causal) @ Vt, was_np)

@@ -464,8 +464,8 @@ class QuantizedKVCache:
         single = qt.ndim == 1
         if single:
             qt, kt, vt = qt[None, None], kt[None, None], vt[None, None]
-        if self._t is None:
-            raise ValueError("decode_step before prefill is not supported on the GPU cache")
+        if self._t is None or self._n == 0 and self.d is None:
+            self._start_empty(qt, kt, single)
         self._ensure_capacity(self._n + 2)
         qt, kt, vt = self._row_dtype(qt), self._row_dtype(kt), self._row_dtype(vt.to(kt.dtype))
         qt = qt.to(kt.dtype)
@@ -477,6 +477,26 @@ class QuantizedKVCache:
         if single:
             return out[0, 0].cpu().numpy().astype(np.float64) if was_np else out[0, 0]
         return out
+
+    def _start_empty(self, qt, kt, single):
+        """decode_step on a cache that was never prefilled: the reference
+        accepts it and takes d from the first token (cache.py:155-166); the
+        shapes come from q [B, Hq, d] / k [B, Hkv, d]."""
+        B, Hq, d = qt.shape
+        Hkv = kt.shape[1]
+        if B != self.B:
+            raise ValueError(f"cache was created for batch {self.B}")
+        if Hq % Hkv:
+            raise ValueError("query heads must be a multiple of KV heads")
+        if d % self.config.vq.d_sub != 0:
+            raise ValueError("head dimension incompatible with codebook")
+        self._single = single
+        self.Hq, self.Hkv = Hq, Hkv
+        dt = kt.dtype if kt.dtype in (torch.float32, torch.bfloat16, torch.float16) else torch.float32
+        dev = kt.device
+        empty = torch.empty((B, Hkv, 0, d), dtype=dt, device=dev)
+        self.build_from(empty, empty, torch.empty((B, 0), dtype=torch.int64, device=dev),
+                        torch.empty((B, Hkv, 0), dtype=torch.int32, device=dev))
 
     # ------------------------------------------------------- inspection
     def dequantize(self):

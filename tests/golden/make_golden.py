@@ -169,8 +169,41 @@ def eval_cases():
     return out
 
 
+def ref_snapshot_case():
+    """A snapshot WRITTEN BY THE REFERENCE (QuantizedKVCache.save,
+    cache.py:245-284) of cache case c2 after its prefill and 64 decode steps,
+    plus the reference's next 16 decode steps from that state: the GPU cache
+    must load the directory (cache.py:286-342 format) and continue
+    identically (tests/test_gpu_parity.py::test_load_reference_written_snapshot)."""
+    import shutil
+    name = "c2_d128_d8m256"
+    seed, n, d, notation, window, frac, count, policy, steps, stride, blk = CACHE_CASES[name]
+    cfg = VqConfig.from_notation(notation)
+    more = 16
+    Q, K, V = qkv(seed, 1, 1, n + steps + more, d, heavy=2)
+    Q, K, V = Q[0].astype(np.float64), K[0].astype(np.float64), V[0].astype(np.float64)
+    ck, cv = codebooks(seed, 1, cfg.m, cfg.d_sub)
+    cache = QuantizedKVCache(
+        CacheConfig(vq=cfg, anchor_fraction=frac, anchor_count=count, window_size=window,
+                    policy=policy, block_q=blk, block_k=blk),
+        Codebook(config=cfg, centroids=ck[0]), Codebook(config=cfg, centroids=cv[0]))
+    cache.prefill(Q[:n], K[:n], V[:n], np.arange(n))
+    for t in range(n, n + steps):
+        cache.decode_step(Q[t], K[t], V[t], t)
+    out_dir = HERE / "ref_snapshot_c2"
+    shutil.rmtree(out_dir, ignore_errors=True)
+    cache.save(out_dir)
+    outs = [cache.decode_step(Q[t], K[t], V[t], t) for t in range(n + steps, n + steps + more)]
+    np.savez_compressed(HERE / "ref_snapshot_c2.npz", decode_out=np.array(outs),
+                        anchors=cache.anchor_indices.copy(),
+                        kinds=np.array([{"anchor": 0, "quantized": 1, "windowed": 2}[k] for k in cache.kinds]))
+
+
 def main():
     print("reference backend:", antkv.kernels.BACKEND, file=sys.stderr)
+    if sys.argv[1:] == ["snapshot"]:
+        ref_snapshot_case()
+        return
     np.savez_compressed(HERE / "kernels.npz", **kernel_cases())
     np.savez_compressed(HERE / "kmeans.npz", **kmeans_cases())
     eval_cases()
@@ -178,6 +211,7 @@ def main():
         res = run_cache_case(name, spec)
         np.savez_compressed(HERE / f"cache_{name}.npz", **res)
         print(name, "anchors", res["anchors0"], "->", res["anchors1"], file=sys.stderr)
+    ref_snapshot_case()
     (HERE / "README.md").write_text(
         "Golden fixtures produced by running the reference `antkv` package\n"
         "(`/root/reference/pkg/src`, kernels backend: "
