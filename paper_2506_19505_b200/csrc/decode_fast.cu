@@ -718,24 +718,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   const int pool_high = c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH];
   const int64_t pos0 = c.positions[(int64_t)b * c.capacity];
   int64_t qp = a.early_q ? a.qpos[b] : 0;
-  // key-rotation constants and frame steps into registers (tables only)
   WarpState w;
-  mbar_wait(&sm.tbar, 0);
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    const float4 st = sm.tab.step[s][t];
-    w.sc[s] = make_float2(st.x, st.z);
-    w.ss[s] = make_float2(st.y, st.w);
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const uint4 k = sm.tab.kc[s][u][t][g];
-      w.kc[s][4 * u] = k.x;
-      w.kc[s][4 * u + 1] = k.y;
-      w.kc[s][4 * u + 2] = k.z;
-      w.kc[s][4 * u + 3] = k.w;
-    }
-  }
-  FK_TR(2);
 
   // ---- phase 1 (needs n / pool_high): work split, bulk copies of the code
   // and pool tiles, qmask words, pool-tile kinds.  Code tiles: the last
@@ -774,6 +757,24 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     if (pt0 + warp < pt1) issue_pool(pt0 + warp);
     for (int it = 0; it < min(nslots, FK_NS); ++it) issue_code(it);
   }
+  // key-rotation constants and frame steps into registers (the tables copy
+  // was issued first; the code / pool copies above are already in flight)
+  mbar_wait(&sm.tbar, 0);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const float4 st = sm.tab.step[s][t];
+    w.sc[s] = make_float2(st.x, st.z);
+    w.ss[s] = make_float2(st.y, st.w);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint4 k = sm.tab.kc[s][u][t][g];
+      w.kc[s][4 * u] = k.x;
+      w.kc[s][4 * u + 1] = k.y;
+      w.kc[s][4 * u + 2] = k.z;
+      w.kc[s][4 * u + 3] = k.w;
+    }
+  }
+  FK_TR(2);
   // qmask words of this warp's range (one word per stage), up to 2 per lane
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
   uint32_t qmv[2];
@@ -832,19 +833,15 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
   __syncthreads();
   FK_TR(14);
-  uint32_t bqa[8][2];
   {
     const int fr = 2 * warp + (g >= 4 ? 1 : 0);
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
       const float4 xq = *reinterpret_cast<const float4 *>(&sm.qf[g & 3][(s * 4 + t) * 2]);
       const float4 cf = *reinterpret_cast<const float4 *>(&sm.ang[fr][(s * 4 + t) * 2]);
-      const float4 ca = *reinterpret_cast<const float4 *>(&sm.ang[2 * FK_WARPS][(s * 4 + t) * 2]);
       // pair u = 0: (xq.x, xq.y) rotated by (cf.x, cf.y); u = 1: (xq.z, xq.w) by (cf.z, cf.w)
       w.fx[s] = make_float2(xq.x * cf.x - xq.y * cf.y, xq.z * cf.z - xq.w * cf.w);
       w.fy[s] = make_float2(xq.x * cf.y + xq.y * cf.x, xq.z * cf.w + xq.w * cf.z);
-      bqa[s][0] = g < 4 ? pack_h2(xq.x * ca.x - xq.y * ca.y, xq.x * ca.y + xq.y * ca.x) : 0u;
-      bqa[s][1] = g < 4 ? pack_h2(xq.z * ca.z - xq.w * ca.w, xq.z * ca.w + xq.w * ca.z) : 0u;
     }
   }
   w.mrun[0] = w.mrun[1] = -INFINITY;
@@ -891,6 +888,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   const bool lo = t < 2;   // owns columns 0-3 (even tile / pool)
   // ---- pool tiles (absolute frame: R(p_q) q, columns 4-7 zero)
   if (pt0 + warp < pt1) {
+    uint32_t bqa[8][2];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const float4 xq = *reinterpret_cast<const float4 *>(&sm.qf[g & 3][(s * 4 + t) * 2]);
+      const float4 ca = *reinterpret_cast<const float4 *>(&sm.ang[2 * FK_WARPS][(s * 4 + t) * 2]);
+      bqa[s][0] = g < 4 ? pack_h2(xq.x * ca.x - xq.y * ca.y, xq.x * ca.y + xq.y * ca.x) : 0u;
+      bqa[s][1] = g < 4 ? pack_h2(xq.z * ca.z - xq.w * ca.w, xq.z * ca.w + xq.w * ca.z) : 0u;
+    }
     int r = 0;
     for (int tile = pt0 + warp; tile < pt1; tile += FK_WARPS, ++r) {
       if (r > 0) {
@@ -1013,11 +1018,17 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   FK_TR(13);
   // ---- tickets: the last CTA of (b, h) combines and commits; the last CTA
   // of sequence b publishes its new length
-  __threadfence();
+  // The CTA barrier orders every thread's partial stores before thread 0's
+  // gpu-scope release (cumulative); the acquire half orders the last CTA's
+  // reads of the other partials after its ticket, and the next barrier
+  // passes that on to the CTA.  (One thread fences: a CTA-wide fence.sc.gpu
+  // -- __threadfence -- took ~4 us here under the other CTAs' streaming.)
   __syncthreads();
   if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     sm.ticket = atomicAdd(&a.cnt[bh], 1);
     sm.gticket = a.knew ? atomicAdd(&a.cnt[(int64_t)c.B * c.Hkv + b], 1) : -1;
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
   if (a.trace && threadIdx.x == 0) {
@@ -1025,7 +1036,9 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     unsigned long long *o =
         a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
     o[0] = smid() | ((unsigned long long)sm.ticket << 32);
-    for (int i = 2; i <= 10; ++i) o[i] = tr[i] - tr[1];
+    for (int i = 2; i <= 9; ++i) o[i] = tr[i] - tr[1];
+    o[10] = tr[10];   // global timer after the tickets (absolute, like o[1])
+    tr[12] = clock64();   // ... and the SM clock at the same point (clock calibration)
     o[1] = g0;
     o[11] = 0;
     o[12] = tr[12] - tr[1];
@@ -1040,7 +1053,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     a.cnt[(int64_t)c.B * c.Hkv + b] = 0;
   }
   if (sm.ticket != S - 1) return;
-  __threadfence();
   if (warp < 4) {
     // warp hh combines head hh: lane = 4 dims; the loads of up to 24 splits
     // are in flight together, then a running max across passes

@@ -598,12 +598,15 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
   }
 
   // ---- the last CTA of (b, h) (atomic ticket) merges the splits' partials
-  __threadfence();
+  // barrier + one thread's acq_rel fences around the ticket (see decode_fast.cu)
   __syncthreads();
-  if (threadIdx.x == 0) sm.ticket = atomicAdd(&a.cnt[bh], 1);
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    sm.ticket = atomicAdd(&a.cnt[bh], 1);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  }
   __syncthreads();
   if (sm.ticket != S - 1) return;
-  __threadfence();
   if (warp < GQ) {   // warp x: query head h GQ + x, lane: 4 dims; loads of 16 splits in flight
     const int64_t rows = (int64_t)c.B * c.Hq;
     const int64_t row = (int64_t)b * c.Hq + (int64_t)h * GQ + warp;

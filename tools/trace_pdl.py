@@ -35,7 +35,7 @@ def main():
             c.attend_device(q, qp, o)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
+        with torch.cuda.graph(g), _lib.exclusive_stream():
             for c, o in zip(caches, (out, out2)):
                 c.attend_device(q, qp, o)
         for _ in range(3):
@@ -62,6 +62,10 @@ def main():
     t0 = A[:, 1].min()
     def col(x, i):   # absolute us of stamp i (cycles since CTA start, converted)
         return (x[:, 1] - t0) / 1e3 + x[:, i] / mhz
+    # SM clock from each CTA's (global timer, clock64) pair at its ticket
+    f = (A[:, 12] / ((A[:, 10] - A[:, 1]) / 1e3))
+    print(f"A: SM clock from (globaltimer, clock64) at the ticket: med {np.median(f):.0f} MHz "
+          f"(min {f.min():.0f}, max {f.max():.0f})")
     a_end = max(np.max((A[:, 1] - t0) / 1e3 + A[:, 15] / mhz), np.max((A[:, 1] - t0) / 1e3 + A[:, 11] / mhz))
     print(f"A: start {0:.1f}  loop start med {np.median(col(A, 8)):.1f}  loop end med {np.median(col(A, 9)):.1f} "
           f"max {np.max(col(A, 9)):.1f}  partial max {np.max(col(A, 13)):.1f}  A done (combine/commit) {a_end:.1f} us")
