@@ -110,11 +110,23 @@ int launch_encode_tc(const void *X, int dtype, int64_t rows, int d, int64_t x_se
                      int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
                      const float *d2, cudaStream_t st);
 
+int launch_encode_tc5(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride, int nsets,
+                      const float *codebooks, int cb_mod, int m, int d_sub, void *codes, int code_bytes,
+                      int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
+                      const float *d2, cudaStream_t st);
+
 int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride,
                   int nsets, const float *codebooks, int cb_mod, int m, int d_sub,
                   void *codes, int code_bytes, int64_t code_set_stride,
                   int64_t code_tile_stride, int64_t code_row_stride, float *d2, cudaStream_t st) {
-  // d = 128, d_sub = 8, m <= 256, 16-bit inputs: tensor-core encoder (encode_mma.cu)
+  // d = 128, d_sub = 8, m <= 256, bf16 inputs: tcgen05 encoder (encode_tc5.cu)
+  {
+    const int rc = launch_encode_tc5(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m, d_sub,
+                                     codes, code_bytes, code_set_stride, code_tile_stride, code_row_stride,
+                                     d2, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+  }
+  // ... fp16 inputs: mma.sync tensor-core encoder (encode_mma.cu)
   {
     const int rc = launch_encode_mma(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m,
                                      d_sub, codes, code_bytes, code_set_stride, code_tile_stride,

@@ -536,18 +536,21 @@ def test_fast_matches_generic_at_128k():
 
 
 # ------------------------------------------------------ tensor-core paths
-@pytest.mark.parametrize("dtype,m,code_bytes", [(torch.bfloat16, 256, 1), (torch.float16, 256, 1),
-                                                (torch.bfloat16, 200, 2)])
-def test_tensor_core_encoder_matches_oracle(dtype, m, code_bytes):
-    """encode_mma.cu (d = 128, d_sub = 8): codes vs the exhaustive float64
-    argmin of the oracle (margin rule), including a duplicated centroid
-    (ties -> lowest index) and rows far from the codebook scale."""
+@pytest.mark.parametrize("dtype,m,code_bytes,n", [(torch.bfloat16, 256, 1, 3000), (torch.float16, 256, 1, 3000),
+                                                  (torch.bfloat16, 200, 2, 3000), (torch.bfloat16, 256, 1, 2999),
+                                                  (torch.bfloat16, 37, 1, 133)])
+def test_tensor_core_encoder_matches_oracle(dtype, m, code_bytes, n):
+    """encode_tc5.cu (bf16: tcgen05 distance GEMM + integer-key argmin) and
+    encode_mma.cu (fp16) for d = 128, d_sub = 8: codes vs the exhaustive
+    float64 argmin of the oracle (margin rule), including a duplicated
+    centroid (ties -> lowest index), rows far from the codebook scale, a
+    ragged last tile (n % 8 != 0) and m < 256 (columns past m never win)."""
     from paper_2506_19505_b200 import _lib
     rng = np.random.default_rng(31)
-    n = 3000
     X = rng.standard_normal((n, 128)).astype(np.float32)
     X[:50] *= 40.0                      # large rows
     X[50:100] *= 1e-3                   # tiny rows
+    X[100:104] = 0.0                    # zero rows: the smallest |c| wins
     C = rng.standard_normal((m, 8)).astype(np.float32)
     C[7] = C[3]                         # duplicate: index 3 must win
     Xt = torch.from_numpy(X).cuda().to(dtype)
