@@ -1157,6 +1157,82 @@ def test_peer_exchange_publish_and_merge_one_device():
             assert merged == [int(j) for j in ref.anchor_indices_of(0, h)]
 
 
+def test_peer_exchange_two_streams_skewed_ranks():
+    """Two emulated ranks, each with its OWN receive buffers and its own CUDA
+    stream on one device, exchanging through the two-half protocol while
+    rank 1 is held back by a sleep kernel before every merge: rank 0 runs
+    ahead as far as the protocol lets it (its merge of step s + 1 waits for
+    rank 1's publish of s + 1, which rank 1 issues only after merging s, so
+    rank 0's publish of s + 2 cannot overwrite the half rank 1 still reads).
+    Every merged output of both ranks equals the single-cache decode
+    (cache.py:176-178: one softmax over the whole context)."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    from paper_2506_19505_b200.parallel import PeerExchange
+    vq = VqConfig.from_notation("d8m256")
+    Hq, Hkv, n, steps, W = 8, 2, 900, 10, 8
+    Q, K, V = qkv(93, Hq, Hkv, n + steps, 128, heavy=2)
+    ck, cv = codebooks(93, Hkv, 256, 8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    cfg = lambda w: CacheConfig(vq=vq, anchor_fraction=0.02, window_size=w)
+    ref = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    ref.prefill(dev(Q[None, :, :n]), dev(K[None, :, :n]), dev(V[None, :, :n]), np.arange(n))
+    want = []
+    for t in range(n, n + steps):
+        want.append(ref.decode_step(dev(Q[None, :, t]), dev(K[None, :, t]), dev(V[None, :, t]), t)[0].cpu().numpy())
+    ref2 = QuantizedKVCache(cfg(W), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    ref2.prefill(dev(Q[None, :, :n]), dev(K[None, :, :n]), dev(V[None, :, :n]), np.arange(n))
+    cut = 448
+    shards = []
+    for lo, hi, w in ((0, cut, 0), (cut, n, W)):
+        c = QuantizedKVCache(cfg(w), Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq, token_offset=lo,
+                             capacity=hi - lo + steps + 64)
+        loc = np.full((Hkv, 64), -1, dtype=np.int32)
+        for h in range(Hkv):
+            a = [j - lo for j in ref2.anchor_indices_of(0, h) if lo <= j < hi]
+            loc[h, :len(a)] = a
+        c.Hq = Hq
+        c.build_from(dev(K[None, :, lo:hi]), dev(V[None, :, lo:hi]),
+                     torch.arange(lo, hi, device="cuda")[None], torch.from_numpy(loc).cuda()[None])
+        shards.append(c)
+    shards[1].tensors["hstate"][:, :, 0] = ref2.config.budget_for(n)
+    exs = [PeerExchange(Hq, 128, local_slots=2), PeerExchange(Hq, 128, local_slots=2)]
+    # rank r publishes into slot r of BOTH ranks' buffers, merges from its own
+    for ex_r, r in zip(exs, (0, 1)):
+        ex_r.rank = r
+        ex_r.dst_o = torch.tensor([e._recv[0] for e in exs], dtype=torch.int64, device="cuda")
+        ex_r.dst_lse = torch.tensor([e._recv[1] for e in exs], dtype=torch.int64, device="cuda")
+        ex_r.dst_flags = torch.tensor([e._recv[2] for e in exs], dtype=torch.int64, device="cuda")
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    qs = [dev(Q[None, :, t]) for t in range(n, n + steps)]
+    ks = [dev(K[None, :, t]) for t in range(n, n + steps)]
+    vs = [dev(V[None, :, t]) for t in range(n, n + steps)]
+    pos = [torch.tensor([t], device="cuda") for t in range(n, n + steps)]
+    outs = [[torch.empty((Hq, 128), device="cuda") for _ in range(steps)] for _ in range(2)]
+    torch.cuda.synchronize()
+    try:
+        for i in range(steps):
+            for r in (0, 1):
+                with torch.cuda.stream(streams[r]):
+                    ex = exs[r]
+                    ex.seq = i + 1
+                    o = torch.empty((1, Hq, 128), device="cuda")
+                    l = torch.empty((1, Hq), device="cuda")
+                    tail = r == 1
+                    shards[r].step_publish(qs[i], ks[i] if tail else None, vs[i] if tail else None, pos[i],
+                                           o, l, ex)
+                    if tail:
+                        shards[r]._n += 1
+                        torch.cuda._sleep(2_000_000)   # ~1 ms: rank 1 merges late
+                    ex.merge(outs[r][i])
+        torch.cuda.synchronize()
+    finally:
+        for e in exs:
+            e.close()
+    for i in range(steps):
+        for r in (0, 1):
+            assert rel(outs[r][i].cpu().numpy(), want[i]) < 2e-2, (r, i)
+
+
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
 def test_packed_12bit_cache_build_d64_d32m4096(dtype):
     """12-bit packed codes written by the tensor-core encoder when a warp's
