@@ -12,6 +12,10 @@
   reference, cache.py:100-194).
 * config #5 positions -- the tail shard of an 8-way 840K context (tokens at
   positions 735K..840K, token_offset = 735K) through the fused decode kernel.
+* 128K prefill (north_star: FA + online AnS + top-k at 128K) -- the anchor
+  scores and anchor sets of QuantizedKVCache.prefill at 131072 tokens, 32 Q /
+  8 KV heads, against the float64 torch restatement tests/fp64_ans.py (pinned
+  to the oracle in the CPU suite, and again here at 2K on the GPU).
 
 Rules (north_star), written in the tests:
   * anchor sets: the GPU's selection is exact on its own float32 scores
@@ -318,3 +322,62 @@ def test_config5_tail_shard_positions_735k_840k():
     for h in range(Hkv):
         assert np.array_equal(cache.anchor_indices_of(0, h), ref.heads[h].anchor_indices)
     record("config5[fused, positions 735K-840K]", code_flips_sample=flips, decode_max_rel=max(errs))
+
+
+def test_prefill_anchors_128k_vs_fp64():
+    """QuantizedKVCache.prefill at 131072 tokens (LLaMA-3-8B attention shapes,
+    bf16, heavy-hitter keys planted per KV head): the tcgen05 FA + AnS scores
+    of every KV head within the reference's 1e-4 relative AnS tolerance of a
+    float64 restatement of Alg. 1, and the anchor sets equal except tokens
+    within twice the measured score error of the selection boundary
+    (anchors.py:66-132, cache.py:100-140).  The restatement itself is
+    checked against the oracle at 2K first."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    from fp64_ans import group_anchor_scores
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    Hq, Hkv, d = 32, 8, 128
+    g = Hq // Hkv
+    vq = VqConfig(8, 256)
+    ck, cv = codebooks(128, Hkv, 256, 8)
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.01, window_size=32, theta_base=5e5)
+    # 2K: fp64 restatement vs the oracle's GQA scores
+    Q2, K2, V2 = qkv(1282, Hq, Hkv, 2048, d, heavy=8)
+    ref2 = O.OracleCache(ck, cv, anchor_fraction=0.01, window_size=32, theta_base=5e5)
+    ref2.prefill(Q2, K2, V2, np.arange(2048))
+    for hk in range(Hkv):
+        sk, sv = group_anchor_scores(torch.from_numpy(Q2[hk * g:(hk + 1) * g]).cuda(),
+                                     torch.from_numpy(K2[hk]).cuda(), torch.arange(2048, device="cuda"),
+                                     theta_base=5e5)
+        assert rel(sk.cpu().numpy(), ref2.last_scores[0][hk]) < 1e-12
+        assert rel(sv.cpu().numpy(), ref2.last_scores[1][hk]) < 1e-12
+    # 128K through the GPU prefill
+    n = 131072
+    gen = torch.Generator(device="cuda").manual_seed(128)
+    Q = torch.randn((1, Hq, n, d), device="cuda", generator=gen).to(torch.bfloat16)
+    K = torch.randn((1, Hkv, n, d), device="cuda", generator=gen).to(torch.bfloat16)
+    V = torch.randn((1, Hkv, n, d), device="cuda", generator=gen).to(torch.bfloat16)
+    for h in range(Hkv):   # heavy hitters: 64 early large-norm keys per head
+        idx = torch.randperm(n // 2, generator=torch.Generator().manual_seed(h))[:64].cuda()
+        K[0, h, idx] = (K[0, h, idx].float() * 5.0).to(torch.bfloat16)
+    cache = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=Hq)
+    t0 = time.time()
+    cache.prefill(Q, K, V, np.arange(n))
+    torch.cuda.synchronize()
+    gk_all, gv_all = (x[0].double().cpu().numpy() for x in cache.last_scores)
+    budget = cfg.budget_for(n)
+    pos = torch.arange(n, device="cuda")
+    bands, diffs, rks, rvs = [], [], [], []
+    for hk in range(Hkv):
+        sk, sv = group_anchor_scores(Q[0, hk * g:(hk + 1) * g], K[0, hk], pos, theta_base=5e5)
+        sk, sv = sk.cpu().numpy(), sv.cpu().numpy()
+        ref_set = O.select_anchors(sk, sv, budget, cfg.policy)
+        got = np.asarray(cache.anchor_indices_of(0, hk), np.int64)
+        band, diff, rk, rv = check_anchor_set(got, ref_set, sk, sv, gk_all[hk], gv_all[hk], budget, cfg.policy)
+        bands.append(band)
+        diffs.append(diff)
+        rks.append(rk)
+        rvs.append(rv)
+    record("prefill 128K anchors vs fp64 (32/8 heads, d8m256 cache, 1% anchors)",
+           ans_rel_k=max(rks), ans_rel_v=max(rvs), band_tokens=sum(bands), differing=sum(diffs),
+           budget_per_head=budget, wall_s=round(time.time() - t0, 1))

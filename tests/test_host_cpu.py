@@ -394,3 +394,27 @@ def test_bench_reference_arm_runs_without_the_native_library():
     assert line["cpu_baseline"]["kind"] == "reference"
     assert line["native_so_loaded"] == []
     assert line["value"] > 0
+
+
+def test_fp64_anchor_score_restatement_matches_oracle():
+    """tests/fp64_ans.py (the float64 torch restatement used to check the
+    128K prefill anchors on the GPU) against the numpy oracle's GQA prefill
+    scores, causal, positions with an offset, several query blocks."""
+    import antkv_oracle as O
+    from fp64_ans import group_anchor_scores
+    rng = np.random.default_rng(3)
+    Hq, Hkv, n, d = 4, 2, 300, 32
+    Q = rng.standard_normal((Hq, n, d))
+    K = rng.standard_normal((Hkv, n, d))
+    V = rng.standard_normal((Hkv, n, d))
+    pos = np.arange(n) + 17
+    ck = rng.standard_normal((Hkv, 16, 8))
+    ref = O.OracleCache(ck, ck, anchor_fraction=0.05, window_size=4)
+    ref.prefill(Q, K, V, pos)
+    sk_ref, sv_ref = ref.last_scores
+    g = Hq // Hkv
+    for hk in range(Hkv):
+        sk, sv = group_anchor_scores(torch.from_numpy(Q[hk * g:(hk + 1) * g]), torch.from_numpy(K[hk]),
+                                     torch.from_numpy(pos), block=128)
+        assert np.abs(sk.numpy() - sk_ref[hk]).max() <= 1e-12 * np.abs(sk_ref[hk]).max()
+        assert np.abs(sv.numpy() - sv_ref[hk]).max() <= 1e-12 * np.abs(sv_ref[hk]).max()
