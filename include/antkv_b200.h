@@ -233,10 +233,10 @@ typedef struct antkv_cache_desc {
   int64_t *positions;  /* [B][capacity]                                     */
   const float *codebook_k; /* [Hkv][m][d_sub] float32                       */
   const float *codebook_v;
-  uint16_t *codebook_f16;  /* fast path: [Hkv][256 codes][2 (K,V)][8 copies][8]
-                              fp16: each centroid replicated across the 8
-                              16-byte bank groups of a 128-byte row (64 KB per
-                              head, one contiguous bulk copy)                */
+  uint16_t *codebook_f16;  /* fast path: 64 KB per head; its first 8 KB hold
+                              [256 codes][K 8 | V 8] fp16 (the fused kernel
+                              replicates each row across the 8 16-byte bank
+                              groups of its shared-memory copy)              */
   uint16_t *pool_f16;  /* fast path: fp16 [B][Hkv][pool_capacity/16] tiles of
                           [2 (K rotated at its position, V)][16 slots][128]
                           with the 16-byte chunks of slot r XOR-swizzled by

@@ -544,21 +544,23 @@ __global__ void cache_dequant_pool_kernel(antkv_cache_desc c, int n, float *__re
   }
 }
 
-// Fast-path codebook: fp16 [Hkv][256][2 (K,V)][8 copies][8] (zero rows beyond m).
-// Row `code` holds the centroid in each of the 8 16-byte bank groups, so the
-// eight ldmatrix row addresses of a phase (copy = lane & 7) never conflict.
+// Fast-path codebook: fp16 [Hkv][256][K 8 | V 8] (zero rows beyond m) at
+// the start of each head's 64 KB block (the fused kernel replicates each row
+// into the 8 16-byte bank groups of its shared copy).
 // Block (Hkv*2) also writes the RoPE constant tables (FastTables).
 __global__ void cache_prepare_fast_kernel(antkv_cache_desc c) {
   if (blockIdx.x == gridDim.x - 1) {
     fill_fast_tables(reinterpret_cast<FastTables *>(c.fast_tables), c.theta_base);
     return;
   }
+  // compact fp16 rows [code][K 8 | V 8] (32 B) at the start of the head's
+  // 64 KB block; decode_fast_kernel replicates them in shared memory
   const int h = blockIdx.x / 2, kv = blockIdx.x % 2;
   const float *cb = (kv ? c.codebook_v : c.codebook_k) + (int64_t)h * c.m * c.d_sub;
-  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + (int64_t)h * 256 * 128 + kv * 64;
-  for (int i = threadIdx.x; i < 256 * 64; i += blockDim.x) {
-    const int code = i / 64, t = i % 8;
-    dst[code * 128 + i % 64] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
+  __half *dst = reinterpret_cast<__half *>(c.codebook_f16) + (int64_t)h * 256 * 128 + kv * 8;
+  for (int i = threadIdx.x; i < 256 * 8; i += blockDim.x) {
+    const int code = i / 8, t = i % 8;
+    dst[code * 16 + t] = __float2half_rn(code < c.m ? cb[(int64_t)code * 8 + t] : 0.f);
   }
 }
 

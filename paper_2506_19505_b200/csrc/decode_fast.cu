@@ -7,12 +7,14 @@
 //   * CTAs: `splits` per (sequence, head), one CTA of 8 warps per SM.  Each
 //     CTA owns a contiguous range of 16-slot code tiles (split into 8
 //     contiguous warp ranges) and a share of the full-precision pool tiles.
-//   * Codebooks: one 64 KB bulk copy per CTA of the prepared fp16 layout
-//     [code][K 8 copies | V 8 copies]: a centroid row sits in all eight
-//     16-byte bank groups, so the eight row addresses of an ldmatrix phase
-//     (copy = lane & 7) never conflict, and an address is ONE prmt:
+//   * Codebooks: the compact fp16 codebook (8 KB per head, [code][K 8 | V 8])
+//     is read with one 32-byte load per thread and replicated in shared
+//     memory as [code][K 8 copies | V 8 copies]: a centroid row sits in all
+//     eight 16-byte bank groups, so the eight row addresses of an ldmatrix
+//     phase (copy = lane & 7) never conflict, and an address is ONE prmt:
 //     (code << 8) | lane_offset, with the codebook base folded into the
-//     ldmatrix uniform operand.
+//     ldmatrix uniform operand.  (A bulk copy of the replicated 64 KB per
+//     CTA moved 9.4 MB through L2 per launch, ahead of the cache state.)
 //   * Code tiles (K codes 256 B + V codes 256 B per tile) stream through a
 //     private 8-stage ring per warp (cp.async.bulk + mbarrier); the warp
 //     refills its own slots, so warps never wait on each other.
@@ -72,7 +74,7 @@ struct __align__(128) FastSmem {
   float2 ang[2 * FK_WARPS + 1][64];          // (cos, sin) per query frame, pairs in lane order
   unsigned long long full[FK_WARPS][FK_NS];
   unsigned long long pfull[FK_WARPS];
-  unsigned long long cbbar, tbar, qbar;
+  unsigned long long tbar, qbar;
   int ticket, gticket;
   unsigned long long t0clk;                  // trace: start clock of the CTA
 };
@@ -691,17 +693,19 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
       for (int s = 0; s < FK_NS; ++s) mbar_init(&sm.full[ww][s], 1);
       mbar_init(&sm.pfull[ww], 1);
     }
-    mbar_init(&sm.cbbar, 1);
     mbar_init(&sm.tbar, 1);
     mbar_init(&sm.qbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // compact fp16 codebook row of code threadIdx.x ([K 8 | V 8] halves, 32 B;
+  // immutable while decoding, so read before the wait), replicated into the
+  // eight bank groups of sm.cb before the frames' barrier
+  const uint4 *cbg = reinterpret_cast<const uint4 *>(c.codebook_f16) + (int64_t)h * (FK_CB_BYTES / 16) +
+                     2 * threadIdx.x;
+  const uint4 cbk = __ldg(cbg), cbv = __ldg(cbg + 1);
   const int qbytes = 4 * 128 * dtype_size(a.qdtype);
   if (threadIdx.x == 0) {
-    mbar_expect_tx(&sm.cbbar, FK_CB_BYTES);
-    tma_bulk_g2s(sm.cb, reinterpret_cast<const uint8_t *>(c.codebook_f16) + (int64_t)h * FK_CB_BYTES,
-                 FK_CB_BYTES, &sm.cbbar);
     mbar_expect_tx(&sm.tbar, sizeof(FastTables));
     tma_bulk_g2s(&sm.tab, c.fast_tables, sizeof(FastTables), &sm.tbar);
     if (a.early_q) {
@@ -775,6 +779,12 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   FK_TR(2);
+  const int8_t *kinds = c.pool_kind + bh * c.pool_capacity;
+  int8_t kd0 = ANTKV_KIND_FREE, kd1 = ANTKV_KIND_FREE;
+  if (pt0 + warp < pt1) {
+    kd0 = kinds[(pt0 + warp) * 16 + g];
+    kd1 = kinds[(pt0 + warp) * 16 + g + 8];
+  }
   // qmask words of this warp's range (one word per stage), up to 2 per lane
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
   uint32_t qmv[2];
@@ -782,12 +792,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   for (int u = 0; u < 2; ++u) {
     const int i = lane + 32 * u, word = (wt0 >> 1) + i;
     qmv[u] = (i < nstages && word * 32 < c.capacity) ? __ldcs(qmg + word) : 0u;
-  }
-  const int8_t *kinds = c.pool_kind + bh * c.pool_capacity;
-  int8_t kd0 = ANTKV_KIND_FREE, kd1 = ANTKV_KIND_FREE;
-  if (pt0 + warp < pt1) {
-    kd0 = kinds[(pt0 + warp) * 16 + g];
-    kd1 = kinds[(pt0 + warp) * 16 + g + 8];
   }
   // (cos, sin) of every query frame of the CTA, cooperatively from
   // integer-reduced angles (frame 2w + e: warp w's even / odd tile frame;
@@ -830,6 +834,16 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     for (int e = threadIdx.x; e < 256; e += FK_THREADS)
       sm.qf[e >> 6][lane_pair_pos(e & 63)] =
           make_float2(load_elem(sm.qraw, 2 * e, a.qdtype) * sc, load_elem(sm.qraw, 2 * e + 1, a.qdtype) * sc);
+  }
+  {
+    static_assert(FK_THREADS == 256, "one codebook row per thread");
+    uint8_t *row = sm.cb + threadIdx.x * 256;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {   // copy (i + code) & 7 first: the 8 lanes of a phase hit 8 bank groups
+      const int cp = (i + threadIdx.x) & 7;
+      *reinterpret_cast<uint4 *>(row + cp * 16) = cbk;
+      *reinterpret_cast<uint4 *>(row + 128 + cp * 16) = cbv;
+    }
   }
   __syncthreads();
   FK_TR(14);
@@ -914,7 +928,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
   FK_TR(6);
   if (prep) {
-    mbar_wait(&sm.cbbar, 0);
     prepare_update(c, a, sm, b, h, n, pq);
   }
   FK_TR(7);
@@ -935,7 +948,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     for (int u = 0; u < 2; ++u)
       if (lane + 32 * u < nstages) sm.qm[warp][lane + 32 * u] = qmv[u];
     __syncwarp();                                         // qm words visible to the warp
-    mbar_wait(&sm.cbbar, 0);
     FK_TR(8);
     for (int it = 0; it < nslots; ++it) {
       const int slot = it % FK_NS;
@@ -957,7 +969,6 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   FK_TR(9);
-  mbar_wait(&sm.cbbar, 0);   // no bulk copy may still be in flight at exit
 
   // ---- merge 8 warps x 2 streams (+ the appended token) -> partial (natural log)
   __syncthreads();   // pool tiles consumed: the pool area becomes merge scratch
