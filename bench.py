@@ -10,11 +10,13 @@ decode attention over codes + anchors + window with RoPE after
 reconstruction, merges the splits and evicts/encodes the oldest window row.
 
 value = decode-attention tok/s as BASELINE.md defines it
-        (batch / time of one layer's decode-attention call, all heads),
-        aggregated over ranks (weak scaling: 128K context per GPU, the
-        sequence is sharded and partials are merged with NCCL).
---impl reference times the reference algorithm (oracle port of
-cache.py:149-194, numpy, one process per KV head on the host cores) on a
+        (batch / time of one layer's decode-attention call, all heads);
+        at N > 1 the context is N x 128K tokens sharded by sequence and the
+        partials are merged over peer memory (or NCCL with --exchange nccl);
+        the rate is not multiplied by N (one token per step).
+--impl reference times the reference package's own
+QuantizedKVCache.decode_step (cache.py:149-194, staged into oracle/_ref by
+oracle/Makefile) on the host cores, one single-head cache per core, on a
 bounded sample of the same workload.
 """
 
