@@ -115,6 +115,11 @@ int launch_encode_tc5(const void *X, int dtype, int64_t rows, int d, int64_t x_s
                       int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
                       const float *d2, cudaStream_t st);
 
+int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride, int nsets,
+                       const float *codebooks, int cb_mod, int m, int d_sub, void *codes, int code_bytes,
+                       int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
+                       const float *d2, cudaStream_t st);
+
 int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride,
                   int nsets, const float *codebooks, int cb_mod, int m, int d_sub,
                   void *codes, int code_bytes, int64_t code_set_stride,
@@ -133,7 +138,14 @@ int launch_encode(const void *X, int dtype, int64_t rows, int d, int64_t x_set_s
                                      code_row_stride, d2, st);
     if (rc != ANTKV_EUNSUPPORTED) return rc;
   }
-  // d_sub 16 / 32 / 64, any m, 16-bit inputs: tensor-core encoder (encode_tc.cu)
+  // d_sub 16 / 32, any m, bf16 inputs: tcgen05 encoder over codebook blocks (encode_tc5.cu)
+  {
+    const int rc = launch_encode_tc5l(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m, d_sub,
+                                      codes, code_bytes, code_set_stride, code_tile_stride, code_row_stride,
+                                      d2, st);
+    if (rc != ANTKV_EUNSUPPORTED) return rc;
+  }
+  // d_sub 16 / 32 / 64, any m, 16-bit inputs: mma.sync tensor-core encoder (encode_tc.cu)
   {
     const int rc = launch_encode_tc(X, dtype, rows, d, x_set_stride, nsets, codebooks, cb_mod, m, d_sub,
                                     codes, code_bytes, code_set_stride, code_tile_stride, code_row_stride,

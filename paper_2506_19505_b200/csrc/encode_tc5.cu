@@ -386,6 +386,321 @@ vq_encode_tc5_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_set
   }
 }
 
+// ------------------------------------------------------------------------
+// Long codebooks (d_sub 16 / 32, any m <= 65536: config #3's d32m4096):
+// the same integer-key argmin over 128-centroid blocks of the codebook.
+//
+// A sub-vector row of DSUB dims spans two 128B-swizzled atoms (K = 128):
+//   k 0 .. 3 DSUB - 1   A: -2 s x (three copies)     B: c hi | mid | lo
+//   k 3 DSUB            A: bf16(s |x|^2)             B: 1
+//   k 3 DSUB + 1 .. +3  A: s                         B: |c|^2 hi | mid | lo
+//   k-step KD (16 KD, 16 KD + 1)  A: 1, 1            B: 2^23, 2^13 (2^24 past m)
+// with KD = ceil((3 DSUB + 4) / 16) distance k-steps (7 for DSUB = 32).  The
+// codebook operand is pre-swizzled once per call into a global image of
+// 128-centroid blocks (32 KB each, L2-resident) that a loader warp streams
+// through a 4-stage ring; a CTA keeps a PAIR of A tiles (2 x 128 sub-vectors)
+// resident while every block passes, so each 32 KB block feeds 2 x (KD + 1)
+// MMAs (M = 128, N = 128).  TMEM: tile t, buffer u at column 256 t + 128 u
+// (two buffers per tile).  Epilogue warps 4-7 reduce tile 0, 8-11 tile 1;
+// a thread keeps its sub-vector's best (key, block) over the blocks (strict
+// <: the earlier block wins ties, so the lowest index overall).  The grid
+// step 1/s lies in (2.5e-7, 5e-7] (|x|^2 + max|c|^2) here: 2 (|x|^2 +
+// max|c|^2) stays below 2^23 steps and one step plus the fp32 accumulation
+// error of the longer dot products stays inside the parity rule's 1e-6.
+constexpr int TL_NB = 128;                      // centroids per block
+constexpr int TL_BS = 4;                        // B ring stages
+constexpr int TL_ATILE = 128 * 256;             // two atoms x 128 rows
+constexpr int TL_BBLK = TL_NB * 256;            // 32 KB
+constexpr int TL_PROD = 4, TL_EPI = 8;
+constexpr int TL_MMA_WARP = TL_PROD + TL_EPI, TL_LOAD_WARP = TL_MMA_WARP + 1;
+constexpr int TL_THREADS = 32 * (TL_LOAD_WARP + 1);
+
+struct TlSmem {
+  uint8_t a[2][TL_ATILE];
+  uint8_t b[TL_BS][TL_BBLK];
+  uint32_t cw[TL_EPI][32];                      // packed-row staging of the epilogue warps
+  unsigned long long afull, aempty, bfull[TL_BS], bempty[TL_BS], dfull[2], dempty[2];
+  uint32_t tmem;
+};
+
+// chunk (16 bytes) c of `row` in a two-atom 128B-swizzled tile of R rows
+template <int R>
+__device__ __forceinline__ uint32_t tl_off(int row, int c) {
+  return (c >> 3) * (R * 128) + row * 128 + (((c & 7) ^ (row & 7)) << 4);
+}
+
+template <int DSUB>
+constexpr int tl_kd() { return (3 * DSUB + 4 + 15) / 16; }
+
+// Codebook image: [codebook][block][two atoms x 128 rows x 128 B]
+template <int DSUB>
+__global__ void __launch_bounds__(TL_NB)
+tl_codebook_image_kernel(const float *__restrict__ codebooks, int m, uint8_t *__restrict__ img, int nblk,
+                         float *__restrict__ blkmax) {
+  constexpr int KD = tl_kd<DSUB>();
+  const int blk = blockIdx.x, cbk = blockIdx.y, r = threadIdx.x;
+  const int c = blk * TL_NB + r;
+  const float *cb = codebooks + ((int64_t)cbk * m + (c < m ? c : 0)) * DSUB;
+  uint8_t *dst = img + ((int64_t)cbk * nblk + blk) * TL_BBLK;
+  for (int ch = 0; ch < 16; ++ch) *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch)) = make_uint4(0u, 0u, 0u, 0u);
+  float nn = 0.f;
+  for (int j0 = 0; j0 < DSUB; j0 += 8) {
+    float hi[8], mi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float x = c < m ? cb[j0 + i] : 0.f;
+      nn = fmaf(x, x, nn);
+      split3_bf16(x, hi[i], mi[i], lo[i]);
+    }
+    const int ch = j0 / 8;
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch)) =
+        make_uint4(bf16_pair(hi[0], hi[1]), bf16_pair(hi[2], hi[3]), bf16_pair(hi[4], hi[5]), bf16_pair(hi[6], hi[7]));
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch + DSUB / 8)) =
+        make_uint4(bf16_pair(mi[0], mi[1]), bf16_pair(mi[2], mi[3]), bf16_pair(mi[4], mi[5]), bf16_pair(mi[6], mi[7]));
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch + DSUB / 4)) =
+        make_uint4(bf16_pair(lo[0], lo[1]), bf16_pair(lo[2], lo[3]), bf16_pair(lo[4], lo[5]), bf16_pair(lo[6], lo[7]));
+  }
+  float nh, nm, nl;
+  split3_bf16(nn, nh, nm, nl);
+  if (c < m)
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 3 * DSUB / 8)) = make_uint4(bf16_pair(1.f, nh), bf16_pair(nm, nl), 0u, 0u);
+  // the block's max |c|^2 (the exactness scale is the max over the blocks)
+  __shared__ float red[TL_NB / 32];
+  float mx = warp_max(c < m ? nn : 0.f);
+  if ((r & 31) == 0) red[r >> 5] = mx;
+  __syncthreads();
+  if (r == 0) {
+    for (int i = 1; i < TL_NB / 32; ++i) mx = fmaxf(mx, red[i]);
+    blkmax[(int64_t)cbk * nblk + blk] = fmaxf(mx, red[0]);
+  }
+  *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 2 * KD)) =
+      make_uint4(bf16_pair(c < m ? 8388608.f : 16777216.f, 8192.f), 0u, 0u, 0u);
+}
+
+template <int DSUB>
+__global__ void __launch_bounds__(TL_THREADS, 1)
+vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_set_stride,
+                      const uint8_t *__restrict__ img, const float *__restrict__ blkmax, int cb_mod, int m,
+                      int nblk, void *__restrict__ codes, int code_bytes, int64_t code_set_stride,
+                      int64_t code_tile_stride, int64_t code_row_stride, int64_t tiles_per_cta, uint32_t mul) {
+  constexpr int G = 128 / DSUB, TOK = 128 / G, KD = tl_kd<DSUB>(), NCH = DSUB / 8;
+  extern __shared__ __align__(128) unsigned char tlraw[];
+  TlSmem &sm = *reinterpret_cast<TlSmem *>(tlraw + ((1024 - (t5_smem(tlraw) & 1023)) & 1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int set = blockIdx.y;
+  // the CTA's tiles [tile0, tile0 + ntl) go in pairs; an odd count ends with a single tile
+  const int64_t nsub = rows * G, ntiles = (nsub + 127) / 128;
+  const int64_t tile0 = blockIdx.x * tiles_per_cta;
+  const int ntl = (int)max((int64_t)0, min(tiles_per_cta, ntiles - tile0));
+  const int items = (ntl + 1) / 2;
+  const int64_t sv_end = min(nsub, (tile0 + ntl) * 128);   // rows past it: zero, not stored
+  const uint8_t *bimg = img + (int64_t)(set % cb_mod) * nblk * TL_BBLK;
+  if (threadIdx.x == 0) {
+    t5_init(&sm.afull, 32 * TL_PROD);
+    t5_init(&sm.aempty, 1);
+    for (int s = 0; s < TL_BS; ++s) {
+      t5_init(&sm.bfull[s], 1);
+      t5_init(&sm.bempty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      t5_init(&sm.dfull[s], 1);
+      t5_init(&sm.dempty[s], 32 * TL_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == TL_MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(t5_smem(&sm.tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // constant A chunks: zeros between the norm chunk and the magic one, the
+  // magic chunk (1, 1, 0...) and the zero tail of the last k-step
+  for (int e = threadIdx.x; e < 2 * 128; e += TL_THREADS) {
+    uint8_t *a = sm.a[e >> 7];
+    const int r = e & 127;
+    for (int ch = 3 * NCH + 1; ch < 16; ++ch)
+      *reinterpret_cast<uint4 *>(a + tl_off<128>(r, ch)) =
+          ch == 2 * KD ? make_uint4(bf16_pair(1.f, 1.f), 0u, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sm.tmem;
+
+  if (warp < TL_PROD) {
+    // ---- A pair producer: thread p builds rows p and p + 128 of the pair
+    // (tile p / 128... = tile 0 rows p, tile 1 rows p), the next pair's inputs
+    // prefetched into registers while the current pair streams the blocks
+    float cbmax = 0.f;
+    for (int i = 0; i < nblk; ++i) cbmax = fmaxf(cbmax, __ldg(blkmax + (int64_t)(set % cb_mod) * nblk + i));
+    const int r = threadIdx.x;   // 0..127: row of both tiles
+    auto load = [&](int it, int t, uint4 (&v)[NCH]) {
+      const int64_t sv = (tile0 + 2 * it + t) * 128 + r;
+      if (sv < sv_end) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(X + set * x_set_stride + (sv / G) * 128 + (sv % G) * DSUB);
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) v[i] = __ldg(src + i);
+      } else {
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) v[i] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    };
+    uint4 nx[2][NCH];
+    if (items > 0) { load(0, 0, nx[0]); load(0, 1, nx[1]); }
+    for (int it = 0; it < items; ++it) {
+      uint4 xv[2][NCH];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) xv[t][i] = nx[t][i];
+      if (it + 1 < items) { load(it + 1, 0, nx[0]); load(it + 1, 1, nx[1]); }
+      if (it > 0) t5_wait(&sm.aempty, (it - 1) & 1);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        float n2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t w4[4] = {xv[t][i].x, xv[t][i].y, xv[t][i].z, xv[t][i].w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float x0 = __uint_as_float(w4[k] << 16), x1 = __uint_as_float(w4[k] & 0xffff0000u);
+            n2 = fmaf(x0, x0, n2);
+            n2 = fmaf(x1, x1, n2);
+          }
+        }
+        // grid step 2^e in (2.5e-7, 5e-7] * (|x|^2 + max|c|^2)
+        const float tt = 5e-7f * (n2 + cbmax);
+        int e = ((__float_as_int(tt) >> 23) & 0xff) - 127;
+        e = max(-126, min(126, e));
+        const float s = __int_as_float((127 - e) << 23);
+        const float m2s = -2.f * s;
+        uint8_t *a = sm.a[t];
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t w4[4] = {xv[t][i].x, xv[t][i].y, xv[t][i].z, xv[t][i].w};
+          uint32_t o[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            o[k] = bf16_pair(__uint_as_float(w4[k] << 16) * m2s, __uint_as_float(w4[k] & 0xffff0000u) * m2s);
+          const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+          *reinterpret_cast<uint4 *>(a + tl_off<128>(r, i)) = ov;
+          *reinterpret_cast<uint4 *>(a + tl_off<128>(r, i + NCH)) = ov;
+          *reinterpret_cast<uint4 *>(a + tl_off<128>(r, i + 2 * NCH)) = ov;
+        }
+        *reinterpret_cast<uint4 *>(a + tl_off<128>(r, 3 * NCH)) =
+            make_uint4(bf16_pair(n2 * s, s), bf16_pair(s, s), 0u, 0u);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      t5_arrive(&sm.afull);
+    }
+  } else if (warp == TL_LOAD_WARP) {
+    // ---- codebook blocks, every block for every pair, through the B ring
+    if (lane == 0) {
+      for (int it = 0, k = 0; it < items; ++it) {
+        for (int blk = 0; blk < nblk; ++blk, ++k) {
+          const int st = k % TL_BS;
+          if (k >= TL_BS) t5_wait(&sm.bempty[st], ((k / TL_BS) - 1) & 1);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(t5_smem(&sm.bfull[st])),
+                       "r"(TL_BBLK) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  t5_smem(sm.b[st])),
+              "l"(bimg + (int64_t)blk * TL_BBLK), "r"(TL_BBLK), "r"(t5_smem(&sm.bfull[st]))
+              : "memory");
+        }
+      }
+    }
+  } else if (warp == TL_MMA_WARP) {
+    // ---- MMA issuer: kind::f16, bf16 A/B, fp32 D, K-major, N = 128, M = 128
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(TL_NB >> 3) << 17) | (8u << 24);
+    for (int it = 0, k = 0; it < items; ++it) {
+      t5_wait(&sm.afull, it & 1);
+      for (int blk = 0; blk < nblk; ++blk, ++k) {
+        const int st = k % TL_BS, buf = k & 1;
+        t5_wait(&sm.bfull[st], (k / TL_BS) & 1);
+        if (k >= 2) t5_wait(&sm.dempty[buf], ((k >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t bs = t5_smem(sm.b[st]);
+          const int npt = min(2, ntl - 2 * it);   // tiles in this pair
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (t >= npt) break;
+            const uint32_t as = t5_smem(sm.a[t]), d = tmem + t * 256 + buf * 128;
+#pragma unroll
+            for (int ks = 0; ks <= KD; ++ks) {
+              const uint32_t ao = (ks >> 2) * (128 * 128) + (ks & 3) * 32, bo = (ks >> 2) * (TL_NB * 128) + (ks & 3) * 32;
+              t5_mma(d, t5_desc(as + ao), t5_desc(bs + bo), idesc, ks > 0);
+            }
+          }
+          t5_commit(&sm.bempty[st]);
+          if (blk == nblk - 1) t5_commit(&sm.aempty);
+          t5_commit(&sm.dfull[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---- epilogue: warps 4-7 tile 0, 8-11 tile 1 (lanes 32 (w % 4).. of its
+    // accumulators); best (key, block) of the thread's sub-vector over the blocks
+    const int ew = warp - TL_PROD, q = warp & 3, t = ew >> 2;
+    const int r = 32 * q + lane;
+    for (int it = 0, k = 0; it < items; ++it) {
+      uint32_t best = 0xffffffffu;
+      int bblk = 0;
+      const bool live = t < ntl - 2 * it;   // a single last tile: the tile-1 warps only keep the barrier count
+      for (int blk = 0; blk < nblk; ++blk, ++k) {
+        const int buf = k & 1;
+        t5_wait(&sm.dfull[buf], (k >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (!live) {
+          t5_arrive(&sm.dempty[buf]);
+          continue;
+        }
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + t * 256 + buf * 128;
+        uint32_t v0[32], v1[32], v2[32], v3[32];
+        t5_ld32(tq, v0);
+        t5_ld32(tq + 32, v1);
+        t5_ld_wait(v0, v1);
+        t5_ld32(tq + 64, v2);
+        t5_ld32(tq + 96, v3);
+        uint32_t bm = min(chunk_min(v0, mul), chunk_min(v1, mul) + 32u);
+        t5_ld_wait(v2, v3);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        t5_arrive(&sm.dempty[buf]);
+        bm = min(bm, min(chunk_min(v2, mul) + 64u, chunk_min(v3, mul) + 96u));
+        if (bm < best) { best = bm; bblk = blk; }   // strict: the earlier block keeps ties
+      }
+      if (!live) continue;
+      const int64_t sv = (tile0 + 2 * it + t) * 128 + r;
+      const uint32_t code = (uint32_t)bblk * TL_NB + (best & 0xffu);
+      if (code_bytes == 3) {   // whole rows of G codes (G consecutive lanes of this warp)
+        sm.cw[ew][lane] = code;
+        __syncwarp();
+        if (lane % G == 0 && sv < sv_end) {
+          const int64_t tok = sv / G;
+          code_put_row(static_cast<uint8_t *>(codes), set * code_set_stride + (tok >> 4) * code_tile_stride +
+                       (tok & 15) * code_row_stride, G, &sm.cw[ew][lane], 3);
+        }
+        __syncwarp();
+      } else if (sv < sv_end) {
+        const int64_t tok = sv / G;
+        const int64_t off = set * code_set_stride + (tok >> 4) * code_tile_stride + (tok & 15) * code_row_stride + sv % G;
+        if (code_bytes == 1) static_cast<uint8_t *>(codes)[off] = static_cast<uint8_t>(code);
+        else if (code_bytes == 2) static_cast<uint16_t *>(codes)[off] = static_cast<uint16_t>(code);
+        else if (code_bytes == 4) static_cast<int32_t *>(codes)[off] = (int32_t)code;
+        else static_cast<int64_t *>(codes)[off] = code;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == TL_MMA_WARP) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 }  // namespace
 
 // Returns ANTKV_EUNSUPPORTED (nothing launched) outside the configuration
@@ -428,6 +743,63 @@ int launch_encode_tc5(const void *X, int dtype, int64_t rows, int d, int64_t x_s
       reinterpret_cast<const uint16_t *>(X), rows, x_set_stride, codebooks, cb_mod, m, codes, code_bytes,
       code_set_stride, code_tile_stride, code_row_stride, per, vec, 256u);
   ANTKV_LAUNCH_CHECK("vq_encode_tc5_kernel");
+  return ANTKV_OK;
+}
+
+// Long codebooks: d_sub 16 / 32, any m <= 65536, bf16 rows, no distance
+// output (ANTKV_NO_TC5_ENC=1 disables it as well).
+int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride, int nsets,
+                       const float *codebooks, int cb_mod, int m, int d_sub, void *codes, int code_bytes,
+                       int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
+                       const float *d2, cudaStream_t st) {
+  if (d != 128 || (d_sub != 16 && d_sub != 32) || m < 1 || m > 65536 || d2 != nullptr || dtype != ANTKV_BF16)
+    return ANTKV_EUNSUPPORTED;
+  if (code_bytes == 3 && m > 4096) return ANTKV_EUNSUPPORTED;
+  static int off = -1;
+  if (off < 0) {
+    const char *e = getenv("ANTKV_NO_TC5_ENC");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (off) return ANTKV_EUNSUPPORTED;
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (x_set_stride & 7) || (reinterpret_cast<uintptr_t>(codebooks) & 15))
+    return ANTKV_EUNSUPPORTED;
+  if (rows == 0 || nsets == 0) return ANTKV_OK;
+  const int G = d / d_sub;
+  const int nblk = (m + TL_NB - 1) / TL_NB;
+  const int ncb = min(cb_mod, nsets);
+  uint8_t *img = nullptr;
+  float *blkmax = nullptr;
+  cudaError_t e = scratch_alloc((void **)&img, (size_t)ncb * nblk * TL_BBLK, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&blkmax, sizeof(float) * ncb * nblk, st);
+  if (e != cudaSuccess) return cuda_status(e, "encoder codebook image");
+  if (d_sub == 32) tl_codebook_image_kernel<32><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
+  else tl_codebook_image_kernel<16><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
+  ANTKV_LAUNCH_CHECK("tl_codebook_image_kernel");
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t ntiles = (rows * G + 127) / 128;
+  const int64_t cps = nsets >= sms ? 1 : sms / nsets;
+  const int64_t per = (ntiles + cps - 1) / cps;
+  dim3 grid((unsigned)((ntiles + per - 1) / per), (unsigned)nsets);
+  const size_t smem = sizeof(TlSmem) + 1024;
+  static bool attr[64] = {};
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    cudaFuncSetAttribute(vq_encode_tc5l_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(vq_encode_tc5l_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (dev >= 0 && dev < 64) attr[dev] = true;
+  }
+  const uint16_t *Xh = reinterpret_cast<const uint16_t *>(X);
+  if (d_sub == 32)
+    vq_encode_tc5l_kernel<32><<<grid, TL_THREADS, smem, st>>>(Xh, rows, x_set_stride, img, blkmax, ncb, m, nblk, codes,
+                                                             code_bytes, code_set_stride, code_tile_stride,
+                                                             code_row_stride, per, 256u);
+  else
+    vq_encode_tc5l_kernel<16><<<grid, TL_THREADS, smem, st>>>(Xh, rows, x_set_stride, img, blkmax, ncb, m, nblk, codes,
+                                                             code_bytes, code_set_stride, code_tile_stride,
+                                                             code_row_stride, per, 256u);
+  ANTKV_LAUNCH_CHECK("vq_encode_tc5l_kernel");
+  cudaFreeAsync(img, st);
+  cudaFreeAsync(blkmax, st);
   return ANTKV_OK;
 }
 
