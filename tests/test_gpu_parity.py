@@ -654,6 +654,55 @@ def test_pdl_early_reads_with_interleaved_caches():
         assert np.array_equal(x, y)
 
 
+def test_step_device_q_written_by_torch_right_before():
+    """q and its position produced by torch kernels immediately before every
+    step_device call (no host sync in between), two caches alternating on
+    the default stream so each fused launch follows another cache's: the
+    kernel must read q / qpos only after griddepcontrol.wait there (early
+    reads are reserved for streams the caller declared exclusive), so the
+    outputs equal those of steps whose inputs were ready long before.  The
+    output is computed before the eviction (cache.py:153-154, 168-193)."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig
+    vq = VqConfig.from_notation("d8m256")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.02, window_size=8)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+
+    def make(seed):
+        Q, K, V = qkv(seed, 8, 2, 700, 128, heavy=2)
+        ck, cv = codebooks(seed, 2, 256, 8)
+        c = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=8, batch=1, capacity=1024)
+        c.prefill(dev(Q[None, :, :640]), dev(K[None, :, :640]), dev(V[None, :, :640]), np.arange(640))
+        return c, Q, K, V
+
+    outs = {}
+    for mode in ("ready", "just_written"):
+        caches = [make(51), make(52)]
+        qbuf = torch.empty((1, 8, 128), dtype=torch.bfloat16, device="cuda")
+        pbuf = torch.empty((1,), dtype=torch.int64, device="cuda")
+        res = [[], []]
+        if mode == "ready":
+            qs = [[dev(c[1][None, :, t]) for t in range(640, 700)] for c in caches]
+            ps = [torch.tensor([t], device="cuda") for t in range(640, 700)]
+            torch.cuda.synchronize()
+        for i, t in enumerate(range(640, 700)):
+            for j, (c, Q, K, V) in enumerate(caches):
+                k, v = dev(K[None, :, t]), dev(V[None, :, t])
+                out = torch.empty((1, 8, 128), device="cuda")
+                if mode == "ready":
+                    c.step_device(qs[j][i], k, v, ps[i], out)
+                else:
+                    src = dev(Q[None, :, t] * 0.5)
+                    torch.mul(src, 2.0, out=qbuf)          # q written by a torch kernel ...
+                    pbuf.fill_(t)                          # ... and its position
+                    c.step_device(qbuf, k, v, pbuf, out)   # ... right before the step
+                c._n += 1
+                res[j].append(out)
+        torch.cuda.synchronize()
+        outs[mode] = [torch.stack(r).cpu().numpy() for r in res]
+    for x, y in zip(outs["ready"], outs["just_written"]):
+        assert np.array_equal(x, y)
+
+
 def test_llama_caller_matches_dense_reference_when_lossless():
     """§8(f) rank 1 caller: with the window covering every token the cache is
     lossless, so the model's prefill and decode logits must match a dense
