@@ -65,6 +65,7 @@ def main():
     ap.add_argument("--configs", default=",".join(CONFIGS))
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--kernels", default="1,2,0")
+    ap.add_argument("--splits", type=int, default=0, help="CTAs per (sequence, head); 0 = the library's plan")
     a = ap.parse_args()
     peak = 6552.3
     try:
@@ -75,6 +76,8 @@ def main():
     for name in a.configs.split(","):
         notation, B, Hq, Hkv, n = CONFIGS[name]
         cache = build(notation, B, Hq, Hkv, n)
+        if a.splits:
+            cache.splits = a.splits
         q = torch.randn((B, Hq, 128), device="cuda").to(torch.bfloat16)
         qp = torch.full((B,), n + 3, device="cuda", dtype=torch.int64)
         out = torch.empty((B, Hq, 128), device="cuda", dtype=torch.float32)
