@@ -689,7 +689,13 @@ int decode_tc_supported(const antkv_cache_desc &c) {
          c.capacity % 32 == 0 && c.pool_capacity % 16 == 0 && c.m >= 1 && c.m <= 65536;
 }
 
+int decode_mha_supported(const antkv_cache_desc &c);   // decode_mha.cu
+int decode_mha_plan(const antkv_cache_desc &c, int requested);
+int decode_mha_launch(const antkv_cache_desc &c, const void *q, int qdtype, const int64_t *qpos, float *ws_o,
+                      float *ws_m, float *ws_l, float *out, float *lse, int *cnt, int splits, cudaStream_t st);
+
 int decode_tc_plan(const antkv_cache_desc &c, int requested) {
+  if (decode_mha_supported(c)) return decode_mha_plan(c, requested);   // MHA d4m256: CUDA-core kernel
   if (requested > 0) return requested;
   const int bh = c.B * c.Hkv;
   return bh >= 148 ? 1 : 148 / bh;
@@ -697,6 +703,8 @@ int decode_tc_plan(const antkv_cache_desc &c, int requested) {
 
 int decode_tc_launch(const antkv_cache_desc &c, const void *q, int qdtype, const int64_t *qpos, float *ws_o,
                      float *ws_m, float *ws_l, float *out, float *lse, int *cnt, int splits, cudaStream_t st) {
+  if (decode_mha_supported(c))
+    return decode_mha_launch(c, q, qdtype, qpos, ws_o, ws_m, ws_l, out, lse, cnt, splits, st);
   TcArgs a;
   a.out = out;
   a.lse = lse;
