@@ -15,8 +15,9 @@
 //     for rebuilding tiles for the tensor cores (decode_tc.cu);
 //   * the key side needs no rotation: score_j = (R((p_q - p_j) w) q) . k_j
 //     (pre-RoPE codes), so each lane rotates only its 2 query pairs, by
-//     R(-w) per token (fp32), re-seeded exactly from integer-reduced angles
-//     at every 32-token chunk;
+//     R(-w) per token (fp32, the Chebyshev recurrence x_{i+1} = 2 cos(w)
+//     x_i - x_{i-1}: one FMA per component), re-seeded exactly from
+//     integer-reduced angles at every 32-token chunk;
 //   * a chunk's 32 x 32 partial dot products are summed by a butterfly
 //     transpose-reduce (31 shuffles), leaving token i's score in lane i; the
 //     online softmax runs there and P_i is broadcast back for O += P_i V_i;
@@ -68,6 +69,7 @@ __device__ __forceinline__ float4 h4(uint2 v) {
   const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&v.y));
   return make_float4(a.x, a.y, b.x, b.y);
 }
+__device__ __forceinline__ float2 h2f(uint32_t v) { return __half22float2(*reinterpret_cast<const __half2 *>(&v)); }
 
 // Butterfly transpose-reduce: on return v[0] of lane l holds the sum over
 // the warp's lanes of their v[l].
@@ -86,7 +88,7 @@ __device__ __forceinline__ float transpose_sum(float (&v)[32], int lane) {
 }
 
 struct MhaLane {
-  float o[4];       // O of dims 4g..4g+3
+  float2 o01, o23;  // O of dims 4g..4g+3
   float m, l;       // running max (log2 units, warp-uniform), this lane's share of the normaliser
 };
 
@@ -97,24 +99,23 @@ __device__ __forceinline__ void chunk_softmax_pv(MhaLane &w, float s, int lane, 
   float cm = s;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
-  if (cm == -INFINITY) return;
+  // (no early exit: cm is warp-uniform but a branch on it would make the
+  // shuffles below collective; an all-masked chunk adds zeros)
   if (cm > w.m) {
     const float al = w.m == -INFINITY ? 0.f : mex2(w.m - cm);
     w.l *= al;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) w.o[e] *= al;
+    w.o01 = __fmul2_rn(w.o01, make_float2(al, al));
+    w.o23 = __fmul2_rn(w.o23, make_float2(al, al));
     w.m = cm;
   }
-  const float p = mex2(s - w.m);   // ex2(-inf) = 0
+  const float p = s == -INFINITY ? 0.f : mex2(s - w.m);
   w.l += p;
 #pragma unroll 8
   for (int i = 0; i < 32; ++i) {
     const float pi = __shfl_sync(0xffffffffu, p, i);
-    const float4 v = vrow(i);
-    w.o[0] = fmaf(pi, v.x, w.o[0]);
-    w.o[1] = fmaf(pi, v.y, w.o[1]);
-    w.o[2] = fmaf(pi, v.z, w.o[2]);
-    w.o[3] = fmaf(pi, v.w, w.o[3]);
+    const uint2 v = vrow(i);   // (d0, d1), (d2, d3) fp16
+    w.o01 = __ffma2_rn(make_float2(pi, pi), h2f(v.x), w.o01);
+    w.o23 = __ffma2_rn(make_float2(pi, pi), h2f(v.y), w.o23);
   }
 }
 
@@ -138,7 +139,9 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
     uint2 *dst = &sm.cb[0][0][0];
     for (int e = threadIdx.x; e < 2 * 256 * 16; e += HT) {
       const int side = e >> 12, code = (e >> 4) & 255;
-      dst[e] = code < c.m ? src[side * c.m + code] : make_uint2(0u, 0u);
+      uint2 v = code < c.m ? src[side * c.m + code] : make_uint2(0u, 0u);
+      if (side == 0) v = make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.x, v.y, 0x7632));
+      dst[e] = v;   // K: (d0, d2), (d1, d3) = the x and y components of pairs 2g, 2g+1
     }
   }
   __syncthreads();
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
   // per-token step R(-w) and the absolute frame R(p_q w) q of the pool rows
   const float sc = rsqrtf(128.f) * 1.4426950408889634f;
   const int64_t qrow = (int64_t)b * c.Hq + h;
-  float qx[2], qy[2], cw[2], sw[2], ax[2], ay[2];
+  float qx[2], qy[2], cw[2], sw[2], ax[2], ay[2];   // [u]: pair 2g + u
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int p = 2 * lane + u;
@@ -190,8 +193,10 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
   MhaLane w;
   w.m = -INFINITY;
   w.l = 0.f;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) w.o[e] = 0.f;
+  w.o01 = w.o23 = make_float2(0.f, 0.f);
+  const float2 C2 = make_float2(cw[0], cw[1]), S2 = make_float2(sw[0], sw[1]);
+  const float2 NS2 = make_float2(-sw[0], -sw[1]);
+  const float2 TC2 = make_float2(2.f * cw[0], 2.f * cw[1]);
   const uint32_t *qmg = c.qmask + bh * (c.capacity / 32);
   const int copy = lane & 15;
 
@@ -199,13 +204,13 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
   for (int k = 0; k < nc; ++k) {
     const int ch = c0 + k, slot = k % HNS;
     const uint32_t qw = __ldg(qmg + ch);
-    float fx[2], fy[2];   // R((p_q - p_j) w) q at the chunk's first token, exact
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      float cs, sn;
-      turns_cs(qp - (pos0 + (int64_t)ch * 32), tab->turns[2 * lane + u], cs, sn);
-      fx[u] = qx[u] * cs - qy[u] * sn;
-      fy[u] = qx[u] * sn + qy[u] * cs;
+    float2 FX, FY, PX, PY;   // R((p_q - p_j) w) q at token j (exact at the chunk's first), and at j - 1
+    {
+      float cs0, sn0, cs1, sn1;
+      turns_cs(qp - (pos0 + (int64_t)ch * 32), tab->turns[2 * lane], cs0, sn0);
+      turns_cs(qp - (pos0 + (int64_t)ch * 32), tab->turns[2 * lane + 1], cs1, sn1);
+      FX = make_float2(qx[0] * cs0 - qy[0] * sn0, qx[1] * cs1 - qy[1] * sn1);
+      FY = make_float2(qx[0] * sn0 + qy[0] * cs0, qx[1] * sn1 + qy[1] * cs1);
     }
     asm volatile(
         "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}\n" ::"r"(
@@ -217,20 +222,27 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int kc = tb[(i >> 4) * HTILE + (i & 15) * 32 + lane];
-      const float4 kv = h4(sm.cb[0][kc][copy]);
-      ps[i] = fmaf(fx[0], kv.x, fmaf(fy[0], kv.y, fmaf(fx[1], kv.z, fy[1] * kv.w)));
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {   // next token: R(-w)
-        const float x = fx[u], y = fy[u];
-        fx[u] = fmaf(cw[u], x, sw[u] * y);
-        fy[u] = fmaf(cw[u], y, -sw[u] * x);
+      const uint2 kv = sm.cb[0][kc][copy];   // (k0, k2), (k1, k3)
+      const float2 d = __ffma2_rn(FY, h2f(kv.y), __fmul2_rn(FX, h2f(kv.x)));
+      ps[i] = d.x + d.y;
+      // next token, R(-w) on both pairs: a rotation by a fixed angle obeys
+      // x_{i+1} = 2 cos(w) x_i - x_{i-1} per component (one FMA each after
+      // the first step, which rotates exactly)
+      if (i == 0) {
+        const float2 nx = __ffma2_rn(S2, FY, __fmul2_rn(C2, FX));
+        const float2 ny = __ffma2_rn(NS2, FX, __fmul2_rn(C2, FY));
+        PX = FX; PY = FY; FX = nx; FY = ny;
+      } else {
+        const float2 nx = __ffma2_rn(TC2, FX, make_float2(-PX.x, -PX.y));
+        const float2 ny = __ffma2_rn(TC2, FY, make_float2(-PY.x, -PY.y));
+        PX = FX; PY = FY; FX = nx; FY = ny;
       }
     }
     float s = transpose_sum(ps, lane);
     if (!((qw >> lane) & 1u)) s = -INFINITY;
     chunk_softmax_pv(w, s, lane, [&](int i) {
       const int vc = tb[(i >> 4) * HTILE + 512 + (i & 15) * 32 + lane];
-      return h4(sm.cb[1][vc][copy]);
+      return sm.cb[1][vc][copy];
     });
     __syncwarp();
     if (lane == 0 && k + HNS < nc) {
@@ -262,8 +274,8 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
       if (!ok) s = -INFINITY;
       chunk_softmax_pv(w, s, lane, [&](int i) {
         const int sl = tile * 16 + (i & 15);
-        return i < 16 ? h4(__ldg(reinterpret_cast<const uint2 *>(pf + pool_f16_offset(sl, 1, 4 * lane))))
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        return i < 16 ? __ldg(reinterpret_cast<const uint2 *>(pf + pool_f16_offset(sl, 1, 4 * lane)))
+                      : make_uint2(0u, 0u);
       });
     }
   }
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
   float lsum = w.l;
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-  *reinterpret_cast<float4 *>(&sm.mo[warp][4 * lane]) = make_float4(w.o[0], w.o[1], w.o[2], w.o[3]);
+  *reinterpret_cast<float4 *>(&sm.mo[warp][4 * lane]) = make_float4(w.o01.x, w.o01.y, w.o23.x, w.o23.y);
   if (lane == 0) {
     sm.mm[warp] = w.m;
     sm.ml[warp] = lsum;
