@@ -328,10 +328,12 @@ class QuantizedKVCache:
             raise ValueError("query heads must be a multiple of KV heads")
         if B != self.B:
             raise ValueError(f"cache was created for batch {self.B}")
-        for name, X in (("Q", Qt), ("K", Kt), ("V", Vt)):
-            if not bool(torch.isfinite(X).all()):
-                from .errors import NumericalError
-                raise NumericalError(f"non-finite values in {name}")
+        # one host synchronisation for the three checks (attention.py:59-67)
+        finite = torch.stack([torch.isfinite(X).all() for X in (Qt, Kt, Vt)]).cpu()
+        if not bool(finite.all()):
+            from .errors import NumericalError
+            name = ("Q", "K", "V")[int((~finite).nonzero()[0, 0])]
+            raise NumericalError(f"non-finite values in {name}")
         self._single = single
         self.Hq, self.Hkv, self.d = Hq, Hkv, d
         pos_np = np.array(positions.detach().cpu().numpy() if isinstance(positions, torch.Tensor)
