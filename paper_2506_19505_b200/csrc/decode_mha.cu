@@ -38,7 +38,8 @@ constexpr int HTILE = 1024;            // d4m256 code tile: [K 16 x 32 | V 16 x 
 constexpr int HSLOT = 2 * HTILE;       // one 32-token chunk
 
 struct MhaSmem {
-  uint2 cb[2][256][16];                // [side][code][copy]: 4 fp16 dims
+  uint2 cbk[256][16];                  // K: [code][copy] 4 fp16 dims (pairs' x | y halves)
+  float4 cbv[256][8];                  // V: [code][copy] 4 fp32 dims (no conversion on the FMA pipe)
   uint8_t ring[HW][HNS][HSLOT];
   float mo[HW][128];
   float mm[HW], ml[HW];
@@ -113,9 +114,9 @@ __device__ __forceinline__ void chunk_softmax_pv(MhaLane &w, float s, int lane, 
 #pragma unroll 8
   for (int i = 0; i < 32; ++i) {
     const float pi = __shfl_sync(0xffffffffu, p, i);
-    const uint2 v = vrow(i);   // (d0, d1), (d2, d3) fp16
-    w.o01 = __ffma2_rn(make_float2(pi, pi), h2f(v.x), w.o01);
-    w.o23 = __ffma2_rn(make_float2(pi, pi), h2f(v.y), w.o23);
+    const float4 v = vrow(i);
+    w.o01 = __ffma2_rn(make_float2(pi, pi), make_float2(v.x, v.y), w.o01);
+    w.o23 = __ffma2_rn(make_float2(pi, pi), make_float2(v.z, v.w), w.o23);
   }
 }
 
@@ -133,15 +134,20 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // the codebook (fp16, [Hkv][K, V][m][4]) replicated 16x
+  // the codebooks: K fp16 ([Hkv][K][m][4]) replicated 16x with its halves as
+  // (d0, d2), (d1, d3) = the x and y components of pairs 2g, 2g+1; V fp32
+  // (the cache's own codebook) replicated 8x (LDS.128 phases of 8 lanes)
   {
     const uint2 *src = reinterpret_cast<const uint2 *>(c.codebook_f16g) + (int64_t)h * 2 * c.m;
-    uint2 *dst = &sm.cb[0][0][0];
-    for (int e = threadIdx.x; e < 2 * 256 * 16; e += HT) {
-      const int side = e >> 12, code = (e >> 4) & 255;
-      uint2 v = code < c.m ? src[side * c.m + code] : make_uint2(0u, 0u);
-      if (side == 0) v = make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.x, v.y, 0x7632));
-      dst[e] = v;   // K: (d0, d2), (d1, d3) = the x and y components of pairs 2g, 2g+1
+    for (int e = threadIdx.x; e < 256 * 16; e += HT) {
+      const int code = e >> 4;
+      const uint2 v = code < c.m ? src[code] : make_uint2(0u, 0u);
+      (&sm.cbk[0][0])[e] = make_uint2(__byte_perm(v.x, v.y, 0x5410), __byte_perm(v.x, v.y, 0x7632));
+    }
+    const float4 *srcv = reinterpret_cast<const float4 *>(c.codebook_v + (int64_t)h * c.m * 4);
+    for (int e = threadIdx.x; e < 256 * 8; e += HT) {
+      const int code = e >> 3;
+      (&sm.cbv[0][0])[e] = code < c.m ? __ldg(srcv + code) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   __syncthreads();
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int kc = tb[(i >> 4) * HTILE + (i & 15) * 32 + lane];
-      const uint2 kv = sm.cb[0][kc][copy];   // (k0, k2), (k1, k3)
+      const uint2 kv = sm.cbk[kc][copy];   // (k0, k2), (k1, k3)
       const float2 d = __ffma2_rn(FY, h2f(kv.y), __fmul2_rn(FX, h2f(kv.x)));
       ps[i] = d.x + d.y;
       // next token, R(-w) on both pairs: a rotation by a fixed angle obeys
@@ -242,7 +248,7 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
     if (!((qw >> lane) & 1u)) s = -INFINITY;
     chunk_softmax_pv(w, s, lane, [&](int i) {
       const int vc = tb[(i >> 4) * HTILE + 512 + (i & 15) * 32 + lane];
-      return sm.cb[1][vc][copy];
+      return sm.cbv[vc][lane & 7];
     });
     __syncwarp();
     if (lane == 0 && k + HNS < nc) {
@@ -274,8 +280,8 @@ __global__ void __launch_bounds__(HT, 2) decode_mha_kernel(antkv_cache_desc c, M
       if (!ok) s = -INFINITY;
       chunk_softmax_pv(w, s, lane, [&](int i) {
         const int sl = tile * 16 + (i & 15);
-        return i < 16 ? __ldg(reinterpret_cast<const uint2 *>(pf + pool_f16_offset(sl, 1, 4 * lane)))
-                      : make_uint2(0u, 0u);
+        return i < 16 ? h4(__ldg(reinterpret_cast<const uint2 *>(pf + pool_f16_offset(sl, 1, 4 * lane))))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
       });
     }
   }
