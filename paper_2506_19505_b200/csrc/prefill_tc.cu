@@ -488,9 +488,12 @@ int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float 
 //
 // Warps: 0 bulk-copy producer (two rings of two stages: K hi | K lo, 64 KB,
 // freed as soon as S(t) completes; V^T, 32 KB, freed by P.V(t)), 1 TMEM owner + MMA issuer (S of tile t is issued before P.V of
-// tile t - 1 so the tensor core works while the softmax of t - 1 runs), 2-9
-// softmax: warps w and w + 4 own the same 32 rows (TMEM lanes) and split the
-// 128 key columns, exchanging half-row maxima through shared memory.  TMEM columns: S/P buffers 0 and 128, O 256..383,
+// tile t - 1 so the tensor core works while the softmax of t - 1 runs), 2-17
+// softmax: warps w, w + 4, w + 8, w + 12 own the same 32 rows (TMEM lanes)
+// and take 32 key columns each, exchanging quarter-row maxima through shared
+// memory (16 softmax warps rather than 8: with two per scheduler the
+// exponentials could not keep up with S(t + 1), tensor pipe 62 %).  TMEM
+// columns: S/P buffers 0 and 128, O 256..383,
 // Q parts 384..511.  Per 16-key step kk the P parts sit at columns 16 kk
 // (hi) and 16 kk + 8 (lo) of the buffer, so the 32 columns a softmax chunk
 // writes are exactly the S columns it has just read.
@@ -498,7 +501,8 @@ constexpr int FT_KR = 128;                   // keys per tile
 constexpr int FT_KPART = FT_KR * 128 * 2;    // 32 KB (one fp16 part of a K tile)
 constexpr int FT_VTILE = 128 * FT_KR * 2;    // 32 KB (V^T bf16)
 constexpr int FT_NS = 2;                     // stages of each ring (K: 64 KB, V^T: 32 KB)
-constexpr int FT_THREADS = 10 * 32;
+constexpr int FT_SOFT = 16;                  // softmax warps: 4 per TMEM lane quarter, 32 key columns each
+constexpr int FT_THREADS = (2 + FT_SOFT) * 32;
 constexpr uint32_t FT_O = 256, FT_QH = 384, FT_QL = 448;
 
 struct FlashTcSmem {
@@ -506,8 +510,8 @@ struct FlashTcSmem {
   uint8_t v[FT_NS][FT_VTILE];       // V^T, released when P.V(t) completes
   unsigned long long kfull[FT_NS], kempty[FT_NS], vfull[FT_NS], vempty[FT_NS];
   unsigned long long sfull[2], pfull[2], pvdone[2], qready;
-  float xm[2][2][TC_ROWS];   // [buffer][column half][row]: half-row maxima
-  float lx[2][TC_ROWS];      // [column half][row]: half-row sums at the end
+  float xm[2][4][TC_ROWS];   // [buffer][column quarter][row]: quarter-row maxima
+  float lx[4][TC_ROWS];      // [column quarter][row]: quarter-row sums at the end
   uint32_t tmem;
 };
 
@@ -558,10 +562,10 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
     }
     for (int b = 0; b < 2; ++b) {
       tc_mbar_init(tc_smem(&sm.sfull[b]), 1);
-      tc_mbar_init(tc_smem(&sm.pfull[b]), 256);
+      tc_mbar_init(tc_smem(&sm.pfull[b]), 32 * FT_SOFT);
       tc_mbar_init(tc_smem(&sm.pvdone[b]), 1);
     }
-    tc_mbar_init(tc_smem(&sm.qready), 256);
+    tc_mbar_init(tc_smem(&sm.qready), 32 * FT_SOFT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -650,25 +654,23 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
         __syncwarp();
       }
     }
-  } else {                          // ---- softmax: warps w, w + 4 share rows, split columns
-    const int quarter = warp & 3, half = (warp - 2) >> 2, row = 32 * quarter + lane, qi = q0 + row;
+  } else {                          // ---- softmax: warps w, w + 4, w + 8, w + 12 share rows, split columns
+    const int quarter = warp & 3, cq = (warp - 2) >> 2, row = 32 * quarter + lane, qi = q0 + row;
     const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
-    const int bar_id = 1 + quarter;                 // named barrier of the warp pair
-    {   // Q tile parts -> TMEM (A operand of S): half 0 the hi part, half 1 the lo part
-      const uint8_t *qg = Qt + ((int64_t)h * nqt + qt) * TC_TILE + half * TC_PART;
+    const int bar_id = 1 + quarter;                 // named barrier of the four warps of a row quarter
+    {   // Q tile parts -> TMEM (A operand of S): column quarters 0, 1 the hi part, 2, 3 the lo part
+      const int part = cq >> 1, cb = cq & 1;
+      const uint8_t *qg = Qt + ((int64_t)h * nqt + qt) * TC_TILE + part * TC_PART;
+      uint32_t r[32];
 #pragma unroll
-      for (int cb = 0; cb < 2; ++cb) {
-        uint32_t r[32];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 v = __ldg(reinterpret_cast<const uint4 *>(qg + sw128_off<>(row, 64 * cb + 8 * c)));
-          r[4 * c] = v.x;
-          r[4 * c + 1] = v.y;
-          r[4 * c + 2] = v.z;
-          r[4 * c + 3] = v.w;
-        }
-        tc_st32(tmem + lane_base + (half ? FT_QL : FT_QH) + 32 * cb, r);
+      for (int c = 0; c < 8; ++c) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(qg + sw128_off<>(row, 64 * cb + 8 * c)));
+        r[4 * c] = v.x;
+        r[4 * c + 1] = v.y;
+        r[4 * c + 2] = v.z;
+        r[4 * c + 3] = v.w;
       }
+      tc_st32(tmem + lane_base + (part ? FT_QL : FT_QH) + 32 * cb, r);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       tc_arrive(tc_smem(&sm.qready));
@@ -677,8 +679,8 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
     float mref = -INFINITY, mex = -INFINITY, l = 0.f, lc = 0.f;
     float ksc_next = T > 0 ? __ldg(Ksc + (int64_t)hk * nkt) : 1.f;
     for (int t = 0; t < T; ++t) {
-      const int b = t & 1, k0 = t * FT_KR + 64 * half;   // first key of this half
-      const uint32_t sb = tmem + lane_base + 128 * b + 64 * half;
+      const int b = t & 1, k0 = t * FT_KR + 32 * cq;   // first key of this quarter
+      const uint32_t sb = tmem + lane_base + 128 * b + 32 * cq;
       const float u = 1.4426950408889634f * qs_inv * __frcp_rn(ksc_next);   // log2 units, exact scales
       if (t + 1 < T) ksc_next = __ldg(Ksc + (int64_t)hk * nkt + t + 1);
       tc_wait(tc_smem(&sm.sfull[b]), (t >> 1) & 1);
@@ -689,62 +691,57 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       continue;
 #endif
       const bool full = (!causal || t * FT_KR + FT_KR - 1 <= q0) && t * FT_KR + FT_KR <= n_k;
-      // pass 1: max of this half (raw accumulator; u > 0 commutes with max),
-      // combined with the partner warp's half through shared memory
+      // pass 1: max of this quarter (raw accumulator; u > 0 commutes with max),
+      // combined with the other three quarters through shared memory
       float mt;
-      uint32_t c0[32], c1[32];   // this half's 64 logits, kept for pass 2
+      uint32_t c0[32];   // this quarter's 32 logits, kept for pass 2
       {
         tc_ld32_nowait(sb, c0);
-        tc_ld32_nowait(sb + 32, c1);
         tc_ld_wait();
         float m8[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) m8[j] = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          float x = __uint_as_float(i < 32 ? c0[i] : c1[i - 32]);
+        for (int i = 0; i < 32; ++i) {
+          float x = __uint_as_float(c0[i]);
           if (!full && (k0 + i >= n_k || (causal && k0 + i > qi))) x = -INFINITY;
           m8[i & 7] = fmaxf(m8[i & 7], x);
         }
         const float pm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-        sm.xm[b][half][row] = pm;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        mt = fmaxf(pm, sm.xm[b][half ^ 1][row]) * u;
+        sm.xm[b][cq][row] = pm;
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        mt = fmaxf(fmaxf(sm.xm[b][0][row], sm.xm[b][1][row]), fmaxf(sm.xm[b][2][row], sm.xm[b][3][row])) * u;
       }
       mex = fmaxf(mex, mt);
-      if (__any_sync(0xffffffffu, mt > mref + 8.f)) {   // same decision in both warps of the pair
+      if (__any_sync(0xffffffffu, mt > mref + 8.f)) {   // same decision in the four warps of the rows
         const float mn = fmaxf(mref, mt);
         const float al = mref == -INFINITY ? 0.f : tc_ex2(mref - mn);
         l *= al;
         lc *= al;
-        if (t > 0) {        // O holds P.V of earlier tiles: wait for the last one, rescale this half
+        if (t > 0) {        // O holds P.V of earlier tiles: wait for the last one, rescale this quarter
           tc_wait(tc_smem(&sm.pvdone[(t - 1) & 1]), ((t - 1) >> 1) & 1);
           tc_fence_after();
+          float ov[32];
+          tc_ld32(tmem + lane_base + FT_O + 32 * cq, ov);
+          uint32_t r[32];
 #pragma unroll
-          for (int cb = 0; cb < 2; ++cb) {
-            float ov[32];
-            tc_ld32(tmem + lane_base + FT_O + 64 * half + 32 * cb, ov);
-            uint32_t r[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(ov[i] * al);
-            tc_st32(tmem + lane_base + FT_O + 64 * half + 32 * cb, r);
-          }
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(ov[i] * al);
+          tc_st32(tmem + lane_base + FT_O + 32 * cq, r);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         mref = mn;
       }
       const float msub = mref == -INFINITY ? 0.f : mref;
-      // pass 2: P in bf16 parts over the S columns read in pass 1, 32 keys at a time
+      // pass 2: P in bf16 parts over the S columns read in pass 1
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      {
         uint32_t w[32];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {   // key pair (2i, 2i+1) of this chunk
-          float x0 = __uint_as_float(c ? c1[2 * i] : c0[2 * i]);
-          float x1 = __uint_as_float(c ? c1[2 * i + 1] : c0[2 * i + 1]);
-          const int kk0 = k0 + 32 * c + 2 * i;
+        for (int i = 0; i < 16; ++i) {   // key pair (2i, 2i+1) of this quarter
+          float x0 = __uint_as_float(c0[2 * i]);
+          float x1 = __uint_as_float(c0[2 * i + 1]);
+          const int kk0 = k0 + 2 * i;
           if (!full) {
             if (kk0 >= n_k || (causal && kk0 > qi)) x0 = -INFINITY;
             if (kk0 + 1 >= n_k || (causal && kk0 + 1 > qi)) x1 = -INFINITY;
@@ -754,11 +751,11 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
           const __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
           const float2 hf = __bfloat1622float2(hh);
           const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
-          // 16-key step s = i / 8 of this chunk: hi words at 16 s + (i % 8), lo at + 8
+          // 16-key step s = i / 8 of this quarter: hi words at 16 s + (i % 8), lo at + 8
           w[16 * (i >> 3) + (i & 7)] = *reinterpret_cast<const uint32_t *>(&hh);
           w[16 * (i >> 3) + 8 + (i & 7)] = *reinterpret_cast<const uint32_t *>(&lo);
         }
-        tc_st32(sb + 32 * c, w);
+        tc_st32(sb, w);
       }
       const float ls = (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       {   // l += ls, compensated (long contexts add thousands of tile sums)
@@ -770,22 +767,21 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       tc_fence_before();
       tc_arrive(tc_smem(&sm.pfull[b]));
     }
-    // the row's l = both halves' sums
-    sm.lx[half][row] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-    const float lrow = l + sm.lx[half ^ 1][row];
-    // O / l (this half's 64 columns), L relative to the exact max M (natural log)
+    // the row's l = the four quarters' sums
+    sm.lx[cq][row] = l;
+    asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+    const float lrow = (sm.lx[0][row] + sm.lx[1][row]) + (sm.lx[2][row] + sm.lx[3][row]);
+    // O / l (this quarter's 32 columns), L relative to the exact max M (natural log)
     if (T > 0) {
       tc_wait(tc_smem(&sm.pvdone[(T - 1) & 1]), ((T - 1) >> 1) & 1);
       tc_fence_after();
     }
     const float inv = lrow > 0.f ? 1.f / lrow : 0.f;
-    float *orow = O + ((int64_t)h * n_q + qi) * 128 + 64 * half;
-#pragma unroll
-    for (int cb = 0; cb < 2; ++cb) {
+    float *orow = O + ((int64_t)h * n_q + qi) * 128 + 32 * cq;
+    {
       float v[32];
       if (T > 0) {
-        tc_ld32(tmem + lane_base + FT_O + 64 * half + 32 * cb, v);
+        tc_ld32(tmem + lane_base + FT_O + 32 * cq, v);
       } else {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
@@ -793,11 +789,10 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       if (qi < n_q) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4)
-          *reinterpret_cast<float4 *>(orow + 32 * cb + i) =
-              make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv, v[i + 3] * inv);
+          *reinterpret_cast<float4 *>(orow + i) = make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv, v[i + 3] * inv);
       }
     }
-    if (qi < n_q && half == 0) {
+    if (qi < n_q && cq == 0) {
       const bool any = mex > -INFINITY;
       Mout[(int64_t)h * n_q + qi] = any ? mex * 0.6931471805599453f : -INFINITY;
       Lout[(int64_t)h * n_q + qi] = any ? lrow * exp2f(mref - mex) : 0.f;
