@@ -478,6 +478,18 @@ def test_staged_matches_generic_at_128k(notation, Hq, Hkv):
         cache.attend_device(q, qp, out, fast=fast)
         outs[fast] = out.cpu().numpy()[0]
     assert rel(outs[1], outs[0]) < 2e-2
+    # the codes the tcgen05 encoders wrote at full size: a random sample of
+    # quantized tokens per side against the float64 argmin (margin rule)
+    rs = np.random.default_rng(7)
+    for h in (0, Hkv - 1):
+        arr = cache.codes_array(0, h)
+        q_tok = np.flatnonzero(cache.kinds_array(0, h) == KIND["quantized"])
+        smp = np.sort(rs.choice(q_tok, size=512, replace=False))
+        for side, (X, C) in enumerate(((K, ck), (V, cv))):
+            Xs = X[0, h, torch.from_numpy(smp).cuda()].float().cpu().numpy().astype(np.float64)
+            Xs = Xs.reshape(-1, vq.d_sub)
+            ref, _ = O.assign_nearest(Xs, C[h].astype(np.float64))
+            assert_codes_parity(Xs, C[h], arr[smp, side].reshape(-1), ref)
     Kh, Vh = cache.dequantize()
     gq = Hq // Hkv
     for h in (0, Hkv - 1):
