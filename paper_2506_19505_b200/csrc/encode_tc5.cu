@@ -387,7 +387,8 @@ vq_encode_tc5_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_set
 }
 
 // ------------------------------------------------------------------------
-// Long codebooks (d_sub 16 / 32, any m <= 65536: config #3's d32m4096):
+// Long codebooks (d_sub 16 / 32, any m <= 65536: config #3's d32m4096) and
+// 4-dim sub-vectors (config #4's d4m256: one distance k-step per block):
 // the same integer-key argmin over 128-centroid blocks of the codebook.
 //
 // A sub-vector row of DSUB dims spans two 128B-swizzled atoms (K = 128):
@@ -444,7 +445,23 @@ tl_codebook_image_kernel(const float *__restrict__ codebooks, int m, uint8_t *__
   uint8_t *dst = img + ((int64_t)cbk * nblk + blk) * TL_BBLK;
   for (int ch = 0; ch < 16; ++ch) *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch)) = make_uint4(0u, 0u, 0u, 0u);
   float nn = 0.f;
-  for (int j0 = 0; j0 < DSUB; j0 += 8) {
+  if constexpr (DSUB == 4) {   // one k-step: (hi | mid), (lo | 1, |c|^2 hi / mid / lo)
+    float hi[4], mi[4], lo[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float x = c < m ? cb[i] : 0.f;
+      nn = fmaf(x, x, nn);
+      split3_bf16(x, hi[i], mi[i], lo[i]);
+    }
+    float nh, nm, nl;
+    split3_bf16(nn, nh, nm, nl);
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 0)) =
+        make_uint4(bf16_pair(hi[0], hi[1]), bf16_pair(hi[2], hi[3]), bf16_pair(mi[0], mi[1]), bf16_pair(mi[2], mi[3]));
+    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 1)) =
+        c < m ? make_uint4(bf16_pair(lo[0], lo[1]), bf16_pair(lo[2], lo[3]), bf16_pair(1.f, nh), bf16_pair(nm, nl))
+              : make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int j0 = 0; DSUB >= 8 && j0 < DSUB; j0 += 8) {
     float hi[8], mi[8], lo[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -460,10 +477,12 @@ tl_codebook_image_kernel(const float *__restrict__ codebooks, int m, uint8_t *__
     *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, ch + DSUB / 4)) =
         make_uint4(bf16_pair(lo[0], lo[1]), bf16_pair(lo[2], lo[3]), bf16_pair(lo[4], lo[5]), bf16_pair(lo[6], lo[7]));
   }
-  float nh, nm, nl;
-  split3_bf16(nn, nh, nm, nl);
-  if (c < m)
-    *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 3 * DSUB / 8)) = make_uint4(bf16_pair(1.f, nh), bf16_pair(nm, nl), 0u, 0u);
+  if constexpr (DSUB >= 8) {
+    float nh, nm, nl;
+    split3_bf16(nn, nh, nm, nl);
+    if (c < m)
+      *reinterpret_cast<uint4 *>(dst + tl_off<TL_NB>(r, 3 * DSUB / 8)) = make_uint4(bf16_pair(1.f, nh), bf16_pair(nm, nl), 0u, 0u);
+  }
   // the block's max |c|^2 (the exactness scale is the max over the blocks)
   __shared__ float red[TL_NB / 32];
   float mx = warp_max(c < m ? nn : 0.f);
@@ -483,7 +502,8 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
                       const uint8_t *__restrict__ img, const float *__restrict__ blkmax, int cb_mod, int m,
                       int nblk, void *__restrict__ codes, int code_bytes, int64_t code_set_stride,
                       int64_t code_tile_stride, int64_t code_row_stride, int64_t tiles_per_cta, uint32_t mul) {
-  constexpr int G = 128 / DSUB, TOK = 128 / G, KD = tl_kd<DSUB>(), NCH = DSUB / 8;
+  constexpr int G = 128 / DSUB, TOK = 128 / G, KD = tl_kd<DSUB>(), NCH = DSUB >= 8 ? DSUB / 8 : 1;
+  constexpr int PT = DSUB == 4 ? 2 : 3 * NCH + 1;   // A chunks rewritten per tile (the rest are constant)
   extern __shared__ __align__(128) unsigned char tlraw[];
   TlSmem &sm = *reinterpret_cast<TlSmem *>(tlraw + ((1024 - (t5_smem(tlraw) & 1023)) & 1023));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -517,7 +537,7 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
   for (int e = threadIdx.x; e < 2 * 128; e += TL_THREADS) {
     uint8_t *a = sm.a[e >> 7];
     const int r = e & 127;
-    for (int ch = 3 * NCH + 1; ch < 16; ++ch)
+    for (int ch = PT; ch < 16; ++ch)
       *reinterpret_cast<uint4 *>(a + tl_off<128>(r, ch)) =
           ch == 2 * KD ? make_uint4(bf16_pair(1.f, 1.f), 0u, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u);
   }
@@ -536,7 +556,10 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
     const int r = threadIdx.x;   // 0..127: row of both tiles
     auto load = [&](int it, int t, uint4 (&v)[NCH]) {
       const int64_t sv = (tile0 + 2 * it + t) * 128 + r;
-      if (sv < sv_end) {
+      if (sv < sv_end && DSUB == 4) {   // 8 bytes: x in .x, .y
+        const uint2 x2 = __ldg(reinterpret_cast<const uint2 *>(X + set * x_set_stride + (sv / G) * 128 + (sv % G) * DSUB));
+        v[0] = make_uint4(x2.x, x2.y, 0u, 0u);
+      } else if (sv < sv_end) {
         const uint4 *src = reinterpret_cast<const uint4 *>(X + set * x_set_stride + (sv / G) * 128 + (sv % G) * DSUB);
 #pragma unroll
         for (int i = 0; i < NCH; ++i) v[i] = __ldg(src + i);
@@ -575,6 +598,13 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
         const float s = __int_as_float((127 - e) << 23);
         const float m2s = -2.f * s;
         uint8_t *a = sm.a[t];
+        if constexpr (DSUB == 4) {   // (x' | x'), (x' | |x|^2 s, s, s, s)
+          const uint32_t o0 = bf16_pair(__uint_as_float(xv[t][0].x << 16) * m2s, __uint_as_float(xv[t][0].x & 0xffff0000u) * m2s);
+          const uint32_t o1 = bf16_pair(__uint_as_float(xv[t][0].y << 16) * m2s, __uint_as_float(xv[t][0].y & 0xffff0000u) * m2s);
+          *reinterpret_cast<uint4 *>(a + tl_off<128>(r, 0)) = make_uint4(o0, o1, o0, o1);
+          *reinterpret_cast<uint4 *>(a + tl_off<128>(r, 1)) = make_uint4(o0, o1, bf16_pair(n2 * s, s), bf16_pair(s, s));
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < NCH; ++i) {
           const uint32_t w4[4] = {xv[t][i].x, xv[t][i].y, xv[t][i].z, xv[t][i].w};
@@ -746,13 +776,14 @@ int launch_encode_tc5(const void *X, int dtype, int64_t rows, int d, int64_t x_s
   return ANTKV_OK;
 }
 
-// Long codebooks: d_sub 16 / 32, any m <= 65536, bf16 rows, no distance
-// output (ANTKV_NO_TC5_ENC=1 disables it as well).
+// Long codebooks and 4-dim sub-vectors: d_sub 4 / 16 / 32, any m <= 65536,
+// bf16 rows, no distance output (ANTKV_NO_TC5_ENC=1 disables it as well).
 int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_set_stride, int nsets,
                        const float *codebooks, int cb_mod, int m, int d_sub, void *codes, int code_bytes,
                        int64_t code_set_stride, int64_t code_tile_stride, int64_t code_row_stride,
                        const float *d2, cudaStream_t st) {
-  if (d != 128 || (d_sub != 16 && d_sub != 32) || m < 1 || m > 65536 || d2 != nullptr || dtype != ANTKV_BF16)
+  if (d != 128 || (d_sub != 4 && d_sub != 16 && d_sub != 32) || m < 1 || m > 65536 || d2 != nullptr ||
+      dtype != ANTKV_BF16)
     return ANTKV_EUNSUPPORTED;
   if (code_bytes == 3 && m > 4096) return ANTKV_EUNSUPPORTED;
   static int off = -1;
@@ -773,7 +804,8 @@ int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_
   if (e == cudaSuccess) e = scratch_alloc((void **)&blkmax, sizeof(float) * ncb * nblk, st);
   if (e != cudaSuccess) return cuda_status(e, "encoder codebook image");
   if (d_sub == 32) tl_codebook_image_kernel<32><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
-  else tl_codebook_image_kernel<16><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
+  else if (d_sub == 16) tl_codebook_image_kernel<16><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
+  else tl_codebook_image_kernel<4><<<dim3(nblk, ncb), TL_NB, 0, st>>>(codebooks, m, img, nblk, blkmax);
   ANTKV_LAUNCH_CHECK("tl_codebook_image_kernel");
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -786,6 +818,7 @@ int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_
   if (dev < 0 || dev >= 64 || !attr[dev]) {
     cudaFuncSetAttribute(vq_encode_tc5l_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(vq_encode_tc5l_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(vq_encode_tc5l_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dev >= 0 && dev < 64) attr[dev] = true;
   }
   const uint16_t *Xh = reinterpret_cast<const uint16_t *>(X);
@@ -793,10 +826,14 @@ int launch_encode_tc5l(const void *X, int dtype, int64_t rows, int d, int64_t x_
     vq_encode_tc5l_kernel<32><<<grid, TL_THREADS, smem, st>>>(Xh, rows, x_set_stride, img, blkmax, ncb, m, nblk, codes,
                                                              code_bytes, code_set_stride, code_tile_stride,
                                                              code_row_stride, per, 256u);
-  else
+  else if (d_sub == 16)
     vq_encode_tc5l_kernel<16><<<grid, TL_THREADS, smem, st>>>(Xh, rows, x_set_stride, img, blkmax, ncb, m, nblk, codes,
                                                              code_bytes, code_set_stride, code_tile_stride,
                                                              code_row_stride, per, 256u);
+  else
+    vq_encode_tc5l_kernel<4><<<grid, TL_THREADS, smem, st>>>(Xh, rows, x_set_stride, img, blkmax, ncb, m, nblk, codes,
+                                                            code_bytes, code_set_stride, code_tile_stride,
+                                                            code_row_stride, per, 256u);
   ANTKV_LAUNCH_CHECK("vq_encode_tc5l_kernel");
   cudaFreeAsync(img, st);
   cudaFreeAsync(blkmax, st);

@@ -579,11 +579,13 @@ def test_tensor_core_encoder_matches_oracle(dtype, m, code_bytes, n):
 
 @pytest.mark.parametrize("dtype,d_sub,m,code_bytes", [(torch.bfloat16, 32, 4096, 2), (torch.float16, 32, 4096, 2),
                                                       (torch.bfloat16, 16, 256, 1), (torch.bfloat16, 64, 300, 2),
-                                                      (torch.bfloat16, 16, 4096, 2)])
+                                                      (torch.bfloat16, 16, 4096, 2), (torch.bfloat16, 4, 256, 1),
+                                                      (torch.bfloat16, 4, 100, 1)])
 def test_tensor_core_encoder_long_codebooks(dtype, d_sub, m, code_bytes):
-    """encode_tc.cu (d_sub 16 / 32 / 64, any m; config #3's d32m4096): codes
-    vs the exhaustive float64 argmin of the oracle (margin rule), with a
-    duplicated centroid (ties -> lowest index), large and tiny rows and a
+    """encode_tc5.cu's block encoder (bf16, d_sub 4 / 16 / 32, any m: config
+    #3's d32m4096, config #4's d4m256) and encode_tc.cu (fp16, d_sub 64):
+    codes vs the exhaustive float64 argmin of the oracle (margin rule), with
+    a duplicated centroid (ties -> lowest index), large and tiny rows and a
     ragged row count."""
     from paper_2506_19505_b200 import _lib
     rng = np.random.default_rng(37)
