@@ -132,6 +132,32 @@ __device__ __forceinline__ float tc_ex2(float x) {   // 2^x, x <= 0 here (-inf -
   return y;
 }
 
+// Packed fp32 pairs (FFMA2 / FADD2 on sm_100): each lane rounds exactly as
+// the scalar instruction would, at half the issue slots.
+__device__ __forceinline__ float2 tc_ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rc, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n mov.b64 rc, {%6,%7};\n"
+      " fma.rn.f32x2 rd, ra, rb, rc;\n mov.b64 {%0,%1}, rd;\n}\n"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 tc_fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      " add.rn.f32x2 rd, ra, rb;\n mov.b64 {%0,%1}, rd;\n}\n"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 tc_fsub2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n .reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n"
+      " sub.rn.f32x2 rd, ra, rb;\n mov.b64 {%0,%1}, rd;\n}\n"
+      : "=f"(d.x), "=f"(d.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 1 / x for a normal power of two x (the tile scales of tc_pow2_scale): exact
+__device__ __forceinline__ float tc_pow2_inv(float x) { return __int_as_float(0x7F000000 - __float_as_int(x)); }
+
 // 32 consecutive 32-bit columns of this thread's TMEM lane <- r[0..31]
 __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -562,10 +588,10 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
     }
     for (int b = 0; b < 2; ++b) {
       tc_mbar_init(tc_smem(&sm.sfull[b]), 1);
-      tc_mbar_init(tc_smem(&sm.pfull[b]), 32 * FT_SOFT);
+      tc_mbar_init(tc_smem(&sm.pfull[b]), FT_SOFT);   // one arrival per softmax warp
       tc_mbar_init(tc_smem(&sm.pvdone[b]), 1);
     }
-    tc_mbar_init(tc_smem(&sm.qready), 32 * FT_SOFT);
+    tc_mbar_init(tc_smem(&sm.qready), FT_SOFT);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -673,21 +699,23 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       tc_st32(tmem + lane_base + (part ? FT_QL : FT_QH) + 32 * cb, r);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      tc_arrive(tc_smem(&sm.qready));
+      __syncwarp();
+      if (lane == 0) tc_arrive(tc_smem(&sm.qready));
     }
-    const float qs_inv = __frcp_rn(__ldg(Qsc + (int64_t)h * nqt + qt));
+    const float qs_inv = tc_pow2_inv(__ldg(Qsc + (int64_t)h * nqt + qt));
     float mref = -INFINITY, mex = -INFINITY, l = 0.f, lc = 0.f;
     float ksc_next = T > 0 ? __ldg(Ksc + (int64_t)hk * nkt) : 1.f;
     for (int t = 0; t < T; ++t) {
       const int b = t & 1, k0 = t * FT_KR + 32 * cq;   // first key of this quarter
       const uint32_t sb = tmem + lane_base + 128 * b + 32 * cq;
-      const float u = 1.4426950408889634f * qs_inv * __frcp_rn(ksc_next);   // log2 units, exact scales
+      const float u = 1.4426950408889634f * qs_inv * tc_pow2_inv(ksc_next);   // log2 units, exact scales
       if (t + 1 < T) ksc_next = __ldg(Ksc + (int64_t)hk * nkt + t + 1);
       tc_wait(tc_smem(&sm.sfull[b]), (t >> 1) & 1);
       tc_fence_after();
 #ifdef FT_EXP_NOSOFT
       tc_fence_before();
-      tc_arrive(tc_smem(&sm.pfull[b]));
+      __syncwarp();
+      if (lane == 0) tc_arrive(tc_smem(&sm.pfull[b]));
       continue;
 #endif
       const bool full = (!causal || t * FT_KR + FT_KR - 1 <= q0) && t * FT_KR + FT_KR <= n_k;
@@ -698,15 +726,16 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       {
         tc_ld32_nowait(sb, c0);
         tc_ld_wait();
+        if (!full) {     // one branch: masked keys become -inf for both passes
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (k0 + i >= n_k || (causal && k0 + i > qi)) c0[i] = 0xff800000u;
+        }
         float m8[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) m8[j] = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x = __uint_as_float(c0[i]);
-          if (!full && (k0 + i >= n_k || (causal && k0 + i > qi))) x = -INFINITY;
-          m8[i & 7] = fmaxf(m8[i & 7], x);
-        }
+        for (int j = 0; j < 8; ++j)
+          m8[j] = fmaxf(fmaxf(__uint_as_float(c0[j]), __uint_as_float(c0[j + 8])),
+                        fmaxf(__uint_as_float(c0[j + 16]), __uint_as_float(c0[j + 24])));
         const float pm = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         sm.xm[b][cq][row] = pm;
@@ -733,31 +762,28 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
         mref = mn;
       }
       const float msub = mref == -INFINITY ? 0.f : mref;
-      // pass 2: P in bf16 parts over the S columns read in pass 1
-      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+      // pass 2: P in bf16 parts over the S columns read in pass 1 (key pairs
+      // in packed fp32: FFMA2 for the exponent argument, FADD2 for the sums
+      // and the lo residuals)
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       {
+        const float2 uu = make_float2(u, u), mm = make_float2(-msub, -msub);
         uint32_t w[32];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {   // key pair (2i, 2i+1) of this quarter
-          float x0 = __uint_as_float(c0[2 * i]);
-          float x1 = __uint_as_float(c0[2 * i + 1]);
-          const int kk0 = k0 + 2 * i;
-          if (!full) {
-            if (kk0 >= n_k || (causal && kk0 > qi)) x0 = -INFINITY;
-            if (kk0 + 1 >= n_k || (causal && kk0 + 1 > qi)) x1 = -INFINITY;
-          }
-          const float p0 = tc_ex2(fmaf(x0, u, -msub)), p1 = tc_ex2(fmaf(x1, u, -msub));
-          ls4[i & 3] += p0 + p1;
-          const __nv_bfloat162 hh = __floats2bfloat162_rn(p0, p1);
-          const float2 hf = __bfloat1622float2(hh);
-          const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+          const float2 e = tc_ffma2(make_float2(__uint_as_float(c0[2 * i]), __uint_as_float(c0[2 * i + 1])), uu, mm);
+          const float2 p = make_float2(tc_ex2(e.x), tc_ex2(e.y));
+          ls2[i & 1] = tc_fadd2(ls2[i & 1], p);
+          const __nv_bfloat162 hh = __floats2bfloat162_rn(p.x, p.y);
+          const float2 r = tc_fsub2(p, __bfloat1622float2(hh));
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(r.x, r.y);
           // 16-key step s = i / 8 of this quarter: hi words at 16 s + (i % 8), lo at + 8
           w[16 * (i >> 3) + (i & 7)] = *reinterpret_cast<const uint32_t *>(&hh);
           w[16 * (i >> 3) + 8 + (i & 7)] = *reinterpret_cast<const uint32_t *>(&lo);
         }
         tc_st32(sb, w);
       }
-      const float ls = (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      const float ls = (ls2[0].x + ls2[1].x) + (ls2[0].y + ls2[1].y);
       {   // l += ls, compensated (long contexts add thousands of tile sums)
         const float y = ls - lc, tt = l + y;
         lc = (tt - l) - y;
@@ -765,7 +791,8 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      tc_arrive(tc_smem(&sm.pfull[b]));
+      __syncwarp();
+      if (lane == 0) tc_arrive(tc_smem(&sm.pfull[b]));
     }
     // the row's l = the four quarters' sums
     sm.lx[cq][row] = l;
