@@ -260,7 +260,7 @@ __global__ void ans_tc_stats_kernel(const float *__restrict__ M, const float *__
 constexpr int TC_QS = 3;      // Q stages; stage 2 first carries the K tile (until it is in TMEM)
 struct AnsTcSmem {
   uint8_t q[TC_QS][TC_TILE];  // 1024-aligned (the struct is placed at a 1024 boundary)
-  float2 stat[2][TC_ROWS];
+  float stat[2][2 * TC_ROWS];   // per column pair p: (-c_2p, -c_2p+1, |q_2p|, |q_2p+1|)
   float red[2][TC_ROWS];
   unsigned long long kbar, aready, qfull[TC_QS], qempty[TC_QS], tfull[2], tempty[2];
   uint32_t tmem;
@@ -377,8 +377,8 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       tc_fence_before();
       tc_arrive(tc_smem(&sm.aready));
     }
-    const float ksc_inv = __frcp_rn(__ldg(Ksc + (int64_t)hk * nkt + kt));   // powers of two: exact
-    float sv = 0.f, sk = 0.f;
+    const float ksc_inv = tc_pow2_inv(__ldg(Ksc + (int64_t)hk * nkt + kt));   // powers of two: exact
+    float sv = 0.f, skn = 0.f;   // skn = -(the A(1 - A)|q| sum), accumulated negated (see below)
     // item it = (head gq of the group, query tile qt0 + qi); the next item's
     // column statistics and scale are loaded one item ahead
     int gq = 0, qi = 0;
@@ -393,7 +393,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       const int s = it & 1;
       const int qt = qt0 + qi;
       const float2 cst = nst;
-      const float u = 1.4426950408889634f * ksc_inv * __frcp_rn(nqsc);
+      const float u = 1.4426950408889634f * ksc_inv * tc_pow2_inv(nqsc);
       if (++qi == per_head) {
         qi = 0;
         ++gq;
@@ -403,51 +403,55 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
         if (et < TC_ROWS) nst = __ldg(stats + (int64_t)h1 * padded + (qt0 + qi) * TC_ROWS + et);
         nqsc = __ldg(Qsc + (int64_t)h1 * nqt + qt0 + qi);
       }
-      if (et < TC_ROWS) sm.stat[s][et] = cst;
+      if (et < TC_ROWS) {
+        sm.stat[s][4 * (et >> 1) + (et & 1)] = -cst.x;
+        sm.stat[s][4 * (et >> 1) + 2 + (et & 1)] = cst.y;
+      }
       asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI) : "memory");
       tc_wait(tc_smem(&sm.tfull[s]), (it >> 1) & 1);
       tc_fence_after();
       const bool diag = causal && qt == kt;
-      float tv = 0.f, tk = 0.f;   // this tile's share (two-level sums over long contexts)
+      // this tile's share (two-level sums over long contexts), columns in
+      // packed fp32 pairs: a = 2^(v u - c); tv += a; tkn += (a a - a) |q|,
+      // i.e. -(A(1 - A)|q|) — fma(a, a, -a) = -fma(-a, a, a) exactly, so the
+      // negated sum is the scalar one with its sign flipped
+      float2 tv2 = make_float2(0.f, 0.f), tk2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int cb = 0; cb < 2; ++cb) {
         const int c0 = 64 * half + 32 * cb;
         float v[32];
         tc_ld32(tmem + ((uint32_t)(32 * quarter) << 16) + s * TC_ROWS + c0, v);
-        const float4 *st4 = reinterpret_cast<const float4 *>(&sm.stat[s][c0]);
-        if (!diag) {
+        if (diag) {                 // keys after the query are masked (causal): A = 0
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            const float4 st = st4[i >> 1];   // (c, |q|) of columns c0 + i, c0 + i + 1
-            const float a0 = tc_ex2(fmaf(v[i], u, -st.x)), a1 = tc_ex2(fmaf(v[i + 1], u, -st.z));
-            tv += a0 + a1;
-            tk = fmaf(fmaf(-a0, a0, a0), st.y, tk);
-            tk = fmaf(fmaf(-a1, a1, a1), st.w, tk);
-          }
-        } else {                    // keys after the query are masked (causal)
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < key_local) v[i] = -INFINITY;
+        }
+        const float4 *st4 = reinterpret_cast<const float4 *>(&sm.stat[s][2 * c0]);
+        const float2 uu = make_float2(u, u);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const float2 st = sm.stat[s][c0 + i];
-            const float a = c0 + i < key_local ? 0.f : tc_ex2(fmaf(v[i], u, -st.x));
-            tv += a;
-            tk = fmaf(fmaf(-a, a, a), st.y, tk);
-          }
+        for (int i = 0; i < 32; i += 2) {
+          const float4 st = st4[i >> 1];   // (-c, -c', |q|, |q'|) of columns c0 + i, c0 + i + 1
+          const float2 e = tc_ffma2(make_float2(v[i], v[i + 1]), uu, make_float2(st.x, st.y));
+          const float2 a = make_float2(tc_ex2(e.x), tc_ex2(e.y));
+          tv2 = tc_fadd2(tv2, a);
+          const float2 w = tc_ffma2(a, a, make_float2(-a.x, -a.y));
+          tk2 = tc_ffma2(w, make_float2(st.z, st.w), tk2);
         }
       }
-      sv += tv;
-      sk += tk;
+      sv += tv2.x + tv2.y;
+      skn += tk2.x + tk2.y;
       tc_fence_before();
       tc_arrive(tc_smem(&sm.tempty[s]));
     }
     // combine the two column halves of each key
     if (half == 1) {
       sm.red[0][key_local] = sv;
-      sm.red[1][key_local] = sk;
+      sm.red[1][key_local] = skn;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI) : "memory");
     if (half == 0 && key < n_k) {
       ans_v[(int64_t)ho * n_k + key] = sv + sm.red[0][key_local];
-      ans_k[(int64_t)ho * n_k + key] = sk + sm.red[1][key_local];
+      ans_k[(int64_t)ho * n_k + key] = -(skn + sm.red[1][key_local]);
     }
   }
   tc_fence_before();
