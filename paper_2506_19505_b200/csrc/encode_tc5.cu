@@ -101,6 +101,22 @@ __device__ __forceinline__ void t5_mma(uint32_t tmem_d, uint64_t a, uint64_t b, 
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+// Warp-wide forms (all lanes call with the same operands, one elected lane
+// issues): from converged code the operands stay uniform and UTCHMMA needs no
+// per-instruction ELECT/BRA.U.ANY waterfall as under lane == 0.
+__device__ __forceinline__ void t5_mma_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void t5_commit_w(unsigned long long *bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(t5_smem(bar))
+      : "memory");
+}
 __device__ __forceinline__ void t5_commit(unsigned long long *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    t5_smem(bar))
@@ -238,6 +254,7 @@ vq_encode_tc5_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_set
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem;
+  if (tmem != 0) __trap();   // 512 columns at one CTA per SM start at column 0 (the MMA warps assume it)
 
   if (warp < T5_PROD) {
     // ---- A producer: thread = sub-vector row (token r / 16, group r % 16)
@@ -323,12 +340,13 @@ vq_encode_tc5_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_set
       t5_wait(&sm.afull[st], (it / T5_AS) & 1);
       if (it >= 2) t5_wait(&sm.dempty[buf], ((it >> 1) - 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
-        const uint32_t asm_ = t5_smem(sm.a[st]), d = tmem + buf * T5_N;
+      {
+        // 512 columns, one CTA per SM: the allocation starts at column 0
+        const uint32_t asm_ = t5_smem(sm.a[st]), d = buf * T5_N;
 #pragma unroll
-        for (int ks = 0; ks < 3; ++ks) t5_mma(d, t5_desc(asm_ + 32 * ks), t5_desc(bsm + 32 * ks), idesc, ks > 0);
-        t5_commit(&sm.aempty[st]);
-        t5_commit(&sm.dfull[buf]);
+        for (int ks = 0; ks < 3; ++ks) t5_mma_w(d, t5_desc(asm_ + 32 * ks), t5_desc(bsm + 32 * ks), idesc, ks > 0);
+        t5_commit_w(&sm.aempty[st]);
+        t5_commit_w(&sm.dfull[buf]);
       }
       __syncwarp();
     }
@@ -546,6 +564,7 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sm.tmem;
+  if (tmem != 0) __trap();   // 512 columns at one CTA per SM start at column 0 (the MMA warps assume it)
 
   if (warp < TL_PROD) {
     // ---- A pair producer: thread p builds rows p and p + 128 of the pair
@@ -650,22 +669,23 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
         t5_wait(&sm.bfull[st], (k / TL_BS) & 1);
         if (k >= 2) t5_wait(&sm.dempty[buf], ((k >> 1) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (lane == 0) {
+        {
           const uint32_t bs = t5_smem(sm.b[st]);
           const int npt = min(2, ntl - 2 * it);   // tiles in this pair
 #pragma unroll
           for (int t = 0; t < 2; ++t) {
             if (t >= npt) break;
-            const uint32_t as = t5_smem(sm.a[t]), d = tmem + t * 256 + buf * 128;
+            // 512 columns, one CTA per SM: the allocation starts at column 0
+            const uint32_t as = t5_smem(sm.a[t]), d = t * 256 + buf * 128;
 #pragma unroll
             for (int ks = 0; ks <= KD; ++ks) {
               const uint32_t ao = (ks >> 2) * (128 * 128) + (ks & 3) * 32, bo = (ks >> 2) * (TL_NB * 128) + (ks & 3) * 32;
-              t5_mma(d, t5_desc(as + ao), t5_desc(bs + bo), idesc, ks > 0);
+              t5_mma_w(d, t5_desc(as + ao), t5_desc(bs + bo), idesc, ks > 0);
             }
           }
-          t5_commit(&sm.bempty[st]);
-          if (blk == nblk - 1) t5_commit(&sm.aempty);
-          t5_commit(&sm.dfull[buf]);
+          t5_commit_w(&sm.bempty[st]);
+          if (blk == nblk - 1) t5_commit_w(&sm.aempty);
+          t5_commit_w(&sm.dfull[buf]);
         }
         __syncwarp();
       }

@@ -169,6 +169,23 @@ __device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t (&r)[32])
       "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
       : "memory");
 }
+// Warp-wide forms: every lane executes the call with the same operands, one
+// elected lane issues.  Called from converged, warp-uniform code the operands
+// stay in uniform registers, so no per-instruction waterfall loop is needed
+// around UTCHMMA (the lane == 0 forms get one: ELECT + BRA.U.ANY each).
+__device__ __forceinline__ void tc_mma_f16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+      : "memory");
+}
 // D[tmem] (+)= A[tmem] . B[smem]
 __device__ __forceinline__ void tc_mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                               uint32_t accumulate) {
@@ -328,25 +345,27 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       // kind::f16, fp16 A/B, fp32 D, both K-major, N = 128 (bits 17-22), M = 128 (bits 24-28)
       const uint32_t idesc = (1u << 4) | ((uint32_t)(TC_ROWS >> 3) << 17) | ((uint32_t)(TC_ROWS >> 4) << 24);
       tc_wait(tc_smem(&sm.aready), 0);   // the K tile is in TMEM (columns 256..383)
+      // 512 columns on a one-CTA-per-SM kernel: the allocation starts at 0, and
+      // a constant keeps the MMA operands uniform (warp-wide elect issue)
+      if (tmem != 0) __trap();
+      constexpr uint32_t tm = 0;
       for (int it = 0; it < items; ++it) {
         const int s = it % TC_QS, b = it & 1;
         tc_wait(tc_smem(&sm.qfull[s]), (it / TC_QS) & 1);
         if (it >= 2) tc_wait(tc_smem(&sm.tempty[b]), ((it >> 1) - 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t qa = tc_smem(sm.q[s]), d = tmem + b * TC_ROWS;
+        const uint32_t qa = tc_smem(sm.q[s]), d = tm + b * TC_ROWS;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-            const uint32_t kh = tmem + TC_AH + 8 * kk, kl = tmem + TC_AL + 8 * kk;
-            const uint64_t qh = sw128_desc(qa + off), ql = sw128_desc(qa + TC_PART + off);
-            tc_mma_f16_ts(d, kh, qh, idesc, kk > 0);
-            tc_mma_f16_ts(d, kh, ql, idesc, 1);
-            tc_mma_f16_ts(d, kl, qh, idesc, 1);
-          }
-          tc_commit(tc_smem(&sm.qempty[s]));
-          tc_commit(tc_smem(&sm.tfull[b]));
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+          const uint32_t kh = tm + TC_AH + 8 * kk, kl = tm + TC_AL + 8 * kk;
+          const uint64_t qh = sw128_desc(qa + off), ql = sw128_desc(qa + TC_PART + off);
+          tc_mma_f16_ts_w(d, kh, qh, idesc, kk > 0);
+          tc_mma_f16_ts_w(d, kh, ql, idesc, 1);
+          tc_mma_f16_ts_w(d, kl, qh, idesc, 1);
         }
+        tc_commit_w(tc_smem(&sm.qempty[s]));
+        tc_commit_w(tc_smem(&sm.tfull[b]));
         __syncwarp();
       }
     }
@@ -542,6 +561,9 @@ struct FlashTcSmem {
   unsigned long long sfull[2], pfull[2], pvdone[2], qready;
   float xm[2][4][TC_ROWS];   // [buffer][column quarter][row]: quarter-row maxima
   float lx[4][TC_ROWS];      // [column quarter][row]: quarter-row sums at the end
+#ifdef FT_TRACE
+  uint32_t tr_sready[64], tr_pdone[64], tr_pfirst[64], tr_mwake[64], tr_pvissued[64], tr_sissued[64];
+#endif
   uint32_t tmem;
 };
 
@@ -596,6 +618,9 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       tc_mbar_init(tc_smem(&sm.pvdone[b]), 1);
     }
     tc_mbar_init(tc_smem(&sm.qready), FT_SOFT);
+#ifdef FT_TRACE
+    for (int i = 0; i < 64; ++i) { sm.tr_pdone[i] = 0; sm.tr_pfirst[i] = 0xffffffffu; }
+#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -634,6 +659,10 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
     const uint32_t idS = (1u << 4) | ((uint32_t)(FT_KR >> 3) << 17) | ((uint32_t)(TC_ROWS >> 4) << 24);
     const uint32_t idPV = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
                           ((uint32_t)(TC_ROWS >> 4) << 24);
+    // all 512 columns belong to this CTA (one CTA per SM), so the allocation
+    // starts at column 0: a constant keeps every MMA operand uniform
+    if (tmem != 0) __trap();
+    constexpr uint32_t tm = 0;
     tc_wait(tc_smem(&sm.qready), 0);
     for (int t = 0; t <= T; ++t) {
       if (t < T) {                  // S(t) = Q . K_t^T into buffer t & 1
@@ -644,18 +673,21 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
         // buffer b still holds P(t-2), read by P.V(t-2): that MMA was issued
         // before this one and tcgen05.mma executes in issue order, so no wait
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t kb = tc_smem(sm.k[st]), d = tmem + 128 * b;
+        {
+          const uint32_t kb = tc_smem(sm.k[st]), d = tm + 128 * b;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t off = (kk >> 2) * (FT_KR * 128) + (kk & 3) * 32;
             const uint64_t kh = sw128_desc(kb + off), kl = sw128_desc(kb + FT_KPART + off);
-            tc_mma_f16_ts(d, tmem + FT_QH + 8 * kk, kh, idS, kk > 0);
-            tc_mma_f16_ts(d, tmem + FT_QH + 8 * kk, kl, idS, 1);
-            tc_mma_f16_ts(d, tmem + FT_QL + 8 * kk, kh, idS, 1);
+            tc_mma_f16_ts_w(d, tm + FT_QH + 8 * kk, kh, idS, kk > 0);
+            tc_mma_f16_ts_w(d, tm + FT_QH + 8 * kk, kl, idS, 1);
+            tc_mma_f16_ts_w(d, tm + FT_QL + 8 * kk, kh, idS, 1);
           }
-          tc_commit(tc_smem(&sm.kempty[st]));
-          tc_commit(tc_smem(&sm.sfull[b]));
+          tc_commit_w(tc_smem(&sm.kempty[st]));
+          tc_commit_w(tc_smem(&sm.sfull[b]));
+#ifdef FT_TRACE
+          if (lane == 0 && t < 64) sm.tr_sissued[t] = (uint32_t)clock();
+#endif
         }
         __syncwarp();
       }
@@ -666,20 +698,26 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
 #endif
         tc_wait(tc_smem(&sm.pfull[b]), (u >> 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
+#ifdef FT_TRACE
+        if (lane == 0 && u < 64) sm.tr_mwake[u] = (uint32_t)clock();
+#endif
+        {
           const uint32_t vb = tc_smem(sm.v[st]);
 #pragma unroll
           for (int kk = 0; kk < FT_KR / 16; ++kk) {
 #ifdef FT_EXP_NOPV
             break;
 #endif
-            const uint32_t ph = tmem + 128 * b + 16 * kk, pl = ph + 8;
+            const uint32_t ph = tm + 128 * b + 16 * kk, pl = ph + 8;
             const uint64_t vh = sw128_desc(vb + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
-            tc_mma_f16_ts(tmem + FT_O, ph, vh, idPV, (u > 0 || kk > 0) ? 1u : 0u);
-            tc_mma_f16_ts(tmem + FT_O, pl, vh, idPV, 1);
+            tc_mma_f16_ts_w(tm + FT_O, ph, vh, idPV, (u > 0 || kk > 0) ? 1u : 0u);
+            tc_mma_f16_ts_w(tm + FT_O, pl, vh, idPV, 1);
           }
-          tc_commit(tc_smem(&sm.vempty[st]));
-          tc_commit(tc_smem(&sm.pvdone[b]));
+          tc_commit_w(tc_smem(&sm.vempty[st]));
+          tc_commit_w(tc_smem(&sm.pvdone[b]));
+#ifdef FT_TRACE
+          if (lane == 0 && u < 64) sm.tr_pvissued[u] = (uint32_t)clock();
+#endif
         }
         __syncwarp();
       }
@@ -716,6 +754,9 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       if (t + 1 < T) ksc_next = __ldg(Ksc + (int64_t)hk * nkt + t + 1);
       tc_wait(tc_smem(&sm.sfull[b]), (t >> 1) & 1);
       tc_fence_after();
+#ifdef FT_TRACE
+      if (warp == 2 && lane == 0 && t < 64) sm.tr_sready[t] = (uint32_t)clock();
+#endif
 #ifdef FT_EXP_NOSOFT
       tc_fence_before();
       __syncwarp();
@@ -796,6 +837,13 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
+#ifdef FT_TRACE
+      if (lane == 0 && t < 64) {
+        const uint32_t c = (uint32_t)clock();
+        atomicMax(&sm.tr_pdone[t], c - sm.tr_sready[0]);
+        atomicMin(&sm.tr_pfirst[t], c - sm.tr_sready[0]);
+      }
+#endif
       if (lane == 0) tc_arrive(tc_smem(&sm.pfull[b]));
     }
     // the row's l = the four quarters' sums
@@ -831,6 +879,31 @@ flash_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, c
   }
   tc_fence_before();
   __syncthreads();
+#ifdef FT_TRACE
+  if (threadIdx.x == 0 && blockIdx.y == 0 && blockIdx.x < 2 && T >= 64) {
+    const uint32_t b0 = sm.tr_sready[0];
+    double ts = 0, tsf = 0, w1 = 0, iss = 0, sq = 0, per = 0, sw = 0;
+    int n = 0;
+    for (int t = 8; t < 60; ++t, ++n) {
+      const uint32_t sr = sm.tr_sready[t] - b0, pd = sm.tr_pdone[t], pf = sm.tr_pfirst[t];
+      ts += (double)(pd - sr);
+      tsf += (double)(pf - sr);
+      w1 += (double)(sm.tr_mwake[t] - b0 - pd);
+      iss += (double)(sm.tr_pvissued[t] - sm.tr_mwake[t]);
+      sq += (double)(sm.tr_sready[t + 2] - sm.tr_pvissued[t]);
+      per += (double)(sm.tr_sready[t + 1] - sm.tr_sready[t]);
+      sw += (double)(sm.tr_sready[t + 1] - b0 - pd);
+    }
+    for (int t = 20; t < 24; ++t)
+      printf("FT_RAW cta %d t %d: S issued %d  S ready %d  P done first %d last %d  mma wake %d  PV issued %d\n",
+             blockIdx.x, t, (int)(sm.tr_sissued[t] - sm.tr_sready[20]), (int)(sm.tr_sready[t] - sm.tr_sready[20]),
+             (int)(sm.tr_pfirst[t] + b0 - sm.tr_sready[20]), (int)(sm.tr_pdone[t] + b0 - sm.tr_sready[20]),
+             (int)(sm.tr_mwake[t] - sm.tr_sready[20]), (int)(sm.tr_pvissued[t] - sm.tr_sready[20]));
+    printf("FT_TRACE cta %d: period %.0f  softmax(first/last) %.0f/%.0f  pfull->mma wake %.0f  pv+S issue %.0f  "
+           "pv issued->S(t+2) ready %.0f  softmax done->S(t+1) ready %.0f\n",
+           blockIdx.x, per / n, tsf / n, ts / n, w1 / n, iss / n, sq / n, sw / n);
+  }
+#endif
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
