@@ -259,25 +259,30 @@ presplit_sw128_kernel(const float *__restrict__ X, int rows, uint8_t *__restrict
 }
 
 // Per query: c_i = M_i log2e + log2 L_i (+inf beyond n_q) and ||q_i||,
-// packed float2 [heads][nqt * 128].
+// [heads][nqt * 128] laid out per column pair p as the float4
+// (-c_2p, -c_2p+1, |q_2p|, |q_2p+1|): the anchor-score epilogue's packed
+// operands, bulk-copied next to each Q tile (1 KB per tile).
 __global__ void ans_tc_stats_kernel(const float *__restrict__ M, const float *__restrict__ L,
                                     const float *__restrict__ qn, int heads, int n_q, int padded,
-                                    float2 *__restrict__ out) {
+                                    float *__restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)heads * padded) return;
   const int h = (int)(i / padded), q = (int)(i % padded);
-  float2 v = make_float2(INFINITY, 0.f);
+  float c = INFINITY, nq = 0.f;
   if (q < n_q) {
     const int64_t k = (int64_t)h * n_q + q;
-    v = make_float2(M[k] * 1.4426950408889634f + log2f(L[k]), qn[k]);
+    c = M[k] * 1.4426950408889634f + log2f(L[k]);
+    nq = qn[k];
   }
-  out[i] = v;
+  float *o = out + 2 * ((int64_t)h * padded + (q & ~1)) + (q & 1);
+  o[0] = -c;
+  o[2] = nq;
 }
 
 constexpr int TC_QS = 3;      // Q stages; stage 2 first carries the K tile (until it is in TMEM)
 struct AnsTcSmem {
   uint8_t q[TC_QS][TC_TILE];  // 1024-aligned (the struct is placed at a 1024 boundary)
-  float stat[2][2 * TC_ROWS];   // per column pair p: (-c_2p, -c_2p+1, |q_2p|, |q_2p+1|)
+  float stat[TC_QS][2 * TC_ROWS];   // the Q stage's column statistics (ans_tc_stats_kernel layout)
   float red[2][TC_ROWS];
   unsigned long long kbar, aready, qfull[TC_QS], qempty[TC_QS], tfull[2], tempty[2];
   uint32_t tmem;
@@ -285,7 +290,7 @@ struct AnsTcSmem {
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
 ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, const uint8_t *__restrict__ Kt,
-              const float *__restrict__ Ksc, const float2 *__restrict__ stats, int group, int sum_group,
+              const float *__restrict__ Ksc, const float *__restrict__ stats, int group, int sum_group,
               int n_q, int n_k, int causal, float *__restrict__ ans_k, float *__restrict__ ans_v) {
   extern __shared__ uint8_t tc_raw[];
   AnsTcSmem &sm = *reinterpret_cast<AnsTcSmem *>(tc_raw + ((1024 - (tc_smem(tc_raw) & 1023)) & 1023));
@@ -303,7 +308,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
     tc_mbar_init(tc_smem(&sm.aready), TC_EPI);
     for (int s = 0; s < TC_QS; ++s) {
       tc_mbar_init(tc_smem(&sm.qfull[s]), 1);
-      tc_mbar_init(tc_smem(&sm.qempty[s]), 1);
+      tc_mbar_init(tc_smem(&sm.qempty[s]), 1 + TC_EPI / 32);   // the MMAs' commit + each epilogue warp
     }
     for (int s = 0; s < 2; ++s) {
       tc_mbar_init(tc_smem(&sm.tfull[s]), 1);
@@ -334,8 +339,10 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
         else if (s == TC_QS - 1) tc_wait(tc_smem(&sm.aready), 0);   // the K tile has left stage 2
         const int h = ho * sum_group + it / per_head, qt = qt0 + it % per_head;
         if (lane == 0) {
-          tc_expect_tx(tc_smem(&sm.qfull[s]), TC_TILE);
+          tc_expect_tx(tc_smem(&sm.qfull[s]), TC_TILE + 8 * TC_ROWS);
           tc_bulk(tc_smem(sm.q[s]), Qt + ((int64_t)h * nqt + qt) * TC_TILE, TC_TILE, tc_smem(&sm.qfull[s]));
+          tc_bulk(tc_smem(sm.stat[s]), stats + 2 * ((int64_t)h * padded + qt * TC_ROWS), 8 * TC_ROWS,
+                  tc_smem(&sm.qfull[s]));
         }
         __syncwarp();
       }
@@ -398,35 +405,22 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
     }
     const float ksc_inv = tc_pow2_inv(__ldg(Ksc + (int64_t)hk * nkt + kt));   // powers of two: exact
     float sv = 0.f, skn = 0.f;   // skn = -(the A(1 - A)|q| sum), accumulated negated (see below)
-    // item it = (head gq of the group, query tile qt0 + qi); the next item's
-    // column statistics and scale are loaded one item ahead
+    // item it = (head gq of the group, query tile qt0 + qi); its column
+    // statistics arrive with the Q tile (stage it % TC_QS; no epilogue-wide
+    // barrier per item), the next item's scale is loaded one item ahead
     int gq = 0, qi = 0;
-    float2 nst = make_float2(0.f, 0.f);
     float nqsc = 1.f;
-    if (items > 0) {
-      const int h = ho * sum_group;
-      if (et < TC_ROWS) nst = __ldg(stats + (int64_t)h * padded + qt0 * TC_ROWS + et);
-      nqsc = __ldg(Qsc + (int64_t)h * nqt + qt0);
-    }
+    if (items > 0) nqsc = __ldg(Qsc + (int64_t)(ho * sum_group) * nqt + qt0);
     for (int it = 0; it < items; ++it) {
-      const int s = it & 1;
+      const int s = it & 1, sq = it % TC_QS;
       const int qt = qt0 + qi;
-      const float2 cst = nst;
       const float u = 1.4426950408889634f * ksc_inv * tc_pow2_inv(nqsc);
       if (++qi == per_head) {
         qi = 0;
         ++gq;
       }
-      if (it + 1 < items) {
-        const int h1 = ho * sum_group + gq;
-        if (et < TC_ROWS) nst = __ldg(stats + (int64_t)h1 * padded + (qt0 + qi) * TC_ROWS + et);
-        nqsc = __ldg(Qsc + (int64_t)h1 * nqt + qt0 + qi);
-      }
-      if (et < TC_ROWS) {
-        sm.stat[s][4 * (et >> 1) + (et & 1)] = -cst.x;
-        sm.stat[s][4 * (et >> 1) + 2 + (et & 1)] = cst.y;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(TC_EPI) : "memory");
+      if (it + 1 < items) nqsc = __ldg(Qsc + (int64_t)(ho * sum_group + gq) * nqt + qt0 + qi);
+      tc_wait(tc_smem(&sm.qfull[sq]), (it / TC_QS) & 1);   // long complete: the MMAs of this item waited on it
       tc_wait(tc_smem(&sm.tfull[s]), (it >> 1) & 1);
       tc_fence_after();
       const bool diag = causal && qt == kt;
@@ -445,7 +439,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
           for (int i = 0; i < 32; ++i)
             if (c0 + i < key_local) v[i] = -INFINITY;
         }
-        const float4 *st4 = reinterpret_cast<const float4 *>(&sm.stat[s][2 * c0]);
+        const float4 *st4 = reinterpret_cast<const float4 *>(&sm.stat[sq][2 * c0]);
         const float2 uu = make_float2(u, u);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
@@ -461,6 +455,8 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       skn += tk2.x + tk2.y;
       tc_fence_before();
       tc_arrive(tc_smem(&sm.tempty[s]));
+      __syncwarp();
+      if (lane == 0) tc_arrive(tc_smem(&sm.qempty[sq]));   // this warp is done with the stage's statistics
     }
     // combine the two column halves of each key
     if (half == 1) {
@@ -490,13 +486,13 @@ int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float 
   const int nqt = ceil_div(n_q, TC_ROWS), nkt = ceil_div(n_k, TC_ROWS);
   uint8_t *qt = nullptr, *kt = nullptr;
   float *qsc = nullptr, *ksc = nullptr;
-  float2 *stats = nullptr;
+  float *stats = nullptr;
   cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * (nqt ? nqt : 1) * TC_TILE, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&kt, (size_t)kv_heads * nkt * TC_TILE, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * (nqt ? nqt : 1), st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nkt, st);
   if (e == cudaSuccess)
-    e = scratch_alloc((void **)&stats, sizeof(float2) * (size_t)heads * (nqt ? nqt : 1) * TC_ROWS, st);
+    e = scratch_alloc((void **)&stats, 2 * sizeof(float) * (size_t)heads * (nqt ? nqt : 1) * TC_ROWS, st);
   if (e != cudaSuccess) return cuda_status(e, "anchor-score tile scratch");
   if (nqt > 0) {
     presplit_sw128_kernel<TC_ROWS><<<dim3(nqt, heads), 256, 0, st>>>(Qs, n_q, qt, qsc);
@@ -1034,13 +1030,13 @@ int prefill_tc_fused(const void *Q, const void *K, const void *V, int dtype, con
   const int heads = B * Hq, kv_heads = B * Hkv, nt = ceil_div(n, TC_ROWS), group = Hq / Hkv;
   uint8_t *qt = nullptr, *kt = nullptr, *vt = nullptr;
   float *qsc = nullptr, *ksc = nullptr;
-  float2 *stats = nullptr;
+  float *stats = nullptr;
   cudaError_t e = scratch_alloc((void **)&qt, (size_t)heads * nt * TC_TILE, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&kt, (size_t)kv_heads * nt * TC_TILE, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&vt, (size_t)kv_heads * nt * FT_VTILE, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&qsc, sizeof(float) * (size_t)heads * nt, st);
   if (e == cudaSuccess) e = scratch_alloc((void **)&ksc, sizeof(float) * (size_t)kv_heads * nt, st);
-  if (e == cudaSuccess) e = scratch_alloc((void **)&stats, sizeof(float2) * (size_t)heads * nt * TC_ROWS, st);
+  if (e == cudaSuccess) e = scratch_alloc((void **)&stats, 2 * sizeof(float) * (size_t)heads * nt * TC_ROWS, st);
   if (e != cudaSuccess) return cuda_status(e, "prefill tile scratch");
   const __nv_bfloat16 *Qb = reinterpret_cast<const __nv_bfloat16 *>(Q);
   const __nv_bfloat16 *Kb = reinterpret_cast<const __nv_bfloat16 *>(K);
