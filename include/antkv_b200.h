@@ -136,6 +136,13 @@ ANTKV_API int antkv_prefill_attention(const void *Q, const void *K, const void *
                             float *O, float *M, float *L, float *q_norms,
                             void *stream);
 
+/* Input validation of the prefill (attention.py:59-67 `_check_finite`,
+ * called from cache.py:100-140 through attention.flash_attention_with_aux):
+ * *flag |= 1 when any of the n elements of X (dtype) is NaN or +-inf.  One
+ * HBM pass; the caller zeroes the flags once and reads them back once for
+ * Q, K and V together. */
+ANTKV_API int antkv_check_finite(const void *X, int dtype, int64_t n, int *flag, void *stream);
+
 /* RoPE (attention.py:89-106): X [B][H][n][d] (dtype) rotated at positions
  * int64 [B][n] (NULL = no rotation), times `scale`, into out float32; norms
  * (optional) float32 [B][H][n] = L2 norm of the un-rotated row. */

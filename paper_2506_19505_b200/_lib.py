@@ -56,6 +56,7 @@ _SIGS = {
     "antkv_ans_blocked": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _vp, _vp, _vp]),
     "antkv_assign_nearest": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]),
     "antkv_rope_rotate": (_i, [_vp, _i, _vp, _i, _i, _i, _i, _d, _f, _vp, _vp, _vp]),
+    "antkv_check_finite": (_i, [_vp, _i, _i64, _vp, _vp]),
     "antkv_prefill_attention": (_i, [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp, _vp, _vp]),
     "antkv_prefill_anchor_scores": (_i, [_vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _d, _vp, _vp, _vp]),
     "antkv_kmeans_assign_f64": (_i, [_vp, _vp, _i64, _i, _i, _vp, _vp, _vp]),

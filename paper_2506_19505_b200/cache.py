@@ -328,11 +328,19 @@ class QuantizedKVCache:
             raise ValueError("query heads must be a multiple of KV heads")
         if B != self.B:
             raise ValueError(f"cache was created for batch {self.B}")
-        # one host synchronisation for the three checks (attention.py:59-67)
-        finite = torch.stack([torch.isfinite(X).all() for X in (Qt, Kt, Vt)]).cpu()
-        if not bool(finite.all()):
+        # the three checks of attention.py:59-67: one HBM pass each on the GPU
+        # (antkv_check_finite), one host synchronisation for all three
+        flags = torch.zeros(3, dtype=torch.int32, device=Qt.device)
+        for i, X in enumerate((Qt, Kt, Vt)):
+            if X.is_contiguous() and X.dtype in (torch.float32, torch.bfloat16, torch.float16):
+                _lib.call("antkv_check_finite", _lib.ptr(X), _lib.dtype_tag(X), X.numel(),
+                          _lib.ptr(flags[i:]), _lib.stream())
+            else:
+                flags[i] = (~torch.isfinite(X)).any().to(torch.int32)
+        bad = flags.cpu()
+        if bool(bad.any()):
             from .errors import NumericalError
-            name = ("Q", "K", "V")[int((~finite).nonzero()[0, 0])]
+            name = ("Q", "K", "V")[int(bad.nonzero()[0, 0])]
             raise NumericalError(f"non-finite values in {name}")
         self._single = single
         self.Hq, self.Hkv, self.d = Hq, Hkv, d

@@ -368,6 +368,48 @@ extern "C" int antkv_flash_aux(const float *Qs, const float *Kr, const float *V,
                       as_stream(stream));
 }
 
+// ---------------------------------------------------------------- finiteness
+// Exponent bits all ones = NaN or +-inf.  16-byte loads, grid-stride; one
+// atomic per thread that saw any.
+__device__ __forceinline__ bool word_nonfinite(uint32_t w, int dtype) {
+  if (dtype == ANTKV_F32) return (w & 0x7F800000u) == 0x7F800000u;
+  const uint32_t m = dtype == ANTKV_BF16 ? 0x7F80u : 0x7C00u;
+  return (w & m) == m || ((w >> 16) & m) == m;
+}
+__global__ void __launch_bounds__(256) check_finite_kernel(const uint8_t *__restrict__ x, int dtype,
+                                                           int64_t bytes, int *__restrict__ flag) {
+  bool bad = false;
+  const int64_t nvec = bytes >> 4, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(x) + i);
+    bad |= word_nonfinite(v.x, dtype) | word_nonfinite(v.y, dtype) | word_nonfinite(v.z, dtype) |
+           word_nonfinite(v.w, dtype);
+  }
+  // tail (< 16 bytes; whole elements, 2- or 4-byte aligned)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int64_t o = nvec << 4; o < bytes; o += (dtype == ANTKV_F32 ? 4 : 2)) {
+      const uint32_t w = dtype == ANTKV_F32 ? *reinterpret_cast<const uint32_t *>(x + o)
+                                            : *reinterpret_cast<const uint16_t *>(x + o);
+      bad |= word_nonfinite(w, dtype);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+extern "C" int antkv_check_finite(const void *X, int dtype, int64_t n, int *flag, void *stream) {
+  ANTKV_REQUIRE(dtype == ANTKV_F32 || dtype == ANTKV_BF16 || dtype == ANTKV_F16, "unknown dtype");
+  ANTKV_REQUIRE(n >= 0 && flag, "bad arguments");
+  ANTKV_REQUIRE((reinterpret_cast<uintptr_t>(X) & 15) == 0, "X must be 16-byte aligned");
+  if (n == 0) return ANTKV_OK;
+  const int64_t bytes = n * (dtype == ANTKV_F32 ? 4 : 2);
+  const int64_t nvec = bytes >> 4;
+  const int blocks = (int)std::min<int64_t>(148 * 8, std::max<int64_t>(1, (nvec + 255) / 256));
+  check_finite_kernel<<<blocks, 256, 0, as_stream(stream)>>>(static_cast<const uint8_t *>(X), dtype, bytes,
+                                                             flag);
+  ANTKV_LAUNCH_CHECK("check_finite_kernel");
+  return ANTKV_OK;
+}
+
 extern "C" int antkv_rope_rotate(const void *X, int dtype, const int64_t *positions, int B,
                                  int H, int n, int d, double theta_base, float scale, float *out,
                                  float *norms, void *stream) {

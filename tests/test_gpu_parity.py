@@ -1476,3 +1476,37 @@ def test_reference_suite_on_the_shim(tmp_path):
     assert r.returncode == 0, r.stdout[-4000:]
     summary = r.stdout.strip().splitlines()[-1]
     assert "passed" in summary and "failed" not in summary, summary
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32])
+def test_prefill_rejects_non_finite_inputs(dtype):
+    """The prefill's input validation (attention.py:59-67, raised through
+    cache.py:100-140) runs on the GPU (antkv_check_finite): a NaN or inf
+    anywhere in Q, K or V -- including the last, sub-16-byte tail element --
+    raises NumericalError naming the tensor; finite inputs pass."""
+    from paper_2506_19505_b200 import (CacheConfig, Codebook, NumericalError, QuantizedKVCache,
+                                       VqConfig, _lib)
+    vq = VqConfig.from_notation("d8m256")
+    rng = np.random.default_rng(21)
+    cb = Codebook(vq, rng.standard_normal((vq.m, vq.d_sub)).astype(np.float32))
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.05, window_size=8)
+    n = 77
+    base = [torch.randn((1, 2, n, 128), device="cuda").to(dtype) for _ in range(3)]
+    QuantizedKVCache(cfg, cb, cb).prefill(*base, np.arange(n))   # finite: accepted
+    for which, name in enumerate("QKV"):
+        for bad in (float("nan"), float("inf"), -float("inf")):
+            for idx in ((0, 0, 0, 0), (0, 1, n - 1, 127), (0, 1, 40, 63)):
+                X = [t.clone() for t in base]
+                X[which][idx] = bad
+                with pytest.raises(NumericalError, match=f"in {name}"):
+                    QuantizedKVCache(cfg, cb, cb).prefill(*X, np.arange(n))
+    # the raw entry point: element counts that leave a tail after the 16-byte vectors
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for count in (1, 7, 9, 1000, 4097):
+        x = torch.randn(count + 8, device="cuda").to(dtype)[:count]
+        flag.zero_()
+        _lib.call("antkv_check_finite", _lib.ptr(x), _lib.dtype_tag(x), count, _lib.ptr(flag), _lib.stream())
+        assert int(flag.item()) == 0
+        x[count - 1] = float("nan")
+        _lib.call("antkv_check_finite", _lib.ptr(x), _lib.dtype_tag(x), count, _lib.ptr(flag), _lib.stream())
+        assert int(flag.item()) == 1
