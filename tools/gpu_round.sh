@@ -19,5 +19,8 @@ if [ "${NCU:-1}" = 1 ]; then
   ncu --set full --clock-control none --import-source on -k regex:'flash_tc|ans_tc' -c 2 \
       -o gpurun_out/prefill_tc_$TAG -f \
       python tools/flash_tc_once.py 32768 > gpurun_out/ncu_prefill_$TAG.log 2>&1; echo "ncu prefill rc=$?"
+  ncu --set full --clock-control none --import-source on -k regex:'ans_tc_kernel' -c 1 \
+      -o gpurun_out/ans_tc_$TAG -f \
+      python tools/ans_tc_once.py 32768 > gpurun_out/ncu_ans_$TAG.log 2>&1; echo "ncu ans rc=$?"
 fi
 tail -c 2500 gpurun_out/bench_$TAG.json; echo; cat gpurun_out/bench_ref_$TAG.json; tail -3 gpurun_out/pytest_gpu_$TAG.log
