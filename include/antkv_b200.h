@@ -75,6 +75,10 @@ extern "C" {
 #define ANTKV_HS_POOL_HIGH 4 /* high-water mark of used pool slots          */
 
 /* dtype tags for row inputs */
+/* Row / tile arrays handed to the prefill, cache-build and encode entry
+ * points (Q, K, V, X) are read with 16-byte vector loads and bulk copies and
+ * must start at a 16-byte aligned address (ANTKV_EINVAL otherwise); any
+ * freshly allocated device buffer is. */
 #define ANTKV_F32 0
 #define ANTKV_BF16 1
 #define ANTKV_F16 2

@@ -307,9 +307,12 @@ class QuantizedKVCache:
         return Qt, Kt, Vt, single, was_np
 
     def _row_dtype(self, t):
-        if t.dtype in (torch.float32, torch.bfloat16, torch.float16):
-            return t.contiguous()
-        return t.float().contiguous()
+        """Contiguous rows in a kernel dtype at a 16-byte aligned address (the
+        kernels read rows with vector loads and bulk copies)."""
+        if t.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+            t = t.float()
+        t = t.contiguous()
+        return t if t.data_ptr() % 16 == 0 else t.clone()
 
     # ----------------------------------------------------------- prefill
     def prefill(self, Q, K, V, positions):
@@ -332,7 +335,8 @@ class QuantizedKVCache:
         # (antkv_check_finite), one host synchronisation for all three
         flags = torch.zeros(3, dtype=torch.int32, device=Qt.device)
         for i, X in enumerate((Qt, Kt, Vt)):
-            if X.is_contiguous() and X.dtype in (torch.float32, torch.bfloat16, torch.float16):
+            if (X.is_contiguous() and X.data_ptr() % 16 == 0
+                    and X.dtype in (torch.float32, torch.bfloat16, torch.float16)):
                 _lib.call("antkv_check_finite", _lib.ptr(X), _lib.dtype_tag(X), X.numel(),
                           _lib.ptr(flags[i:]), _lib.stream())
             else:

@@ -611,6 +611,7 @@ extern "C" int antkv_vq_encode(const void *X, int dtype, int64_t rows, int d,
   ANTKV_REQUIRE(code_bytes == 1 || code_bytes == 2 || code_bytes == 4 || code_bytes == 8,
                 "code_bytes must be 1, 2, 4 or 8");
   ANTKV_REQUIRE(code_bytes >= 8 || m <= (1 << (8 * code_bytes)), "codes do not fit");
+  ANTKV_REQUIRE_ALIGNED16(X, "X");
   return launch_encode(X, dtype, rows, d, 0, 1, codebook, 1, m, d_sub, codes, code_bytes, 0,
                        16 * (d / d_sub), d / d_sub, nullptr, as_stream(stream));
 }
@@ -633,6 +634,8 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
   if (rc) return rc;
   previous_cache_on_stream(as_stream(stream), c->codes);   // this stream now touched c
   ANTKV_REQUIRE(n >= 0 && n <= c->capacity, "prefill length exceeds capacity");
+  ANTKV_REQUIRE_ALIGNED16(K, "K");
+  ANTKV_REQUIRE_ALIGNED16(V, "V");
   ANTKV_REQUIRE(n_anchors + c->window_size + 1 <= c->pool_capacity, "pool capacity too small");
   cudaStream_t st = as_stream(stream);
   const int nsets = c->B * c->Hkv;

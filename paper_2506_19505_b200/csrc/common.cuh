@@ -16,6 +16,9 @@ namespace antkv {
 void set_error(const char *fmt, ...);
 int cuda_status(cudaError_t e, const char *where);
 
+// Row / tile inputs are read with 16-byte vector loads and bulk copies.
+#define ANTKV_REQUIRE_ALIGNED16(ptr, name) \
+  ANTKV_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, name " must be 16-byte aligned")
 #define ANTKV_REQUIRE(cond, ...)                                              \
   do {                                                                        \
     if (!(cond)) {                                                            \

@@ -437,6 +437,9 @@ extern "C" int antkv_prefill_attention_block(const void *Q, const void *K, const
                                              int n_q, int n_k, int d, double theta_base,
                                              int causal, float *O, float *M, float *L,
                                              float *q_norms, void *stream) {
+  ANTKV_REQUIRE_ALIGNED16(Q, "Q");
+  ANTKV_REQUIRE_ALIGNED16(K, "K");
+  ANTKV_REQUIRE_ALIGNED16(V, "V");
   ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
   ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
   ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
@@ -484,6 +487,8 @@ extern "C" int antkv_prefill_anchor_scores_block(const void *Q, const void *K, i
                                                  int Hq, int Hkv, int n_q, int n_k, int d,
                                                  double theta_base, int causal, float *ans_k,
                                                  float *ans_v, void *stream) {
+  ANTKV_REQUIRE_ALIGNED16(Q, "Q");
+  ANTKV_REQUIRE_ALIGNED16(K, "K");
   ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
   ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
   ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");
@@ -528,6 +533,9 @@ extern "C" int antkv_prefill_attention_scores(const void *Q, const void *K, cons
                                               const int64_t *positions, int B, int Hq, int Hkv, int n,
                                               int d, double theta_base, float *O, float *M, float *L,
                                               float *q_norms, float *ans_k, float *ans_v, void *stream) {
+  ANTKV_REQUIRE_ALIGNED16(Q, "Q");
+  ANTKV_REQUIRE_ALIGNED16(K, "K");
+  ANTKV_REQUIRE_ALIGNED16(V, "V");
   ANTKV_REQUIRE(d % 2 == 0, "head dimension must be even for RoPE");
   ANTKV_REQUIRE(theta_base > 0, "theta_base must be positive");
   ANTKV_REQUIRE(Hkv >= 1 && Hq % Hkv == 0, "Hq must be a multiple of Hkv");

@@ -1500,6 +1500,15 @@ def test_prefill_rejects_non_finite_inputs(dtype):
                 X[which][idx] = bad
                 with pytest.raises(NumericalError, match=f"in {name}"):
                     QuantizedKVCache(cfg, cb, cb).prefill(*X, np.arange(n))
+    # a contiguous but 16-byte-misaligned view takes the torch check, same error
+    X = [torch.randn((1, 2, n + 1, 128), device="cuda").to(dtype).flatten()[1:1 + 2 * n * 128]
+         .view(1, 2, n, 128) for _ in range(3)]
+    O_view = QuantizedKVCache(cfg, cb, cb).prefill(*X, np.arange(n))     # finite: accepted
+    O_copy = QuantizedKVCache(cfg, cb, cb).prefill(*[x.clone() for x in X], np.arange(n))
+    assert torch.equal(O_view, O_copy)
+    X[2][0, 0, 5, 7] = float("nan")
+    with pytest.raises(NumericalError, match="in V"):
+        QuantizedKVCache(cfg, cb, cb).prefill(*X, np.arange(n))
     # the raw entry point: element counts that leave a tail after the 16-byte vectors
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
     for count in (1, 7, 9, 1000, 4097):
@@ -1510,3 +1519,24 @@ def test_prefill_rejects_non_finite_inputs(dtype):
         x[count - 1] = float("nan")
         _lib.call("antkv_check_finite", _lib.ptr(x), _lib.dtype_tag(x), count, _lib.ptr(flag), _lib.stream())
         assert int(flag.item()) == 1
+
+
+def test_misaligned_rows_rejected_at_the_abi_and_copied_by_the_api():
+    """Row arrays must be 16-byte aligned at the C ABI (vector loads, bulk
+    copies): a misaligned pointer is ANTKV_EINVAL (ValueError here) with no
+    sticky CUDA error, while the Python API copies misaligned views."""
+    from paper_2506_19505_b200 import Codebook, VqConfig, _lib, encode_rows
+    vq = VqConfig.from_notation("d8m256")
+    rng = np.random.default_rng(5)
+    C = torch.from_numpy(rng.standard_normal((vq.m, vq.d_sub)).astype(np.float32)).cuda()
+    X = torch.randn(65 * 128 + 8, device="cuda").to(torch.bfloat16)
+    codes = torch.empty((64, 16), dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError, match="aligned"):
+        _lib.call("antkv_vq_encode", _lib.ptr(X[1:]), _lib.BF16, 64, 128, _lib.ptr(C), vq.m, vq.d_sub,
+                  _lib.ptr(codes), 1, _lib.stream())
+    torch.cuda.synchronize()          # no sticky error
+    view = X[1:1 + 64 * 128].view(64, 128)
+    cb = Codebook(vq, C.cpu().numpy())
+    a = encode_rows(view, cb)
+    b = encode_rows(view.clone(), cb)
+    assert torch.equal(torch.as_tensor(a), torch.as_tensor(b))
