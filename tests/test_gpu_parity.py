@@ -1540,3 +1540,42 @@ def test_misaligned_rows_rejected_at_the_abi_and_copied_by_the_api():
     a = encode_rows(view, cb)
     b = encode_rows(view.clone(), cb)
     assert torch.equal(torch.as_tensor(a), torch.as_tensor(b))
+
+
+@pytest.mark.parametrize("n,Hq,Hkv", [(1, 2, 2), (127, 8, 1), (129, 4, 4), (256, 8, 2)])
+def test_tcgen05_prefill_small_and_ragged_vs_oracle(n, Hq, Hkv):
+    """The tcgen05 attention and anchor-score kernels on single-token, sub-tile,
+    tile + 1 and exact-tile causal prefills with GQA 1 / 4 / 8 (the masked
+    diagonal tile, the one-branch masking and the per-item column statistics
+    of every query-tile / key-tile combination) against the float64 oracle at
+    the reference's tolerances."""
+    from paper_2506_19505_b200.parallel import CudaPrefillOps
+    d, theta = 128, 5e5
+    Q, K, V = qkv(90 + n, Hq, Hkv, n, d, heavy=min(3, n))
+    pos = np.arange(n)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+    ops = CudaPrefillOps()
+    Qd, Kd, Vd = dev(Q[None]), dev(K[None]), dev(V[None])
+    p = torch.from_numpy(pos).cuda()[None].contiguous()
+    Og, Mg, Lg, qn = ops.attention_block(Qd, Kd, Vd, p, p, True, theta)
+    ak, av = ops.score_block(Qd, Kd, p, p, Mg, Lg, qn, True, theta)
+    g = Hq // Hkv
+    ref_k, ref_v = np.zeros((Hkv, n)), np.zeros((Hkv, n))
+    for h in range(Hq):
+        q = Q[h].astype(np.float64)
+        k, v = K[h // g].astype(np.float64), V[h // g].astype(np.float64)
+        Qs = O.apply_rope(q, pos, theta) / np.sqrt(d)
+        Kr = O.apply_rope(k, pos, theta)
+        Or, Lr, Mr = O.flash_aux(Qs, Kr, v, 64, 64, True)
+        assert rel(Og[0, h].cpu().numpy(), Or) < 1e-4
+        assert np.abs(Mg[0, h].cpu().numpy() - Mr).max() < 1e-5 * max(1.0, np.abs(Mr).max())
+        assert np.abs(Lg[0, h].cpu().numpy() / Lr - 1).max() < 1e-5
+        kk, vv = O.ans_blocked(Qs, Kr, Mr, Lr, np.sqrt((q ** 2).sum(1)), 64, 64, True)
+        ref_k[h // g] += kk
+        ref_v[h // g] += vv
+    # ans_k = sum A (1 - A) |q| vanishes where one key takes all the weight
+    # (n = 1: A = 1): measure it against at least one query norm, the scale of
+    # its terms before the (1 - A) factor
+    qmax = float(np.sqrt((Q.astype(np.float64) ** 2).sum(-1)).max())
+    assert np.abs(ak[0].cpu().numpy() - ref_k).max() < 1e-4 * max(np.abs(ref_k).max(), qmax)
+    assert rel(av[0].cpu().numpy(), ref_v) < 1e-4
