@@ -63,11 +63,8 @@ class AnTKVLlama:
         for _ in range(cfg.layers):
             ck = rng.standard_normal((cfg.kv_heads, vq.m, vq.d_sub)).astype(np.float32)
             cv = rng.standard_normal((cfg.kv_heads, vq.m, vq.d_sub)).astype(np.float32)
-            cache = QuantizedKVCache(
-                CacheConfig(vq=vq, anchor_fraction=cfg.anchor_fraction, window_size=cfg.window,
-                            theta_base=cfg.theta),
-                Codebook(vq, ck), Codebook(vq, cv), batch=batch, q_heads=cfg.q_heads,
-                kv_heads=cfg.kv_heads, capacity=capacity)
+            self._cache_args = (vq, batch, capacity)
+            cache = self._new_cache(Codebook(vq, ck), Codebook(vq, cv))
             self.layers.append({
                 "wqkv": w((cfg.q_heads + 2 * cfg.kv_heads) * D, H),
                 "wo": w(H, cfg.q_heads * D),
@@ -79,6 +76,22 @@ class AnTKVLlama:
             })
         self.pos = 0
         self._out = torch.empty((batch, cfg.q_heads, D), dtype=torch.float32, device=device)
+
+    def _new_cache(self, cbk, cbv):
+        cfg = self.cfg
+        vq, batch, capacity = self._cache_args
+        return QuantizedKVCache(
+            CacheConfig(vq=vq, anchor_fraction=cfg.anchor_fraction, window_size=cfg.window,
+                        theta_base=cfg.theta),
+            cbk, cbv, batch=batch, q_heads=cfg.q_heads, kv_heads=cfg.kv_heads, capacity=capacity)
+
+    def reset(self):
+        """Empty every layer's cache (same codebooks), position 0: the next
+        prefill starts a new sequence with warm allocators and libraries."""
+        for L in self.layers:
+            c = L["cache"]
+            L["cache"] = self._new_cache(c.codebook_k, c.codebook_v)
+        self.pos = 0
 
     def _split(self, qkv, n):
         c = self.cfg

@@ -23,6 +23,11 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 logits = model.prefill(toks)
 torch.cuda.synchronize()
+t_cold = time.perf_counter() - t0
+model.reset()                       # the same prompt again: warm allocator, cuBLAS, kernels
+t0 = time.perf_counter()
+logits = model.prefill(toks)
+torch.cuda.synchronize()
 t_prefill = time.perf_counter() - t0
 tok = logits.argmax(-1)
 qpos = torch.full((1,), model.pos, dtype=torch.int64, device="cuda")
@@ -62,5 +67,5 @@ for _ in range(10):
 a1.record()
 torch.cuda.synchronize()
 att_ms = a0.elapsed_time(a1) / 10
-print(f"ctx {args.ctx} x {args.layers} layers: prefill {t_prefill:.2f} s, decode {ms:.3f} ms/token "
+print(f"ctx {args.ctx} x {args.layers} layers: prefill {t_prefill:.2f} s (cold first call {t_cold:.2f} s), decode {ms:.3f} ms/token "
       f"({1e3 / ms:.1f} tok/s), attention {att_ms:.3f} ms/token ({att_ms / ms:.0%})")
