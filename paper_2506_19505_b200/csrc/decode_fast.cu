@@ -75,7 +75,7 @@ struct __align__(128) FastSmem {
   unsigned long long full[FK_WARPS][FK_NS];
   unsigned long long pfull[FK_WARPS];
   unsigned long long tbar, qbar;
-  int ticket, gticket;
+  int ticket;
   unsigned long long t0clk;                  // trace: start clock of the CTA
 };
 
@@ -200,8 +200,11 @@ struct StepArgs {
   int splits;              // CTAs per (b, head)
   int early;               // the previous kernel in the stream wrote no state of this
                            // cache: read cache state before griddepcontrol.wait
-  int early_q;             // ... and none of q / qpos: the query rows, its position and
-                           // the frame angles come before the wait too
+  int early_q;             // ... and none of q / qpos / the appended rows: then nothing
+                           // this launch reads was written by the previous kernel, and
+                           // the wait (with the dependents' release) moves to the end of
+                           // the streaming loop -- the whole prologue, the pool tiles
+                           // and the loop overlap the previous launch's tail
   unsigned long long *trace;   // optional per-CTA timeline (ANTKV_TRACE=1)
 };
 
@@ -666,7 +669,12 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   extern __shared__ __align__(128) unsigned char smraw[];
   FastSmem &sm = *reinterpret_cast<FastSmem *>(smraw);
   MergeSmem &mg = *reinterpret_cast<MergeSmem *>(&sm.pool[0][0]);
-  const int b = blockIdx.z, h = blockIdx.y, split = blockIdx.x;
+  // grid (heads, splits, sequences), heads fastest: the CTAs are dispatched
+  // split-major, so each head's last split -- the one with the reduced share
+  // that also prepares the cache update -- goes out last, onto the SMs the
+  // previous launch frees last (its combining CTAs), where the smaller share
+  // absorbs the late start
+  const int b = blockIdx.z, h = blockIdx.x, split = blockIdx.y;
   const int S = a.splits;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -812,9 +820,15 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   // inputs produced by earlier kernels (q, positions, the appended rows) are
   // read after the previous kernel completed unless the host vouched for
   // them (early / early_q); only then may the next kernel start (a
-  // dependency chain of depth one)
-  if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // dependency chain of depth one).  With early_q nothing read here comes
+  // from the previous kernel: wait and release after the streaming loop
+  // instead (every launch still waits before it completes, so completion
+  // keeps implying the predecessor's, and the dependents still launch only
+  // after this launch has waited).
+  if (!a.early_q) {
+    if (a.early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   if (!a.early_q) {
     qp = a.qpos[b];
     if (threadIdx.x == 0) {
@@ -969,6 +983,10 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   FK_TR(9);
+  if (a.early_q) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 
   // ---- merge 8 warps x 2 streams (+ the appended token) -> partial (natural log)
   __syncthreads();   // pool tiles consumed: the pool area becomes merge scratch
@@ -1027,8 +1045,11 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
 
   FK_TR(13);
-  // ---- tickets: the last CTA of (b, h) combines and commits; the last CTA
-  // of sequence b publishes its new length
+  // ---- tickets: the last CTA of (b, h) combines and commits; the last of
+  // those per sequence publishes its new length.  (Only the heads' last CTAs
+  // touch the per-sequence counter: with every CTA incrementing that single
+  // address, the 144 serialized L2 atomics held each CTA's exit -- and with
+  // it the next launch's start on that SM -- ~5 us past its partial.)
   // The CTA barrier orders every thread's partial stores before thread 0's
   // gpu-scope release (cumulative); the acquire half orders the last CTA's
   // reads of the other partials after its ticket, and the next barrier
@@ -1038,14 +1059,13 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   if (threadIdx.x == 0) {
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     sm.ticket = atomicAdd(&a.cnt[bh], 1);
-    sm.gticket = a.knew ? atomicAdd(&a.cnt[(int64_t)c.B * c.Hkv + b], 1) : -1;
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
   if (a.trace && threadIdx.x == 0) {
     tr[10] = gtimer();
     unsigned long long *o =
-        a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+        a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.x + blockIdx.x) * gridDim.y + blockIdx.y);
     o[0] = smid() | ((unsigned long long)sm.ticket << 32);
     for (int i = 2; i <= 9; ++i) o[i] = tr[i] - tr[1];
     o[10] = tr[10];   // global timer after the tickets (absolute, like o[1])
@@ -1058,12 +1078,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     o[15] = 0;
     sm.t0clk = tr[1];
   }
-  if (threadIdx.x == 0 && sm.gticket == c.Hkv * S - 1) {
-    // every CTA of sequence b has read seq_len: publish the appended token
+  if (sm.ticket != S - 1) return;
+  if (threadIdx.x == 0 && a.knew &&
+      atomicAdd(&a.cnt[(int64_t)c.B * c.Hkv + b], 1) == c.Hkv - 1) {
+    // the last CTA of every head of sequence b is here, so every CTA of the
+    // sequence has read seq_len: publish the appended token
     c.seq_len[b] = n + 1;
     a.cnt[(int64_t)c.B * c.Hkv + b] = 0;
   }
-  if (sm.ticket != S - 1) return;
   if (warp < 4) {
     // warp hh combines head hh: lane = 4 dims; the loads of up to 24 splits
     // are in flight together, then a running max across passes
@@ -1107,14 +1129,14 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     if (lane == 0 && a.lse) a.lse[row] = M + logf(L);
     if (a.trace && threadIdx.x == 0) {
       unsigned long long *o =
-          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.x + blockIdx.x) * gridDim.y + blockIdx.y);
       o[15] = clock64() - sm.t0clk;
     }
   } else if (threadIdx.x == 128) {
     if (a.knew) commit_update(c, a, b, h, n);   // overlaps the combine
     if (a.trace) {
       unsigned long long *o =
-          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+          a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.x + blockIdx.x) * gridDim.y + blockIdx.y);
       o[11] = clock64() - sm.t0clk;
     }
     a.cnt[bh] = 0;
@@ -1223,7 +1245,9 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   // ... and q / qpos, unless the previous fused launch on this stream (the
   // only kernel that can still be running then) wrote them
   a.early_q = a.early && !overlaps_previous_fast_outputs(st, q, (int64_t)c.B * c.Hq * 128 * dtype_size(qdtype)) &&
-              !overlaps_previous_fast_outputs(st, qpos, (int64_t)c.B * sizeof(int64_t));
+              !overlaps_previous_fast_outputs(st, qpos, (int64_t)c.B * sizeof(int64_t)) &&
+              (!knew || !overlaps_previous_fast_outputs(st, knew, (int64_t)c.B * c.Hkv * 128 * dtype_size(kvdtype))) &&
+              (!vnew || !overlaps_previous_fast_outputs(st, vnew, (int64_t)c.B * c.Hkv * 128 * dtype_size(kvdtype)));
   record_fast_outputs(st, out, (int64_t)c.B * c.Hq * 128 * sizeof(float), lse,
                       lse ? (int64_t)c.B * c.Hq * sizeof(float) : 0);
   const size_t smem = sizeof(FastSmem);
@@ -1237,7 +1261,7 @@ int decode_fast_launch(const antkv_cache_desc &c, const void *q, int qdtype, con
   // programmatic dependent launch: the prologue's immutable prefetch overlaps
   // the previous kernel's tail (griddepcontrol.wait orders the rest)
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.splits, c.Hkv, c.B);
+  cfg.gridDim = dim3(c.Hkv, a.splits, c.B);
   cfg.blockDim = dim3(FK_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

@@ -66,6 +66,7 @@ def main():
     f = (A[:, 12] / ((A[:, 10] - A[:, 1]) / 1e3))
     print(f"A: SM clock from (globaltimer, clock64) at the ticket: med {np.median(f):.0f} MHz "
           f"(min {f.min():.0f}, max {f.max():.0f})")
+    mhz = float(np.median(f))   # cycle stamps converted at the measured clock, not the nominal one
     a_end = max(np.max((A[:, 1] - t0) / 1e3 + A[:, 15] / mhz), np.max((A[:, 1] - t0) / 1e3 + A[:, 11] / mhz))
     print(f"A: start {0:.1f}  loop start med {np.median(col(A, 8)):.1f}  loop end med {np.median(col(A, 9)):.1f} "
           f"max {np.max(col(A, 9)):.1f}  partial max {np.max(col(A, 13)):.1f}  A done (combine/commit) {a_end:.1f} us")
