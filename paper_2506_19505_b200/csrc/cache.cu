@@ -189,98 +189,119 @@ __global__ void vq_decode_kernel(const void *__restrict__ codes, int code_bytes,
 // ------------------------------------------------------------ cache state
 __device__ __forceinline__ int64_t bh_index(int b, int h, int H) { return (int64_t)b * H + h; }
 
-// Per (b, head) layout from the sorted anchor list (cache.py:126-139).
-// One CTA per (b, head); the codes were written by the bulk encoder.
-__global__ void cache_build_kernel(antkv_cache_desc c, const void *__restrict__ K,
-                                   const void *__restrict__ V, int dtype,
-                                   const int64_t *__restrict__ positions, int n,
-                                   const int32_t *__restrict__ anchors, int anchor_stride) {
+// Per (b, head) layout from the sorted anchor list (cache.py:126-139):
+// qmask, pool slots (anchors, then the window), free stack, head state.
+// One CTA per (b, head); the codes were written by the bulk encoder, the
+// pool rows and positions are copied by the launcher's next steps.
+__global__ void cache_build_kernel(antkv_cache_desc c, int n, const int32_t *__restrict__ anchors,
+                                   int anchor_stride) {
   const int b = blockIdx.x / c.Hkv, h = blockIdx.x % c.Hkv;
   const int64_t bh = bh_index(b, h, c.Hkv);
   const int32_t *anc = anchors + bh * anchor_stride;
+  // Every step in parallel: the serial thread-0 loops this replaces ran one
+  // dependent global round trip per anchor (~0.5 ms at 128K).
   // a list may end in -1 padding (sequence shards hold different anchor
   // counts per head); the valid prefix is sorted ascending
-  __shared__ int s_na;
-  if (threadIdx.x == 0) {
-    int k = 0;
-    while (k < anchor_stride && anc[k] >= 0) ++k;
-    s_na = k;
+  constexpr int kWinWords = 64;                 // window-anchor bitmap (windows <= 2048)
+  __shared__ int s_na, s_nw;
+  __shared__ uint32_t s_winanc[kWinWords];
+  const int wstart = n - c.window_size > 0 ? n - c.window_size : 0;
+  const int W = n - wstart;                     // windowed-or-anchor tail tokens
+  if (threadIdx.x == 0) s_na = 0;
+  for (int i = threadIdx.x; i < kWinWords; i += blockDim.x) s_winanc[i] = 0u;
+  __syncthreads();
+  {
+    int cnt = 0;
+    for (int k = threadIdx.x; k < anchor_stride; k += blockDim.x) cnt += anc[k] >= 0 ? 1 : 0;
+    if (cnt) atomicAdd(&s_na, cnt);
   }
   __syncthreads();
   const int n_anchors = s_na;
   uint32_t *qm = c.qmask + bh * (c.capacity / 32);
   // quantized bit = not anchor and j < n - window
-  const int wstart = n - c.window_size > 0 ? n - c.window_size : 0;
   for (int w = threadIdx.x; w < c.capacity / 32; w += blockDim.x) {
-    uint32_t bits = 0;
-    for (int k = 0; k < 32; ++k) {
-      int j = w * 32 + k;
-      if (j < wstart) bits |= 1u << k;
-    }
-    qm[w] = bits;
+    const int lo = w * 32;
+    qm[w] = lo + 32 <= wstart ? 0xffffffffu : (lo >= wstart ? 0u : (1u << (wstart - lo)) - 1u);
   }
   __syncthreads();
-  for (int a = threadIdx.x; a < n_anchors; a += blockDim.x) {
-    int j = anc[a];
-    if (j < wstart) atomicAnd(&qm[j / 32], ~(1u << (j % 32)));
-  }
+  int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
+  int8_t *pkind = c.pool_kind + bh * c.pool_capacity;
   // pool: anchors first (ascending), then windowed tokens (ascending)
-  __shared__ int s_used;
-  __shared__ int s_win;
+  for (int a = threadIdx.x; a < n_anchors; a += blockDim.x) {
+    const int j = anc[a];
+    if (j < wstart) atomicAnd(&qm[j / 32], ~(1u << (j % 32)));
+    else if (W <= 32 * kWinWords) atomicOr(&s_winanc[(j - wstart) / 32], 1u << ((j - wstart) % 32));
+    ptok[a] = j;
+    pkind[a] = ANTKV_KIND_ANCHOR;
+  }
+  __syncthreads();
+  int32_t *ring = c.win_ring + bh * (c.window_size + 1);
+  if (threadIdx.x < 32) {           // warp 0: the tail tokens that are not anchors, in order
+    const int lane = threadIdx.x;
+    int off = 0;
+    if (W <= 32 * kWinWords) {
+      for (int base = 0; base < W; base += 32) {
+        const int i = base + lane;
+        const bool keep = i < W && !((s_winanc[i / 32] >> (i % 32)) & 1u);
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const int pos = off + __popc(m & ((1u << lane) - 1u)), slot = n_anchors + pos;
+          ptok[slot] = wstart + i;
+          pkind[slot] = ANTKV_KIND_WINDOWED;
+          ring[pos] = slot;
+        }
+        off += __popc(m);
+      }
+    } else if (lane == 0) {         // windows beyond the bitmap: the serial merge
+      int ai = 0;
+      for (int j = wstart; j < n; ++j) {
+        while (ai < n_anchors && anc[ai] < j) ++ai;
+        if (ai < n_anchors && anc[ai] == j) continue;
+        ptok[n_anchors + off] = j;
+        pkind[n_anchors + off] = ANTKV_KIND_WINDOWED;
+        ring[off] = n_anchors + off;
+        ++off;
+      }
+    }
+    if (lane == 0) s_nw = off;
+  }
+  __syncthreads();
+  const int nw = s_nw, used = n_anchors + nw;
+  int32_t *fs = c.free_stack + bh * c.pool_capacity;
+  for (int s2 = used + threadIdx.x; s2 < c.pool_capacity; s2 += blockDim.x) {
+    ptok[s2] = -1;
+    pkind[s2] = ANTKV_KIND_FREE;
+    fs[c.pool_capacity - 1 - s2] = s2;         // the stack pops the lowest free slot first
+  }
   if (threadIdx.x == 0) {
-    int slot = 0;
-    int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
-    int8_t *pkind = c.pool_kind + bh * c.pool_capacity;
-    for (int a = 0; a < n_anchors; ++a) {
-      ptok[slot] = anc[a];
-      pkind[slot] = ANTKV_KIND_ANCHOR;
-      ++slot;
-    }
-    int32_t *ring = c.win_ring + bh * (c.window_size + 1);
-    int ai = 0, nw = 0;
-    for (int j = wstart; j < n; ++j) {
-      while (ai < n_anchors && anc[ai] < j) ++ai;
-      if (ai < n_anchors && anc[ai] == j) continue;
-      ptok[slot] = j;
-      pkind[slot] = ANTKV_KIND_WINDOWED;
-      ring[nw++] = slot;
-      ++slot;
-    }
-    for (int s = slot; s < c.pool_capacity; ++s) {
-      ptok[s] = -1;
-      pkind[s] = ANTKV_KIND_FREE;
-    }
-    int32_t *fs = c.free_stack + bh * c.pool_capacity;
-    int top = 0;
-    for (int s = c.pool_capacity - 1; s >= slot; --s) fs[top++] = s;
     int32_t *hs = c.hstate + bh * ANTKV_HSTATE_WORDS;
     hs[ANTKV_HS_ANCHORS] = n_anchors;
     hs[ANTKV_HS_WIN_HEAD] = 0;
     hs[ANTKV_HS_WIN_COUNT] = nw;
-    hs[ANTKV_HS_FREE_TOP] = top;
-    hs[ANTKV_HS_POOL_HIGH] = slot;
-    s_used = slot;
-    s_win = nw;
+    hs[ANTKV_HS_FREE_TOP] = c.pool_capacity - used;
+    hs[ANTKV_HS_POOL_HIGH] = used;
   }
-  __syncthreads();
-  // copy rows into the pool (bf16)
-  const int used = s_used;
-  const int32_t *ptok = c.pool_tok + bh * c.pool_capacity;
-  for (int s = 0; s < used; ++s) {
-    const int j = ptok[s];
-    const int64_t src = (bh * n + j) * c.d;
-    const int64_t dst = (bh * c.pool_capacity + s) * 2 * c.d;
-    for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-      store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(K, src + t, dtype));
-      store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(V, src + t, dtype));
-    }
+  // (the rows themselves are copied by cache_pool_rows_kernel, one CTA per
+  // pool slot: a loop here over the ~1300 slots of a 128K cache ran one
+  // dependent global round trip per row, 1.3 ms)
+  // (positions are copied by the launcher: one CTA copying 1 MB of them at
+  // 128K took ~0.3 ms)
+  if (h == 0 && threadIdx.x == 0) c.seq_len[b] = n;
+}
+
+// K / V rows of the used pool slots (after cache_build_kernel): slot = blockIdx.x.
+__global__ void cache_pool_rows_kernel(antkv_cache_desc c, const void *__restrict__ K,
+                                       const void *__restrict__ V, int dtype, int n) {
+  const int slot = blockIdx.x;
+  const int64_t bh = blockIdx.y;
+  if (slot >= c.hstate[bh * ANTKV_HSTATE_WORDS + ANTKV_HS_POOL_HIGH]) return;
+  const int j = c.pool_tok[bh * c.pool_capacity + slot];
+  const int64_t src = (bh * n + j) * c.d;
+  const int64_t dst = (bh * c.pool_capacity + slot) * 2 * c.d;
+  for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
+    store_elem(c.pool_rows, dst + t, c.row_dtype, load_elem(K, src + t, dtype));
+    store_elem(c.pool_rows, dst + c.d + t, c.row_dtype, load_elem(V, src + t, dtype));
   }
-  if (h == 0) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x)
-      c.positions[(int64_t)b * c.capacity + j] = positions[(int64_t)b * n + j];
-    if (threadIdx.x == 0) c.seq_len[b] = n;
-  }
-  (void)s_win;
 }
 
 // Fast path: fp16 copy of pool row `slot` (K with RoPE applied at `pos`, V)
@@ -650,8 +671,16 @@ extern "C" int antkv_cache_build(const antkv_cache_desc *c, const void *K, const
                      c->d_sub, c->codes + code_stream_bytes(16 * G, c->code_bytes), c->code_bytes,
                      (int64_t)c->capacity * 2 * G, 32 * G, G, nullptr, st);
   if (rc) return rc;
-  cache_build_kernel<<<nsets, 256, 0, st>>>(*c, K, V, dtype, positions, n, anchors, n_anchors);
+  cache_build_kernel<<<nsets, 256, 0, st>>>(*c, n, anchors, n_anchors);
   ANTKV_LAUNCH_CHECK("cache_build_kernel");
+  cache_pool_rows_kernel<<<dim3(c->pool_capacity, nsets), 128, 0, st>>>(*c, K, V, dtype, n);
+  ANTKV_LAUNCH_CHECK("cache_pool_rows_kernel");
+  if (n > 0) {   // positions [B][n] -> [B][capacity]
+    const cudaError_t e = cudaMemcpy2DAsync(c->positions, (size_t)c->capacity * sizeof(int64_t), positions,
+                                            (size_t)n * sizeof(int64_t), (size_t)n * sizeof(int64_t), c->B,
+                                            cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "positions copy");
+  }
   if (c->pool_f16) {
     cache_pool_f16_kernel<<<dim3(c->pool_capacity, nsets), 64, 0, st>>>(*c);
     ANTKV_LAUNCH_CHECK("cache_pool_f16_kernel");
