@@ -14,11 +14,12 @@
 // splits of power-of-two-scaled tiles (Kh.Qh + Kh.Ql + Kl.Qh, float32
 // accumulation), scale removed exactly.
 //
-// Warp roles (10 warps): warp 0 lane 0 issues the bulk copies (K tile once,
-// Q tiles through a 2-stage ring); warp 1 owns the TMEM allocation and its
-// lane 0 issues the 24 MMAs per query tile; warps 2-9 are the epilogue —
-// warps w and w + 4 share TMEM lanes 32 (w % 4) .. + 31 and split the 128
-// query columns.  TMEM: two 128-column logit buffers (the MMAs of tile t + 1
+// Warp roles (2 + 4 TC_EG warps): warp 0 lane 0 issues the bulk copies (K
+// tile once, Q tiles with their 1 KB of packed column statistics through a
+// 3-stage ring); warp 1 owns the TMEM allocation and issues the 24 MMAs per
+// query tile warp-wide (elect.sync); the other warps are the epilogue —
+// warps w, w + 4, ... share TMEM lanes 32 (w % 4) .. + 31 and split the 128
+// query columns into TC_EG groups.  TMEM: two 128-column logit buffers (the MMAs of tile t + 1
 // overlap the exponentials of tile t) and the K tile's fp16 parts (128
 // columns), which the epilogue warps copy there once so the MMAs read only
 // the Q tile from shared memory (at N = 128 both operands from shared memory
@@ -380,7 +381,7 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
         __syncwarp();
       }
     }
-  } else {                          // ---- epilogue: 8 warps
+  } else {                          // ---- epilogue: 4 TC_EG warps
     const int et = threadIdx.x - 64;                  // 0 .. 255
     const int quarter = warp & 3, cg = (warp - 2) >> 2;     // TMEM lanes, column group
     const int key_local = 32 * quarter + lane;
