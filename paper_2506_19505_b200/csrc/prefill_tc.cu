@@ -544,7 +544,8 @@ int launch_ans_tc(const float *Qs, const float *Kr, const float *M, const float 
 // float32 accumulation in TMEM.
 //
 // Warps: 0 bulk-copy producer (two rings of two stages: K hi | K lo, 64 KB,
-// freed as soon as S(t) completes; V^T, 32 KB, freed by P.V(t)), 1 TMEM owner + MMA issuer (S of tile t is issued before P.V of
+// freed as soon as S(t) completes; V^T, 32 KB, freed by P.V(t)), 1 TMEM owner + MMA issuer, warp-wide
+// with elect.sync so the operands stay uniform (S of tile t is issued before P.V of
 // tile t - 1 so the tensor core works while the softmax of t - 1 runs), 2-17
 // softmax: warps w, w + 4, w + 8, w + 12 own the same 32 rows (TMEM lanes)
 // and take 32 key columns each, exchanging quarter-row maxima through shared
