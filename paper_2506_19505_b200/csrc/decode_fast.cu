@@ -75,7 +75,6 @@ struct __align__(128) FastSmem {
   unsigned long long full[FK_WARPS][FK_NS];
   unsigned long long pfull[FK_WARPS];
   unsigned long long tbar, qbar;
-  int ticket;
   unsigned long long t0clk;                  // trace: start clock of the CTA
 };
 
@@ -1045,30 +1044,41 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
   }
 
   FK_TR(13);
-  // ---- tickets: the last CTA of (b, h) combines and commits; the last of
-  // those per sequence publishes its new length.  (Only the heads' last CTAs
-  // touch the per-sequence counter: with every CTA incrementing that single
-  // address, the 144 serialized L2 atomics held each CTA's exit -- and with
-  // it the next launch's start on that SM -- ~5 us past its partial.)
+  // ---- arrivals: the head's last split (the reduced-share CTA that also
+  // prepared the cache update, dispatched last) combines and commits; every
+  // other CTA releases its partial with a fire-and-forget red.release and
+  // exits at once, so the next launch's CTA can take its SM without waiting
+  // for a gpu-scope fence round trip (a returned ticket cost ~1-2 us here).
   // The CTA barrier orders every thread's partial stores before thread 0's
-  // gpu-scope release (cumulative); the acquire half orders the last CTA's
-  // reads of the other partials after its ticket, and the next barrier
-  // passes that on to the CTA.  (One thread fences: a CTA-wide fence.sc.gpu
-  // -- __threadfence -- took ~4 us here under the other CTAs' streaming.)
+  // release (cumulative); the combiner's acquire load of the count orders
+  // its reads of the partials after them, and the next barrier passes that
+  // on to the CTA.  The combiners are the last CTAs in dispatch order (split
+  // major), and the ones waiting hold at most one SM per (b, head) -- never
+  // all SMs -- while every other CTA runs to completion, so the CTAs a
+  // combiner waits for always get an SM (also when S x B x Hkv exceeds the
+  // SM count, e.g. the minimum splits of very long caches).  The last CTA of
+  // the heads' combiners publishes the sequence's new length.
   __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    sm.ticket = atomicAdd(&a.cnt[bh], 1);
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  const bool combiner = split == S - 1;
+  if (!combiner) {
+    if (threadIdx.x == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt + bh) : "memory");
+  } else if (threadIdx.x == 0) {
+    uint32_t seen;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(a.cnt + bh) : "memory");
+      if ((int)seen >= S - 1) break;
+      __nanosleep(64);
+    }
   }
-  __syncthreads();
+  if (combiner) __syncthreads();
   if (a.trace && threadIdx.x == 0) {
     tr[10] = gtimer();
     unsigned long long *o =
         a.trace + FK_TRACE_WORDS * ((blockIdx.z * gridDim.x + blockIdx.x) * gridDim.y + blockIdx.y);
-    o[0] = smid() | ((unsigned long long)sm.ticket << 32);
+    o[0] = smid() | ((unsigned long long)split << 32);   // (the split stands in for the old ticket)
     for (int i = 2; i <= 9; ++i) o[i] = tr[i] - tr[1];
-    o[10] = tr[10];   // global timer after the tickets (absolute, like o[1])
+    o[10] = tr[10];   // global timer after the arrival (absolute, like o[1])
     tr[12] = clock64();   // ... and the SM clock at the same point (clock calibration)
     o[1] = g0;
     o[11] = 0;
@@ -1078,7 +1088,7 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     o[15] = 0;
     sm.t0clk = tr[1];
   }
-  if (sm.ticket != S - 1) return;
+  if (!combiner) return;
   if (threadIdx.x == 0 && a.knew &&
       atomicAdd(&a.cnt[(int64_t)c.B * c.Hkv + b], 1) == c.Hkv - 1) {
     // the last CTA of every head of sequence b is here, so every CTA of the
