@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(TT, 1) decode_tc_kernel(antkv_cache_desc c, Tc
         // two token rows per instruction, lanes of one centroid adjacent: the
         // 32 chunks of an instruction touch 2 G cache lines (L1 / L2 gathers
         // cost one wavefront per line, not per lane)
-        constexpr int CPC = DSUB / 8;   // 16-byte chunks per centroid
+        constexpr int CPC = DSUB >= 8 ? DSUB / 8 : 1;   // 16-byte chunks per centroid
         const int jc = lane & 15, rsel = lane >> 4, gq = jc / CPC, within = jc % CPC;
         const uint8_t *cpt = &sm.code[warp][slot][(j % TPS) * TILEB];
         const uint32_t sb = su32(&sm.stage[j % TNST][warp][0]);

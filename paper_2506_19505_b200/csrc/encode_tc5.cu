@@ -94,13 +94,6 @@ __device__ __forceinline__ uint64_t t5_desc(uint32_t addr) {
   return (uint64_t)((addr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-__device__ __forceinline__ void t5_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                       uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
 // Warp-wide forms (all lanes call with the same operands, one elected lane
 // issues): from converged code the operands stay uniform and UTCHMMA needs no
 // per-instruction ELECT/BRA.U.ANY waterfall as under lane == 0.
@@ -116,11 +109,6 @@ __device__ __forceinline__ void t5_commit_w(unsigned long long *bar) {
       "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
       " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(t5_smem(bar))
       : "memory");
-}
-__device__ __forceinline__ void t5_commit(unsigned long long *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   t5_smem(bar))
-               : "memory");
 }
 __device__ __forceinline__ void t5_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
@@ -520,7 +508,7 @@ vq_encode_tc5l_kernel(const uint16_t *__restrict__ X, int64_t rows, int64_t x_se
                       const uint8_t *__restrict__ img, const float *__restrict__ blkmax, int cb_mod, int m,
                       int nblk, void *__restrict__ codes, int code_bytes, int64_t code_set_stride,
                       int64_t code_tile_stride, int64_t code_row_stride, int64_t tiles_per_cta, uint32_t mul) {
-  constexpr int G = 128 / DSUB, TOK = 128 / G, KD = tl_kd<DSUB>(), NCH = DSUB >= 8 ? DSUB / 8 : 1;
+  constexpr int G = 128 / DSUB, KD = tl_kd<DSUB>(), NCH = DSUB >= 8 ? DSUB / 8 : 1;
   constexpr int PT = DSUB == 4 ? 2 : 3 * NCH + 1;   // A chunks rewritten per tile (the rest are constant)
   extern __shared__ __align__(128) unsigned char tlraw[];
   TlSmem &sm = *reinterpret_cast<TlSmem *>(tlraw + ((1024 - (t5_smem(tlraw) & 1023)) & 1023));

@@ -382,7 +382,6 @@ ans_tc_kernel(const uint8_t *__restrict__ Qt, const float *__restrict__ Qsc, con
       }
     }
   } else {                          // ---- epilogue: 4 TC_EG warps
-    const int et = threadIdx.x - 64;                  // 0 .. 255
     const int quarter = warp & 3, cg = (warp - 2) >> 2;     // TMEM lanes, column group
     const int key_local = 32 * quarter + lane;
     const int key = kt * TC_ROWS + key_local;
