@@ -93,7 +93,9 @@ ANTKV_API int antkv_device_check(int device);
  * Only then may the fused decode kernel, launched with programmatic
  * dependent launch, read the cache state, q and the position before
  * griddepcontrol.wait (its predecessor is then known to be one of ours and
- * to leave them untouched).  Default off: a foreign kernel writing q (a
+ * to leave them untouched); when none of its inputs (q, the position, the
+ * appended k / v rows) is an output of that predecessor, the wait moves
+ * behind the streaming loop.  Default off: a foreign kernel writing q (a
  * GEMM, RoPE, a torch copy) may be the predecessor, so everything is read
  * after the wait.  New (no reference counterpart). */
 ANTKV_API int antkv_stream_exclusive(void *stream, int exclusive);
