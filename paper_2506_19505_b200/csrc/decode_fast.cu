@@ -764,9 +764,13 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     tma_bulk_g2s(&sm.pool[warp][0], pool_g + (int64_t)tile * FK_POOL_TILE_BYTES, FK_POOL_TILE_BYTES,
                  &sm.pfull[warp]);
   };
+#ifndef FK_EARLY_SLOTS
+#define FK_EARLY_SLOTS 2   // slots 2-3 after the prologue: 33.4 -> 33.2 us (less shared-memory contention while the tables load)
+#endif
+  constexpr int kEarlySlots = FK_EARLY_SLOTS < FK_NS ? FK_EARLY_SLOTS : FK_NS;
   if (lane == 0) {
     if (pt0 + warp < pt1) issue_pool(pt0 + warp);
-    for (int it = 0; it < min(nslots, FK_NS); ++it) issue_code(it);
+    for (int it = 0; it < min(nslots, kEarlySlots); ++it) issue_code(it);
   }
   // key-rotation constants and frame steps into registers (the tables copy
   // was issued first; the code / pool copies above are already in flight)
@@ -859,6 +863,8 @@ decode_fast_kernel(antkv_cache_desc c, StepArgs a) {
     }
   }
   __syncthreads();
+  if (kEarlySlots < FK_NS && lane == 0)   // the rest of the ring's first fill
+    for (int it = kEarlySlots; it < min(nslots, FK_NS); ++it) issue_code(it);
   FK_TR(14);
   {
     const int fr = 2 * warp + (g >= 4 ? 1 : 0);
