@@ -1579,3 +1579,50 @@ def test_tcgen05_prefill_small_and_ragged_vs_oracle(n, Hq, Hkv):
     qmax = float(np.sqrt((Q.astype(np.float64) ** 2).sum(-1)).max())
     assert np.abs(ak[0].cpu().numpy() - ref_k).max() < 1e-4 * max(np.abs(ref_k).max(), qmax)
     assert rel(av[0].cpu().numpy(), ref_v) < 1e-4
+
+
+def test_exclusive_stream_late_wait_matches_plain_launches():
+    """Two caches alternating on a stream declared exclusive (the bench's
+    graph situation): each fused launch follows the other cache's, so it
+    reads its cache state early and, when none of q / qpos / k / v is the
+    previous launch's output, waits for that launch only after its streaming
+    loop.  Every fourth step takes as its (fp32) q the output the previous
+    launch just wrote, which must put the wait back in front.  Outputs are
+    bitwise those of the same steps on the default stream (everything read
+    after the wait)."""
+    from paper_2506_19505_b200 import CacheConfig, Codebook, QuantizedKVCache, VqConfig, _lib
+    vq = VqConfig.from_notation("d8m256")
+    cfg = CacheConfig(vq=vq, anchor_fraction=0.02, window_size=8)
+    dev = lambda x, dt=torch.float32: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(dt)
+
+    def make(seed):
+        Q, K, V = qkv(seed, 8, 2, 700, 128, heavy=2)
+        ck, cv = codebooks(seed, 2, 256, 8)
+        c = QuantizedKVCache(cfg, Codebook(vq, ck), Codebook(vq, cv), q_heads=8, batch=1, capacity=1024)
+        c.prefill(dev(Q[None, :, :640], torch.bfloat16), dev(K[None, :, :640], torch.bfloat16),
+                  dev(V[None, :, :640], torch.bfloat16), np.arange(640))
+        return c, Q, K, V
+
+    outs = {}
+    for mode in ("plain", "exclusive"):
+        caches = [make(61), make(62)]
+        steps = range(640, 680)
+        qs = [[dev(c[1][None, :, t]) for t in steps] for c in caches]
+        ks = [[dev(c[2][None, :, t]) for t in steps] for c in caches]
+        vs = [[dev(c[3][None, :, t]) for t in steps] for c in caches]
+        ps = [torch.tensor([t], device="cuda") for t in steps]
+        obufs = [[torch.empty((1, 8, 128), device="cuda") for _ in steps] for _ in caches]
+        torch.cuda.synchronize()
+        ctx = _lib.exclusive_stream() if mode == "exclusive" else __import__("contextlib").nullcontext()
+        prev = None
+        with ctx:
+            for i, t in enumerate(steps):
+                for j, (c, Q, K, V) in enumerate(caches):
+                    q = prev if (prev is not None and i % 4 == 3) else qs[j][i]
+                    c.step_device(q, ks[j][i], vs[j][i], ps[i], obufs[j][i])
+                    c._n += 1
+                    prev = obufs[j][i]
+        torch.cuda.synchronize()
+        outs[mode] = [torch.stack(o).cpu().numpy() for o in obufs]
+    for x, y in zip(outs["plain"], outs["exclusive"]):
+        assert np.array_equal(x, y)
